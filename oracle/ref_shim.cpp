@@ -1,0 +1,207 @@
+// ref_shim.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" entry points over the UNMODIFIED reference library (moesim,
+// compiled from /root/reference/proj/src/*.cpp by oracle/Makefile into
+// oracle/_ref/libmoesim_ref.so). Used by the tests to pin the oracle and the
+// product against the reference itself, by tests/golden/make_golden.py, and
+// by bench.py's reference arm for the count-level CPU path timing.
+// No reference source is copied: this file only calls the public API in
+// proj/include/moesim/*.hpp.
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "moesim/baselines.hpp"
+#include "moesim/placement.hpp"
+#include "moesim/policy.hpp"
+#include "moesim/router.hpp"
+#include "moesim/sim_engine.hpp"
+#include "moesim/topology.hpp"
+#include "moesim/workload.hpp"
+
+using namespace moesim;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return 4;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+TokenDemand to_demand(const int64_t* D, int N, int G) {
+  TokenDemand d(0, N, G);
+  std::memcpy(d.demand.data(), D, sizeof(int64_t) * N * G);
+  return d;
+}
+
+Placement to_placement(const int32_t* cnt, int N, int G, int slots) {
+  std::vector<int> counts(cnt, cnt + static_cast<size_t>(N) * G);
+  return Placement::from_counts(counts, N, G, slots);
+}
+
+std::vector<TokenDemand> to_trace(const int64_t* D, int steps, int N, int G) {
+  std::vector<TokenDemand> tr;
+  for (int s = 0; s < steps; ++s) {
+    TokenDemand d = to_demand(D + static_cast<size_t>(s) * N * G, N, G);
+    d.step = s;
+    tr.push_back(std::move(d));
+  }
+  return tr;
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_route(const int64_t* D, const int32_t* cnt, int N, int G, int slots, int64_t* flows) {
+  return guarded([&] {
+    RoutingPlan plan = route(to_demand(D, N, G), to_placement(cnt, N, G, slots));
+    std::memcpy(flows, plan.flows.data(), sizeof(int64_t) * plan.flows.size());
+  });
+}
+
+// Route with a placement given slot-by-slot (slots_GE[g][s] = expert or -1),
+// so placements built by expand/shrink sequences can be reproduced exactly.
+int ref_balance_ratio(const int64_t* D, const int32_t* cnt, int N, int G, int slots,
+                      double* ratio) {
+  return guarded([&] {
+    TokenDemand d = to_demand(D, N, G);
+    Placement p = to_placement(cnt, N, G, slots);
+    *ratio = balance_ratio(d, p, route(d, p));
+  });
+}
+
+int ref_largest_remainder_round(const double* exact, int n, int64_t total, int64_t* out) {
+  return guarded([&] {
+    std::vector<int64_t> r = largest_remainder_round(std::span<const double>(exact, n), total);
+    std::memcpy(out, r.data(), sizeof(int64_t) * r.size());
+  });
+}
+
+int ref_generate_trace(int N, int G, int64_t tokens, double zipf, double drift, uint64_t seed,
+                       int steps, int64_t* out) {
+  return guarded([&] {
+    TraceGeneratorConfig cfg;
+    cfg.num_experts = N;
+    cfg.num_gpus = G;
+    cfg.tokens_per_step = tokens;
+    cfg.zipf_exponent = zipf;
+    cfg.drift_rate = drift;
+    cfg.seed = seed;
+    cfg.num_steps = steps;
+    std::vector<TokenDemand> tr = generate_trace(cfg);
+    for (int s = 0; s < steps; ++s)
+      std::memcpy(out + static_cast<size_t>(s) * N * G, tr[s].demand.data(),
+                  sizeof(int64_t) * N * G);
+  });
+}
+
+// StaticEP baseline through the reference's run_baseline: per-step dropped
+// tokens and balance ratio (of the post-drop routing).
+int ref_static_ep(const int64_t* trace, int steps, int N, int G, double cf, int64_t* dropped,
+                  double* ratio) {
+  return guarded([&] {
+    std::vector<TokenDemand> tr = to_trace(trace, steps, N, G);
+    ClusterTopology topo = ClusterTopology::from_json(
+        ClusterTopology::default_profile(G, (N + G - 1) / G));
+    BaselineConfig b;
+    b.kind = BaselineKind::StaticEP;
+    b.capacity_factor = cf;
+    SimConfig sc;
+    std::vector<StepReport> reps = run_baseline(tr, topo, b, sc);
+    for (int s = 0; s < steps; ++s) {
+      dropped[s] = reps[s].tokens_dropped;
+      ratio[s] = reps[s].balance_ratio;
+    }
+  });
+}
+
+// The dynamic engine (SimEngine::run) on a trace with the default profile
+// (slots per GPU given): per-step balance ratio, replica counts [steps][N],
+// and totals of applied Expand / Shrink / Migrate ops.
+int ref_engine_run(const int64_t* trace, int steps, int N, int G, int slots, int policy_mode,
+                   int interval, double* ratio, int32_t* replicas, int64_t* op_totals) {
+  return guarded([&] {
+    std::vector<TokenDemand> tr = to_trace(trace, steps, N, G);
+    ClusterTopology topo = ClusterTopology::from_json(ClusterTopology::default_profile(G, slots));
+    SimConfig sc;
+    sc.policy_mode = static_cast<PolicyMode>(policy_mode);
+    sc.interval_steps = interval;
+    std::vector<StepReport> reps = run_simulation(tr, topo, sc);
+    op_totals[0] = op_totals[1] = op_totals[2] = 0;
+    for (int s = 0; s < steps; ++s) {
+      ratio[s] = reps[s].balance_ratio;
+      for (int e = 0; e < N; ++e) replicas[static_cast<size_t>(s) * N + e] = reps[s].replica_counts[e];
+      for (const PlacementOp& op : reps[s].plan_applied) op_totals[static_cast<int>(op.kind)] += 1;
+    }
+  });
+}
+
+// One policy round on (D, placement): ops as [kind, expert, gpu, a.gpu, a.slot, b.gpu, b.slot].
+int ref_make_scheduling_plan(const int64_t* D, const int32_t* cnt, int N, int G, int slots,
+                             int horizon, int32_t* ops, int* n_ops, int max_ops) {
+  return guarded([&] {
+    ClusterTopology topo = ClusterTopology::from_json(ClusterTopology::default_profile(G, slots));
+    PolicyConfig pc;
+    pc.amortization_horizon = horizon;
+    SchedulingPlan plan =
+        make_scheduling_plan(to_demand(D, N, G), to_placement(cnt, N, G, slots), topo, pc);
+    int n = 0;
+    for (const PlacementOp& op : plan.ops) {
+      if (n >= max_ops) break;
+      int32_t* o = ops + 7 * n;
+      o[0] = static_cast<int>(op.kind);
+      o[1] = op.expert;
+      o[2] = op.gpu;
+      o[3] = op.a.gpu;
+      o[4] = op.a.slot;
+      o[5] = op.b.gpu;
+      o[6] = op.b.slot;
+      ++n;
+    }
+    *n_ops = n;
+  });
+}
+
+// CPU-baseline timing of the reference's per-step count-level path:
+// `iters` calls of route() + balance_ratio() on the same inputs; returns
+// seconds per call.
+int ref_time_route(const int64_t* D, const int32_t* cnt, int N, int G, int slots, int iters,
+                   double* sec_per_call) {
+  return guarded([&] {
+    TokenDemand d = to_demand(D, N, G);
+    Placement p = to_placement(cnt, N, G, slots);
+    double sink = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < iters; ++i) {
+      RoutingPlan plan = route(d, p);
+      sink += balance_ratio(d, p, plan);
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    *sec_per_call = std::chrono::duration<double>(t1 - t0).count() / iters + sink * 0.0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+// C-ABI glue: error plumbing, device queries, TMA descriptor encoding and the
+// thin extern "C" wrappers that translate exceptions into status codes.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <string>
+
+#include "fm_internal.h"
+
+namespace fm {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+int num_sms() {
+  static int sms = [] {
+    int dev = 0, n = 0;
+    FM_CUDA(cudaGetDevice(&dev));
+    FM_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+  }();
+  return sms;
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    FM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw cuda_error("cuTensorMapEncodeTiled not found");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+}  // namespace
+
+CUtensorMap make_tmap_bf16(const void* base, uint64_t inner, uint64_t outer,
+                           uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer) {
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_stride_elems * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    throw cuda_error("cuTensorMapEncodeTiled failed (code " + std::to_string(static_cast<int>(r)) +
+                     ")");
+  }
+  return map;
+}
+
+void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
+                  const void* aux, const int* seg_start, const int* seg_rows,
+                  const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
+                  cudaStream_t stream);
+
+}  // namespace fm
+
+extern "C" {
+
+const char* fm_last_error(void) { return fm::g_last_error.c_str(); }
+
+const char* fm_version(void) { return "flexmoe_b200 0.1 (sm_100a)"; }
+
+int fm_grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
+                    const void* aux, const int32_t* seg_start, const int32_t* seg_rows,
+                    const int32_t* tile_prefix, int num_groups, int total_rows, int M_w, int N,
+                    int K, void* stream) {
+  return fm::guarded([&] {
+    fm::grouped_gemm(variant, A, B, C, bias, aux, seg_start, seg_rows, tile_prefix, num_groups,
+                     total_rows, M_w, N, K, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+// Internal helpers shared by the C-ABI translation units: status codes,
+// thread-local error text, CUDA error checks and TMA descriptor encoding.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/flexmoe_b200.h"
+
+namespace fm {
+
+// Exception types mirror the reference's error convention:
+// invalid_argument -> FM_ERR_INVALID_ARGUMENT, logic_error -> FM_ERR_LOGIC, ...
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void set_last_error(const std::string& msg);
+
+// Runs `body`, translating exceptions into C status codes.
+template <class F>
+int guarded(F&& body) {
+  try {
+    body();
+    return FM_OK;
+  } catch (const cuda_error& e) {
+    set_last_error(e.what());
+    return FM_ERR_CUDA;
+  } catch (const std::invalid_argument& e) {
+    set_last_error(e.what());
+    return FM_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    set_last_error(e.what());
+    return FM_ERR_OUT_OF_RANGE;
+  } catch (const std::logic_error& e) {
+    set_last_error(e.what());
+    return FM_ERR_LOGIC;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return FM_ERR_RUNTIME;
+  }
+}
+
+inline void check_cuda(cudaError_t err, const char* what) {
+  if (err != cudaSuccess) {
+    throw cuda_error(std::string(what) + ": " + cudaGetErrorString(err));
+  }
+}
+
+#define FM_CUDA(call) ::fm::check_cuda((call), #call)
+#define FM_LAUNCH_CHECK(name) ::fm::check_cuda(cudaGetLastError(), name)
+
+// 2-D bf16 tensor map, 128B swizzle: inner dimension `inner` (contiguous),
+// `outer` rows `row_stride_elems` apart; box = box_inner x box_outer.
+CUtensorMap make_tmap_bf16(const void* base, uint64_t inner, uint64_t outer,
+                           uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer);
+
+int num_sms();
+
+}  // namespace fm

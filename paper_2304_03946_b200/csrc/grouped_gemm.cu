@@ -1,0 +1,392 @@
+// Grouped bf16 GEMM on tcgen05 / TMEM, fed by TMA — the expert FFN of the
+// FlexMoE layer (Eq. 2) forward and backward.
+//
+// The reference models this contraction as `compute_cost = tokens / TPS`
+// (proj/src/cost_model.cpp:30-35); here it is the one real dense op.
+//
+// Layout contract: tokens of each local expert ("group") are
+// contiguous in the permuted buffers, every group padded to a multiple of
+// 128 rows with zero rows. Two schedules share one kernel body:
+//   kRows  : token rows are GEMM-M  (fwd1, fwd2, dgrad1, dgrad2)
+//            C[g][rows, N] = A[rows, K] . B_g      (K fixed)
+//   kWgrad : token rows are GEMM-K  (wgrad)
+//            C[g][M_w, N]  = A[rows_g, M_w]^T . B[rows_g, N]
+//
+// Warp roles (256 threads, one CTA per SM, persistent over tiles):
+//   warp 0  : TMA producer (one elected lane)
+//   warp 1  : MMA issuer   (one elected lane), 128x256x16 UMMA, f32 in TMEM
+//   warp 2  : TMEM allocator (512 columns = two 128x256 f32 accumulators)
+//   warps 4-7: epilogue — tcgen05.ld, bias / ReLU / ReLU-mask, store.
+// Smem ring: 4 stages x (A 16 KB + B 32 KB).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "fm_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace fm {
+namespace gemm {
+
+constexpr int kBM = 128;
+constexpr int kBN = 256;
+constexpr int kBK = 64;
+constexpr int kStages = 4;
+constexpr int kABytes = kBM * kBK * 2;
+constexpr int kBBytes = kBN * kBK * 2;
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kThreads = 256;
+constexpr int kTmemCols = 512;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+constexpr uint32_t kMnChunkBytes = kBK * 128;  // one 64-wide MN chunk of a stage (8 KB)
+
+enum Schedule { kRows = 0, kWgrad = 1 };
+enum Epilogue { kEpiBiasRelu = 0, kEpiBias = 1, kEpiReluMask = 2, kEpiNone = 3, kEpiF32 = 4 };
+
+struct Args {
+  int num_groups;
+  const int* seg_start;    // [groups] first token row of the group (padded layout)
+  const int* seg_rows;     // [groups] rows of the group, multiple of 128
+  const int* tile_prefix;  // [groups+1] kRows: exclusive prefix of tiles per group
+  int M_w;                 // kWgrad: output rows per group
+  int N;                   // output columns
+  int K;                   // kRows: reduction depth
+  int b_rows_per_group;    // kRows: B tensor-map rows between consecutive groups
+  void* out;
+  int ldc;
+  const float* bias;                // [groups][N]
+  const __nv_bfloat16* aux;         // kEpiReluMask: activation [rows][ldc]
+};
+
+struct Tile {
+  int group;
+  int m0;      // kRows: token row; kWgrad: output row
+  int n0;
+  int k_row0;  // kWgrad: first token row of the reduction
+  int num_kb;
+};
+
+template <int SCHED>
+__device__ __forceinline__ int total_tiles(const Args& a) {
+  if (SCHED == kRows) return __ldg(a.tile_prefix + a.num_groups);
+  return a.num_groups * (a.M_w / kBM) * (a.N / kBN);
+}
+
+template <int SCHED>
+__device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g) {
+  Tile tl;
+  const int n_tiles = a.N / kBN;
+  if (SCHED == kRows) {
+    while (__ldg(a.tile_prefix + g + 1) <= t) ++g;
+    const int local = t - __ldg(a.tile_prefix + g);
+    tl.group = g;
+    tl.m0 = __ldg(a.seg_start + g) + (local / n_tiles) * kBM;
+    tl.n0 = (local % n_tiles) * kBN;
+    tl.k_row0 = 0;
+    tl.num_kb = a.K / kBK;
+  } else {
+    const int per_group = (a.M_w / kBM) * n_tiles;
+    g = t / per_group;
+    const int local = t - g * per_group;
+    tl.group = g;
+    tl.m0 = (local / n_tiles) * kBM;
+    tl.n0 = (local % n_tiles) * kBN;
+    tl.k_row0 = __ldg(a.seg_start + g);
+    tl.num_kb = __ldg(a.seg_rows + g) / kBK;
+  }
+  return tl;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int SCHED, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b, const Args args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + kStages * kABytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&map_a);
+    ptx::tma_prefetch_desc(&map_b);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull_bar[b], 1);
+      ptx::mbar_init(&tempty_bar[b], 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_holder, kTmemCols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int ntiles = total_tiles<SCHED>(args);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int g = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile tl = decode_tile<SCHED>(args, t, g);
+        const int b_row_base = tl.group * args.b_rows_per_group;
+        for (int kb = 0; kb < tl.num_kb; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
+          uint8_t* sa = smem_a + stage * kABytes;
+          uint8_t* sb = smem_b + stage * kBBytes;
+          const int k0 = kb * kBK;
+          if (!A_MN) {
+            ptx::tma_load_2d(sa, &map_a, &full_bar[stage], k0, tl.m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j)
+              ptx::tma_load_2d(sa + j * kMnChunkBytes, &map_a, &full_bar[stage], tl.m0 + j * 64,
+                               tl.k_row0 + k0);
+          }
+          if (!B_MN) {
+            ptx::tma_load_2d(sb, &map_b, &full_bar[stage], k0, b_row_base + tl.n0);
+          } else {
+            const int krow = (SCHED == kRows) ? b_row_base + k0 : tl.k_row0 + k0;
+#pragma unroll
+            for (int j = 0; j < kBN / 64; ++j)
+              ptx::tma_load_2d(sb + j * kMnChunkBytes, &map_b, &full_bar[stage], tl.n0 + j * 64,
+                               krow);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBM, kBN, A_MN, B_MN);
+      constexpr uint32_t a_lbo = A_MN ? kMnChunkBytes : 16;
+      constexpr uint32_t b_lbo = B_MN ? kMnChunkBytes : 16;
+      // Advance per UMMA_K=16 step: 32 B inside a K-major swizzle row,
+      // 16 K-rows (2 KB) for MN-major.
+      constexpr uint32_t a_kstep = A_MN ? 16 * 128 : 32;
+      constexpr uint32_t b_kstep = B_MN ? 16 * 128 : 32;
+      int stage = 0;
+      uint32_t phase = 0;
+      int g = 0;
+      int iter = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
+        const Tile tl = decode_tile<SCHED>(args, t, g);
+        const int ab = iter & 1;
+        ptx::mbar_wait(&tempty_bar[ab], ((iter >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + ab * kBN;
+        for (int kb = 0; kb < tl.num_kb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
+          const uint32_t sb = ptx::smem_u32(smem_b + stage * kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t da = ptx::umma_desc_sw128(sa + k * a_kstep, a_lbo, 1024);
+            const uint64_t db = ptx::umma_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
+            ptx::mma_bf16_ss(d_tmem, da, db, idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit(&empty_bar[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit(&tfull_bar[ab]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    int g = 0;
+    int iter = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
+      const Tile tl = decode_tile<SCHED>(args, t, g);
+      const int ab = iter & 1;
+      ptx::mbar_wait(&tfull_bar[ab], (iter >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + ab * kBN;
+      const bool empty_k = tl.num_kb == 0;
+#pragma unroll 1
+      for (int c = 0; c < kBN / 32; ++c) {
+        uint32_t r[32];
+        if (!empty_k) {
+          ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+          ptx::tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0;
+        }
+        const int col = tl.n0 + c * 32;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (EPI == kEpiF32) {
+          float* dst = reinterpret_cast<float*>(args.out) +
+                       (static_cast<size_t>(tl.group) * args.M_w + tl.m0 + row) * args.ldc + col;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+          if (EPI == kEpiBiasRelu || EPI == kEpiBias) {
+            const float4* bp = reinterpret_cast<const float4*>(
+                args.bias + static_cast<size_t>(tl.group) * args.N + col);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 b4 = __ldg(bp + i);
+              v[4 * i] += b4.x;
+              v[4 * i + 1] += b4.y;
+              v[4 * i + 2] += b4.z;
+              v[4 * i + 3] += b4.w;
+            }
+          }
+          if (EPI == kEpiBiasRelu) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+          }
+          const size_t off = static_cast<size_t>(tl.m0 + row) * args.ldc + col;
+          if (EPI == kEpiReluMask) {
+            const uint4* ap = reinterpret_cast<const uint4*>(args.aux + off);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint4 m = __ldg(ap + i);
+              const uint32_t w[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                // bf16 pair: positive iff sign clear and magnitude non-zero.
+                const uint32_t lo = w[j] & 0xFFFFu, hi = w[j] >> 16;
+                if (!(lo != 0 && lo < 0x8000u)) v[8 * i + 2 * j] = 0.0f;
+                if (!(hi != 0 && hi < 0x8000u)) v[8 * i + 2 * j + 1] = 0.0f;
+              }
+            }
+          }
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) + off);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            dst[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                                pack_bf16(v[8 * i + 4], v[8 * i + 5]),
+                                pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty_bar[ab]);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+template <int SCHED, bool A_MN, bool B_MN, int EPI>
+void launch(const CUtensorMap& ma, const CUtensorMap& mb, const Args& args, cudaStream_t stream) {
+  auto kern = grouped_gemm_kernel<SCHED, A_MN, B_MN, EPI>;
+  static bool configured = false;
+  if (!configured) {
+    FM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    configured = true;
+  }
+  int grid = num_sms();
+  if (SCHED == kWgrad) grid = std::min(grid, std::max(1, args.num_groups * (args.M_w / kBM) * (args.N / kBN)));
+  kern<<<grid, kThreads, kSmemBytes, stream>>>(ma, mb, args);
+  FM_LAUNCH_CHECK("grouped_gemm_kernel");
+}
+
+}  // namespace gemm
+
+// Host entry used by the layer and by the C-ABI test hook.
+void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
+                  const void* aux, const int* seg_start, const int* seg_rows,
+                  const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
+                  cudaStream_t stream) {
+  using namespace gemm;
+  if (N % kBN != 0) throw std::invalid_argument("grouped_gemm: N must be a multiple of 256");
+  if (num_groups < 1) throw std::invalid_argument("grouped_gemm: num_groups must be >= 1");
+  if (total_rows % kBM != 0 || total_rows <= 0)
+    throw std::invalid_argument("grouped_gemm: total_rows must be a positive multiple of 128");
+  Args a{};
+  a.num_groups = num_groups;
+  a.seg_start = seg_start;
+  a.seg_rows = seg_rows;
+  a.tile_prefix = tile_prefix;
+  a.M_w = M_w;
+  a.N = N;
+  a.K = K;
+  a.out = C;
+  a.ldc = N;
+  a.bias = bias;
+  a.aux = static_cast<const __nv_bfloat16*>(aux);
+  switch (variant) {
+    case FM_GEMM_FWD_BIAS_RELU:
+    case FM_GEMM_FWD_BIAS: {
+      if (K % kBK != 0) throw std::invalid_argument("grouped_gemm: K must be a multiple of 64");
+      // A [rows, K] K-major; B = W_g [N, K] K-major, groups stacked.
+      CUtensorMap ma = make_tmap_bf16(A, K, total_rows, K, 64, kBM);
+      CUtensorMap mb = make_tmap_bf16(B, K, static_cast<uint64_t>(num_groups) * N, K, 64, kBN);
+      a.b_rows_per_group = N;
+      if (variant == FM_GEMM_FWD_BIAS_RELU)
+        launch<kRows, false, false, kEpiBiasRelu>(ma, mb, a, stream);
+      else
+        launch<kRows, false, false, kEpiBias>(ma, mb, a, stream);
+      break;
+    }
+    case FM_GEMM_DGRAD_RELU_MASK:
+    case FM_GEMM_DGRAD: {
+      if (K % kBK != 0) throw std::invalid_argument("grouped_gemm: K must be a multiple of 64");
+      // A [rows, K] K-major; B = W_g viewed [K, N] (N contiguous) -> MN-major.
+      CUtensorMap ma = make_tmap_bf16(A, K, total_rows, K, 64, kBM);
+      CUtensorMap mb = make_tmap_bf16(B, N, static_cast<uint64_t>(num_groups) * K, N, 64, kBK);
+      a.b_rows_per_group = K;
+      if (variant == FM_GEMM_DGRAD_RELU_MASK) {
+        if (!aux) throw std::invalid_argument("grouped_gemm: relu-mask dgrad needs the activation");
+        launch<kRows, false, true, kEpiReluMask>(ma, mb, a, stream);
+      } else {
+        launch<kRows, false, true, kEpiNone>(ma, mb, a, stream);
+      }
+      break;
+    }
+    case FM_GEMM_WGRAD: {
+      if (M_w % kBM != 0) throw std::invalid_argument("grouped_gemm: M_w must be a multiple of 128");
+      // A = tokens x M_w (M contiguous) -> MN-major; B = tokens x N -> MN-major.
+      CUtensorMap ma = make_tmap_bf16(A, M_w, total_rows, M_w, 64, kBK);
+      CUtensorMap mb = make_tmap_bf16(B, N, total_rows, N, 64, kBK);
+      a.b_rows_per_group = 0;
+      launch<kWgrad, true, true, kEpiF32>(ma, mb, a, stream);
+      break;
+    }
+    default:
+      throw std::invalid_argument("grouped_gemm: unknown variant");
+  }
+}
+
+}  // namespace fm
