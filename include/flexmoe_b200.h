@@ -98,6 +98,75 @@ int fm_grouped_gemm(int variant, const void* A, const void* B, void* C, const fl
                     const int32_t* tile_prefix, int num_groups, int total_rows, int M_w, int N,
                     int K, void* stream);
 
+/* ------------------------------------------------------------------------
+ * The MoE layer (one process per GPU).
+ *
+ * The reference has no layer: gate, expert FFN and combine are cost terms
+ * (compute_cost / a2a_cost, proj/src/cost_model.cpp:30-51) and token identity
+ * is not tracked. This is the executing replacement of the
+ * per-step `route(d, effective)` call in SimEngine::run_step
+ * (proj/src/sim_engine.cpp:342): the demand it routes is the device
+ * histogram of the real gate, and the flows it produces drive the real
+ * dispatch. Math: PAPER.md:206-229 (Eqs. 2-4), ReLU FFN, softmax over the
+ * top-k kept logits, ties to the lower expert id.
+ *
+ * dtypes: x / y / dy / dx and all weights bf16; biases f32; weight gradients
+ * f32 (dw1 [Nl,f,d], dw2 [Nl,d,f], db1 [Nl,f], db2 [Nl,d], dwg [N,d]).
+ * Expert weights are packed for the Nl local experts in ascending expert id
+ * (fm_layer_local_experts): w1 [Nl,f,d], w2 [Nl,d,f], b1 [Nl,f], b2 [Nl,d];
+ * the gate weight wg is [N,d]. d % 256 == 0, f % 256 == 0, N <= 256, k <= 8.
+ * ---------------------------------------------------------------------- */
+typedef struct fm_layer_config {
+  int num_experts;   /* N */
+  int top_k;         /* k */
+  int d_model;       /* d */
+  int d_ff;          /* f */
+  int num_gpus;      /* G */
+  int rank;          /* this GPU's id in [0, G) */
+  int max_tokens;    /* T capacity per call on this GPU */
+  int slots_per_gpu; /* vExpert slots E (placement validation); 0 = unchecked */
+} fm_layer_config;
+
+typedef struct fm_layer fm_layer;
+
+/* replica_counts_NG as Placement::replica_count_on (placement.hpp:80-82). */
+int fm_layer_create(const fm_layer_config* cfg, const int32_t* replica_counts_NG, fm_layer** out);
+int fm_layer_destroy(fm_layer* layer);
+/* Placement change (Expand / Shrink / Migrate applied, placement.hpp:92-104). */
+int fm_layer_set_placement(fm_layer* layer, const int32_t* replica_counts_NG);
+int fm_layer_local_experts(const fm_layer* layer, int* num_local, int32_t* experts_out);
+
+/* Single-GPU (num_gpus == 1) fused step; no host synchronisation.
+ * forward keeps what backward needs (routing, permuted activations). */
+int fm_layer_forward(fm_layer* layer, const void* x, int num_tokens, const void* wg,
+                     const void* w1, const float* b1, const void* w2, const float* b2, void* y,
+                     void* stream);
+int fm_layer_backward(fm_layer* layer, const void* dy, void* dx, float* dwg, float* dw1,
+                      float* db1, float* dw2, float* db2, void* stream);
+
+/* Introspection (synchronous device->host copy, for tests / metrics). */
+#define FM_FIELD_TOPK_IDX 0     /* int32 [T,k] */
+#define FM_FIELD_TOPK_W 1       /* f32   [T,k] */
+#define FM_FIELD_UNIT_POS 2     /* int32 [T,k] row of each unit in the dispatch buffer */
+#define FM_FIELD_GATE_GRAD 3    /* f32   [T,k] d loss / d kept logit */
+#define FM_FIELD_HIST 4         /* int64 [N]   this GPU's TokenDemand column */
+#define FM_FIELD_DEMAND 5       /* int64 [N,G] */
+#define FM_FIELD_FLOWS 6        /* int64 [N,G,G] RoutingPlan.flows */
+#define FM_FIELD_SEG_START 7    /* int32 [Nl] */
+#define FM_FIELD_SEG_REAL 8     /* int32 [Nl] */
+#define FM_FIELD_SEG_ROWS 9     /* int32 [Nl] */
+#define FM_FIELD_TOTALS 10      /* int32 [4] padded rows, units sent, units received */
+#define FM_FIELD_SEND_ROWS 11   /* int32 [G] */
+#define FM_FIELD_RECV_ROWS 12   /* int32 [G] */
+#define FM_FIELD_X_PERM 13      /* bf16 [rows,d] */
+#define FM_FIELD_ACT 14         /* bf16 [rows,f] */
+#define FM_FIELD_Y_PERM 15      /* bf16 [rows,d] */
+#define FM_FIELD_DY_PERM 16     /* bf16 [rows,d] */
+#define FM_FIELD_DH 17          /* bf16 [rows,f] */
+#define FM_FIELD_DX_PERM 18     /* bf16 [rows,d] */
+#define FM_FIELD_ROUTE_STATUS 19 /* int32 [1] device route status */
+int fm_layer_copy_out(fm_layer* layer, int field, void* host, size_t max_bytes, size_t* written);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -1,0 +1,196 @@
+"""TEST INFRASTRUCTURE ONLY — numpy restatement of the MoE-layer math.
+
+The reference has no implementation of the gate, token permutation, expert
+FFN or combine ("parity for these is unpinned by the
+reference"); this module restates them from the paper and the SPEC:
+
+* gate      g(x) = softmax(TopK(x . W_g))          PAPER.md:219-223 (Eq. 3)
+             TopK ties -> lower expert id           SPEC.md:436 convention
+             one demand unit per (token, k-slot)
+* FFN       W2 . ReLU(W1 . x + b1) + b2            PAPER.md:206-210 (Eq. 2)
+* combine   y = sum_i g(x)_i e_i(x)                 PAPER.md:225-229 (Eq. 4)
+* counts    route()                                 proj/src/router.cpp:57-169
+            (via the C oracle, itself pinned to the reference)
+* layout    canonical permutation of DESIGN.md §2.
+
+Arithmetic: float64 with the product's bf16 storage points mirrored
+(activations after ReLU, expert outputs, dY rows, dH, dX rows, y, dx are
+rounded to bf16 exactly where the device stores bf16), so remaining
+differences are f32-vs-f64 accumulation order only.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import Oracle
+
+ROW_ALIGN = 128
+
+
+def bf16(a) -> np.ndarray:
+    """Round to bfloat16 (round-to-nearest-even), returned as float64."""
+    f = np.ascontiguousarray(a, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def gate(x, wg, k):
+    """Returns (idx [T,k] int32, w [T,k] f64, logits [T,N])."""
+    logits = np.asarray(x, np.float64) @ np.asarray(wg, np.float64).T
+    order = np.argsort(-logits, axis=1, kind="stable")  # equal logits keep ascending id
+    idx = order[:, :k].astype(np.int32)
+    kept = np.take_along_axis(logits, idx, axis=1)
+    ex = np.exp(kept - kept[:, :1])
+    w = ex / ex.sum(axis=1, keepdims=True)
+    return idx, w, logits
+
+
+def histogram(idx, N):
+    return np.bincount(idx.reshape(-1), minlength=N).astype(np.int64)
+
+
+def unit_ranks(idx, N):
+    """Rank of each unit among units of the same expert, ascending token order."""
+    T, k = idx.shape
+    flat = idx.reshape(-1)
+    ranks = np.zeros(flat.shape[0], np.int64)
+    seen = np.zeros(N, np.int64)
+    for u, e in enumerate(flat):  # units are already in (token, slot) order
+        ranks[u] = seen[e]
+        seen[e] += 1
+    return ranks.reshape(T, k)
+
+
+def dispatch_rows(idx, ranks, flows, me, G, N):
+    """Row of each unit in the source's dispatch buffer (dst-major, expert-minor).
+
+    Chunk order within (me, e): me first, then ascending dst != me.
+    """
+    T, k = idx.shape
+    send_off = np.zeros((N, G), np.int64)
+    off = 0
+    for dst in range(G):
+        for e in range(N):
+            send_off[e, dst] = off
+            off += flows[e, me, dst]
+    rows = np.zeros((T, k), np.int64)
+    dsts = np.zeros((T, k), np.int64)
+    order = [me] + [g for g in range(G) if g != me]
+    for t in range(T):
+        for j in range(k):
+            e, r = idx[t, j], ranks[t, j]
+            lo = 0
+            for dst in order:
+                c = flows[e, me, dst]
+                if r < lo + c:
+                    rows[t, j] = send_off[e, dst] + r - lo
+                    dsts[t, j] = dst
+                    break
+                lo += c
+    return rows, dsts
+
+
+def segments(flows, local_experts, me):
+    """(seg_start, seg_real, seg_rows) of the padded expert segments on `me`."""
+    start, out = 0, []
+    for e in local_experts:
+        real = int(flows[e, :, me].sum())
+        rows = (real + ROW_ALIGN - 1) // ROW_ALIGN * ROW_ALIGN
+        out.append((start, real, rows))
+        start += rows
+    return out
+
+
+def single_gpu_positions(idx, N):
+    """G == 1: X_perm row of each unit and the segment table."""
+    ranks = unit_ranks(idx, N)
+    hist = histogram(idx, N)
+    flows = Oracle().route(hist.reshape(N, 1), np.ones((N, 1), np.int32))
+    segs = segments(flows, list(range(N)), 0)
+    seg_start = np.array([s[0] for s in segs], np.int64)
+    pos = seg_start[idx] + ranks
+    return pos, segs, flows, hist
+
+
+def forward(x, wg, w1, b1, w2, b2, k):
+    """Single-GPU layer forward. Weights [N,...] in expert order. Returns a state dict."""
+    x = np.asarray(x, np.float64)
+    T, d = x.shape
+    N = wg.shape[0]
+    idx, w, logits = gate(x, wg, k)
+    pos, segs, flows, hist = single_gpu_positions(idx, N)
+    rows = sum(s[2] for s in segs)
+    f = w1.shape[1]
+    x_perm = np.zeros((rows, d))
+    for j in range(k):
+        x_perm[pos[:, j]] = x
+    act = np.zeros((rows, f))
+    y_perm = np.zeros((rows, d))
+    for e, (s0, real, r) in enumerate(segs):
+        if r == 0:
+            continue
+        seg = slice(s0, s0 + r)
+        act[seg] = bf16(np.maximum(x_perm[seg] @ np.asarray(w1[e], np.float64).T + b1[e], 0.0))
+        y_perm[seg] = bf16(act[seg] @ np.asarray(w2[e], np.float64).T + b2[e])
+    y = bf16(np.einsum("tk,tkd->td", w.astype(np.float32).astype(np.float64), y_perm[pos]))
+    return dict(x=x, wg=np.asarray(wg, np.float64), w1=w1, w2=w2, idx=idx, w=w, logits=logits,
+                pos=pos, segs=segs, flows=flows, hist=hist, x_perm=x_perm, act=act,
+                y_perm=y_perm, y=y, k=k)
+
+
+def backward(st, dy):
+    dy = np.asarray(dy, np.float64)
+    idx, w, pos, segs = st["idx"], st["w"], st["pos"], st["segs"]
+    x_perm, act, y_perm = st["x_perm"], st["act"], st["y_perm"]
+    T, k = idx.shape
+    N, d = st["wg"].shape
+    f = act.shape[1]
+    wf = w.astype(np.float32).astype(np.float64)
+    dy_perm = np.zeros_like(y_perm)
+    for j in range(k):
+        dy_perm[pos[:, j]] = bf16(wf[:, j : j + 1] * dy)
+    dw = np.einsum("td,tkd->tk", dy, y_perm[pos])
+    dl = wf * (dw - (wf * dw).sum(axis=1, keepdims=True))
+    dh = np.zeros((x_perm.shape[0], f))
+    dx_perm = np.zeros_like(x_perm)
+    dw1 = np.zeros((N, f, d))
+    dw2 = np.zeros((N, d, f))
+    db1 = np.zeros((N, f))
+    db2 = np.zeros((N, d))
+    for e, (s0, real, r) in enumerate(segs):
+        if r == 0:
+            continue
+        seg = slice(s0, s0 + r)
+        da = dy_perm[seg] @ np.asarray(st["w2"][e], np.float64)
+        dh[seg] = bf16(da * (act[seg] > 0))
+        dx_perm[seg] = bf16(dh[seg] @ np.asarray(st["w1"][e], np.float64))
+        dw1[e] = dh[seg].T @ x_perm[seg]
+        dw2[e] = dy_perm[seg].T @ act[seg]
+        db1[e] = dh[seg].sum(axis=0)
+        db2[e] = dy_perm[seg].sum(axis=0)
+    gate_in = np.einsum("tk,tkd->td", dl, st["wg"][idx]) if k > 1 else 0.0
+    dx = bf16(dx_perm[pos].sum(axis=1) + gate_in)
+    dwg = np.zeros((N, d))
+    if k > 1:
+        np.add.at(dwg, idx.reshape(-1), dl.reshape(-1, 1) * np.repeat(st["x"], k, axis=0))
+    return dict(dx=dx, dwg=dwg, dw1=dw1, dw2=dw2, db1=db1, db2=db2, dl=dl, dy_perm=dy_perm,
+                dh=dh, dx_perm=dx_perm)
+
+
+def exact_inputs(rng, T, d, N, f, skew=None):
+    """Exact-arithmetic parity inputs: x in {j/8}, Wg in {j/64}
+    (|j| <= 8), so every logit is a multiple of 2^-9 with |logit| <= d/8 and is
+    computed exactly in f32 in any order -> top-k comparable bit for bit.
+    `skew` (log-popularity per expert) is added through a constant feature
+    column, quantised to multiples of 1/64, as in the bench's Zipf gate."""
+    x = rng.integers(-8, 9, size=(T, d)) / 8.0
+    wg = rng.integers(-8, 9, size=(N, d)) / 64.0
+    if skew is not None:
+        x[:, 0] = 1.0
+        wg[:, 0] = np.clip(np.round(np.asarray(skew) * 64) / 64, -8, 8)
+    w1 = bf16(rng.standard_normal((N, f, d)) * d**-0.5)
+    w2 = bf16(rng.standard_normal((N, d, f)) * f**-0.5)
+    b1 = (rng.standard_normal((N, f)) * 0.1).astype(np.float32).astype(np.float64)
+    b2 = (rng.standard_normal((N, d)) * 0.1).astype(np.float32).astype(np.float64)
+    return x, wg, w1, b1, w2, b2

@@ -78,6 +78,13 @@ _SIGNATURES = {
     "fm_largest_remainder_round": [_P, _I, C.c_int64, _P],
     "fm_static_ep_kept": [_P, _I, _I, C.c_double, _P, _I64P],
     "fm_grouped_gemm": [_I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P],
+    "fm_layer_create": [_P, _P, C.POINTER(_P)],
+    "fm_layer_destroy": [_P],
+    "fm_layer_set_placement": [_P, _P],
+    "fm_layer_local_experts": [_P, C.POINTER(_I), _P],
+    "fm_layer_forward": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P],
+    "fm_layer_backward": [_P] * 9,
+    "fm_layer_copy_out": [_P, _I, _P, C.c_size_t, C.POINTER(C.c_size_t)],
 }
 _RESTYPES = {"fm_last_error": C.c_char_p, "fm_version": C.c_char_p}
 

@@ -1,0 +1,507 @@
+// Token dispatch / combine for the FlexMoE layer (HBM-bound kernels).
+//
+// Canonical permutation (the reference tracks counts only,
+// SPEC.md:278, and leaves the expert-wise layout open):
+//   * a demand unit is (token t, k-slot j); units of expert e produced on
+//     source GPU s are ranked in ascending token order (a token's k experts
+//     are distinct, so the k-slot never breaks a tie);
+//   * the first flows[e][s][s] ranks stay on s, the next flows[e][s][d] go to
+//     d for d ascending (d != s) — the local-then-remote order of
+//     route(), router.cpp:86-153;
+//   * on a destination, expert segments are ascending expert id, each padded
+//     to a multiple of 128 rows with zero rows (the grouped GEMM's M/K tile);
+//     inside a segment rows are ordered by source GPU, then rank.
+// Everything here is integer-exact and deterministic; the only atomics are
+// fp32 additions into bias / gate-weight gradients.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "fm_internal.h"
+#include "layer_plan.h"
+
+namespace fm {
+namespace {
+
+constexpr int kRowAlign = 128;
+
+__device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ----------------------------------------------------------------- scan
+// Block per expert: exclusive prefix of the gate's per-tile counts, and the
+// expert's total demand on this GPU (one column of TokenDemand, int64).
+__global__ void expert_scan_kernel(const int32_t* __restrict__ tile_counts, int num_tiles, int N,
+                                   int32_t* __restrict__ tile_base, int64_t* __restrict__ hist,
+                                   int64_t* __restrict__ demand_col, int G, int src) {
+  const int e = blockIdx.x;
+  const int per = (num_tiles + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * per;
+  const int hi = min(lo + per, num_tiles);
+  int sum = 0;
+  for (int t = lo; t < hi; ++t) sum += tile_counts[static_cast<size_t>(t) * N + e];
+  // block exclusive scan of `sum`
+  __shared__ int warp_tot[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    int v = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane < nw) warp_tot[lane] = v;  // inclusive warp totals
+  }
+  __syncthreads();
+  int run = incl - sum + (wid > 0 ? warp_tot[wid - 1] : 0);
+  for (int t = lo; t < hi; ++t) {
+    tile_base[static_cast<size_t>(t) * N + e] = run;
+    run += tile_counts[static_cast<size_t>(t) * N + e];
+  }
+  if (threadIdx.x == blockDim.x - 1) {
+    hist[e] = run;
+    if (demand_col) demand_col[static_cast<size_t>(e) * G + src] = run;
+  }
+}
+
+// ----------------------------------------------------------------- plan
+// One block. Turns flows[e][src][dst] into the offsets every later kernel
+// uses (see PlanDev in layer_plan.h).
+__global__ void plan_kernel(const int64_t* __restrict__ flows, int N, int G, int me,
+                            const int32_t* __restrict__ local_expert, int Nl, PlanDev p) {
+  extern __shared__ int32_t sf[];  // flows as int32 [N][G][G]
+  const int nflow = N * G * G;
+  for (int i = threadIdx.x; i < nflow; i += blockDim.x) sf[i] = static_cast<int32_t>(flows[i]);
+  __syncthreads();
+#define FL(e, s, d) sf[((e) * G + (s)) * G + (d)]
+  // --- source side: chunk order of each expert's ranks (me first, then ascending)
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    int lo = 0;
+    for (int i = 0; i < G; ++i) {
+      const int dst = (i == 0) ? me : (i <= me ? i - 1 : i);
+      p.chunk_lo[e * G + dst] = lo;
+      p.chunk_cnt[e * G + dst] = FL(e, me, dst);
+      lo += FL(e, me, dst);
+    }
+  }
+  // --- destination side: local segments (rows padded to 128)
+  if (threadIdx.x == 0) {
+    int start = 0, mt = 0;
+    for (int li = 0; li < Nl; ++li) {
+      const int e = local_expert[li];
+      int real = 0;
+      for (int s = 0; s < G; ++s) real += FL(e, s, me);
+      const int rows = (real + kRowAlign - 1) / kRowAlign * kRowAlign;
+      p.seg_start[li] = start;
+      p.seg_real[li] = real;
+      p.seg_rows[li] = rows;
+      p.mtile_prefix[li] = mt;
+      start += rows;
+      mt += rows / kRowAlign;
+    }
+    p.mtile_prefix[Nl] = mt;
+    p.totals[0] = start;  // padded rows on this GPU
+    // send side totals per destination, and send offsets (dst-major, expert-minor)
+    int off = 0;
+    for (int dst = 0; dst < G; ++dst) {
+      const int begin = off;
+      for (int e = 0; e < N; ++e) {
+        p.send_off[e * G + dst] = off;
+        off += FL(e, me, dst);
+      }
+      p.send_rows[dst] = off - begin;
+    }
+    p.totals[1] = off;  // units sent (== T * k)
+    // receive side: chunk offsets in the a2a receive buffer (src-major,
+    // local-expert-minor) and their X_perm destinations
+    int roff = 0;
+    for (int s = 0; s < G; ++s) {
+      const int base = roff;
+      for (int li = 0; li < Nl; ++li) {
+        const int e = local_expert[li];
+        int before = 0;
+        for (int s2 = 0; s2 < s; ++s2) before += FL(e, s2, me);
+        p.recv_chunk_off[s * Nl + li] = roff;
+        p.recv_chunk_dst[s * Nl + li] = p.seg_start[li] + before;
+        roff += FL(e, s, me);
+      }
+      p.recv_rows[s] = roff - base;
+    }
+    p.recv_chunk_off[G * Nl] = roff;
+    p.totals[2] = roff;  // units received
+  }
+#undef FL
+}
+
+// ----------------------------------------------------------------- dispatch
+// Warp per token: resolve each unit's row in the dispatch buffer and copy the
+// token's activations there (k copies). When `direct` (G == 1), the dispatch
+// buffer is X_perm itself and send_off is replaced by the expert's segment.
+__global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int k, int N,
+                                int G, int me, int direct, const int32_t* __restrict__ idx,
+                                const int32_t* __restrict__ tile_rank,
+                                const int32_t* __restrict__ tile_base, PlanDev p,
+                                int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const int nvec = d / 8;  // uint4 per row
+  const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * d);
+  uint4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (lane + 32 * i < nvec) v[i] = __ldg(src + lane + 32 * i);
+  const int tile = t >> 7;
+  for (int j = 0; j < k; ++j) {
+    const int u = t * k + j;
+    const int e = idx[u];
+    const int r = tile_base[static_cast<size_t>(tile) * N + e] + tile_rank[u];
+    int row;
+    if (direct) {
+      row = p.seg_start[p.local_index[e]] + r;
+    } else {
+      row = -1;
+      for (int i = 0; i < G; ++i) {
+        const int dst = (i == 0) ? me : (i <= me ? i - 1 : i);
+        const int lo = p.chunk_lo[e * G + dst];
+        if (r < lo + p.chunk_cnt[e * G + dst]) {
+          row = p.send_off[e * G + dst] + (r - lo);
+          break;
+        }
+      }
+    }
+    if (lane == 0) pos_out[u] = row;
+    uint4* dst = reinterpret_cast<uint4*>(buf + static_cast<size_t>(row) * d);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (lane + 32 * i < nvec) dst[lane + 32 * i] = v[i];
+  }
+}
+
+// Zero the padding rows of each segment: [seg_start + real, seg_start + rows).
+__global__ void zero_pad_kernel(__nv_bfloat16* __restrict__ buf, int d, PlanDev p, int Nl) {
+  const int li = blockIdx.y;
+  if (li >= Nl) return;
+  const int first = p.seg_start[li] + p.seg_real[li];
+  const int last = p.seg_start[li] + p.seg_rows[li];
+  const int nvec = d / 8;
+  const size_t begin = static_cast<size_t>(first) * nvec, end = static_cast<size_t>(last) * nvec;
+  uint4* b = reinterpret_cast<uint4*>(buf);
+  for (size_t i = begin + blockIdx.x * blockDim.x + threadIdx.x; i < end;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    b[i] = make_uint4(0, 0, 0, 0);
+}
+
+// a2a receive buffer (src-major, expert-minor) <-> X_perm segments.
+// dir = 0: recv -> perm; dir = 1: perm -> recv.
+__global__ void relayout_kernel(__nv_bfloat16* __restrict__ recv, __nv_bfloat16* __restrict__ perm,
+                                int d, int G, int Nl, PlanDev p, int dir) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int total = p.recv_chunk_off[G * Nl];
+  if (row >= total) return;
+  int lo = 0, hi = G * Nl;  // find chunk c with off[c] <= row < off[c+1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (p.recv_chunk_off[mid] <= row) lo = mid; else hi = mid;
+  }
+  const int prow = p.recv_chunk_dst[lo] + (row - p.recv_chunk_off[lo]);
+  const int nvec = d / 8;
+  uint4* a = reinterpret_cast<uint4*>(recv + static_cast<size_t>(row) * d);
+  uint4* b = reinterpret_cast<uint4*>(perm + static_cast<size_t>(prow) * d);
+  for (int i = lane; i < nvec; i += 32) {
+    if (dir == 0) b[i] = a[i]; else a[i] = b[i];
+  }
+}
+
+// ----------------------------------------------------------------- combine
+// y[t] = sum_j w[t,j] * Y[pos[t,j]]  (Eq. 4), f32 accumulation.
+__global__ void combine_fwd_kernel(const __nv_bfloat16* __restrict__ Y, const int32_t* __restrict__ pos,
+                                   const float* __restrict__ w, int T, int d, int k,
+                                   __nv_bfloat16* __restrict__ y) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const int nvec = d / 8;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[i][c] = 0.0f;
+  for (int j = 0; j < k; ++j) {
+    const int u = t * k + j;
+    const float wj = w[u];
+    const uint4* src = reinterpret_cast<const uint4*>(Y + static_cast<size_t>(pos[u]) * d);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (lane + 32 * i < nvec) {
+        const uint4 q = __ldg(src + lane + 32 * i);
+        const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[i][2 * c] += wj * bf16lo(qs[c]);
+          acc[i][2 * c + 1] += wj * bf16hi(qs[c]);
+        }
+      }
+    }
+  }
+  uint4* dst = reinterpret_cast<uint4*>(y + static_cast<size_t>(t) * d);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (lane + 32 * i < nvec)
+      dst[lane + 32 * i] = make_uint4(pack2(acc[i][0], acc[i][1]), pack2(acc[i][2], acc[i][3]),
+                                      pack2(acc[i][4], acc[i][5]), pack2(acc[i][6], acc[i][7]));
+}
+
+// Backward of the combine and of the gate softmax:
+//   dYbuf[pos] = w_j * dy[t]             (bf16)
+//   dw_j       = <dy[t], Y[pos]>
+//   dl_j       = w_j * (dw_j - sum_i w_i dw_i)   (softmax over the kept logits)
+// dl is written per unit and, when dl_rows != null, per dispatch row.
+__global__ void combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+                                   const __nv_bfloat16* __restrict__ Y,
+                                   const int32_t* __restrict__ pos, const float* __restrict__ w,
+                                   int T, int d, int k, __nv_bfloat16* __restrict__ dYbuf,
+                                   float* __restrict__ dl, float* __restrict__ dl_rows) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const int nvec = d / 8;
+  uint4 g[8];
+  const uint4* gsrc = reinterpret_cast<const uint4*>(dy + static_cast<size_t>(t) * d);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (lane + 32 * i < nvec) g[i] = __ldg(gsrc + lane + 32 * i);
+  float dw[8];
+  float wv[8];
+  for (int j = 0; j < k && j < 8; ++j) {
+    const int u = t * k + j;
+    const int row = pos[u];
+    const float wj = w[u];
+    wv[j] = wj;
+    const uint4* ysrc = reinterpret_cast<const uint4*>(Y + static_cast<size_t>(row) * d);
+    uint4* dst = reinterpret_cast<uint4*>(dYbuf + static_cast<size_t>(row) * d);
+    float dot = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (lane + 32 * i < nvec) {
+        const uint4 q = __ldg(ysrc + lane + 32 * i);
+        const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
+        const uint32_t gs[4] = {g[i].x, g[i].y, g[i].z, g[i].w};
+        uint32_t o[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          dot += bf16lo(gs[c]) * bf16lo(qs[c]) + bf16hi(gs[c]) * bf16hi(qs[c]);
+          o[c] = pack2(wj * bf16lo(gs[c]), wj * bf16hi(gs[c]));
+        }
+        dst[lane + 32 * i] = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    dw[j] = warp_sum(dot);
+  }
+  if (lane == 0) {
+    float s = 0.0f;
+    for (int j = 0; j < k && j < 8; ++j) s += wv[j] * dw[j];
+    for (int j = 0; j < k && j < 8; ++j) {
+      const float g_l = wv[j] * (dw[j] - s);
+      dl[t * k + j] = g_l;
+      if (dl_rows) dl_rows[pos[t * k + j]] = g_l;
+    }
+  }
+}
+
+// dx[t] = sum_j dXbuf[pos[t,j]] + sum_j dl[t,j] * Wg[idx[t,j], :]
+__global__ void unpermute_bwd_kernel(const __nv_bfloat16* __restrict__ dXbuf,
+                                     const int32_t* __restrict__ pos, const int32_t* __restrict__ idx,
+                                     const float* __restrict__ dl, const __nv_bfloat16* __restrict__ wg,
+                                     int T, int d, int k, int gate_grad,
+                                     __nv_bfloat16* __restrict__ dx) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const int nvec = d / 8;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[i][c] = 0.0f;
+  for (int j = 0; j < k; ++j) {
+    const int u = t * k + j;
+    const uint4* src = reinterpret_cast<const uint4*>(dXbuf + static_cast<size_t>(pos[u]) * d);
+    const float g_l = gate_grad ? dl[u] : 0.0f;
+    const uint4* wrow = reinterpret_cast<const uint4*>(wg + static_cast<size_t>(idx[u]) * d);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (lane + 32 * i < nvec) {
+        const uint4 q = __ldg(src + lane + 32 * i);
+        const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[i][2 * c] += bf16lo(qs[c]);
+          acc[i][2 * c + 1] += bf16hi(qs[c]);
+        }
+        if (gate_grad) {
+          const uint4 m = __ldg(wrow + lane + 32 * i);
+          const uint32_t ms[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            acc[i][2 * c] += g_l * bf16lo(ms[c]);
+            acc[i][2 * c + 1] += g_l * bf16hi(ms[c]);
+          }
+        }
+      }
+    }
+  }
+  uint4* dst = reinterpret_cast<uint4*>(dx + static_cast<size_t>(t) * d);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (lane + 32 * i < nvec)
+      dst[lane + 32 * i] = make_uint4(pack2(acc[i][0], acc[i][1]), pack2(acc[i][2], acc[i][3]),
+                                      pack2(acc[i][4], acc[i][5]), pack2(acc[i][6], acc[i][7]));
+}
+
+// Column sums per 128-row block of a segmented [rows, cols] bf16 buffer,
+// accumulated (f32 atomics) into out[segment][cols]; optionally row-weighted
+// (weights per row, f32), which gives the gate-weight gradient when the
+// weights are dl_rows and the buffer is the dispatched activations.
+__global__ void segment_colsum_kernel(const __nv_bfloat16* __restrict__ buf, int cols,
+                                      const float* __restrict__ row_w, PlanDev p, int Nl,
+                                      const int32_t* __restrict__ seg_out_index,
+                                      float* __restrict__ out) {
+  const int rb = blockIdx.x;  // 128-row block
+  const int total = p.totals[0];
+  const int r0 = rb * kRowAlign;
+  if (r0 >= total) return;
+  int lo = 0, hi = Nl;  // segment with seg_start <= r0 (segments are 128-aligned)
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (p.seg_start[mid] <= r0) lo = mid; else hi = mid;
+  }
+  // skip empty segments that share the same start
+  while (lo + 1 < Nl && p.seg_start[lo + 1] <= r0) ++lo;
+  const int seg_end = p.seg_start[lo] + p.seg_real[lo];
+  const int rend = min(r0 + kRowAlign, seg_end);
+  const int c2 = (blockIdx.y * blockDim.x + threadIdx.x) * 2;
+  if (c2 >= cols || r0 >= rend) return;
+  float a0 = 0.0f, a1 = 0.0f;
+  for (int r = r0; r < rend; ++r) {
+    const uint32_t v = *reinterpret_cast<const uint32_t*>(buf + static_cast<size_t>(r) * cols + c2);
+    const float s = row_w ? row_w[r] : 1.0f;
+    a0 += s * bf16lo(v);
+    a1 += s * bf16hi(v);
+  }
+  const int oi = seg_out_index ? seg_out_index[lo] : lo;
+  atomicAdd(out + static_cast<size_t>(oi) * cols + c2, a0);
+  atomicAdd(out + static_cast<size_t>(oi) * cols + c2 + 1, a1);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_t* tile_base,
+                        int64_t* hist, int64_t* demand_NG, int G, int me, cudaStream_t s) {
+  expert_scan_kernel<<<N, 256, 0, s>>>(tile_counts, num_tiles, N, tile_base, hist, demand_NG, G, me);
+  FM_LAUNCH_CHECK("expert_scan_kernel");
+}
+
+void launch_plan(const int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
+                 const PlanDev& p, cudaStream_t s) {
+  const int smem = N * G * G * 4;
+  if (smem > 200 * 1024) throw std::invalid_argument("plan: N*G*G too large");
+  static int configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    FM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = smem;
+  }
+  plan_kernel<<<1, 256, smem, s>>>(flows, N, G, me, local_expert, Nl, p);
+  FM_LAUNCH_CHECK("plan_kernel");
+}
+
+void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
+                     const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
+                     const PlanDev& p, int32_t* pos, void* buf, cudaStream_t s) {
+  if (d % 8 != 0 || d > 2048) throw std::invalid_argument("dispatch: d_model must be a multiple of 8, <= 2048");
+  if (T <= 0) return;
+  const int warps = 8;
+  dispatch_kernel<<<(T + warps - 1) / warps, warps * 32, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(x), T, d, k, N, G, me, direct ? 1 : 0, idx, tile_rank,
+      tile_base, p, pos, static_cast<__nv_bfloat16*>(buf));
+  FM_LAUNCH_CHECK("dispatch_kernel");
+}
+
+void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, cudaStream_t s) {
+  if (Nl <= 0) return;
+  dim3 grid(4, Nl);
+  zero_pad_kernel<<<grid, 256, 0, s>>>(static_cast<__nv_bfloat16*>(buf), d, p, Nl);
+  FM_LAUNCH_CHECK("zero_pad_kernel");
+}
+
+void launch_relayout(void* recv, void* perm, int d, int G, int Nl, const PlanDev& p, int max_rows,
+                     int dir, cudaStream_t s) {
+  if (max_rows <= 0) return;
+  const int warps = 8;
+  relayout_kernel<<<(max_rows + warps - 1) / warps, warps * 32, 0, s>>>(
+      static_cast<__nv_bfloat16*>(recv), static_cast<__nv_bfloat16*>(perm), d, G, Nl, p, dir);
+  FM_LAUNCH_CHECK("relayout_kernel");
+}
+
+void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T, int d, int k,
+                        void* y, cudaStream_t s) {
+  if (T <= 0) return;
+  const int warps = 8;
+  combine_fwd_kernel<<<(T + warps - 1) / warps, warps * 32, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(Y), pos, w, T, d, k, static_cast<__nv_bfloat16*>(y));
+  FM_LAUNCH_CHECK("combine_fwd_kernel");
+}
+
+void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const float* w, int T,
+                        int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s) {
+  if (T <= 0) return;
+  if (k > 8) throw std::invalid_argument("combine_bwd: top_k <= 8");
+  const int warps = 8;
+  combine_bwd_kernel<<<(T + warps - 1) / warps, warps * 32, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(Y), pos, w, T, d, k,
+      static_cast<__nv_bfloat16*>(dYbuf), dl, dl_rows);
+  FM_LAUNCH_CHECK("combine_bwd_kernel");
+}
+
+void launch_unpermute_bwd(const void* dXbuf, const int32_t* pos, const int32_t* idx, const float* dl,
+                          const void* wg, int T, int d, int k, bool gate_grad, void* dx,
+                          cudaStream_t s) {
+  if (T <= 0) return;
+  const int warps = 8;
+  unpermute_bwd_kernel<<<(T + warps - 1) / warps, warps * 32, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(dXbuf), pos, idx, dl, static_cast<const __nv_bfloat16*>(wg),
+      T, d, k, gate_grad ? 1 : 0, static_cast<__nv_bfloat16*>(dx));
+  FM_LAUNCH_CHECK("unpermute_bwd_kernel");
+}
+
+void launch_segment_colsum(const void* buf, int cols, const float* row_w, const PlanDev& p, int Nl,
+                           const int32_t* seg_out_index, float* out, int max_rows, cudaStream_t s) {
+  if (max_rows <= 0 || Nl <= 0) return;
+  dim3 grid((max_rows + kRowAlign - 1) / kRowAlign, (cols / 2 + 255) / 256);
+  segment_colsum_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(buf), cols, row_w, p,
+                                              Nl, seg_out_index, out);
+  FM_LAUNCH_CHECK("segment_colsum_kernel");
+}
+
+}  // namespace fm

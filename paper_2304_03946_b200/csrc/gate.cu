@@ -1,0 +1,266 @@
+// Fused gate: logits = x . Wg^T on tcgen05 (TMEM accumulator), then in the
+// epilogue Top-K (ties -> lower expert id), softmax over the kept logits
+// (Eq. 3: g(x) = softmax(TopK(x . W_g))), and the
+// warp-aggregated per-tile expert histogram + per-unit rank that the
+// dispatch scan turns into the token permutation.
+//
+// No reference implementation exists (the reference consumes the gate as a
+// trace); the tie rule is the reference's lower-id convention
+// (workload.hpp:88-89) and the unit of demand is one
+// (token, k-slot) pair.
+//
+// Per 128-token tile (one tcgen05 M=128 accumulator, N = experts padded to 32):
+//   warp 0: TMA x / Wg K-slices; warp 1: MMA; warp 2: TMEM alloc;
+//   warps 4-7: epilogue, thread = token row.
+// Outputs per unit u = t*k + j: topk_idx[u], topk_w[u], tile_rank[u] (rank of
+// the unit among this tile's units of the same expert, token order);
+// per tile: tile_counts[tile][e].
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "fm_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace fm {
+namespace gate {
+
+constexpr int kTM = 128;
+constexpr int kBK = 64;
+constexpr int kStages = 4;
+constexpr int kMaxExperts = 256;
+constexpr int kMaxTopK = 8;
+constexpr int kABytes = kTM * kBK * 2;
+constexpr int kThreads = 256;
+
+struct Args {
+  int T, N, Npad, K, top_k;
+  int32_t* topk_idx;
+  float* topk_w;
+  int32_t* tile_rank;
+  int32_t* tile_counts;  // [num_tiles][N]
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gate_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                const Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int b_bytes = a.Npad * kBK * 2;
+  const int stage_bytes = kABytes + b_bytes;  // multiple of 1024 since Npad % 32 == 0... (Npad*128)
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + kStages * kABytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint32_t* masks = tmem_holder + 4;  // [4 warps][Npad]
+
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = ptx::lane_id();
+  const int num_tiles = (a.T + kTM - 1) / kTM;
+  const int num_kb = a.K / kBK;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < static_cast<uint32_t>(2 * a.Npad)) tmem_cols <<= 1;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&map_x);
+    ptx::tma_prefetch_desc(&map_w);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull_bar[b], 1);
+      ptx::mbar_init(&tempty_bar[b], 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < 4 * a.Npad; i += blockDim.x) masks[i] = 0;
+  if (warp == 2) ptx::tmem_alloc(tmem_holder, tmem_cols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
+          ptx::tma_load_2d(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM);
+          ptx::tma_load_2d(smem_b + stage * b_bytes, &map_w, &full_bar[stage], kb * kBK, 0);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16_f32(kTM, a.Npad, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+        const int ab = iter & 1;
+        ptx::mbar_wait(&tempty_bar[ab], ((iter >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + ab * a.Npad;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
+          const uint32_t sb = ptx::smem_u32(smem_b + stage * b_bytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            ptx::mma_bf16_ss(d_tmem, ptx::umma_desc_sw128(sa + k * 32, 16, 1024),
+                             ptx::umma_desc_sw128(sb + k * 32, 16, 1024), idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit(&empty_bar[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit(&tfull_bar[ab]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int k = a.top_k;
+    uint32_t* my_mask = masks + q * a.Npad;
+    int iter = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+      const int ab = iter & 1;
+      const int t = tile * kTM + q * 32 + lane;
+      const bool valid = t < a.T;
+      ptx::mbar_wait(&tfull_bar[ab], (iter >> 1) & 1);
+      ptx::tc_fence_after();
+
+      float best_v[kMaxTopK];
+      int best_e[kMaxTopK];
+#pragma unroll
+      for (int j = 0; j < kMaxTopK; ++j) {
+        best_v[j] = -INFINITY;
+        best_e[j] = -1;
+      }
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + ab * a.Npad;
+      for (int c = 0; c < a.Npad; c += 32) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(t_row + c, r);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int e = c + i;
+          const float v = __uint_as_float(r[i]);
+          // Strict '>' while scanning ids upward keeps the lower id ahead on ties.
+          if (e < a.N && (best_e[k - 1] < 0 || v > best_v[k - 1])) {
+            int pos = k - 1;
+#pragma unroll
+            for (int j = kMaxTopK - 1; j > 0; --j) {
+              if (j <= pos && j < k && (best_e[j - 1] < 0 || v > best_v[j - 1])) {
+                best_v[j] = best_v[j - 1];
+                best_e[j] = best_e[j - 1];
+                pos = j - 1;
+              }
+            }
+            best_v[pos] = v;
+            best_e[pos] = e;
+          }
+        }
+      }
+      // TMEM buffer no longer needed: release it to the MMA warp early.
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty_bar[ab]);
+
+      // softmax over the kept logits (k = 1 gives weight 1)
+      float wsum = 0.0f, wexp[kMaxTopK];
+#pragma unroll
+      for (int j = 0; j < kMaxTopK; ++j) {
+        wexp[j] = (j < k) ? expf(best_v[j] - best_v[0]) : 0.0f;
+        wsum += wexp[j];
+      }
+
+      // warp-aggregated histogram: one bit per (lane, expert) in this warp's mask row
+      if (valid) {
+#pragma unroll
+        for (int j = 0; j < kMaxTopK; ++j)
+          if (j < k) atomicOr(&my_mask[best_e[j]], 1u << lane);
+      }
+      named_bar_sync(1, 128);  // all four masks of this tile are final
+      if (valid) {
+        const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int j = 0; j < kMaxTopK; ++j) {
+          if (j < k) {
+            const int e = best_e[j];
+            int rank = __popc(masks[q * a.Npad + e] & lt);
+            for (int w = 0; w < q; ++w) rank += __popc(masks[w * a.Npad + e]);
+            const size_t u = static_cast<size_t>(t) * k + j;
+            a.topk_idx[u] = e;
+            a.topk_w[u] = wexp[j] / wsum;
+            a.tile_rank[u] = rank;
+          }
+        }
+      }
+      const int et = q * 32 + lane;
+      for (int e = et; e < a.N; e += 128) {
+        a.tile_counts[static_cast<size_t>(tile) * a.N + e] =
+            __popc(masks[e]) + __popc(masks[a.Npad + e]) + __popc(masks[2 * a.Npad + e]) +
+            __popc(masks[3 * a.Npad + e]);
+      }
+      named_bar_sync(1, 128);  // everyone done reading masks
+      for (int e = lane; e < a.Npad; e += 32) my_mask[e] = 0;
+      __syncwarp();
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, tmem_cols);
+  }
+}
+
+}  // namespace gate
+
+int gate_num_tiles(int T) { return (T + gate::kTM - 1) / gate::kTM; }
+
+void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, int32_t* topk_idx,
+                 float* topk_w, int32_t* tile_rank, int32_t* tile_counts, cudaStream_t stream) {
+  using namespace gate;
+  if (N < 1 || N > kMaxExperts) throw std::invalid_argument("gate: 1 <= num_experts <= 256");
+  if (top_k < 1 || top_k > kMaxTopK || top_k > N)
+    throw std::invalid_argument("gate: 1 <= top_k <= min(8, num_experts)");
+  if (d % kBK != 0) throw std::invalid_argument("gate: d_model must be a multiple of 64");
+  if (T <= 0) return;
+  const int Npad = ((N + 31) / 32) * 32;
+  Args a{T, N, Npad, d, top_k, topk_idx, topk_w, tile_rank, tile_counts};
+  CUtensorMap mx = make_tmap_bf16(x, d, T, d, 64, kTM);
+  CUtensorMap mw = make_tmap_bf16(wg, d, N, d, 64, Npad);
+  const int stage_bytes = kABytes + Npad * kBK * 2;
+  const int smem = 1024 + kStages * stage_bytes + 128 + 16 + 4 * Npad * 4;
+  static int configured_smem = 0;
+  if (smem > configured_smem) {
+    FM_CUDA(cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured_smem = smem;
+  }
+  const int tiles = gate_num_tiles(T);
+  const int grid = std::min(tiles, num_sms());
+  gate_kernel<<<grid, kThreads, smem, stream>>>(mx, mw, a);
+  FM_LAUNCH_CHECK("gate_kernel");
+}
+
+}  // namespace fm

@@ -47,7 +47,7 @@ struct Args {
   int num_groups;
   const int* seg_start;    // [groups] first token row of the group (padded layout)
   const int* seg_rows;     // [groups] rows of the group, multiple of 128
-  const int* tile_prefix;  // [groups+1] kRows: exclusive prefix of tiles per group
+  const int* tile_prefix;  // [groups+1] kRows: exclusive prefix of 128-row M-tiles
   int M_w;                 // kWgrad: output rows per group
   int N;                   // output columns
   int K;                   // kRows: reduction depth
@@ -68,7 +68,7 @@ struct Tile {
 
 template <int SCHED>
 __device__ __forceinline__ int total_tiles(const Args& a) {
-  if (SCHED == kRows) return __ldg(a.tile_prefix + a.num_groups);
+  if (SCHED == kRows) return __ldg(a.tile_prefix + a.num_groups) * (a.N / kBN);
   return a.num_groups * (a.M_w / kBM) * (a.N / kBN);
 }
 
@@ -77,8 +77,8 @@ __device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g) {
   Tile tl;
   const int n_tiles = a.N / kBN;
   if (SCHED == kRows) {
-    while (__ldg(a.tile_prefix + g + 1) <= t) ++g;
-    const int local = t - __ldg(a.tile_prefix + g);
+    while (__ldg(a.tile_prefix + g + 1) * n_tiles <= t) ++g;
+    const int local = t - __ldg(a.tile_prefix + g) * n_tiles;
     tl.group = g;
     tl.m0 = __ldg(a.seg_start + g) + (local / n_tiles) * kBM;
     tl.n0 = (local % n_tiles) * kBN;

@@ -1,0 +1,402 @@
+// fm_layer: the FlexMoE MoE layer on one GPU (one process per GPU).
+//
+// Owns the device workspace (routing state, dispatch plan, permuted
+// activations) sized for `max_tokens`, and runs the hot path on a caller
+// stream with no host synchronisation when num_gpus == 1:
+//   forward : gate(+hist) -> scan -> route -> plan -> dispatch -> FFN1 -> FFN2 -> combine
+//   backward: combine^T(+gate softmax^T) -> dgrad1 -> dgrad2 -> wgrad2 -> wgrad1
+//             -> bias grads -> un-permute (+gate input grad) -> gate weight grad
+// With num_gpus > 1 the same kernels run as phases around the host's
+// all-to-all (see the fm_layer_* phase entry points in flexmoe_b200.h).
+//
+// Placement: replica counts [N][G] as in Placement::replica_count_on
+// (placement.hpp:80-82). The experts hosted on this rank (count > 0) are the
+// local experts, in ascending id; their weights are packed in that order.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "fm_internal.h"
+#include "layer_plan.h"
+#include "routing.cuh"
+
+namespace fm {
+
+// launchers (gate.cu, dispatch.cu, grouped_gemm.cu)
+int gate_num_tiles(int T);
+void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, int32_t* topk_idx,
+                 float* topk_w, int32_t* tile_rank, int32_t* tile_counts, cudaStream_t stream);
+void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_t* tile_base,
+                        int64_t* hist, int64_t* demand_NG, int G, int me, cudaStream_t s);
+void launch_plan(const int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
+                 const PlanDev& p, cudaStream_t s);
+void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
+                     const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
+                     const PlanDev& p, int32_t* pos, void* buf, cudaStream_t s);
+void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, cudaStream_t s);
+void launch_relayout(void* recv, void* perm, int d, int G, int Nl, const PlanDev& p, int max_rows,
+                     int dir, cudaStream_t s);
+void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T, int d, int k,
+                        void* y, cudaStream_t s);
+void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const float* w, int T,
+                        int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s);
+void launch_unpermute_bwd(const void* dXbuf, const int32_t* pos, const int32_t* idx, const float* dl,
+                          const void* wg, int T, int d, int k, bool gate_grad, void* dx,
+                          cudaStream_t s);
+void launch_segment_colsum(const void* buf, int cols, const float* row_w, const PlanDev& p, int Nl,
+                           const int32_t* seg_out_index, float* out, int max_rows, cudaStream_t s);
+void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
+                  const void* aux, const int* seg_start, const int* seg_rows,
+                  const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
+                  cudaStream_t stream);
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void reset(size_t n) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (n) {
+      FM_CUDA(cudaMalloc(&p, n));
+      bytes = n;
+    }
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+class Layer {
+ public:
+  explicit Layer(const fm_layer_config& c) : cfg_(c) {
+    if (c.num_experts < 1 || c.num_experts > 256)
+      throw std::invalid_argument("fm_layer: 1 <= num_experts <= 256");
+    if (c.top_k < 1 || c.top_k > 8 || c.top_k > c.num_experts)
+      throw std::invalid_argument("fm_layer: 1 <= top_k <= min(8, num_experts)");
+    if (c.d_model % 256 != 0 || c.d_model > 2048)
+      throw std::invalid_argument("fm_layer: d_model must be a multiple of 256 and <= 2048");
+    if (c.d_ff % 256 != 0) throw std::invalid_argument("fm_layer: d_ff must be a multiple of 256");
+    if (c.num_gpus < 1 || c.num_gpus > kMaxGpus)
+      throw std::invalid_argument("fm_layer: 1 <= num_gpus <= 64");
+    if (c.rank < 0 || c.rank >= c.num_gpus) throw std::out_of_range("fm_layer: rank out of range");
+    if (c.max_tokens < 1) throw std::invalid_argument("fm_layer: max_tokens must be >= 1");
+    const int N = c.num_experts, G = c.num_gpus, T = c.max_tokens, k = c.top_k;
+    const int tiles = gate_num_tiles(T);
+    topk_idx_.reset(sizeof(int32_t) * T * k);
+    topk_w_.reset(sizeof(float) * T * k);
+    tile_rank_.reset(sizeof(int32_t) * T * k);
+    pos_.reset(sizeof(int32_t) * T * k);
+    dl_.reset(sizeof(float) * T * k);
+    tile_counts_.reset(sizeof(int32_t) * tiles * N);
+    tile_base_.reset(sizeof(int32_t) * tiles * N);
+    hist_.reset(sizeof(int64_t) * N);
+    demand_.reset(sizeof(int64_t) * N * G);
+    flows_.reset(sizeof(int64_t) * N * G * G);
+    counts_dev_.reset(sizeof(int32_t) * N * G);
+    route_status_.reset(sizeof(int32_t));
+    counts_.assign(static_cast<size_t>(N) * G, 0);
+  }
+
+  void set_placement(const int32_t* counts_NG) {
+    const int N = cfg_.num_experts, G = cfg_.num_gpus;
+    std::vector<int32_t> c(counts_NG, counts_NG + static_cast<size_t>(N) * G);
+    std::vector<int32_t> local;
+    for (int e = 0; e < N; ++e) {
+      int total = 0;
+      for (int g = 0; g < G; ++g) {
+        if (c[static_cast<size_t>(e) * G + g] < 0)
+          throw std::invalid_argument("fm_layer: negative replica count");
+        total += c[static_cast<size_t>(e) * G + g];
+      }
+      if (total < 1)
+        throw std::invalid_argument("fm_layer: expert " + std::to_string(e) + " has no replica");
+      if (c[static_cast<size_t>(e) * G + cfg_.rank] > 0) local.push_back(e);
+    }
+    if (cfg_.slots_per_gpu > 0) {
+      for (int g = 0; g < G; ++g) {
+        int used = 0;
+        for (int e = 0; e < N; ++e) used += c[static_cast<size_t>(e) * G + g];
+        if (used > cfg_.slots_per_gpu)
+          throw std::invalid_argument("fm_layer: GPU " + std::to_string(g) +
+                                      " over its slot budget");
+      }
+    }
+    if (G == 1 && static_cast<int>(local.size()) != N)
+      throw std::logic_error("fm_layer: single GPU must host every expert");
+    counts_ = c;
+    local_ = local;
+    const int Nl = static_cast<int>(local_.size());
+    // plan arrays: one int32 allocation
+    const size_t n_plan = 3 * N * G + 2 * G + N + 3 * Nl + (Nl + 1) + (G * Nl + 1) + G * Nl + 4 +
+                          Nl /*local_expert*/;
+    plan_mem_.reset(sizeof(int32_t) * n_plan);
+    int32_t* q = plan_mem_.as<int32_t>();
+    auto take = [&](size_t n) {
+      int32_t* r = q;
+      q += n;
+      return r;
+    };
+    plan_.chunk_lo = take(N * G);
+    plan_.chunk_cnt = take(N * G);
+    plan_.send_off = take(N * G);
+    plan_.send_rows = take(G);
+    plan_.recv_rows = take(G);
+    plan_.local_index = take(N);
+    plan_.seg_start = take(Nl);
+    plan_.seg_real = take(Nl);
+    plan_.seg_rows = take(Nl);
+    plan_.mtile_prefix = take(Nl + 1);
+    plan_.recv_chunk_off = take(G * Nl + 1);
+    plan_.recv_chunk_dst = take(G * Nl);
+    plan_.totals = take(4);
+    local_expert_dev_ = take(Nl);
+    std::vector<int32_t> li(N, -1);
+    for (int i = 0; i < Nl; ++i) li[local_[i]] = i;
+    FM_CUDA(cudaMemcpy(plan_.local_index, li.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+    if (Nl)
+      FM_CUDA(cudaMemcpy(local_expert_dev_, local_.data(), sizeof(int32_t) * Nl,
+                         cudaMemcpyHostToDevice));
+    FM_CUDA(cudaMemcpy(counts_dev_.p, counts_.data(), sizeof(int32_t) * N * G,
+                       cudaMemcpyHostToDevice));
+    // Row capacity of the permuted buffers: every unit could land here
+    // (worst case of route()), plus per-segment padding.
+    const size_t units = static_cast<size_t>(cfg_.max_tokens) * cfg_.top_k * (G == 1 ? 1 : G);
+    ensure_rows(round_up(units + static_cast<size_t>(Nl) * 127, 128));
+  }
+
+  void ensure_rows(size_t rows) {
+    if (rows <= row_cap_) return;
+    const size_t d = cfg_.d_model, f = cfg_.d_ff;
+    row_cap_ = std::max<size_t>(rows, 128);
+    x_perm_.reset(2 * row_cap_ * d);
+    act_.reset(2 * row_cap_ * f);
+    y_perm_.reset(2 * row_cap_ * d);
+    dy_perm_.reset(2 * row_cap_ * d);
+    dh_.reset(2 * row_cap_ * f);
+    dx_perm_.reset(2 * row_cap_ * d);
+    dl_rows_.reset(4 * row_cap_);
+  }
+
+  // ------------------------------------------------------------ forward
+  void forward(const void* x, int T, const void* wg, const void* w1, const float* b1,
+               const void* w2, const float* b2, void* y, cudaStream_t s) {
+    if (cfg_.num_gpus != 1)
+      throw std::logic_error("fm_layer_forward: fused path is single-GPU; use the phase API");
+    check_tokens(T);
+    gate(x, T, wg, s);
+    route_and_plan(s);
+    launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), s);
+    launch_dispatch(x, T, cfg_.d_model, cfg_.top_k, cfg_.num_experts, 1, 0, true,
+                    topk_idx_.as<int32_t>(), tile_rank_.as<int32_t>(), tile_base_.as<int32_t>(),
+                    plan_, pos_.as<int32_t>(), x_perm_.p, s);
+    expert_forward(w1, b1, w2, b2, s);
+    launch_combine_fwd(y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), T, cfg_.d_model,
+                       cfg_.top_k, y, s);
+    saved_T_ = T;
+    saved_wg_ = wg;
+    saved_w1_ = w1;
+    saved_w2_ = w2;
+  }
+
+  void backward(const void* dy, void* dx, float* dwg, float* dw1, float* db1, float* dw2,
+                float* db2, cudaStream_t s) {
+    if (cfg_.num_gpus != 1)
+      throw std::logic_error("fm_layer_backward: fused path is single-GPU; use the phase API");
+    if (saved_T_ < 0) throw std::logic_error("fm_layer_backward: no forward state");
+    const int T = saved_T_, d = cfg_.d_model, k = cfg_.top_k, N = cfg_.num_experts;
+    const bool gate_grad = k > 1;
+    launch_combine_bwd(dy, y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), T, d, k, dy_perm_.p,
+                       dl_.as<float>(), gate_grad ? dl_rows_.as<float>() : nullptr, s);
+    launch_zero_pad(dy_perm_.p, d, plan_, nl(), s);
+    expert_backward(saved_w1_, saved_w2_, dw1, db1, dw2, db2, s);
+    launch_unpermute_bwd(dx_perm_.p, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(),
+                         saved_wg_, T, d, k, gate_grad, dx, s);
+    if (dwg) {
+      FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
+      if (gate_grad)
+        launch_segment_colsum(x_perm_.p, d, dl_rows_.as<float>(), plan_, nl(), local_expert_dev_,
+                              dwg, static_cast<int>(row_cap_), s);
+    }
+  }
+
+  // ------------------------------------------------------------ phases
+  void gate(const void* x, int T, const void* wg, cudaStream_t s) {
+    const int N = cfg_.num_experts, G = cfg_.num_gpus;
+    launch_gate(x, wg, T, N, cfg_.d_model, cfg_.top_k, topk_idx_.as<int32_t>(),
+                topk_w_.as<float>(), tile_rank_.as<int32_t>(), tile_counts_.as<int32_t>(), s);
+    if (G > 1) FM_CUDA(cudaMemsetAsync(demand_.p, 0, sizeof(int64_t) * N * G, s));
+    launch_expert_scan(tile_counts_.as<int32_t>(), gate_num_tiles(T), N, tile_base_.as<int32_t>(),
+                       hist_.as<int64_t>(), demand_.as<int64_t>(), G, cfg_.rank, s);
+    cur_T_ = T;
+  }
+
+  void route_and_plan(cudaStream_t s) {
+    const int N = cfg_.num_experts, G = cfg_.num_gpus;
+    route_counts_device(demand_.as<int64_t>(), counts_dev_.as<int32_t>(), N, G,
+                        flows_.as<int64_t>(), route_status_.as<int32_t>(), s);
+    launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s);
+  }
+
+  void expert_forward(const void* w1, const float* b1, const void* w2, const float* b2,
+                      cudaStream_t s) {
+    const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
+    if (Nl == 0) return;
+    const int rows = static_cast<int>(row_cap_);
+    grouped_gemm(FM_GEMM_FWD_BIAS_RELU, x_perm_.p, w1, act_.p, b1, nullptr, plan_.seg_start,
+                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s);
+    grouped_gemm(FM_GEMM_FWD_BIAS, act_.p, w2, y_perm_.p, b2, nullptr, plan_.seg_start,
+                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s);
+  }
+
+  void expert_backward(const void* w1, const void* w2, float* dw1, float* db1, float* dw2,
+                       float* db2, cudaStream_t s) {
+    const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
+    if (Nl == 0) return;
+    const int rows = static_cast<int>(row_cap_);
+    // dA = dY . W2 masked by relu'(H)  -> dH [rows, f]
+    grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p, nullptr, act_.p, plan_.seg_start,
+                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s);
+    // dX = dH . W1 -> [rows, d]
+    grouped_gemm(FM_GEMM_DGRAD, dh_.p, w1, dx_perm_.p, nullptr, nullptr, plan_.seg_start,
+                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s);
+    // dW2[li] = dY^T . act  [d, f];  dW1[li] = dH^T . X  [f, d]
+    if (dw2)
+      grouped_gemm(FM_GEMM_WGRAD, dy_perm_.p, act_.p, dw2, nullptr, nullptr, plan_.seg_start,
+                   plan_.seg_rows, nullptr, Nl, rows, d, f, 0, s);
+    if (dw1)
+      grouped_gemm(FM_GEMM_WGRAD, dh_.p, x_perm_.p, dw1, nullptr, nullptr, plan_.seg_start,
+                   plan_.seg_rows, nullptr, Nl, rows, f, d, 0, s);
+    if (db1) {
+      FM_CUDA(cudaMemsetAsync(db1, 0, sizeof(float) * Nl * f, s));
+      launch_segment_colsum(dh_.p, f, nullptr, plan_, Nl, nullptr, db1, rows, s);
+    }
+    if (db2) {
+      FM_CUDA(cudaMemsetAsync(db2, 0, sizeof(float) * Nl * d, s));
+      launch_segment_colsum(dy_perm_.p, d, nullptr, plan_, Nl, nullptr, db2, rows, s);
+    }
+  }
+
+  // ------------------------------------------------------------ introspection
+  int nl() const { return static_cast<int>(local_.size()); }
+  const std::vector<int32_t>& local() const { return local_; }
+  const fm_layer_config& cfg() const { return cfg_; }
+
+  void copy_out(int field, void* host, size_t max_bytes, size_t* written) {
+    const int T = std::max(cur_T_, 0), k = cfg_.top_k, N = cfg_.num_experts, G = cfg_.num_gpus;
+    const void* src = nullptr;
+    size_t bytes = 0;
+    switch (field) {
+      case FM_FIELD_TOPK_IDX: src = topk_idx_.p; bytes = 4ull * T * k; break;
+      case FM_FIELD_TOPK_W: src = topk_w_.p; bytes = 4ull * T * k; break;
+      case FM_FIELD_UNIT_POS: src = pos_.p; bytes = 4ull * T * k; break;
+      case FM_FIELD_GATE_GRAD: src = dl_.p; bytes = 4ull * T * k; break;
+      case FM_FIELD_HIST: src = hist_.p; bytes = 8ull * N; break;
+      case FM_FIELD_DEMAND: src = demand_.p; bytes = 8ull * N * G; break;
+      case FM_FIELD_FLOWS: src = flows_.p; bytes = 8ull * N * G * G; break;
+      case FM_FIELD_SEG_START: src = plan_.seg_start; bytes = 4ull * nl(); break;
+      case FM_FIELD_SEG_REAL: src = plan_.seg_real; bytes = 4ull * nl(); break;
+      case FM_FIELD_SEG_ROWS: src = plan_.seg_rows; bytes = 4ull * nl(); break;
+      case FM_FIELD_TOTALS: src = plan_.totals; bytes = 16; break;
+      case FM_FIELD_SEND_ROWS: src = plan_.send_rows; bytes = 4ull * G; break;
+      case FM_FIELD_RECV_ROWS: src = plan_.recv_rows; bytes = 4ull * G; break;
+      case FM_FIELD_X_PERM: src = x_perm_.p; bytes = x_perm_.bytes; break;
+      case FM_FIELD_ACT: src = act_.p; bytes = act_.bytes; break;
+      case FM_FIELD_Y_PERM: src = y_perm_.p; bytes = y_perm_.bytes; break;
+      case FM_FIELD_DY_PERM: src = dy_perm_.p; bytes = dy_perm_.bytes; break;
+      case FM_FIELD_DH: src = dh_.p; bytes = dh_.bytes; break;
+      case FM_FIELD_DX_PERM: src = dx_perm_.p; bytes = dx_perm_.bytes; break;
+      case FM_FIELD_ROUTE_STATUS: src = route_status_.p; bytes = 4; break;
+      default: throw std::invalid_argument("fm_layer_copy_out: unknown field");
+    }
+    bytes = std::min(bytes, max_bytes);
+    FM_CUDA(cudaDeviceSynchronize());
+    if (bytes) FM_CUDA(cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost));
+    if (written) *written = bytes;
+  }
+
+  size_t row_capacity() const { return row_cap_; }
+
+ private:
+  void check_tokens(int T) const {
+    if (T < 0 || T > cfg_.max_tokens)
+      throw std::invalid_argument("fm_layer: token count exceeds max_tokens");
+  }
+
+  fm_layer_config cfg_;
+  std::vector<int32_t> counts_, local_;
+  DevBuf topk_idx_, topk_w_, tile_rank_, pos_, dl_, tile_counts_, tile_base_, hist_, demand_,
+      flows_, counts_dev_, route_status_, plan_mem_;
+  DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_;
+  PlanDev plan_{};
+  int32_t* local_expert_dev_ = nullptr;
+  size_t row_cap_ = 0;
+  int cur_T_ = -1, saved_T_ = -1;
+  const void *saved_wg_ = nullptr, *saved_w1_ = nullptr, *saved_w2_ = nullptr;
+};
+
+}  // namespace fm
+
+struct fm_layer {
+  std::unique_ptr<fm::Layer> impl;
+};
+
+extern "C" {
+
+int fm_layer_create(const fm_layer_config* cfg, const int32_t* replica_counts_NG, fm_layer** out) {
+  return fm::guarded([&] {
+    if (!cfg || !replica_counts_NG || !out) throw std::invalid_argument("fm_layer_create: null argument");
+    auto h = std::make_unique<fm_layer>();
+    h->impl = std::make_unique<fm::Layer>(*cfg);
+    h->impl->set_placement(replica_counts_NG);
+    *out = h.release();
+  });
+}
+
+int fm_layer_destroy(fm_layer* h) {
+  return fm::guarded([&] { delete h; });
+}
+
+int fm_layer_set_placement(fm_layer* h, const int32_t* replica_counts_NG) {
+  return fm::guarded([&] { h->impl->set_placement(replica_counts_NG); });
+}
+
+int fm_layer_local_experts(const fm_layer* h, int* num_local, int32_t* experts) {
+  return fm::guarded([&] {
+    const auto& l = h->impl->local();
+    *num_local = static_cast<int>(l.size());
+    if (experts) std::memcpy(experts, l.data(), sizeof(int32_t) * l.size());
+  });
+}
+
+int fm_layer_forward(fm_layer* h, const void* x, int T, const void* wg, const void* w1,
+                     const float* b1, const void* w2, const float* b2, void* y, void* stream) {
+  return fm::guarded([&] {
+    h->impl->forward(x, T, wg, w1, b1, w2, b2, y, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fm_layer_backward(fm_layer* h, const void* dy, void* dx, float* dwg, float* dw1, float* db1,
+                      float* dw2, float* db2, void* stream) {
+  return fm::guarded([&] {
+    h->impl->backward(dy, dx, dwg, dw1, db1, dw2, db2, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fm_layer_copy_out(fm_layer* h, int field, void* host, size_t max_bytes, size_t* written) {
+  return fm::guarded([&] { h->impl->copy_out(field, host, max_bytes, written); });
+}
+
+}  // extern "C"

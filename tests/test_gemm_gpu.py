@@ -51,7 +51,7 @@ def test_fwd(rows, relu):
     W = (torch.randn(G, N, K, device="cuda") * K**-0.5).to(torch.bfloat16)
     b = torch.randn(G, N, device="cuda")
     C = torch.full((total, N), float("nan"), device="cuda", dtype=torch.bfloat16)
-    st, pr, tp = i32(start), i32(pad), i32(tiles(N // 256))
+    st, pr, tp = i32(start), i32(pad), i32(tiles(1))
     variant = L.FM_GEMM_FWD_BIAS_RELU if relu else L.FM_GEMM_FWD_BIAS
     L.call("fm_grouped_gemm", variant, L.ptr(A), L.ptr(W), L.ptr(C), L.ptr(b), None, L.ptr(st),
            L.ptr(pr), L.ptr(tp), G, total, 0, N, K, L.stream_ptr())
@@ -74,7 +74,7 @@ def test_dgrad(mask):
     W = (torch.randn(G, K, N, device="cuda") * K**-0.5).to(torch.bfloat16)
     aux = torch.randn(total, N, device="cuda").clamp_min(0).to(torch.bfloat16)
     C = torch.full((total, N), float("nan"), device="cuda", dtype=torch.bfloat16)
-    st, pr, tp = i32(start), i32(pad), i32(tiles(N // 256))
+    st, pr, tp = i32(start), i32(pad), i32(tiles(1))
     variant = L.FM_GEMM_DGRAD_RELU_MASK if mask else L.FM_GEMM_DGRAD
     L.call("fm_grouped_gemm", variant, L.ptr(A), L.ptr(W), L.ptr(C), None, L.ptr(aux), L.ptr(st),
            L.ptr(pr), L.ptr(tp), G, total, 0, N, K, L.stream_ptr())

@@ -1,0 +1,135 @@
+"""Single-GPU MoE layer parity: CUDA path (C-ABI) vs the CPU oracle.
+
+Bit-exact: top-k indices, per-expert histogram (TokenDemand column), routing
+flows, unit positions (the token permutation), segment table, dispatched
+rows (X_perm is a pure copy). Inputs use the exact-arithmetic gate grid
+(oracle.layer.exact_inputs) so logits are exact in any summation order.
+
+Floating point (bf16 storage, f32 accumulation vs the oracle's f64 with the
+same bf16 rounding points), tolerances stated here:
+  * gate weights w:        |d| <= 1e-6
+  * bf16 tensors (act, y_perm, y, dy_perm, dh, dx):
+        relative Frobenius error <= 1e-2 and
+        elementwise |d| <= 2^-6 |ref| + 2e-2 rms(ref) on >= 99.9% of elements
+  * f32 gradients (dw1, dw2, db1, db2, dwg): relative Frobenius error <= 1e-2
+    (the inputs to these sums are bf16 tensors that may differ by one ulp).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import layer as OL  # noqa: E402
+from paper_2304_03946_b200.layer import MoELayer  # noqa: E402
+
+
+def bf16_from_u16(a):
+    return (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def close_bf16(out, ref, name):
+    out = np.asarray(out, np.float64)
+    ref = np.asarray(ref, np.float64)
+    denom = max(np.linalg.norm(ref), 1e-30)
+    rel = np.linalg.norm(out - ref) / denom
+    rms = np.sqrt(np.mean(ref**2)) if ref.size else 0.0
+    bad = np.abs(out - ref) > (np.abs(ref) * 2**-6 + 2e-2 * rms)
+    assert rel <= 1e-2, f"{name}: rel {rel:.3e}"
+    assert bad.mean() <= 1e-3, f"{name}: {bad.sum()} of {bad.size} outside tolerance"
+
+
+def close_f32(out, ref, name, tol=1e-2):
+    rel = np.linalg.norm(np.asarray(out, np.float64) - ref) / max(np.linalg.norm(ref), 1e-30)
+    assert rel <= tol, f"{name}: rel {rel:.3e}"
+
+
+def to_dev(a, dt):
+    return torch.tensor(np.asarray(a), dtype=dt, device="cuda")
+
+
+CASES = [
+    # (N, k, d, f, T, skew)  — config 1 of BASELINE.json has N=8,k=2,d=256,f=1024,T=4096
+    (8, 2, 256, 1024, 4096, "zipf"),
+    (8, 2, 256, 512, 1000, None),
+    (16, 2, 512, 768, 777, "zipf"),
+    (64, 1, 256, 256, 3000, "zipf"),
+    (32, 4, 256, 512, 129, None),
+]
+
+
+@pytest.mark.parametrize("N,k,d,f,T,skew", CASES)
+def test_layer_forward_backward_parity(N, k, d, f, T, skew):
+    rng = np.random.default_rng(N * 1000 + T)
+    sk = None
+    if skew == "zipf":
+        p = 1.0 / np.arange(1, N + 1) ** 1.25
+        sk = np.log(p / p.sum())[rng.permutation(N)] + 3
+    x, wg, w1, b1, w2, b2 = OL.exact_inputs(rng, T, d, N, f, skew=sk)
+    st = OL.forward(x, wg, w1, b1, w2, b2, k)
+    dy = OL.bf16(rng.standard_normal((T, d)) * 0.5)
+    gr = OL.backward(st, dy)
+
+    layer = MoELayer(N, k, d, f, max_tokens=T)
+    bf = torch.bfloat16
+    X, WG, W1, W2 = to_dev(x, bf), to_dev(wg, bf), to_dev(w1, bf), to_dev(w2, bf)
+    B1, B2 = to_dev(b1, torch.float32), to_dev(b2, torch.float32)
+    y = layer.forward(X, WG, W1, B1, W2, B2)
+    grads = layer.backward(to_dev(dy, bf))
+    torch.cuda.synchronize()
+
+    # ---- bit-exact integer state
+    idx = layer.read("topk_idx", T * k).reshape(T, k)
+    assert (idx == st["idx"]).all(), "top-k indices differ"
+    assert (layer.read("hist", N) == st["hist"]).all()
+    assert (layer.read("flows", N).reshape(N, 1, 1) == st["flows"]).all()
+    assert (layer.read("unit_pos", T * k).reshape(T, k) == st["pos"]).all(), "permutation differs"
+    segs = np.array(st["segs"])
+    assert (layer.read("seg_start", N) == segs[:, 0]).all()
+    assert (layer.read("seg_real", N) == segs[:, 1]).all()
+    assert (layer.read("seg_rows", N) == segs[:, 2]).all()
+    rows = int(segs[:, 2].sum())
+    assert layer.read("totals", 4)[0] == rows
+    xp = bf16_from_u16(layer.read("x_perm", rows * d)).reshape(rows, d)
+    assert (xp == st["x_perm"]).all(), "dispatched rows differ"
+    assert layer.read("route_status", 1)[0] == 0
+
+    # ---- floating point
+    w = layer.read("topk_w", T * k).reshape(T, k)
+    assert np.abs(w - st["w"]).max() <= 1e-6
+    act = bf16_from_u16(layer.read("act", rows * f)).reshape(rows, f)
+    close_bf16(act, st["act"], "act")
+    yp = bf16_from_u16(layer.read("y_perm", rows * d)).reshape(rows, d)
+    close_bf16(yp, st["y_perm"], "y_perm")
+    close_bf16(y.float().cpu().numpy(), st["y"], "y")
+    dyp = bf16_from_u16(layer.read("dy_perm", rows * d)).reshape(rows, d)
+    close_bf16(dyp, gr["dy_perm"], "dy_perm")
+    dh = bf16_from_u16(layer.read("dh", rows * f)).reshape(rows, f)
+    close_bf16(dh, gr["dh"], "dh")
+    close_bf16(grads.dx.float().cpu().numpy(), gr["dx"], "dx")
+    close_f32(grads.dw1.cpu().numpy(), gr["dw1"], "dw1")
+    close_f32(grads.dw2.cpu().numpy(), gr["dw2"], "dw2")
+    close_f32(grads.db1.cpu().numpy(), gr["db1"], "db1")
+    close_f32(grads.db2.cpu().numpy(), gr["db2"], "db2")
+    if k > 1:
+        dl = layer.read("gate_grad", T * k).reshape(T, k)
+        close_f32(dl, gr["dl"], "gate_grad", tol=2e-2)
+        close_f32(grads.dwg.cpu().numpy(), gr["dwg"], "dwg", tol=2e-2)
+    else:
+        assert (grads.dwg.cpu().numpy() == 0).all()
+
+
+def test_layer_repeatable_and_deterministic_permutation():
+    N, k, d, f, T = 16, 2, 256, 256, 5000
+    rng = np.random.default_rng(3)
+    x, wg, w1, b1, w2, b2 = OL.exact_inputs(rng, T, d, N, f)
+    layer = MoELayer(N, k, d, f, max_tokens=T)
+    bf = torch.bfloat16
+    args = [to_dev(x, bf), to_dev(wg, bf), to_dev(w1, bf), to_dev(b1, torch.float32),
+            to_dev(w2, bf), to_dev(b2, torch.float32)]
+    y1 = layer.forward(*args).clone()
+    p1 = layer.read("unit_pos", T * k)
+    y2 = layer.forward(*args)
+    p2 = layer.read("unit_pos", T * k)
+    assert (p1 == p2).all()
+    assert torch.equal(y1, y2)
