@@ -167,6 +167,28 @@ int fm_layer_backward(fm_layer* layer, const void* dy, void* dx, float* dwg, flo
 #define FM_FIELD_ROUTE_STATUS 19 /* int32 [1] device route status */
 int fm_layer_copy_out(fm_layer* layer, int field, void* host, size_t max_bytes, size_t* written);
 
+/* Per-phase CUDA-event timing on the launching stream (off by default).
+ * fm_layer_read_timing synchronises the device and returns accumulated
+ * milliseconds and launch counts per phase since timing was enabled. */
+#define FM_PHASE_GATE 0         /* gate GEMM + top-k + softmax + tile histogram */
+#define FM_PHASE_SCAN 1         /* per-expert scan over tiles (TokenDemand column) */
+#define FM_PHASE_ROUTE 2        /* device route() + dispatch plan */
+#define FM_PHASE_DISPATCH 3     /* pad zeroing + permute/dispatch copy */
+#define FM_PHASE_FFN1_FWD 4     /* grouped GEMM relu(X W1^T + b1) */
+#define FM_PHASE_FFN2_FWD 5     /* grouped GEMM A W2^T + b2 */
+#define FM_PHASE_COMBINE_FWD 6  /* gate-weighted un-permute */
+#define FM_PHASE_COMBINE_BWD 7  /* dY rows, gate-weight grads */
+#define FM_PHASE_FFN2_DGRAD 8   /* dY W2 * relu' */
+#define FM_PHASE_FFN1_DGRAD 9   /* dH W1 */
+#define FM_PHASE_FFN2_WGRAD 10  /* dY^T A */
+#define FM_PHASE_FFN1_WGRAD 11  /* dH^T X */
+#define FM_PHASE_BIAS_GRAD 12   /* db1, db2 */
+#define FM_PHASE_UNPERMUTE 13   /* dx gather + gate input grad */
+#define FM_PHASE_GATE_WGRAD 14  /* dWg */
+#define FM_NUM_PHASES 15
+int fm_layer_set_timing(fm_layer* layer, int enable);
+int fm_layer_read_timing(fm_layer* layer, double* ms_by_phase, int* launches_by_phase);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

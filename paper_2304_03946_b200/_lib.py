@@ -85,6 +85,8 @@ _SIGNATURES = {
     "fm_layer_forward": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P],
     "fm_layer_backward": [_P] * 9,
     "fm_layer_copy_out": [_P, _I, _P, C.c_size_t, C.POINTER(C.c_size_t)],
+    "fm_layer_set_timing": [_P, _I],
+    "fm_layer_read_timing": [_P, _P, _P],
 }
 _RESTYPES = {"fm_last_error": C.c_char_p, "fm_version": C.c_char_p}
 

@@ -79,6 +79,73 @@ size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace
 
+// Optional CUDA-event timing of each phase on the launching stream (bench.py
+// reads it to compute per-kernel roofline fractions live).
+class PhaseTimer {
+ public:
+  ~PhaseTimer() {
+    for (auto& e : pool_) cudaEventDestroy(e);
+  }
+  void enable(bool on) {
+    on_ = on;
+    marks_.clear();
+    used_ = 0;
+    for (auto& v : ms_) v = 0;
+    for (auto& c : n_) c = 0;
+  }
+  bool on() const { return on_; }
+  void begin(int phase, cudaStream_t s) {
+    if (!on_) return;
+    cur_phase_ = phase;
+    cur_start_ = event();
+    FM_CUDA(cudaEventRecord(cur_start_, s));
+  }
+  void end(cudaStream_t s) {
+    if (!on_) return;
+    cudaEvent_t stop = event();
+    FM_CUDA(cudaEventRecord(stop, s));
+    marks_.push_back({cur_phase_, cur_start_, stop});
+  }
+  // Synchronises, folds recorded intervals into the totals, returns them.
+  void read(double* ms, int* counts) {
+    FM_CUDA(cudaDeviceSynchronize());
+    for (const Mark& m : marks_) {
+      float t = 0;
+      FM_CUDA(cudaEventElapsedTime(&t, m.start, m.stop));
+      ms_[m.phase] += t;
+      n_[m.phase] += 1;
+    }
+    marks_.clear();
+    used_ = 0;
+    for (int i = 0; i < FM_NUM_PHASES; ++i) {
+      ms[i] = ms_[i];
+      counts[i] = n_[i];
+    }
+  }
+
+ private:
+  struct Mark {
+    int phase;
+    cudaEvent_t start, stop;
+  };
+  cudaEvent_t event() {
+    if (used_ == pool_.size()) {
+      cudaEvent_t e;
+      FM_CUDA(cudaEventCreate(&e));
+      pool_.push_back(e);
+    }
+    return pool_[used_++];
+  }
+  bool on_ = false;
+  int cur_phase_ = 0;
+  cudaEvent_t cur_start_{};
+  std::vector<cudaEvent_t> pool_;
+  size_t used_ = 0;
+  std::vector<Mark> marks_;
+  double ms_[FM_NUM_PHASES] = {};
+  int n_[FM_NUM_PHASES] = {};
+};
+
 class Layer {
  public:
   explicit Layer(const fm_layer_config& c) : cfg_(c) {
@@ -198,13 +265,17 @@ class Layer {
     check_tokens(T);
     gate(x, T, wg, s);
     route_and_plan(s);
+    timer_.begin(FM_PHASE_DISPATCH, s);
     launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), s);
     launch_dispatch(x, T, cfg_.d_model, cfg_.top_k, cfg_.num_experts, 1, 0, true,
                     topk_idx_.as<int32_t>(), tile_rank_.as<int32_t>(), tile_base_.as<int32_t>(),
                     plan_, pos_.as<int32_t>(), x_perm_.p, s);
+    timer_.end(s);
     expert_forward(w1, b1, w2, b2, s);
+    timer_.begin(FM_PHASE_COMBINE_FWD, s);
     launch_combine_fwd(y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), T, cfg_.d_model,
                        cfg_.top_k, y, s);
+    timer_.end(s);
     saved_T_ = T;
     saved_wg_ = wg;
     saved_w1_ = w1;
@@ -218,36 +289,48 @@ class Layer {
     if (saved_T_ < 0) throw std::logic_error("fm_layer_backward: no forward state");
     const int T = saved_T_, d = cfg_.d_model, k = cfg_.top_k, N = cfg_.num_experts;
     const bool gate_grad = k > 1;
+    timer_.begin(FM_PHASE_COMBINE_BWD, s);
     launch_combine_bwd(dy, y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), T, d, k, dy_perm_.p,
                        dl_.as<float>(), gate_grad ? dl_rows_.as<float>() : nullptr, s);
     launch_zero_pad(dy_perm_.p, d, plan_, nl(), s);
+    timer_.end(s);
     expert_backward(saved_w1_, saved_w2_, dw1, db1, dw2, db2, s);
+    timer_.begin(FM_PHASE_UNPERMUTE, s);
     launch_unpermute_bwd(dx_perm_.p, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(),
                          saved_wg_, T, d, k, gate_grad, dx, s);
+    timer_.end(s);
     if (dwg) {
+      timer_.begin(FM_PHASE_GATE_WGRAD, s);
       FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
       if (gate_grad)
         launch_segment_colsum(x_perm_.p, d, dl_rows_.as<float>(), plan_, nl(), local_expert_dev_,
                               dwg, static_cast<int>(row_cap_), s);
+      timer_.end(s);
     }
   }
 
   // ------------------------------------------------------------ phases
   void gate(const void* x, int T, const void* wg, cudaStream_t s) {
     const int N = cfg_.num_experts, G = cfg_.num_gpus;
+    timer_.begin(FM_PHASE_GATE, s);
     launch_gate(x, wg, T, N, cfg_.d_model, cfg_.top_k, topk_idx_.as<int32_t>(),
                 topk_w_.as<float>(), tile_rank_.as<int32_t>(), tile_counts_.as<int32_t>(), s);
+    timer_.end(s);
+    timer_.begin(FM_PHASE_SCAN, s);
     if (G > 1) FM_CUDA(cudaMemsetAsync(demand_.p, 0, sizeof(int64_t) * N * G, s));
     launch_expert_scan(tile_counts_.as<int32_t>(), gate_num_tiles(T), N, tile_base_.as<int32_t>(),
                        hist_.as<int64_t>(), demand_.as<int64_t>(), G, cfg_.rank, s);
+    timer_.end(s);
     cur_T_ = T;
   }
 
   void route_and_plan(cudaStream_t s) {
     const int N = cfg_.num_experts, G = cfg_.num_gpus;
+    timer_.begin(FM_PHASE_ROUTE, s);
     route_counts_device(demand_.as<int64_t>(), counts_dev_.as<int32_t>(), N, G,
                         flows_.as<int64_t>(), route_status_.as<int32_t>(), s);
     launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s);
+    timer_.end(s);
   }
 
   void expert_forward(const void* w1, const float* b1, const void* w2, const float* b2,
@@ -255,10 +338,14 @@ class Layer {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0) return;
     const int rows = static_cast<int>(row_cap_);
+    timer_.begin(FM_PHASE_FFN1_FWD, s);
     grouped_gemm(FM_GEMM_FWD_BIAS_RELU, x_perm_.p, w1, act_.p, b1, nullptr, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s);
+    timer_.end(s);
+    timer_.begin(FM_PHASE_FFN2_FWD, s);
     grouped_gemm(FM_GEMM_FWD_BIAS, act_.p, w2, y_perm_.p, b2, nullptr, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s);
+    timer_.end(s);
   }
 
   void expert_backward(const void* w1, const void* w2, float* dw1, float* db1, float* dw2,
@@ -267,18 +354,29 @@ class Layer {
     if (Nl == 0) return;
     const int rows = static_cast<int>(row_cap_);
     // dA = dY . W2 masked by relu'(H)  -> dH [rows, f]
+    timer_.begin(FM_PHASE_FFN2_DGRAD, s);
     grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p, nullptr, act_.p, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s);
+    timer_.end(s);
     // dX = dH . W1 -> [rows, d]
+    timer_.begin(FM_PHASE_FFN1_DGRAD, s);
     grouped_gemm(FM_GEMM_DGRAD, dh_.p, w1, dx_perm_.p, nullptr, nullptr, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s);
+    timer_.end(s);
     // dW2[li] = dY^T . act  [d, f];  dW1[li] = dH^T . X  [f, d]
-    if (dw2)
+    if (dw2) {
+      timer_.begin(FM_PHASE_FFN2_WGRAD, s);
       grouped_gemm(FM_GEMM_WGRAD, dy_perm_.p, act_.p, dw2, nullptr, nullptr, plan_.seg_start,
                    plan_.seg_rows, nullptr, Nl, rows, d, f, 0, s);
-    if (dw1)
+      timer_.end(s);
+    }
+    if (dw1) {
+      timer_.begin(FM_PHASE_FFN1_WGRAD, s);
       grouped_gemm(FM_GEMM_WGRAD, dh_.p, x_perm_.p, dw1, nullptr, nullptr, plan_.seg_start,
                    plan_.seg_rows, nullptr, Nl, rows, f, d, 0, s);
+      timer_.end(s);
+    }
+    timer_.begin(FM_PHASE_BIAS_GRAD, s);
     if (db1) {
       FM_CUDA(cudaMemsetAsync(db1, 0, sizeof(float) * Nl * f, s));
       launch_segment_colsum(dh_.p, f, nullptr, plan_, Nl, nullptr, db1, rows, s);
@@ -287,6 +385,7 @@ class Layer {
       FM_CUDA(cudaMemsetAsync(db2, 0, sizeof(float) * Nl * d, s));
       launch_segment_colsum(dy_perm_.p, d, nullptr, plan_, Nl, nullptr, db2, rows, s);
     }
+    timer_.end(s);
   }
 
   // ------------------------------------------------------------ introspection
@@ -328,6 +427,7 @@ class Layer {
   }
 
   size_t row_capacity() const { return row_cap_; }
+  PhaseTimer& timer() { return timer_; }
 
  private:
   void check_tokens(int T) const {
@@ -341,6 +441,7 @@ class Layer {
       flows_, counts_dev_, route_status_, plan_mem_;
   DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_;
   PlanDev plan_{};
+  PhaseTimer timer_;
   int32_t* local_expert_dev_ = nullptr;
   size_t row_cap_ = 0;
   int cur_T_ = -1, saved_T_ = -1;
@@ -393,6 +494,14 @@ int fm_layer_backward(fm_layer* h, const void* dy, void* dx, float* dwg, float* 
   return fm::guarded([&] {
     h->impl->backward(dy, dx, dwg, dw1, db1, dw2, db2, static_cast<cudaStream_t>(stream));
   });
+}
+
+int fm_layer_set_timing(fm_layer* h, int enable) {
+  return fm::guarded([&] { h->impl->timer().enable(enable != 0); });
+}
+
+int fm_layer_read_timing(fm_layer* h, double* ms_by_phase, int* launches_by_phase) {
+  return fm::guarded([&] { h->impl->timer().read(ms_by_phase, launches_by_phase); });
 }
 
 int fm_layer_copy_out(fm_layer* h, int field, void* host, size_t max_bytes, size_t* written) {

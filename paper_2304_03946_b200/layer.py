@@ -30,6 +30,11 @@ FIELDS = {
 }
 
 
+PHASES = ["gate", "scan", "route", "dispatch", "ffn1_fwd", "ffn2_fwd", "combine_fwd",
+          "combine_bwd", "ffn2_dgrad", "ffn1_dgrad", "ffn2_wgrad", "ffn1_wgrad", "bias_grad",
+          "unpermute", "gate_wgrad"]  # FM_PHASE_* order
+
+
 class _Config(C.Structure):
     _fields_ = [(n, C.c_int) for n in (
         "num_experts", "top_k", "d_model", "d_ff", "num_gpus", "rank", "max_tokens", "slots_per_gpu")]
@@ -120,6 +125,17 @@ class MoELayer:
                                           grads.db1.data_ptr(), grads.dw2.data_ptr(),
                                           grads.db2.data_ptr(), L.stream_ptr(stream)))
         return grads
+
+    # ---------------------------------------------------------------- timing
+    def set_timing(self, enable: bool) -> None:
+        L.check(L.lib().fm_layer_set_timing(self._h, 1 if enable else 0))
+
+    def read_timing(self) -> dict[str, tuple[float, int]]:
+        """{phase: (total ms, launches)} since timing was enabled (synchronises)."""
+        ms = np.zeros(len(PHASES), np.float64)
+        n = np.zeros(len(PHASES), np.int32)
+        L.check(L.lib().fm_layer_read_timing(self._h, ms.ctypes.data, n.ctypes.data))
+        return {name: (float(ms[i]), int(n[i])) for i, name in enumerate(PHASES)}
 
     # ---------------------------------------------------------------- introspection
     def read(self, field: str, count: int | None = None) -> np.ndarray:
