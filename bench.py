@@ -173,9 +173,10 @@ def run_reference_arm(args, world, rank):
     import oracle
 
     cfg = dict(CFG2)
-    budget = 6.0
-    t_small, hist = cpu_layer_sample(cfg, 512)
-    tokens = max(512, int(512 * budget / max(t_small, 1e-3)) // 512 * 512)
+    # whole run bounded to ~2 minutes of host work: per-step sample sized to it
+    budget = max(0.25, 120.0 / max(1, args.steps + args.warmup))
+    t_small, hist = cpu_layer_sample(cfg, 256)
+    tokens = max(128, int(256 * budget / max(t_small, 1e-3)) // 128 * 128)
     tokens = min(tokens, 16384)
     ref = oracle.Reference() if oracle.Reference.available() else None
     times = []

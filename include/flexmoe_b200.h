@@ -87,9 +87,12 @@ int fm_static_ep_kept(const int64_t* demand_NG, int num_experts, int num_gpus,
  * seg_start, seg_rows, tile_prefix are device int32 arrays describing the
  * per-group token segments of the permuted buffers (rows multiple of 128).
  * ---------------------------------------------------------------------- */
-#define FM_GEMM_FWD_BIAS_RELU 0   /* C[rows,N] = relu(A[rows,K] W_g[N,K]^T + b_g)   bf16 */
+#define FM_GEMM_FWD_BIAS_RELU 0   /* C[rows,N] = relu(A[rows,K] W_g[N,K]^T + b_g)   bf16;
+                                     aux (optional) <- ReLU bits uint32 [rows][N/32], bit i of
+                                     word j = (pre-activation of column 32j+i > 0) */
 #define FM_GEMM_FWD_BIAS 1        /* C[rows,N] = A W_g^T + b_g                       bf16 */
-#define FM_GEMM_DGRAD_RELU_MASK 2 /* C[rows,N] = (A[rows,K] W_g[K,N]) * (aux > 0)    bf16 */
+#define FM_GEMM_DGRAD_RELU_MASK 2 /* C[rows,N] = (A[rows,K] W_g[K,N]) * bit(aux)     bf16;
+                                     aux = the ReLU bits written by FWD_BIAS_RELU */
 #define FM_GEMM_DGRAD 3           /* C[rows,N] = A[rows,K] W_g[K,N]                  bf16 */
 #define FM_GEMM_WGRAD 4           /* C[g][M_w,N] = A[seg_g, M_w]^T B[seg_g, N]       f32  */
 

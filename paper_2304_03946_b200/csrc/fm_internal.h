@@ -59,6 +59,11 @@ inline void check_cuda(cudaError_t err, const char* what) {
 CUtensorMap make_tmap_bf16(const void* base, uint64_t inner, uint64_t outer,
                            uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer);
 
+// General 2-D map (bf16 or f32 elements) with the given swizzle span (0/32/64/128 B).
+CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t outer,
+                         uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer,
+                         int swizzle_bytes);
+
 int num_sms();
 
 }  // namespace fm

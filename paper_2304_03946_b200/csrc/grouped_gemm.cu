@@ -37,7 +37,11 @@ constexpr int kBBytes = kBN * kBK * 2;
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 256;
 constexpr int kTmemCols = 512;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+// Epilogue staging: per epilogue warp two 32-row x 64-byte buffers (SWIZZLE_64B
+// TMA store boxes): 4 warps x 2 x 2 KB.
+constexpr int kStageOutBytes = 32 * 64;
+constexpr int kOutBytes = 4 * 2 * kStageOutBytes;
+constexpr int kSmemBytes = kStages * kStageBytes + kOutBytes + 1024 + 256 + 2 * kBN * 4;
 constexpr uint32_t kMnChunkBytes = kBK * 128;  // one 64-wide MN chunk of a stage (8 KB)
 
 enum Schedule { kRows = 0, kWgrad = 1 };
@@ -54,8 +58,8 @@ struct Args {
   int b_rows_per_group;    // kRows: B tensor-map rows between consecutive groups
   void* out;
   int ldc;
-  const float* bias;                // [groups][N]
-  const __nv_bfloat16* aux;         // kEpiReluMask: activation [rows][ldc]
+  const float* bias;  // [groups][N]
+  uint32_t* mask;     // ReLU bits [rows][N/32]: written by kEpiBiasRelu, read by kEpiReluMask
 };
 
 struct Tile {
@@ -105,13 +109,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 template <int SCHED, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                        const __grid_constant__ CUtensorMap map_b, const Args args) {
+                        const __grid_constant__ CUtensorMap map_b,
+                        const __grid_constant__ CUtensorMap map_c, const Args args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * kABytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint8_t* smem_out = smem + kStages * kStageBytes;  // 1024-aligned
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_out + kOutBytes);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -123,6 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&map_a);
     ptx::tma_prefetch_desc(&map_b);
+    ptx::tma_prefetch_desc(&map_c);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
@@ -224,80 +231,142 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
+    const int et = static_cast<int>(threadIdx.x) - 128;  // 0..127 among epilogue threads
+    float* bias_s = reinterpret_cast<float*>(tmem_holder + 4);  // [2][kBN]
+    constexpr bool kBias = (EPI == kEpiBiasRelu || EPI == kEpiBias);
+    const int mask_ld = args.N / 32;  // mask words per token row
+    uint8_t* warp_out = smem_out + q * 2 * kStageOutBytes;
+    uint32_t out_seq = 0;
     int g = 0;
     int iter = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
       const Tile tl = decode_tile<SCHED>(args, t, g);
       const int ab = iter & 1;
+      // Everything that does not depend on the accumulator is fetched before
+      // waiting on it: the tile's bias slice (to smem) and the ReLU mask bits.
+      float* bs = bias_s + ab * kBN;
+      if (kBias) {
+        const float* bp = args.bias + static_cast<size_t>(tl.group) * args.N + tl.n0;
+        bs[et] = __ldg(bp + et);
+        bs[et + 128] = __ldg(bp + et + 128);
+        ptx::named_bar_sync(1, 128);
+      }
+      uint32_t mbits[kBN / 32];
+      if (EPI == kEpiReluMask) {
+        const uint4* mp = reinterpret_cast<const uint4*>(
+            args.mask + static_cast<size_t>(tl.m0 + row) * mask_ld + tl.n0 / 32);
+        const uint4 m0 = __ldg(mp), m1 = __ldg(mp + 1);
+        mbits[0] = m0.x; mbits[1] = m0.y; mbits[2] = m0.z; mbits[3] = m0.w;
+        mbits[4] = m1.x; mbits[5] = m1.y; mbits[6] = m1.z; mbits[7] = m1.w;
+      }
       ptx::mbar_wait(&tfull_bar[ab], (iter >> 1) & 1);
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + ab * kBN;
       const bool empty_k = tl.num_kb == 0;
-#pragma unroll 1
-      for (int c = 0; c < kBN / 32; ++c) {
-        uint32_t r[32];
-        if (!empty_k) {
-          ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
-          ptx::tmem_ld_wait();
-        } else {
+      uint32_t ra[32], rb[32];
+      uint32_t relu_bits[kBN / 32];
+      // Output staging: this warp's 32 rows x 64 B go to a swizzled smem box
+      // (SWIZZLE_64B: 16-byte chunk j of row r sits at chunk j ^ ((r >> 1) & 3)),
+      // then one lane issues the TMA store. Two buffers per warp alternate.
+      auto stage_begin = [&]() -> uint8_t* {
+        uint8_t* buf = warp_out + (out_seq & 1) * kStageOutBytes;
+        if (lane == 0) ptx::bulk_wait_read<1>();  // the store that last used `buf` has read it
+        __syncwarp();
+        return buf;
+      };
+      auto stage_row = [&](uint8_t* buf, const uint4 (&p)[4]) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = 0;
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = p[j];
+      };
+      auto stage_commit = [&](uint8_t* buf, int x, int y) {
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_2d(&map_c, buf, x, y);
+          ptx::bulk_commit();
         }
+        ++out_seq;
+      };
+      // chunk c of 32 columns: bias / activation / mask, convert, store
+      auto process = [&](int c, uint32_t (&r)[32]) {
         const int col = tl.n0 + c * 32;
         float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        for (int i = 0; i < 32; ++i) v[i] = empty_k ? 0.0f : __uint_as_float(r[i]);
         if (EPI == kEpiF32) {
-          float* dst = reinterpret_cast<float*>(args.out) +
-                       (static_cast<size_t>(tl.group) * args.M_w + tl.m0 + row) * args.ldc + col;
+          // two 16-column halves, 64 B per row each
+          const int yrow = tl.group * args.M_w + tl.m0 + q * 32;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-          if (EPI == kEpiBiasRelu || EPI == kEpiBias) {
-            const float4* bp = reinterpret_cast<const float4*>(
-                args.bias + static_cast<size_t>(tl.group) * args.N + col);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float4 b4 = __ldg(bp + i);
-              v[4 * i] += b4.x;
-              v[4 * i + 1] += b4.y;
-              v[4 * i + 2] += b4.z;
-              v[4 * i + 3] += b4.w;
-            }
+          for (int h = 0; h < 2; ++h) {
+            uint8_t* buf = stage_begin();
+            const uint4 p[4] = {make_uint4(__float_as_uint(v[16 * h + 0]), __float_as_uint(v[16 * h + 1]),
+                                           __float_as_uint(v[16 * h + 2]), __float_as_uint(v[16 * h + 3])),
+                                make_uint4(__float_as_uint(v[16 * h + 4]), __float_as_uint(v[16 * h + 5]),
+                                           __float_as_uint(v[16 * h + 6]), __float_as_uint(v[16 * h + 7])),
+                                make_uint4(__float_as_uint(v[16 * h + 8]), __float_as_uint(v[16 * h + 9]),
+                                           __float_as_uint(v[16 * h + 10]), __float_as_uint(v[16 * h + 11])),
+                                make_uint4(__float_as_uint(v[16 * h + 12]), __float_as_uint(v[16 * h + 13]),
+                                           __float_as_uint(v[16 * h + 14]), __float_as_uint(v[16 * h + 15]))};
+            stage_row(buf, p);
+            stage_commit(buf, col + 16 * h, yrow);
           }
-          if (EPI == kEpiBiasRelu) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
-          }
-          const size_t off = static_cast<size_t>(tl.m0 + row) * args.ldc + col;
-          if (EPI == kEpiReluMask) {
-            const uint4* ap = reinterpret_cast<const uint4*>(args.aux + off);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint4 m = __ldg(ap + i);
-              const uint32_t w[4] = {m.x, m.y, m.z, m.w};
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                // bf16 pair: positive iff sign clear and magnitude non-zero.
-                const uint32_t lo = w[j] & 0xFFFFu, hi = w[j] >> 16;
-                if (!(lo != 0 && lo < 0x8000u)) v[8 * i + 2 * j] = 0.0f;
-                if (!(hi != 0 && hi < 0x8000u)) v[8 * i + 2 * j + 1] = 0.0f;
-              }
-            }
-          }
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) + off);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            dst[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                                pack_bf16(v[8 * i + 4], v[8 * i + 5]),
-                                pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-          }
+          return;
         }
+        if (kBias) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += bs[c * 32 + i];
+        }
+        if (EPI == kEpiBiasRelu) {
+          uint32_t bits = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            bits |= (v[i] > 0.0f ? 1u : 0u) << i;
+            v[i] = fmaxf(v[i], 0.0f);
+          }
+          relu_bits[c] = bits;
+        }
+        if (EPI == kEpiReluMask) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (!((mbits[c] >> i) & 1u)) v[i] = 0.0f;
+        }
+        uint4 p[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          p[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                            pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+        uint8_t* buf = stage_begin();
+        stage_row(buf, p);
+        stage_commit(buf, col, tl.m0 + q * 32);
+      };
+      // TMEM reads double-buffered: chunk c+1 is in flight while c is processed.
+      if (!empty_k) {
+        ptx::tmem_ld_32x32b_x32(t_row, ra);
+        ptx::tmem_ld_wait_regs(ra);
+      }
+#pragma unroll
+      for (int c = 0; c < kBN / 32; c += 2) {
+        if (!empty_k) ptx::tmem_ld_32x32b_x32(t_row + (c + 1) * 32, rb);
+        process(c, ra);
+        if (!empty_k) {
+          ptx::tmem_ld_wait_regs(rb);
+          if (c + 2 < kBN / 32) ptx::tmem_ld_32x32b_x32(t_row + (c + 2) * 32, ra);
+        }
+        process(c + 1, rb);
+        if (!empty_k && c + 2 < kBN / 32) ptx::tmem_ld_wait_regs(ra);
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty_bar[ab]);
+      if (EPI == kEpiBiasRelu && args.mask) {
+        uint4* mp = reinterpret_cast<uint4*>(args.mask + static_cast<size_t>(tl.m0 + row) * mask_ld +
+                                             tl.n0 / 32);
+        mp[0] = make_uint4(relu_bits[0], relu_bits[1], relu_bits[2], relu_bits[3]);
+        mp[1] = make_uint4(relu_bits[4], relu_bits[5], relu_bits[6], relu_bits[7]);
+      }
     }
+    if (lane == 0) ptx::bulk_wait<0>();  // all output stores complete before exit
+    __syncwarp();
   }
 
   ptx::tc_fence_before();
@@ -309,7 +378,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int SCHED, bool A_MN, bool B_MN, int EPI>
-void launch(const CUtensorMap& ma, const CUtensorMap& mb, const Args& args, cudaStream_t stream) {
+void launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Args& args,
+            cudaStream_t stream) {
   auto kern = grouped_gemm_kernel<SCHED, A_MN, B_MN, EPI>;
   static bool configured = false;
   if (!configured) {
@@ -318,7 +388,7 @@ void launch(const CUtensorMap& ma, const CUtensorMap& mb, const Args& args, cuda
   }
   int grid = num_sms();
   if (SCHED == kWgrad) grid = std::min(grid, std::max(1, args.num_groups * (args.M_w / kBM) * (args.N / kBN)));
-  kern<<<grid, kThreads, kSmemBytes, stream>>>(ma, mb, args);
+  kern<<<grid, kThreads, kSmemBytes, stream>>>(ma, mb, mc, args);
   FM_LAUNCH_CHECK("grouped_gemm_kernel");
 }
 
@@ -345,7 +415,7 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
   a.out = C;
   a.ldc = N;
   a.bias = bias;
-  a.aux = static_cast<const __nv_bfloat16*>(aux);
+  a.mask = static_cast<uint32_t*>(const_cast<void*>(aux));
   switch (variant) {
     case FM_GEMM_FWD_BIAS_RELU:
     case FM_GEMM_FWD_BIAS: {
@@ -353,11 +423,12 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
       // A [rows, K] K-major; B = W_g [N, K] K-major, groups stacked.
       CUtensorMap ma = make_tmap_bf16(A, K, total_rows, K, 64, kBM);
       CUtensorMap mb = make_tmap_bf16(B, K, static_cast<uint64_t>(num_groups) * N, K, 64, kBN);
+      CUtensorMap mc = make_tmap_2d(C, false, N, total_rows, N, 32, 32, 64);
       a.b_rows_per_group = N;
       if (variant == FM_GEMM_FWD_BIAS_RELU)
-        launch<kRows, false, false, kEpiBiasRelu>(ma, mb, a, stream);
+        launch<kRows, false, false, kEpiBiasRelu>(ma, mb, mc, a, stream);
       else
-        launch<kRows, false, false, kEpiBias>(ma, mb, a, stream);
+        launch<kRows, false, false, kEpiBias>(ma, mb, mc, a, stream);
       break;
     }
     case FM_GEMM_DGRAD_RELU_MASK:
@@ -366,12 +437,13 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
       // A [rows, K] K-major; B = W_g viewed [K, N] (N contiguous) -> MN-major.
       CUtensorMap ma = make_tmap_bf16(A, K, total_rows, K, 64, kBM);
       CUtensorMap mb = make_tmap_bf16(B, N, static_cast<uint64_t>(num_groups) * K, N, 64, kBK);
+      CUtensorMap mc = make_tmap_2d(C, false, N, total_rows, N, 32, 32, 64);
       a.b_rows_per_group = K;
       if (variant == FM_GEMM_DGRAD_RELU_MASK) {
-        if (!aux) throw std::invalid_argument("grouped_gemm: relu-mask dgrad needs the activation");
-        launch<kRows, false, true, kEpiReluMask>(ma, mb, a, stream);
+        if (!aux) throw std::invalid_argument("grouped_gemm: relu-mask dgrad needs the ReLU bit mask");
+        launch<kRows, false, true, kEpiReluMask>(ma, mb, mc, a, stream);
       } else {
-        launch<kRows, false, true, kEpiNone>(ma, mb, a, stream);
+        launch<kRows, false, true, kEpiNone>(ma, mb, mc, a, stream);
       }
       break;
     }
@@ -380,8 +452,9 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
       // A = tokens x M_w (M contiguous) -> MN-major; B = tokens x N -> MN-major.
       CUtensorMap ma = make_tmap_bf16(A, M_w, total_rows, M_w, 64, kBK);
       CUtensorMap mb = make_tmap_bf16(B, N, total_rows, N, 64, kBK);
+      CUtensorMap mc = make_tmap_2d(C, true, N, static_cast<uint64_t>(num_groups) * M_w, N, 16, 32, 64);
       a.b_rows_per_group = 0;
-      launch<kWgrad, true, true, kEpiF32>(ma, mb, a, stream);
+      launch<kWgrad, true, true, kEpiF32>(ma, mb, mc, a, stream);
       break;
     }
     default:

@@ -255,6 +255,7 @@ class Layer {
     dh_.reset(2 * row_cap_ * f);
     dx_perm_.reset(2 * row_cap_ * d);
     dl_rows_.reset(4 * row_cap_);
+    relu_mask_.reset(4 * row_cap_ * (f / 32));
   }
 
   // ------------------------------------------------------------ forward
@@ -339,7 +340,7 @@ class Layer {
     if (Nl == 0) return;
     const int rows = static_cast<int>(row_cap_);
     timer_.begin(FM_PHASE_FFN1_FWD, s);
-    grouped_gemm(FM_GEMM_FWD_BIAS_RELU, x_perm_.p, w1, act_.p, b1, nullptr, plan_.seg_start,
+    grouped_gemm(FM_GEMM_FWD_BIAS_RELU, x_perm_.p, w1, act_.p, b1, relu_mask_.p, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s);
     timer_.end(s);
     timer_.begin(FM_PHASE_FFN2_FWD, s);
@@ -355,7 +356,7 @@ class Layer {
     const int rows = static_cast<int>(row_cap_);
     // dA = dY . W2 masked by relu'(H)  -> dH [rows, f]
     timer_.begin(FM_PHASE_FFN2_DGRAD, s);
-    grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p, nullptr, act_.p, plan_.seg_start,
+    grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p, nullptr, relu_mask_.p, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s);
     timer_.end(s);
     // dX = dH . W1 -> [rows, d]
@@ -439,7 +440,7 @@ class Layer {
   std::vector<int32_t> counts_, local_;
   DevBuf topk_idx_, topk_w_, tile_rank_, pos_, dl_, tile_counts_, tile_base_, hist_, demand_,
       flows_, counts_dev_, route_status_, plan_mem_;
-  DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_;
+  DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_, relu_mask_;
   PlanDev plan_{};
   PhaseTimer timer_;
   int32_t* local_expert_dev_ = nullptr;

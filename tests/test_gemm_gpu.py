@@ -21,6 +21,19 @@ def _segments(rows_per_group, device):
     return pad, start, tiles
 
 
+def _unpack_bits(words, N):
+    w = words.to(torch.int64) & 0xFFFFFFFF
+    sh = torch.arange(32, device=words.device)
+    return ((w.unsqueeze(-1) >> sh) & 1).reshape(words.shape[0], N).bool()
+
+
+def _pack_bits(b):
+    rows, N = b.shape
+    sh = torch.arange(32, device=b.device)
+    w = (b.reshape(rows, N // 32, 32).to(torch.int64) << sh).sum(-1)
+    return torch.where(w >= 2**31, w - 2**32, w).to(torch.int32).contiguous()
+
+
 def _close_bf16(out, ref):
     out = out.float()
     rms = ref.pow(2).mean().sqrt().item()
@@ -51,18 +64,23 @@ def test_fwd(rows, relu):
     W = (torch.randn(G, N, K, device="cuda") * K**-0.5).to(torch.bfloat16)
     b = torch.randn(G, N, device="cuda")
     C = torch.full((total, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    mask = torch.zeros(total, N // 32, device="cuda", dtype=torch.int32)
     st, pr, tp = i32(start), i32(pad), i32(tiles(1))
     variant = L.FM_GEMM_FWD_BIAS_RELU if relu else L.FM_GEMM_FWD_BIAS
-    L.call("fm_grouped_gemm", variant, L.ptr(A), L.ptr(W), L.ptr(C), L.ptr(b), None, L.ptr(st),
-           L.ptr(pr), L.ptr(tp), G, total, 0, N, K, L.stream_ptr())
+    L.call("fm_grouped_gemm", variant, L.ptr(A), L.ptr(W), L.ptr(C), L.ptr(b),
+           L.ptr(mask) if relu else None, L.ptr(st), L.ptr(pr), L.ptr(tp), G, total, 0, N, K,
+           L.stream_ptr())
     torch.cuda.synchronize()
     for g in range(G):
         seg = slice(start[g], start[g] + pad[g])
-        ref = A[seg].float() @ W[g].float().T + b[g]
-        if relu:
-            ref = ref.clamp_min(0)
+        pre = A[seg].float() @ W[g].float().T + b[g]
+        ref = pre.clamp_min(0) if relu else pre
         if pad[g]:
             _close_bf16(C[seg], ref)
+            if relu:  # ReLU bits agree with the kernel's own output wherever it is not ~0
+                bits = _unpack_bits(mask[seg], N)
+                assert torch.equal(bits, C[seg].float() > 0) or \
+                    ((bits != (C[seg].float() > 0)) & (pre.abs() > 1e-3)).sum() == 0
 
 
 @pytest.mark.parametrize("mask", [True, False])
@@ -73,10 +91,11 @@ def test_dgrad(mask):
     G = len(rows)
     W = (torch.randn(G, K, N, device="cuda") * K**-0.5).to(torch.bfloat16)
     aux = torch.randn(total, N, device="cuda").clamp_min(0).to(torch.bfloat16)
+    bits = _pack_bits(aux.float() > 0)
     C = torch.full((total, N), float("nan"), device="cuda", dtype=torch.bfloat16)
     st, pr, tp = i32(start), i32(pad), i32(tiles(1))
     variant = L.FM_GEMM_DGRAD_RELU_MASK if mask else L.FM_GEMM_DGRAD
-    L.call("fm_grouped_gemm", variant, L.ptr(A), L.ptr(W), L.ptr(C), None, L.ptr(aux), L.ptr(st),
+    L.call("fm_grouped_gemm", variant, L.ptr(A), L.ptr(W), L.ptr(C), None, L.ptr(bits), L.ptr(st),
            L.ptr(pr), L.ptr(tp), G, total, 0, N, K, L.stream_ptr())
     torch.cuda.synchronize()
     for g in range(G):
