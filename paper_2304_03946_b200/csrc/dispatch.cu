@@ -234,42 +234,83 @@ __global__ void relayout_kernel(__nv_bfloat16* __restrict__ recv, __nv_bfloat16*
 }
 
 // ----------------------------------------------------------------- combine
+// ----------------------------------------------------------------- gathers
+// Warp per token; VPL = uint4 (8 bf16) vectors per lane = d / 256. The k unit
+// indices of the token are fetched by lanes 0..k-1 in one load and broadcast;
+// row loads are issued two units at a time so both are in flight together.
+
+__device__ __forceinline__ void unit_meta(const int32_t* __restrict__ pos, const float* __restrict__ w,
+                                          size_t base, int k, int lane, int& my_pos, float& my_w) {
+  my_pos = 0;
+  my_w = 0.0f;
+  if (lane < k) {
+    my_pos = __ldg(pos + base + lane);
+    if (w) my_w = __ldg(w + base + lane);
+  }
+}
+
+template <int VPL>
+__device__ __forceinline__ void load_row(const __nv_bfloat16* __restrict__ base, size_t row, int d,
+                                         int lane, uint4 (&q)[VPL]) {
+  const uint4* src = reinterpret_cast<const uint4*>(base + row * static_cast<size_t>(d));
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) q[i] = __ldg(src + lane + 32 * i);
+}
+
+template <int VPL>
+__device__ __forceinline__ void axpy_row(float (&acc)[VPL][8], const uint4 (&q)[VPL], float a) {
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const uint32_t qs[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      acc[i][2 * c] = fmaf(a, bf16lo(qs[c]), acc[i][2 * c]);
+      acc[i][2 * c + 1] = fmaf(a, bf16hi(qs[c]), acc[i][2 * c + 1]);
+    }
+  }
+}
+
+template <int VPL>
+__device__ __forceinline__ void store_row(__nv_bfloat16* __restrict__ base, size_t row, int d, int lane,
+                                          const float (&acc)[VPL][8]) {
+  uint4* dst = reinterpret_cast<uint4*>(base + row * static_cast<size_t>(d));
+#pragma unroll
+  for (int i = 0; i < VPL; ++i)
+    dst[lane + 32 * i] = make_uint4(pack2(acc[i][0], acc[i][1]), pack2(acc[i][2], acc[i][3]),
+                                    pack2(acc[i][4], acc[i][5]), pack2(acc[i][6], acc[i][7]));
+}
+
 // y[t] = sum_j w[t,j] * Y[pos[t,j]]  (Eq. 4), f32 accumulation.
-__global__ void combine_fwd_kernel(const __nv_bfloat16* __restrict__ Y, const int32_t* __restrict__ pos,
-                                   const float* __restrict__ w, int T, int d, int k,
-                                   __nv_bfloat16* __restrict__ y) {
+template <int VPL>
+__global__ void __launch_bounds__(256) combine_fwd_kernel(const __nv_bfloat16* __restrict__ Y,
+                                                          const int32_t* __restrict__ pos,
+                                                          const float* __restrict__ w, int T, int k,
+                                                          __nv_bfloat16* __restrict__ y) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
-  const int nvec = d / 8;
-  float acc[8][8];
+  const int d = VPL * 256;
+  int my_pos;
+  float my_w;
+  unit_meta(pos, w, static_cast<size_t>(t) * k, k, lane, my_pos, my_w);
+  float acc[VPL][8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < VPL; ++i)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[i][c] = 0.0f;
-  for (int j = 0; j < k; ++j) {
-    const int u = t * k + j;
-    const float wj = w[u];
-    const uint4* src = reinterpret_cast<const uint4*>(Y + static_cast<size_t>(pos[u]) * d);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (lane + 32 * i < nvec) {
-        const uint4 q = __ldg(src + lane + 32 * i);
-        const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          acc[i][2 * c] += wj * bf16lo(qs[c]);
-          acc[i][2 * c + 1] += wj * bf16hi(qs[c]);
-        }
-      }
-    }
+  for (int j = 0; j < k; j += 2) {
+    uint4 q0[VPL], q1[VPL];
+    const int p0 = __shfl_sync(0xffffffffu, my_pos, j);
+    const float w0 = __shfl_sync(0xffffffffu, my_w, j);
+    const bool two = j + 1 < k;
+    const int p1 = __shfl_sync(0xffffffffu, my_pos, two ? j + 1 : j);
+    const float w1 = __shfl_sync(0xffffffffu, my_w, two ? j + 1 : j);
+    load_row<VPL>(Y, p0, d, lane, q0);
+    if (two) load_row<VPL>(Y, p1, d, lane, q1);
+    axpy_row<VPL>(acc, q0, w0);
+    if (two) axpy_row<VPL>(acc, q1, w1);
   }
-  uint4* dst = reinterpret_cast<uint4*>(y + static_cast<size_t>(t) * d);
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    if (lane + 32 * i < nvec)
-      dst[lane + 32 * i] = make_uint4(pack2(acc[i][0], acc[i][1]), pack2(acc[i][2], acc[i][3]),
-                                      pack2(acc[i][4], acc[i][5]), pack2(acc[i][6], acc[i][7]));
+  store_row<VPL>(y, t, d, lane, acc);
 }
 
 // Backward of the combine and of the gate softmax:
@@ -277,106 +318,95 @@ __global__ void combine_fwd_kernel(const __nv_bfloat16* __restrict__ Y, const in
 //   dw_j       = <dy[t], Y[pos]>
 //   dl_j       = w_j * (dw_j - sum_i w_i dw_i)   (softmax over the kept logits)
 // dl is written per unit and, when dl_rows != null, per dispatch row.
-__global__ void combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
-                                   const __nv_bfloat16* __restrict__ Y,
-                                   const int32_t* __restrict__ pos, const float* __restrict__ w,
-                                   int T, int d, int k, __nv_bfloat16* __restrict__ dYbuf,
-                                   float* __restrict__ dl, float* __restrict__ dl_rows) {
+template <int VPL>
+__global__ void __launch_bounds__(256) combine_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Y,
+    const int32_t* __restrict__ pos, const float* __restrict__ w, int T, int k,
+    __nv_bfloat16* __restrict__ dYbuf, float* __restrict__ dl, float* __restrict__ dl_rows) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
-  const int nvec = d / 8;
-  uint4 g[8];
-  const uint4* gsrc = reinterpret_cast<const uint4*>(dy + static_cast<size_t>(t) * d);
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    if (lane + 32 * i < nvec) g[i] = __ldg(gsrc + lane + 32 * i);
-  float dw[8];
-  float wv[8];
-  for (int j = 0; j < k && j < 8; ++j) {
-    const int u = t * k + j;
-    const int row = pos[u];
-    const float wj = w[u];
-    wv[j] = wj;
-    const uint4* ysrc = reinterpret_cast<const uint4*>(Y + static_cast<size_t>(row) * d);
+  const int d = VPL * 256;
+  int my_pos;
+  float my_w;
+  unit_meta(pos, w, static_cast<size_t>(t) * k, k, lane, my_pos, my_w);
+  uint4 g[VPL];
+  load_row<VPL>(dy, t, d, lane, g);
+  float my_dw = 0.0f;  // lane j keeps dw_j
+  for (int j = 0; j < k; ++j) {
+    const int row = __shfl_sync(0xffffffffu, my_pos, j);
+    const float wj = __shfl_sync(0xffffffffu, my_w, j);
+    uint4 q[VPL];
+    load_row<VPL>(Y, row, d, lane, q);
     uint4* dst = reinterpret_cast<uint4*>(dYbuf + static_cast<size_t>(row) * d);
     float dot = 0.0f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (lane + 32 * i < nvec) {
-        const uint4 q = __ldg(ysrc + lane + 32 * i);
-        const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
-        const uint32_t gs[4] = {g[i].x, g[i].y, g[i].z, g[i].w};
-        uint32_t o[4];
+    for (int i = 0; i < VPL; ++i) {
+      const uint32_t qs[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+      const uint32_t gs[4] = {g[i].x, g[i].y, g[i].z, g[i].w};
+      uint32_t o[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          dot += bf16lo(gs[c]) * bf16lo(qs[c]) + bf16hi(gs[c]) * bf16hi(qs[c]);
-          o[c] = pack2(wj * bf16lo(gs[c]), wj * bf16hi(gs[c]));
-        }
-        dst[lane + 32 * i] = make_uint4(o[0], o[1], o[2], o[3]);
+      for (int c = 0; c < 4; ++c) {
+        dot = fmaf(bf16lo(gs[c]), bf16lo(qs[c]), dot);
+        dot = fmaf(bf16hi(gs[c]), bf16hi(qs[c]), dot);
+        o[c] = pack2(wj * bf16lo(gs[c]), wj * bf16hi(gs[c]));
       }
+      dst[lane + 32 * i] = make_uint4(o[0], o[1], o[2], o[3]);
     }
-    dw[j] = warp_sum(dot);
+    dot = warp_sum(dot);
+    if (lane == j) my_dw = dot;
   }
-  if (lane == 0) {
-    float s = 0.0f;
-    for (int j = 0; j < k && j < 8; ++j) s += wv[j] * dw[j];
-    for (int j = 0; j < k && j < 8; ++j) {
-      const float g_l = wv[j] * (dw[j] - s);
-      dl[t * k + j] = g_l;
-      if (dl_rows) dl_rows[pos[t * k + j]] = g_l;
-    }
+  // softmax backward on lanes 0..k-1
+  float wdw = lane < k ? my_w * my_dw : 0.0f;
+  wdw = warp_sum(wdw);
+  if (lane < k) {
+    const float g_l = my_w * (my_dw - wdw);
+    dl[static_cast<size_t>(t) * k + lane] = g_l;
+    if (dl_rows) dl_rows[my_pos] = g_l;
   }
 }
 
 // dx[t] = sum_j dXbuf[pos[t,j]] + sum_j dl[t,j] * Wg[idx[t,j], :]
-__global__ void unpermute_bwd_kernel(const __nv_bfloat16* __restrict__ dXbuf,
-                                     const int32_t* __restrict__ pos, const int32_t* __restrict__ idx,
-                                     const float* __restrict__ dl, const __nv_bfloat16* __restrict__ wg,
-                                     int T, int d, int k, int gate_grad,
-                                     __nv_bfloat16* __restrict__ dx) {
+template <int VPL>
+__global__ void __launch_bounds__(256) unpermute_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dXbuf, const int32_t* __restrict__ pos,
+    const int32_t* __restrict__ idx, const float* __restrict__ dl,
+    const __nv_bfloat16* __restrict__ wg, int T, int k, int gate_grad,
+    __nv_bfloat16* __restrict__ dx) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
-  const int nvec = d / 8;
-  float acc[8][8];
+  const int d = VPL * 256;
+  int my_pos, my_e;
+  float my_dl;
+  unit_meta(pos, gate_grad ? dl : nullptr, static_cast<size_t>(t) * k, k, lane, my_pos, my_dl);
+  unit_meta(idx, nullptr, static_cast<size_t>(t) * k, k, lane, my_e, my_dl);
+  if (gate_grad && lane < k) my_dl = __ldg(dl + static_cast<size_t>(t) * k + lane);
+  float acc[VPL][8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < VPL; ++i)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[i][c] = 0.0f;
-  for (int j = 0; j < k; ++j) {
-    const int u = t * k + j;
-    const uint4* src = reinterpret_cast<const uint4*>(dXbuf + static_cast<size_t>(pos[u]) * d);
-    const float g_l = gate_grad ? dl[u] : 0.0f;
-    const uint4* wrow = reinterpret_cast<const uint4*>(wg + static_cast<size_t>(idx[u]) * d);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (lane + 32 * i < nvec) {
-        const uint4 q = __ldg(src + lane + 32 * i);
-        const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          acc[i][2 * c] += bf16lo(qs[c]);
-          acc[i][2 * c + 1] += bf16hi(qs[c]);
-        }
-        if (gate_grad) {
-          const uint4 m = __ldg(wrow + lane + 32 * i);
-          const uint32_t ms[4] = {m.x, m.y, m.z, m.w};
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            acc[i][2 * c] += g_l * bf16lo(ms[c]);
-            acc[i][2 * c + 1] += g_l * bf16hi(ms[c]);
-          }
-        }
-      }
+  for (int j = 0; j < k; j += 2) {
+    const bool two = j + 1 < k;
+    const int p0 = __shfl_sync(0xffffffffu, my_pos, j);
+    const int p1 = __shfl_sync(0xffffffffu, my_pos, two ? j + 1 : j);
+    uint4 q0[VPL], q1[VPL];
+    load_row<VPL>(dXbuf, p0, d, lane, q0);
+    if (two) load_row<VPL>(dXbuf, p1, d, lane, q1);
+    axpy_row<VPL>(acc, q0, 1.0f);
+    if (two) axpy_row<VPL>(acc, q1, 1.0f);
+  }
+  if (gate_grad) {
+    for (int j = 0; j < k; ++j) {
+      const int e = __shfl_sync(0xffffffffu, my_e, j);
+      const float g_l = __shfl_sync(0xffffffffu, my_dl, j);
+      uint4 q[VPL];
+      load_row<VPL>(wg, e, d, lane, q);
+      axpy_row<VPL>(acc, q, g_l);
     }
   }
-  uint4* dst = reinterpret_cast<uint4*>(dx + static_cast<size_t>(t) * d);
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    if (lane + 32 * i < nvec)
-      dst[lane + 32 * i] = make_uint4(pack2(acc[i][0], acc[i][1]), pack2(acc[i][2], acc[i][3]),
-                                      pack2(acc[i][4], acc[i][5]), pack2(acc[i][6], acc[i][7]));
+  store_row<VPL>(dx, t, d, lane, acc);
 }
 
 // Column sums per 128-row block of a segmented [rows, cols] bf16 buffer,
@@ -464,23 +494,38 @@ void launch_relayout(void* recv, void* perm, int d, int G, int Nl, const PlanDev
   FM_LAUNCH_CHECK("relayout_kernel");
 }
 
+#define FM_VPL_DISPATCH(d, KERNEL_CALL)                                  \
+  switch ((d) / 256) {                                                   \
+    case 1: { constexpr int V = 1; KERNEL_CALL; break; }                 \
+    case 2: { constexpr int V = 2; KERNEL_CALL; break; }                 \
+    case 3: { constexpr int V = 3; KERNEL_CALL; break; }                 \
+    case 4: { constexpr int V = 4; KERNEL_CALL; break; }                 \
+    case 6: { constexpr int V = 6; KERNEL_CALL; break; }                 \
+    case 8: { constexpr int V = 8; KERNEL_CALL; break; }                 \
+    default: throw std::invalid_argument("d_model must be 256*{1,2,3,4,6,8}"); \
+  }
+
 void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T, int d, int k,
                         void* y, cudaStream_t s) {
   if (T <= 0) return;
+  if (d % 256 != 0) throw std::invalid_argument("combine: d_model must be a multiple of 256");
   const int warps = 8;
-  combine_fwd_kernel<<<(T + warps - 1) / warps, warps * 32, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(Y), pos, w, T, d, k, static_cast<__nv_bfloat16*>(y));
+  const int grid = (T + warps - 1) / warps;
+  FM_VPL_DISPATCH(d, (combine_fwd_kernel<V><<<grid, warps * 32, 0, s>>>(
+                         static_cast<const __nv_bfloat16*>(Y), pos, w, T, k,
+                         static_cast<__nv_bfloat16*>(y))));
   FM_LAUNCH_CHECK("combine_fwd_kernel");
 }
 
 void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const float* w, int T,
                         int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s) {
   if (T <= 0) return;
-  if (k > 8) throw std::invalid_argument("combine_bwd: top_k <= 8");
+  if (k > 32) throw std::invalid_argument("combine_bwd: top_k <= 32");
   const int warps = 8;
-  combine_bwd_kernel<<<(T + warps - 1) / warps, warps * 32, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(Y), pos, w, T, d, k,
-      static_cast<__nv_bfloat16*>(dYbuf), dl, dl_rows);
+  const int grid = (T + warps - 1) / warps;
+  FM_VPL_DISPATCH(d, (combine_bwd_kernel<V><<<grid, warps * 32, 0, s>>>(
+                         static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(Y),
+                         pos, w, T, k, static_cast<__nv_bfloat16*>(dYbuf), dl, dl_rows)));
   FM_LAUNCH_CHECK("combine_bwd_kernel");
 }
 
@@ -489,9 +534,11 @@ void launch_unpermute_bwd(const void* dXbuf, const int32_t* pos, const int32_t* 
                           cudaStream_t s) {
   if (T <= 0) return;
   const int warps = 8;
-  unpermute_bwd_kernel<<<(T + warps - 1) / warps, warps * 32, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(dXbuf), pos, idx, dl, static_cast<const __nv_bfloat16*>(wg),
-      T, d, k, gate_grad ? 1 : 0, static_cast<__nv_bfloat16*>(dx));
+  const int grid = (T + warps - 1) / warps;
+  FM_VPL_DISPATCH(d, (unpermute_bwd_kernel<V><<<grid, warps * 32, 0, s>>>(
+                         static_cast<const __nv_bfloat16*>(dXbuf), pos, idx, dl,
+                         static_cast<const __nv_bfloat16*>(wg), T, k, gate_grad ? 1 : 0,
+                         static_cast<__nv_bfloat16*>(dx))));
   FM_LAUNCH_CHECK("unpermute_bwd_kernel");
 }
 

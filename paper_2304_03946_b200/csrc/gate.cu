@@ -27,14 +27,14 @@ namespace gate {
 
 constexpr int kTM = 128;
 constexpr int kBK = 64;
-constexpr int kStages = 4;
+constexpr int kMaxStages = 8;
 constexpr int kMaxExperts = 256;
 constexpr int kMaxTopK = 8;
 constexpr int kABytes = kTM * kBK * 2;
 constexpr int kThreads = 256;
 
 struct Args {
-  int T, N, Npad, K, top_k;
+  int T, N, Npad, K, top_k, stages;
   int32_t* topk_idx;
   float* topk_w;
   int32_t* tile_rank;
@@ -54,10 +54,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int b_bytes = a.Npad * kBK * 2;
   const int stage_bytes = kABytes + b_bytes;  // multiple of 1024 since Npad % 32 == 0... (Npad*128)
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + kStages * kABytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
-  uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* tfull_bar = empty_bar + kStages;
+  uint8_t* smem_b = smem + a.stages * kABytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
+  uint64_t* empty_bar = full_bar + kMaxStages;
+  uint64_t* tfull_bar = empty_bar + kMaxStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   uint32_t* masks = tmem_holder + 4;  // [4 warps][Npad]
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&map_x);
     ptx::tma_prefetch_desc(&map_w);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < a.stages; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
     }
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
           ptx::tma_load_2d(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM);
           ptx::tma_load_2d(smem_b + stage * b_bytes, &map_w, &full_bar[stage], kb * kBK, 0);
-          if (++stage == kStages) {
+          if (++stage == a.stages) {
             stage = 0;
             phase ^= 1;
           }
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                              ptx::umma_desc_sw128(sb + k * 32, 16, 1024), idesc, (kb | k) != 0);
           }
           ptx::mma_commit(&empty_bar[stage]);
-          if (++stage == kStages) {
+          if (++stage == a.stages) {
             stage = 0;
             phase ^= 1;
           }
@@ -164,19 +164,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 32; ++i) {
           const int e = c + i;
           const float v = __uint_as_float(r[i]);
-          // Strict '>' while scanning ids upward keeps the lower id ahead on ties.
-          if (e < a.N && (best_e[k - 1] < 0 || v > best_v[k - 1])) {
-            int pos = k - 1;
+          // Sorted insertion, walking slots bottom-up: slot j takes slot j-1's
+          // entry when v beats it, else v itself when v beats slot j. Strict '>'
+          // while ids ascend keeps the lower id ahead on ties.
+          if (e < a.N) {
 #pragma unroll
-            for (int j = kMaxTopK - 1; j > 0; --j) {
-              if (j <= pos && j < k && (best_e[j - 1] < 0 || v > best_v[j - 1])) {
+            for (int j = kMaxTopK - 1; j >= 0; --j) {
+              if (j >= k) continue;
+              const bool beats_prev = j > 0 && (best_e[j - 1] < 0 || v > best_v[j - 1]);
+              const bool beats_cur = best_e[j] < 0 || v > best_v[j];
+              if (beats_prev) {
                 best_v[j] = best_v[j - 1];
                 best_e[j] = best_e[j - 1];
-                pos = j - 1;
+              } else if (beats_cur) {
+                best_v[j] = v;
+                best_e[j] = e;
               }
             }
-            best_v[pos] = v;
-            best_e[pos] = e;
           }
         }
       }
@@ -247,11 +251,13 @@ void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, 
   if (d % kBK != 0) throw std::invalid_argument("gate: d_model must be a multiple of 64");
   if (T <= 0) return;
   const int Npad = ((N + 31) / 32) * 32;
-  Args a{T, N, Npad, d, top_k, topk_idx, topk_w, tile_rank, tile_counts};
+  const int stage_bytes0 = kABytes + Npad * kBK * 2;
+  const int stages = std::max(2, std::min(kMaxStages, (200 * 1024) / stage_bytes0));
+  Args a{T, N, Npad, d, top_k, stages, topk_idx, topk_w, tile_rank, tile_counts};
   CUtensorMap mx = make_tmap_bf16(x, d, T, d, 64, kTM);
   CUtensorMap mw = make_tmap_bf16(wg, d, N, d, 64, Npad);
   const int stage_bytes = kABytes + Npad * kBK * 2;
-  const int smem = 1024 + kStages * stage_bytes + 128 + 16 + 4 * Npad * 4;
+  const int smem = 1024 + stages * stage_bytes + 2 * kMaxStages * 8 + 64 + 4 * Npad * 4;
   static int configured_smem = 0;
   if (smem > configured_smem) {
     FM_CUDA(cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
