@@ -92,7 +92,9 @@ int fm_static_ep_kept(const int64_t* demand_NG, int num_experts, int num_gpus,
                                      word j = (pre-activation of column 32j+i > 0) */
 #define FM_GEMM_FWD_BIAS 1        /* C[rows,N] = A W_g^T + b_g                       bf16 */
 #define FM_GEMM_DGRAD_RELU_MASK 2 /* C[rows,N] = (A[rows,K] W_g[K,N]) * bit(aux)     bf16;
-                                     aux = the ReLU bits written by FWD_BIAS_RELU */
+                                     aux = the ReLU bits written by FWD_BIAS_RELU; `bias`,
+                                     if non-null, receives f32 column sums of C per 128-row
+                                     tile [total_rows/128][N] (bias gradient partials) */
 #define FM_GEMM_DGRAD 3           /* C[rows,N] = A[rows,K] W_g[K,N]                  bf16 */
 #define FM_GEMM_WGRAD 4           /* C[g][M_w,N] = A[seg_g, M_w]^T B[seg_g, N]       f32  */
 

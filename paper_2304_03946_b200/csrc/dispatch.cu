@@ -444,9 +444,30 @@ __global__ void segment_colsum_kernel(const __nv_bfloat16* __restrict__ buf, int
   atomicAdd(out + static_cast<size_t>(oi) * cols + c2 + 1, a1);
 }
 
+// out[li][col] = sum over the 128-row tiles of segment li of partial[tile][col]
+// (fixed order: deterministic).
+__global__ void segment_tile_reduce_kernel(const float* __restrict__ partial, int cols, PlanDev p,
+                                           float* __restrict__ out) {
+  const int li = blockIdx.x;
+  const int col = blockIdx.y * blockDim.x + threadIdx.x;
+  if (col >= cols) return;
+  const int t0 = p.mtile_prefix[li], t1 = p.mtile_prefix[li + 1];
+  float acc = 0.0f;
+  for (int t = t0; t < t1; ++t) acc += partial[static_cast<size_t>(t) * cols + col];
+  out[static_cast<size_t>(li) * cols + col] = acc;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+void launch_segment_tile_reduce(const float* partial, int cols, const PlanDev& p, int Nl, float* out,
+                                cudaStream_t s) {
+  if (Nl <= 0) return;
+  dim3 grid(Nl, (cols + 255) / 256);
+  segment_tile_reduce_kernel<<<grid, 256, 0, s>>>(partial, cols, p, out);
+  FM_LAUNCH_CHECK("segment_tile_reduce_kernel");
+}
+
 void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_t* tile_base,
                         int64_t* hist, int64_t* demand_NG, int G, int me, cudaStream_t s) {
   expert_scan_kernel<<<N, 256, 0, s>>>(tile_counts, num_tiles, N, tile_base, hist, demand_NG, G, me);

@@ -41,7 +41,9 @@ constexpr int kTmemCols = 512;
 // TMA store boxes): 4 warps x 2 x 2 KB.
 constexpr int kStageOutBytes = 32 * 64;
 constexpr int kOutBytes = 4 * 2 * kStageOutBytes;
-constexpr int kSmemBytes = kStages * kStageBytes + kOutBytes + 1024 + 256 + 2 * kBN * 4;
+constexpr int kMaxGroups = 256;
+constexpr int kSmemBytes =
+    kStages * kStageBytes + kOutBytes + 1024 + 256 + 2 * kBN * 4 + 2 * 4 * kBN * 4 + kMaxGroups * 4;
 constexpr uint32_t kMnChunkBytes = kBK * 128;  // one 64-wide MN chunk of a stage (8 KB)
 
 enum Schedule { kRows = 0, kWgrad = 1 };
@@ -60,6 +62,7 @@ struct Args {
   int ldc;
   const float* bias;  // [groups][N]
   uint32_t* mask;     // ReLU bits [rows][N/32]: written by kEpiBiasRelu, read by kEpiReluMask
+  float* colsum;      // kEpiReluMask (optional): per-128-row-tile column sums [mtiles][N]
 };
 
 struct Tile {
@@ -68,6 +71,7 @@ struct Tile {
   int n0;
   int k_row0;  // kWgrad: first token row of the reduction
   int num_kb;
+  int mtile;   // kRows: global 128-row tile index (for per-tile column partials)
 };
 
 template <int SCHED>
@@ -76,27 +80,33 @@ __device__ __forceinline__ int total_tiles(const Args& a) {
   return a.num_groups * (a.M_w / kBM) * (a.N / kBN);
 }
 
+// kWgrad walks groups longest-reduction-first (LPT): `order` lists group ids by
+// descending token count, so the long tiles start in the first waves and the
+// tail of the persistent schedule is made of the short ones.
 template <int SCHED>
-__device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g) {
+__device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g, const int* order) {
   Tile tl;
   const int n_tiles = a.N / kBN;
   if (SCHED == kRows) {
     while (__ldg(a.tile_prefix + g + 1) * n_tiles <= t) ++g;
     const int local = t - __ldg(a.tile_prefix + g) * n_tiles;
     tl.group = g;
+    tl.mtile = __ldg(a.tile_prefix + g) + local / n_tiles;
     tl.m0 = __ldg(a.seg_start + g) + (local / n_tiles) * kBM;
     tl.n0 = (local % n_tiles) * kBN;
     tl.k_row0 = 0;
     tl.num_kb = a.K / kBK;
   } else {
     const int per_group = (a.M_w / kBM) * n_tiles;
-    g = t / per_group;
-    const int local = t - g * per_group;
+    const int slot = t / per_group;
+    const int local = t - slot * per_group;
+    g = order[slot];
     tl.group = g;
     tl.m0 = (local / n_tiles) * kBM;
     tl.n0 = (local % n_tiles) * kBN;
     tl.k_row0 = __ldg(a.seg_start + g);
     tl.num_kb = __ldg(a.seg_rows + g) / kBK;
+    tl.mtile = 0;
   }
   return tl;
 }
@@ -125,6 +135,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
+  // [tmem holder | bias 2x256 f32 | colsum 2x4x256 f32 | group order 256 i32]
+  int* order_s = reinterpret_cast<int*>(reinterpret_cast<float*>(tmem_holder + 4) + 2 * kBN + 8 * kBN);
+  if (SCHED == kWgrad) {
+    for (int i = threadIdx.x; i < args.num_groups; i += blockDim.x) {
+      const int ri = __ldg(args.seg_rows + i);
+      int rank = 0;
+      for (int j = 0; j < args.num_groups; ++j) {
+        const int rj = __ldg(args.seg_rows + j);
+        rank += (rj > ri) || (rj == ri && j < i);
+      }
+      order_s[rank] = i;
+    }
+  }
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&map_a);
@@ -155,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int g = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const Tile tl = decode_tile<SCHED>(args, t, g);
+        const Tile tl = decode_tile<SCHED>(args, t, g, order_s);
         const int b_row_base = tl.group * args.b_rows_per_group;
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -202,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int g = 0;
       int iter = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
-        const Tile tl = decode_tile<SCHED>(args, t, g);
+        const Tile tl = decode_tile<SCHED>(args, t, g, order_s);
         const int ab = iter & 1;
         ptx::mbar_wait(&tempty_bar[ab], ((iter >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
@@ -233,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;
     const int et = static_cast<int>(threadIdx.x) - 128;  // 0..127 among epilogue threads
     float* bias_s = reinterpret_cast<float*>(tmem_holder + 4);  // [2][kBN]
+    float* colsum_s = bias_s + 2 * kBN;                          // [2][4 warps][kBN]
     constexpr bool kBias = (EPI == kEpiBiasRelu || EPI == kEpiBias);
     const int mask_ld = args.N / 32;  // mask words per token row
     uint8_t* warp_out = smem_out + q * 2 * kStageOutBytes;
@@ -240,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int g = 0;
     int iter = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
-      const Tile tl = decode_tile<SCHED>(args, t, g);
+      const Tile tl = decode_tile<SCHED>(args, t, g, order_s);
       const int ab = iter & 1;
       // Everything that does not depend on the accumulator is fetched before
       // waiting on it: the tile's bias slice (to smem) and the ReLU mask bits.
@@ -330,6 +354,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (!((mbits[c] >> i) & 1u)) v[i] = 0.0f;
+          if (args.colsum) {
+            // Column sums of the stored (bf16) values over this warp's 32 rows:
+            // transposed butterfly, lane l ends with column l of the chunk.
+            float cs[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) cs[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+#pragma unroll
+            for (int sh = 16; sh >= 1; sh >>= 1) {
+              const bool up = (lane & sh) != 0;
+#pragma unroll
+              for (int i = 0; i < sh; ++i) {
+                const float send = up ? cs[i] : cs[i + sh];
+                const float keep = up ? cs[i + sh] : cs[i];
+                cs[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+              }
+            }
+            colsum_s[(ab * 4 + q) * kBN + c * 32 + lane] = cs[0];
+          }
         }
         uint4 p[4];
 #pragma unroll
@@ -358,6 +400,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty_bar[ab]);
+      if (EPI == kEpiReluMask && args.colsum) {
+        // combine the four warps in a fixed order (deterministic), one row per tile
+        ptx::named_bar_sync(2, 128);
+        const float* cs = colsum_s + ab * 4 * kBN;
+        float* dst = args.colsum + static_cast<size_t>(tl.mtile) * args.N + tl.n0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = et + h * 128;
+          dst[col] = ((cs[col] + cs[kBN + col]) + cs[2 * kBN + col]) + cs[3 * kBN + col];
+        }
+      }
       if (EPI == kEpiBiasRelu && args.mask) {
         uint4* mp = reinterpret_cast<uint4*>(args.mask + static_cast<size_t>(tl.m0 + row) * mask_ld +
                                              tl.n0 / 32);
@@ -401,7 +454,8 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
                   cudaStream_t stream) {
   using namespace gemm;
   if (N % kBN != 0) throw std::invalid_argument("grouped_gemm: N must be a multiple of 256");
-  if (num_groups < 1) throw std::invalid_argument("grouped_gemm: num_groups must be >= 1");
+  if (num_groups < 1 || num_groups > kMaxGroups)
+    throw std::invalid_argument("grouped_gemm: 1 <= num_groups <= 256");
   if (total_rows % kBM != 0 || total_rows <= 0)
     throw std::invalid_argument("grouped_gemm: total_rows must be a positive multiple of 128");
   Args a{};
@@ -441,6 +495,9 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
       a.b_rows_per_group = K;
       if (variant == FM_GEMM_DGRAD_RELU_MASK) {
         if (!aux) throw std::invalid_argument("grouped_gemm: relu-mask dgrad needs the ReLU bit mask");
+        // `bias` doubles as the optional per-tile column-sum output here
+        a.colsum = const_cast<float*>(bias);
+        a.bias = nullptr;
         launch<kRows, false, true, kEpiReluMask>(ma, mb, mc, a, stream);
       } else {
         launch<kRows, false, true, kEpiNone>(ma, mb, mc, a, stream);

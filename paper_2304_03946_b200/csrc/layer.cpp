@@ -47,6 +47,8 @@ void launch_unpermute_bwd(const void* dXbuf, const int32_t* pos, const int32_t* 
                           cudaStream_t s);
 void launch_segment_colsum(const void* buf, int cols, const float* row_w, const PlanDev& p, int Nl,
                            const int32_t* seg_out_index, float* out, int max_rows, cudaStream_t s);
+void launch_segment_tile_reduce(const float* partial, int cols, const PlanDev& p, int Nl, float* out,
+                                cudaStream_t s);
 void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
@@ -256,6 +258,7 @@ class Layer {
     dx_perm_.reset(2 * row_cap_ * d);
     dl_rows_.reset(4 * row_cap_);
     relu_mask_.reset(4 * row_cap_ * (f / 32));
+    tile_colsum_.reset(4 * (row_cap_ / 128) * f);
   }
 
   // ------------------------------------------------------------ forward
@@ -356,7 +359,8 @@ class Layer {
     const int rows = static_cast<int>(row_cap_);
     // dA = dY . W2 masked by relu'(H)  -> dH [rows, f]
     timer_.begin(FM_PHASE_FFN2_DGRAD, s);
-    grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p, nullptr, relu_mask_.p, plan_.seg_start,
+    grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p, db1 ? tile_colsum_.as<float>() : nullptr,
+                 relu_mask_.p, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s);
     timer_.end(s);
     // dX = dH . W1 -> [rows, d]
@@ -378,10 +382,7 @@ class Layer {
       timer_.end(s);
     }
     timer_.begin(FM_PHASE_BIAS_GRAD, s);
-    if (db1) {
-      FM_CUDA(cudaMemsetAsync(db1, 0, sizeof(float) * Nl * f, s));
-      launch_segment_colsum(dh_.p, f, nullptr, plan_, Nl, nullptr, db1, rows, s);
-    }
+    if (db1) launch_segment_tile_reduce(tile_colsum_.as<float>(), f, plan_, Nl, db1, s);
     if (db2) {
       FM_CUDA(cudaMemsetAsync(db2, 0, sizeof(float) * Nl * d, s));
       launch_segment_colsum(dy_perm_.p, d, nullptr, plan_, Nl, nullptr, db2, rows, s);
@@ -440,7 +441,7 @@ class Layer {
   std::vector<int32_t> counts_, local_;
   DevBuf topk_idx_, topk_w_, tile_rank_, pos_, dl_, tile_counts_, tile_base_, hist_, demand_,
       flows_, counts_dev_, route_status_, plan_mem_;
-  DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_, relu_mask_;
+  DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_, relu_mask_, tile_colsum_;
   PlanDev plan_{};
   PhaseTimer timer_;
   int32_t* local_expert_dev_ = nullptr;

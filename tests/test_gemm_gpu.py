@@ -95,9 +95,13 @@ def test_dgrad(mask):
     C = torch.full((total, N), float("nan"), device="cuda", dtype=torch.bfloat16)
     st, pr, tp = i32(start), i32(pad), i32(tiles(1))
     variant = L.FM_GEMM_DGRAD_RELU_MASK if mask else L.FM_GEMM_DGRAD
-    L.call("fm_grouped_gemm", variant, L.ptr(A), L.ptr(W), L.ptr(C), None, L.ptr(bits), L.ptr(st),
-           L.ptr(pr), L.ptr(tp), G, total, 0, N, K, L.stream_ptr())
+    colsum = torch.full((total // 128, N), float("nan"), device="cuda") if mask else None
+    L.call("fm_grouped_gemm", variant, L.ptr(A), L.ptr(W), L.ptr(C), L.ptr(colsum), L.ptr(bits),
+           L.ptr(st), L.ptr(pr), L.ptr(tp), G, total, 0, N, K, L.stream_ptr())
     torch.cuda.synchronize()
+    if mask:  # per-128-row-tile column sums of the stored bf16 output (bias-grad partials)
+        ref_cs = C.float().reshape(total // 128, 128, N).sum(1)
+        assert torch.allclose(colsum, ref_cs, rtol=1e-5, atol=1e-4)
     for g in range(G):
         seg = slice(start[g], start[g] + pad[g])
         ref = A[seg].float() @ W[g].float()
