@@ -149,6 +149,40 @@ int fm_layer_forward(fm_layer* layer, const void* x, int num_tokens, const void*
 int fm_layer_backward(fm_layer* layer, const void* dy, void* dx, float* dwg, float* dw1,
                       float* db1, float* dw2, float* db2, void* stream);
 
+/* Phase API (any num_gpus; one process per GPU). The host runs the
+ * collectives between phases:
+ *   fm_layer_gate        -> hist_out: this GPU's TokenDemand column, int64 [N] (device)
+ *   host: all-gather hist_out of every GPU -> gathered [G][N] (device)
+ *   fm_layer_route       -> route() over the full demand + dispatch plan; returns the
+ *                           per-peer row counts (host int32 [G] each). Synchronises the
+ *                           stream (the all-to-all needs the counts on the host).
+ *   fm_layer_dispatch    -> send_buf [sum(send_rows), d] bf16, peer-major (dst ascending,
+ *                           then expert ascending, then the canonical unit order)
+ *   host: all-to-all send_buf -> recv_buf (split sizes send_rows / recv_rows)
+ *   fm_layer_expert_forward  recv_buf (src-major) -> expert FFN -> ret_buf (same order)
+ *   host: all-to-all ret_buf -> back_buf (split sizes reversed)
+ *   fm_layer_combine     back_buf -> y
+ * backward mirrors it: fm_layer_combine_backward (dy -> dsend_buf),
+ * all-to-all, fm_layer_expert_backward (drecv -> weight grads, dret),
+ * all-to-all, fm_layer_unpermute_backward (dback -> dx, gate-weight grad from
+ * the still-valid send_buf). Weight gradients of replicated experts are then
+ * summed over each replica group (ascending expert id); dwg over all GPUs. */
+int fm_layer_gate(fm_layer* layer, const void* x, int num_tokens, const void* wg, int64_t* hist_out,
+                  void* stream);
+int fm_layer_route(fm_layer* layer, const int64_t* gathered_hist_GN, int32_t* send_rows,
+                   int32_t* recv_rows, void* stream);
+int fm_layer_dispatch(fm_layer* layer, const void* x, void* send_buf, void* stream);
+int fm_layer_expert_forward(fm_layer* layer, const void* recv_buf, const void* w1, const float* b1,
+                            const void* w2, const float* b2, void* ret_buf, void* stream);
+int fm_layer_combine(fm_layer* layer, const void* back_buf, void* y, void* stream);
+int fm_layer_combine_backward(fm_layer* layer, const void* dy, const void* back_buf,
+                              void* dsend_buf, void* stream);
+int fm_layer_expert_backward(fm_layer* layer, const void* drecv_buf, const void* w1,
+                             const void* w2, float* dw1, float* db1, float* dw2, float* db2,
+                             void* dret_buf, void* stream);
+int fm_layer_unpermute_backward(fm_layer* layer, const void* dback_buf, const void* send_buf,
+                                const void* wg, void* dx, float* dwg, void* stream);
+
 /* Introspection (synchronous device->host copy, for tests / metrics). */
 #define FM_FIELD_TOPK_IDX 0     /* int32 [T,k] */
 #define FM_FIELD_TOPK_W 1       /* f32   [T,k] */
@@ -190,7 +224,8 @@ int fm_layer_copy_out(fm_layer* layer, int field, void* host, size_t max_bytes, 
 #define FM_PHASE_BIAS_GRAD 12   /* db1, db2 */
 #define FM_PHASE_UNPERMUTE 13   /* dx gather + gate input grad */
 #define FM_PHASE_GATE_WGRAD 14  /* dWg */
-#define FM_NUM_PHASES 15
+#define FM_PHASE_RELAYOUT 15    /* a2a order <-> expert segments (multi-GPU) */
+#define FM_NUM_PHASES 16
 int fm_layer_set_timing(fm_layer* layer, int enable);
 int fm_layer_read_timing(fm_layer* layer, double* ms_by_phase, int* launches_by_phase);
 

@@ -86,6 +86,14 @@ _SIGNATURES = {
     "fm_layer_backward": [_P] * 9,
     "fm_layer_copy_out": [_P, _I, _P, C.c_size_t, C.POINTER(C.c_size_t)],
     "fm_layer_set_timing": [_P, _I],
+    "fm_layer_gate": [_P, _P, _I, _P, _P, _P],
+    "fm_layer_route": [_P, _P, _P, _P, _P],
+    "fm_layer_dispatch": [_P, _P, _P, _P],
+    "fm_layer_expert_forward": [_P] * 8,
+    "fm_layer_combine": [_P] * 4,
+    "fm_layer_combine_backward": [_P] * 5,
+    "fm_layer_expert_backward": [_P] * 10,
+    "fm_layer_unpermute_backward": [_P] * 7,
     "fm_layer_read_timing": [_P, _P, _P],
 }
 _RESTYPES = {"fm_last_error": C.c_char_p, "fm_version": C.c_char_p}

@@ -160,7 +160,8 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
                                 int G, int me, int direct, const int32_t* __restrict__ idx,
                                 const int32_t* __restrict__ tile_rank,
                                 const int32_t* __restrict__ tile_base, PlanDev p,
-                                int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf) {
+                                int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf,
+                                int32_t* __restrict__ row_expert) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -189,7 +190,10 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
         }
       }
     }
-    if (lane == 0) pos_out[u] = row;
+    if (lane == 0) {
+      pos_out[u] = row;
+      if (row_expert) row_expert[row] = e;
+    }
     uint4* dst = reinterpret_cast<uint4*>(buf + static_cast<size_t>(row) * d);
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -197,12 +201,16 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
   }
 }
 
-// Zero the padding rows of each segment: [seg_start + real, seg_start + rows).
-__global__ void zero_pad_kernel(__nv_bfloat16* __restrict__ buf, int d, PlanDev p, int Nl) {
+// Zero the padding rows of each segment: [seg_start + real, seg_start + rows);
+// optionally mark them as carrying no expert (row_expert = -1).
+__global__ void zero_pad_kernel(__nv_bfloat16* __restrict__ buf, int d, PlanDev p, int Nl,
+                                int32_t* __restrict__ row_expert) {
   const int li = blockIdx.y;
   if (li >= Nl) return;
   const int first = p.seg_start[li] + p.seg_real[li];
   const int last = p.seg_start[li] + p.seg_rows[li];
+  if (row_expert && blockIdx.x == 0)
+    for (int r = first + threadIdx.x; r < last; r += blockDim.x) row_expert[r] = -1;
   const int nvec = d / 8;
   const size_t begin = static_cast<size_t>(first) * nvec, end = static_cast<size_t>(last) * nvec;
   uint4* b = reinterpret_cast<uint4*>(buf);
@@ -444,6 +452,52 @@ __global__ void segment_colsum_kernel(const __nv_bfloat16* __restrict__ buf, int
   atomicAdd(out + static_cast<size_t>(oi) * cols + c2 + 1, a1);
 }
 
+// Gate-weight gradient: dWg[e][:] += sum over dispatch rows r with
+// row_expert[r] == e of dl_rows[r] * buf[r][:]. Rows of one expert are
+// contiguous runs (segments / send chunks), so each block accumulates a run
+// and flushes one f32 atomic per column when the expert changes.
+__global__ void gate_wgrad_kernel(const __nv_bfloat16* __restrict__ buf, const int* __restrict__ rows_ptr,
+                                  int rows_fixed, int d, const float* __restrict__ dl_rows,
+                                  const int32_t* __restrict__ row_expert, float* __restrict__ dwg) {
+  const int rows = rows_ptr ? *rows_ptr : rows_fixed;
+  const int r0 = blockIdx.x * 64;
+  if (r0 >= rows) return;
+  const int r1 = min(r0 + 64, rows);
+  const int c2 = (blockIdx.y * blockDim.x + threadIdx.x) * 2;
+  if (c2 >= d) return;
+  int cur = -1;
+  float a0 = 0.0f, a1 = 0.0f;
+  for (int r = r0; r < r1; ++r) {
+    const int e = row_expert[r];
+    if (e != cur) {
+      if (cur >= 0) {
+        atomicAdd(dwg + static_cast<size_t>(cur) * d + c2, a0);
+        atomicAdd(dwg + static_cast<size_t>(cur) * d + c2 + 1, a1);
+      }
+      cur = e;
+      a0 = a1 = 0.0f;
+    }
+    if (e < 0) continue;
+    const uint32_t v = *reinterpret_cast<const uint32_t*>(buf + static_cast<size_t>(r) * d + c2);
+    const float g = dl_rows[r];
+    a0 = fmaf(g, bf16lo(v), a0);
+    a1 = fmaf(g, bf16hi(v), a1);
+  }
+  if (cur >= 0) {
+    atomicAdd(dwg + static_cast<size_t>(cur) * d + c2, a0);
+    atomicAdd(dwg + static_cast<size_t>(cur) * d + c2 + 1, a1);
+  }
+}
+
+// demand[e][g] = gathered[g][e]  (all-gathered per-GPU histograms -> TokenDemand layout)
+__global__ void demand_transpose_kernel(const int64_t* __restrict__ gathered_GN, int N, int G,
+                                        int64_t* __restrict__ demand_NG) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N * G) return;
+  const int e = i / G, g = i % G;
+  demand_NG[i] = gathered_GN[static_cast<size_t>(g) * N + e];
+}
+
 // out[li][col] = sum over the 128-row tiles of segment li of partial[tile][col]
 // (fixed order: deterministic).
 __global__ void segment_tile_reduce_kernel(const float* __restrict__ partial, int cols, PlanDev p,
@@ -460,6 +514,21 @@ __global__ void segment_tile_reduce_kernel(const float* __restrict__ partial, in
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int max_rows, int d,
+                       const float* dl_rows, const int32_t* row_expert, float* dwg, cudaStream_t s) {
+  if (max_rows <= 0) return;
+  dim3 grid((max_rows + 63) / 64, (d / 2 + 255) / 256);
+  gate_wgrad_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(buf), rows_dev, rows_fixed,
+                                         d, dl_rows, row_expert, dwg);
+  FM_LAUNCH_CHECK("gate_wgrad_kernel");
+}
+
+void launch_demand_transpose(const int64_t* gathered_GN, int N, int G, int64_t* demand_NG,
+                             cudaStream_t s) {
+  demand_transpose_kernel<<<(N * G + 255) / 256, 256, 0, s>>>(gathered_GN, N, G, demand_NG);
+  FM_LAUNCH_CHECK("demand_transpose_kernel");
+}
+
 void launch_segment_tile_reduce(const float* partial, int cols, const PlanDev& p, int Nl, float* out,
                                 cudaStream_t s) {
   if (Nl <= 0) return;
@@ -489,20 +558,21 @@ void launch_plan(const int64_t* flows, int N, int G, int me, const int32_t* loca
 
 void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
                      const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
-                     const PlanDev& p, int32_t* pos, void* buf, cudaStream_t s) {
+                     const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
+                     cudaStream_t s) {
   if (d % 8 != 0 || d > 2048) throw std::invalid_argument("dispatch: d_model must be a multiple of 8, <= 2048");
   if (T <= 0) return;
   const int warps = 8;
   dispatch_kernel<<<(T + warps - 1) / warps, warps * 32, 0, s>>>(
       static_cast<const __nv_bfloat16*>(x), T, d, k, N, G, me, direct ? 1 : 0, idx, tile_rank,
-      tile_base, p, pos, static_cast<__nv_bfloat16*>(buf));
+      tile_base, p, pos, static_cast<__nv_bfloat16*>(buf), row_expert);
   FM_LAUNCH_CHECK("dispatch_kernel");
 }
 
-void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, cudaStream_t s) {
+void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, int32_t* row_expert, cudaStream_t s) {
   if (Nl <= 0) return;
   dim3 grid(4, Nl);
-  zero_pad_kernel<<<grid, 256, 0, s>>>(static_cast<__nv_bfloat16*>(buf), d, p, Nl);
+  zero_pad_kernel<<<grid, 256, 0, s>>>(static_cast<__nv_bfloat16*>(buf), d, p, Nl, row_expert);
   FM_LAUNCH_CHECK("zero_pad_kernel");
 }
 

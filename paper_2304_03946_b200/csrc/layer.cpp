@@ -34,8 +34,13 @@ void launch_plan(const int64_t* flows, int N, int G, int me, const int32_t* loca
                  const PlanDev& p, cudaStream_t s);
 void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
                      const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
-                     const PlanDev& p, int32_t* pos, void* buf, cudaStream_t s);
-void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, cudaStream_t s);
+                     const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
+                     cudaStream_t s);
+void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, int32_t* row_expert, cudaStream_t s);
+void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int max_rows, int d,
+                       const float* dl_rows, const int32_t* row_expert, float* dwg, cudaStream_t s);
+void launch_demand_transpose(const int64_t* gathered_GN, int N, int G, int64_t* demand_NG,
+                             cudaStream_t s);
 void launch_relayout(void* recv, void* perm, int d, int G, int Nl, const PlanDev& p, int max_rows,
                      int dir, cudaStream_t s);
 void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T, int d, int k,
@@ -177,6 +182,7 @@ class Layer {
     counts_dev_.reset(sizeof(int32_t) * N * G);
     route_status_.reset(sizeof(int32_t));
     counts_.assign(static_cast<size_t>(N) * G, 0);
+    host_counts_.assign(2 * G + 1, 0);
   }
 
   void set_placement(const int32_t* counts_NG) {
@@ -242,7 +248,8 @@ class Layer {
                        cudaMemcpyHostToDevice));
     // Row capacity of the permuted buffers: every unit could land here
     // (worst case of route()), plus per-segment padding.
-    const size_t units = static_cast<size_t>(cfg_.max_tokens) * cfg_.top_k * (G == 1 ? 1 : G);
+    // (G > 1 starts at twice the local units and grows in route_gathered.)
+    const size_t units = static_cast<size_t>(cfg_.max_tokens) * cfg_.top_k * (G == 1 ? 1 : 2);
     ensure_rows(round_up(units + static_cast<size_t>(Nl) * 127, 128));
   }
 
@@ -257,64 +264,52 @@ class Layer {
     dh_.reset(2 * row_cap_ * f);
     dx_perm_.reset(2 * row_cap_ * d);
     dl_rows_.reset(4 * row_cap_);
+    row_expert_.reset(4 * row_cap_);
     relu_mask_.reset(4 * row_cap_ * (f / 32));
     tile_colsum_.reset(4 * (row_cap_ / 128) * f);
   }
 
-  // ------------------------------------------------------------ forward
+  // ------------------------------------------------------------ fused single-GPU step
   void forward(const void* x, int T, const void* wg, const void* w1, const float* b1,
                const void* w2, const float* b2, void* y, cudaStream_t s) {
     if (cfg_.num_gpus != 1)
       throw std::logic_error("fm_layer_forward: fused path is single-GPU; use the phase API");
     check_tokens(T);
-    gate(x, T, wg, s);
-    route_and_plan(s);
+    gate(x, T, wg, nullptr, s);
+    route_device(s);
     timer_.begin(FM_PHASE_DISPATCH, s);
-    launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), s);
+    launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), row_expert_.as<int32_t>(), s);
     launch_dispatch(x, T, cfg_.d_model, cfg_.top_k, cfg_.num_experts, 1, 0, true,
                     topk_idx_.as<int32_t>(), tile_rank_.as<int32_t>(), tile_base_.as<int32_t>(),
-                    plan_, pos_.as<int32_t>(), x_perm_.p, s);
+                    plan_, pos_.as<int32_t>(), x_perm_.p, row_expert_.as<int32_t>(), s);
     timer_.end(s);
     expert_forward(w1, b1, w2, b2, s);
-    timer_.begin(FM_PHASE_COMBINE_FWD, s);
-    launch_combine_fwd(y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), T, cfg_.d_model,
-                       cfg_.top_k, y, s);
-    timer_.end(s);
-    saved_T_ = T;
+    combine(y_perm_.p, y, s);
     saved_wg_ = wg;
     saved_w1_ = w1;
     saved_w2_ = w2;
+    fused_state_ = true;
   }
 
   void backward(const void* dy, void* dx, float* dwg, float* dw1, float* db1, float* dw2,
                 float* db2, cudaStream_t s) {
     if (cfg_.num_gpus != 1)
       throw std::logic_error("fm_layer_backward: fused path is single-GPU; use the phase API");
-    if (saved_T_ < 0) throw std::logic_error("fm_layer_backward: no forward state");
-    const int T = saved_T_, d = cfg_.d_model, k = cfg_.top_k, N = cfg_.num_experts;
-    const bool gate_grad = k > 1;
+    if (!fused_state_) throw std::logic_error("fm_layer_backward: no forward state");
+    combine_backward(dy, y_perm_.p, dy_perm_.p, s);
     timer_.begin(FM_PHASE_COMBINE_BWD, s);
-    launch_combine_bwd(dy, y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), T, d, k, dy_perm_.p,
-                       dl_.as<float>(), gate_grad ? dl_rows_.as<float>() : nullptr, s);
-    launch_zero_pad(dy_perm_.p, d, plan_, nl(), s);
+    launch_zero_pad(dy_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);
     timer_.end(s);
     expert_backward(saved_w1_, saved_w2_, dw1, db1, dw2, db2, s);
-    timer_.begin(FM_PHASE_UNPERMUTE, s);
-    launch_unpermute_bwd(dx_perm_.p, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(),
-                         saved_wg_, T, d, k, gate_grad, dx, s);
-    timer_.end(s);
-    if (dwg) {
-      timer_.begin(FM_PHASE_GATE_WGRAD, s);
-      FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
-      if (gate_grad)
-        launch_segment_colsum(x_perm_.p, d, dl_rows_.as<float>(), plan_, nl(), local_expert_dev_,
-                              dwg, static_cast<int>(row_cap_), s);
-      timer_.end(s);
-    }
+    unpermute_backward(dx_perm_.p, x_perm_.p, plan_.totals, static_cast<int>(row_cap_), saved_wg_, dx,
+                       dwg, s);
   }
 
   // ------------------------------------------------------------ phases
-  void gate(const void* x, int T, const void* wg, cudaStream_t s) {
+  // Gate + per-expert scan. hist_out (device int64 [N], optional) receives
+  // this GPU's TokenDemand column for the all-gather.
+  void gate(const void* x, int T, const void* wg, int64_t* hist_out, cudaStream_t s) {
+    check_tokens(T);
     const int N = cfg_.num_experts, G = cfg_.num_gpus;
     timer_.begin(FM_PHASE_GATE, s);
     launch_gate(x, wg, T, N, cfg_.d_model, cfg_.top_k, topk_idx_.as<int32_t>(),
@@ -324,16 +319,71 @@ class Layer {
     if (G > 1) FM_CUDA(cudaMemsetAsync(demand_.p, 0, sizeof(int64_t) * N * G, s));
     launch_expert_scan(tile_counts_.as<int32_t>(), gate_num_tiles(T), N, tile_base_.as<int32_t>(),
                        hist_.as<int64_t>(), demand_.as<int64_t>(), G, cfg_.rank, s);
+    if (hist_out)
+      FM_CUDA(cudaMemcpyAsync(hist_out, hist_.p, sizeof(int64_t) * N, cudaMemcpyDeviceToDevice, s));
     timer_.end(s);
     cur_T_ = T;
+    fused_state_ = false;
   }
 
-  void route_and_plan(cudaStream_t s) {
+  // route() on the device over demand_ (already complete), then the plan.
+  void route_device(cudaStream_t s) {
     const int N = cfg_.num_experts, G = cfg_.num_gpus;
     timer_.begin(FM_PHASE_ROUTE, s);
     route_counts_device(demand_.as<int64_t>(), counts_dev_.as<int32_t>(), N, G,
                         flows_.as<int64_t>(), route_status_.as<int32_t>(), s);
     launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s);
+    timer_.end(s);
+  }
+
+  // Multi-GPU: full demand from the all-gathered per-GPU histograms
+  // (gathered_GN[g][e], device), route + plan, then the per-peer row counts
+  // for the all-to-all (host; synchronises the stream: NCCL needs them).
+  void route_gathered(const int64_t* gathered_GN, int32_t* send_rows, int32_t* recv_rows,
+                      cudaStream_t s) {
+    const int N = cfg_.num_experts, G = cfg_.num_gpus;
+    launch_demand_transpose(gathered_GN, N, G, demand_.as<int64_t>(), s);
+    route_device(s);
+    FM_CUDA(cudaMemcpyAsync(host_counts_.data(), plan_.send_rows, sizeof(int32_t) * 2 * G,
+                            cudaMemcpyDeviceToHost, s));
+    FM_CUDA(cudaMemcpyAsync(host_counts_.data() + 2 * G, route_status_.p, sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, s));
+    FM_CUDA(cudaStreamSynchronize(s));
+    if (host_counts_[2 * G] != 0)
+      throw std::invalid_argument("route: an expert has demand but no replica");
+    int recv_total = 0, send_total = 0;
+    for (int g = 0; g < G; ++g) {
+      send_rows[g] = host_counts_[g];
+      recv_rows[g] = host_counts_[G + g];
+      send_total += send_rows[g];
+      recv_total += recv_rows[g];
+    }
+    recv_total_ = recv_total;
+    send_total_ = send_total;
+    ensure_rows(round_up(static_cast<size_t>(recv_total) + static_cast<size_t>(nl()) * 127, 128));
+  }
+
+  void dispatch_send(const void* x, void* send_buf, cudaStream_t s) {
+    timer_.begin(FM_PHASE_DISPATCH, s);
+    launch_dispatch(x, cur_T_, cfg_.d_model, cfg_.top_k, cfg_.num_experts, cfg_.num_gpus, cfg_.rank,
+                    false, topk_idx_.as<int32_t>(), tile_rank_.as<int32_t>(),
+                    tile_base_.as<int32_t>(), plan_, pos_.as<int32_t>(), send_buf,
+                    row_expert_.as<int32_t>(), s);
+    timer_.end(s);
+  }
+
+  // a2a receive order (src-major, expert-minor) -> padded expert segments, and back.
+  void recv_to_perm(const void* recv_buf, void* perm, cudaStream_t s) {
+    timer_.begin(FM_PHASE_RELAYOUT, s);
+    launch_zero_pad(perm, cfg_.d_model, plan_, nl(), nullptr, s);
+    launch_relayout(const_cast<void*>(recv_buf), perm, cfg_.d_model, cfg_.num_gpus, nl(), plan_,
+                    recv_total_, 0, s);
+    timer_.end(s);
+  }
+  void perm_to_recv(const void* perm, void* recv_buf, cudaStream_t s) {
+    timer_.begin(FM_PHASE_RELAYOUT, s);
+    launch_relayout(recv_buf, const_cast<void*>(perm), cfg_.d_model, cfg_.num_gpus, nl(), plan_,
+                    recv_total_, 1, s);
     timer_.end(s);
   }
 
@@ -357,10 +407,10 @@ class Layer {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0) return;
     const int rows = static_cast<int>(row_cap_);
-    // dA = dY . W2 masked by relu'(H)  -> dH [rows, f]
+    // dA = dY . W2 masked by relu'(H) -> dH [rows, f]; db1 partials per 128-row tile
     timer_.begin(FM_PHASE_FFN2_DGRAD, s);
-    grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p, db1 ? tile_colsum_.as<float>() : nullptr,
-                 relu_mask_.p, plan_.seg_start,
+    grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p,
+                 db1 ? tile_colsum_.as<float>() : nullptr, relu_mask_.p, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s);
     timer_.end(s);
     // dX = dH . W1 -> [rows, d]
@@ -388,6 +438,63 @@ class Layer {
       launch_segment_colsum(dy_perm_.p, d, nullptr, plan_, Nl, nullptr, db2, rows, s);
     }
     timer_.end(s);
+  }
+
+  // y[t] = sum_j w[t,j] back[pos[t,j]] — back is Y_perm (G == 1) or the
+  // returned rows in dispatch order (G > 1).
+  void combine(const void* back, void* y, cudaStream_t s) {
+    timer_.begin(FM_PHASE_COMBINE_FWD, s);
+    launch_combine_fwd(back, pos_.as<int32_t>(), topk_w_.as<float>(), cur_T_, cfg_.d_model,
+                       cfg_.top_k, y, s);
+    timer_.end(s);
+  }
+
+  void combine_backward(const void* dy, const void* back, void* dsend, cudaStream_t s) {
+    const bool gate_grad = cfg_.top_k > 1;
+    timer_.begin(FM_PHASE_COMBINE_BWD, s);
+    launch_combine_bwd(dy, back, pos_.as<int32_t>(), topk_w_.as<float>(), cur_T_, cfg_.d_model,
+                       cfg_.top_k, dsend, dl_.as<float>(), gate_grad ? dl_rows_.as<float>() : nullptr,
+                       s);
+    timer_.end(s);
+  }
+
+  // dx and the gate weight gradient. dback: dX rows in dispatch order;
+  // xrows: the dispatched activations in the same order (X_perm or the send
+  // buffer); rows_dev / rows: how many of them.
+  void unpermute_backward(const void* dback, const void* xrows, const int* rows_dev, int rows,
+                          const void* wg, void* dx, float* dwg, cudaStream_t s) {
+    const int T = cur_T_, d = cfg_.d_model, k = cfg_.top_k, N = cfg_.num_experts;
+    const bool gate_grad = k > 1;
+    timer_.begin(FM_PHASE_UNPERMUTE, s);
+    launch_unpermute_bwd(dback, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(), wg, T,
+                         d, k, gate_grad, dx, s);
+    timer_.end(s);
+    if (dwg) {
+      timer_.begin(FM_PHASE_GATE_WGRAD, s);
+      FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
+      if (gate_grad)
+        launch_gate_wgrad(xrows, rows_dev, rows, rows, d, dl_rows_.as<float>(),
+                          row_expert_.as<int32_t>(), dwg, s);
+      timer_.end(s);
+    }
+  }
+
+  // phase wrappers (G >= 1)
+  void ph_expert_forward(const void* recv_buf, const void* w1, const float* b1, const void* w2,
+                         const float* b2, void* ret_buf, cudaStream_t s) {
+    recv_to_perm(recv_buf, x_perm_.p, s);
+    expert_forward(w1, b1, w2, b2, s);
+    perm_to_recv(y_perm_.p, ret_buf, s);
+  }
+  void ph_expert_backward(const void* drecv, const void* w1, const void* w2, float* dw1,
+                          float* db1, float* dw2, float* db2, void* dret, cudaStream_t s) {
+    recv_to_perm(drecv, dy_perm_.p, s);
+    expert_backward(w1, w2, dw1, db1, dw2, db2, s);
+    perm_to_recv(dx_perm_.p, dret, s);
+  }
+  void ph_unpermute_backward(const void* dback, const void* send_buf, const void* wg, void* dx,
+                             float* dwg, cudaStream_t s) {
+    unpermute_backward(dback, send_buf, nullptr, send_total_, wg, dx, dwg, s);
   }
 
   // ------------------------------------------------------------ introspection
@@ -441,12 +548,16 @@ class Layer {
   std::vector<int32_t> counts_, local_;
   DevBuf topk_idx_, topk_w_, tile_rank_, pos_, dl_, tile_counts_, tile_base_, hist_, demand_,
       flows_, counts_dev_, route_status_, plan_mem_;
-  DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_, relu_mask_, tile_colsum_;
+  DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_, relu_mask_, tile_colsum_,
+      row_expert_;
+  std::vector<int32_t> host_counts_;
+  int recv_total_ = 0, send_total_ = 0;
+  bool fused_state_ = false;
   PlanDev plan_{};
   PhaseTimer timer_;
   int32_t* local_expert_dev_ = nullptr;
   size_t row_cap_ = 0;
-  int cur_T_ = -1, saved_T_ = -1;
+  int cur_T_ = -1;
   const void *saved_wg_ = nullptr, *saved_w1_ = nullptr, *saved_w2_ = nullptr;
 };
 
@@ -495,6 +606,57 @@ int fm_layer_backward(fm_layer* h, const void* dy, void* dx, float* dwg, float* 
                       float* dw2, float* db2, void* stream) {
   return fm::guarded([&] {
     h->impl->backward(dy, dx, dwg, dw1, db1, dw2, db2, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fm_layer_gate(fm_layer* h, const void* x, int T, const void* wg, int64_t* hist_out,
+                  void* stream) {
+  return fm::guarded(
+      [&] { h->impl->gate(x, T, wg, hist_out, static_cast<cudaStream_t>(stream)); });
+}
+
+int fm_layer_route(fm_layer* h, const int64_t* gathered_hist_GN, int32_t* send_rows,
+                   int32_t* recv_rows, void* stream) {
+  return fm::guarded([&] {
+    h->impl->route_gathered(gathered_hist_GN, send_rows, recv_rows, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fm_layer_dispatch(fm_layer* h, const void* x, void* send_buf, void* stream) {
+  return fm::guarded([&] { h->impl->dispatch_send(x, send_buf, static_cast<cudaStream_t>(stream)); });
+}
+
+int fm_layer_expert_forward(fm_layer* h, const void* recv_buf, const void* w1, const float* b1,
+                            const void* w2, const float* b2, void* ret_buf, void* stream) {
+  return fm::guarded([&] {
+    h->impl->ph_expert_forward(recv_buf, w1, b1, w2, b2, ret_buf, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fm_layer_combine(fm_layer* h, const void* back_buf, void* y, void* stream) {
+  return fm::guarded([&] { h->impl->combine(back_buf, y, static_cast<cudaStream_t>(stream)); });
+}
+
+int fm_layer_combine_backward(fm_layer* h, const void* dy, const void* back_buf, void* dsend_buf,
+                              void* stream) {
+  return fm::guarded([&] {
+    h->impl->combine_backward(dy, back_buf, dsend_buf, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fm_layer_expert_backward(fm_layer* h, const void* drecv_buf, const void* w1, const void* w2,
+                             float* dw1, float* db1, float* dw2, float* db2, void* dret_buf,
+                             void* stream) {
+  return fm::guarded([&] {
+    h->impl->ph_expert_backward(drecv_buf, w1, w2, dw1, db1, dw2, db2, dret_buf,
+                                static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fm_layer_unpermute_backward(fm_layer* h, const void* dback_buf, const void* send_buf,
+                                const void* wg, void* dx, float* dwg, void* stream) {
+  return fm::guarded([&] {
+    h->impl->ph_unpermute_backward(dback_buf, send_buf, wg, dx, dwg, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -1,0 +1,338 @@
+"""Multi-GPU FlexMoE layer: one process per GPU, collectives between phases.
+
+Per step (the exchanges the reference models in
+cost_model.cpp:37-64):
+  1. all-gather of each GPU's expert histogram -> full TokenDemand D[e][g],
+     so every rank runs the identical deterministic route() (no broadcast);
+  2. dispatch all-to-all (per-peer row counts from the flows);
+  3. combine all-to-all back;
+  4. the two backward mirrors;
+  5. for every expert with >= 2 hosting GPUs, SUM all-reduce of its weight
+     gradients within its replica group, issued in ascending expert id on
+     every GPU (the deadlock-free order of proj/src/sim_engine.cpp:67-113),
+     groups cached in an LRU (sim_engine.cpp:45-65, capacity 64);
+     the data-parallel gate weight gradient is summed over all GPUs.
+SUM (not mean) is the right reduction: tokens are partitioned across the
+replicas, so the replica-group sum equals the single-replica gradient.
+
+The compute phases run in libflexmoe_b200.so (`fm_layer_*` phase API);
+torch.distributed (NCCL) is only the transport. `Exchange` abstracts the
+transport so the same orchestration runs over NCCL, gloo, or an in-process
+loopback (G virtual ranks on one GPU, used by the GPU tests).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+# ---------------------------------------------------------------- placement helpers
+def replica_gpus(replica_counts, e) -> tuple[int, ...]:
+    """Placement::replica_gpus (placement.cpp:109-117): ascending GPU ids hosting e."""
+    row = np.asarray(replica_counts)[e]
+    return tuple(int(g) for g in np.nonzero(row > 0)[0])
+
+
+def collective_order(replica_counts) -> list[list[int]]:
+    """Per GPU, the replicated experts it synchronises, ascending (sim_engine.cpp:67-79)."""
+    cnt = np.asarray(replica_counts)
+    G = cnt.shape[1]
+    order = [[] for _ in range(G)]
+    for e in range(cnt.shape[0]):
+        grp = replica_gpus(cnt, e)
+        if len(grp) >= 2:
+            for g in grp:
+                order[g].append(e)
+    return order
+
+
+def collective_order_deadlock_free(replica_counts) -> bool:
+    """Simulates blocking collectives in the per-GPU order (sim_engine.cpp:81-113)."""
+    cnt = np.asarray(replica_counts)
+    order = collective_order(cnt)
+    pos = [0] * cnt.shape[1]
+    progress = True
+    while progress:
+        progress = False
+        for e in range(cnt.shape[0]):
+            grp = replica_gpus(cnt, e)
+            if len(grp) < 2:
+                continue
+            if all(pos[g] < len(order[g]) and order[g][pos[g]] == e for g in grp):
+                for g in grp:
+                    pos[g] += 1
+                progress = True
+    return all(pos[g] == len(order[g]) for g in range(cnt.shape[1]))
+
+
+class LruGroupCache:
+    """LRU over replica-group keys (sorted GPU tuples); a miss creates the
+    group. Mirrors LruGroupCache (sim_engine.hpp:70-86 / .cpp:45-65): touch()
+    returns True on a hit; the least recently used group is evicted beyond
+    `capacity`. `create` / `destroy` hook the real communicator lifetime."""
+
+    def __init__(self, capacity=64, create=None, destroy=None):
+        if capacity < 1:
+            raise ValueError("LruGroupCache: capacity must be >= 1")
+        self.capacity = capacity
+        self._entries: OrderedDict[tuple, object] = OrderedDict()
+        self.misses = 0
+        self._create = create
+        self._destroy = destroy
+
+    def touch(self, group) -> bool:
+        key = tuple(sorted(group))
+        if key in self._entries:
+            self._entries.move_to_end(key, last=False)
+            return True
+        self.misses += 1
+        self._entries[key] = self._create(key) if self._create else key
+        self._entries.move_to_end(key, last=False)
+        if len(self._entries) > self.capacity:
+            old_key, old = self._entries.popitem(last=True)
+            if self._destroy:
+                self._destroy(old)
+        return False
+
+    def get(self, group):
+        self.touch(group)
+        return self._entries[tuple(sorted(group))]
+
+    def __len__(self):
+        return len(self._entries)
+
+
+# ---------------------------------------------------------------- transports
+class Exchange:
+    rank: int
+    world: int
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:  # -> [world, *t.shape]
+        raise NotImplementedError
+
+    def all_to_all(self, out, inp, out_splits, in_splits) -> None:
+        raise NotImplementedError
+
+    def all_reduce(self, t: torch.Tensor | None, group: tuple[int, ...] | None) -> None:
+        """SUM over `group` (None = all ranks). Every rank calls it for every
+        group in the same order; ranks outside the group pass t=None."""
+        raise NotImplementedError
+
+    def sync_group(self, group: tuple[int, ...]) -> None:
+        """Called on EVERY rank, in ascending expert id, for every replica group
+        (group creation is collective over the world in torch.distributed)."""
+
+
+class TorchExchange(Exchange):
+    """torch.distributed transport (NCCL on B200 / NVLink; gloo on CPU)."""
+
+    def __init__(self, max_live_groups=64):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.groups = LruGroupCache(max_live_groups, create=lambda key: dist.new_group(list(key)),
+                                    destroy=lambda pg: dist.destroy_process_group(pg))
+
+    def all_gather(self, t):
+        out = torch.empty((self.world, *t.shape), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out, t.contiguous())
+        return out
+
+    def all_to_all(self, out, inp, out_splits, in_splits):
+        self.dist.all_to_all_single(out, inp, output_split_sizes=list(out_splits),
+                                    input_split_sizes=list(in_splits))
+
+    def sync_group(self, group):
+        self.groups.touch(group)
+
+    def all_reduce(self, t, group):
+        if group is None:
+            self.dist.all_reduce(t)
+        elif t is not None and self.rank in group:
+            self.dist.all_reduce(t, group=self.groups.get(group))
+
+
+class LoopbackHub:
+    """In-process stand-in for G ranks (threads) sharing one device: used to
+    run the real multi-GPU kernels and layouts on a single B200."""
+
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+        self.groups = LruGroupCache(64)
+
+    def endpoint(self, rank):
+        return LoopbackExchange(self, rank)
+
+
+class LoopbackExchange(Exchange):
+    def __init__(self, hub: LoopbackHub, rank: int):
+        self.hub, self.rank, self.world = hub, rank, hub.world
+
+    def _swap(self, obj):
+        self.hub.barrier.wait()
+        self.hub.slots[self.rank] = obj
+        self.hub.barrier.wait()
+        got = list(self.hub.slots)
+        self.hub.barrier.wait()
+        return got
+
+    def all_gather(self, t):
+        return torch.stack(self._swap(t.clone()))
+
+    def all_to_all(self, out, inp, out_splits, in_splits):
+        offs = np.concatenate([[0], np.cumsum(in_splits)]).astype(int)
+        chunks = [inp[offs[i]:offs[i + 1]] for i in range(self.world)]
+        allc = self._swap(chunks)
+        o = 0
+        for src in range(self.world):
+            c = allc[src][self.rank]
+            out[o:o + c.shape[0]].copy_(c)
+            o += c.shape[0]
+        self._swap(None)  # keep sources alive until everyone copied
+
+    def sync_group(self, group):
+        if self.rank == 0:
+            self.hub.groups.touch(group)
+
+    def all_reduce(self, t, group):
+        members = range(self.world) if group is None else group
+        allv = self._swap(t.clone() if (t is not None and self.rank in members) else None)
+        if t is not None and self.rank in members:
+            acc = torch.zeros_like(t)
+            for g in members:
+                acc += allv[g]
+            t.copy_(acc)
+
+
+# ---------------------------------------------------------------- the layer
+@dataclass
+class StepBuffers:
+    send: torch.Tensor
+    recv: torch.Tensor
+    ret: torch.Tensor
+    back: torch.Tensor
+    send_rows: list[int]
+    recv_rows: list[int]
+
+
+class DistributedMoELayer:
+    """FlexMoE layer on one GPU of G, driving fm_layer_* phases around `exchange`."""
+
+    def __init__(self, layer, exchange: Exchange):
+        from .layer import MoELayer
+
+        assert isinstance(layer, MoELayer)
+        self.layer, self.ex = layer, exchange
+        if layer.G != exchange.world or layer.rank != exchange.rank:
+            raise L.InvalidArgument("DistributedMoELayer: layer and exchange disagree on rank/world")
+        self._st: StepBuffers | None = None
+        self._saved = None
+
+    @property
+    def replica_counts(self):
+        return self.layer.replica_counts
+
+    def _call(self, name, *args):
+        L.check(getattr(L.lib(), name)(self.layer._h, *args))
+
+    def forward(self, x, wg, w1, b1, w2, b2):
+        lay, d, N, k = self.layer, self.layer.d, self.layer.N, self.layer.k
+        T = x.shape[0]
+        dev = x.device
+        stream = L.stream_ptr()
+        hist = torch.empty(N, dtype=torch.int64, device=dev)
+        self._call("fm_layer_gate", x.data_ptr(), T, wg.data_ptr(), hist.data_ptr(), stream)
+        gathered = self.ex.all_gather(hist)  # [G, N]
+        G = lay.G
+        send_rows = np.zeros(G, np.int32)
+        recv_rows = np.zeros(G, np.int32)
+        self._call("fm_layer_route", gathered.data_ptr(), send_rows.ctypes.data, recv_rows.ctypes.data,
+                   stream)
+        send_rows, recv_rows = send_rows.tolist(), recv_rows.tolist()
+        bf = torch.bfloat16
+        send = torch.empty(max(T * k, 1), d, dtype=bf, device=dev)
+        recv = torch.empty(max(sum(recv_rows), 1), d, dtype=bf, device=dev)
+        ret = torch.empty_like(recv)
+        back = torch.empty_like(send)
+        self._call("fm_layer_dispatch", x.data_ptr(), send.data_ptr(), stream)
+        self.ex.all_to_all(recv[: sum(recv_rows)], send[: T * k], recv_rows, send_rows)
+        self._call("fm_layer_expert_forward", recv.data_ptr(), w1.data_ptr(), b1.data_ptr(),
+                   w2.data_ptr(), b2.data_ptr(), ret.data_ptr(), stream)
+        self.ex.all_to_all(back[: T * k], ret[: sum(recv_rows)], send_rows, recv_rows)
+        y = torch.empty(T, d, dtype=bf, device=dev)
+        self._call("fm_layer_combine", back.data_ptr(), y.data_ptr(), stream)
+        self._st = StepBuffers(send, recv, ret, back, send_rows, recv_rows)
+        self._saved = (T, wg, w1, w2)
+        self.last_demand = gathered
+        return y
+
+    def backward(self, dy, sync=True):
+        from .layer import LayerGrads
+
+        T, wg, w1, w2 = self._saved
+        st = self._st
+        lay = self.layer
+        dev = dy.device
+        stream = L.stream_ptr()
+        nl = len(lay.local_experts)
+        k, d, f, N = lay.k, lay.d, lay.f, lay.N
+        dsend = torch.empty_like(st.send)
+        drecv = torch.empty_like(st.recv)
+        dret = torch.empty_like(st.recv)
+        dback = torch.empty_like(st.send)
+        z = lambda *s: torch.empty(*s, device=dev, dtype=torch.float32)
+        g = LayerGrads(dx=torch.empty(T, d, device=dev, dtype=torch.bfloat16), dwg=z(N, d),
+                       dw1=z(max(nl, 1), f, d), db1=z(max(nl, 1), f), dw2=z(max(nl, 1), d, f),
+                       db2=z(max(nl, 1), d))
+        R = sum(st.recv_rows)
+        self._call("fm_layer_combine_backward", dy.data_ptr(), st.back.data_ptr(), dsend.data_ptr(),
+                   stream)
+        self.ex.all_to_all(drecv[:R], dsend[: T * k], st.recv_rows, st.send_rows)
+        self._call("fm_layer_expert_backward", drecv.data_ptr(), w1.data_ptr(), w2.data_ptr(),
+                   g.dw1.data_ptr(), g.db1.data_ptr(), g.dw2.data_ptr(), g.db2.data_ptr(),
+                   dret.data_ptr(), stream)
+        self.ex.all_to_all(dback[: T * k], dret[:R], st.send_rows, st.recv_rows)
+        self._call("fm_layer_unpermute_backward", dback.data_ptr(), st.send.data_ptr(),
+                   wg.data_ptr(), g.dx.data_ptr(), g.dwg.data_ptr(), stream)
+        if nl == 0:
+            g.dw1, g.db1, g.dw2, g.db2 = (t[:0] for t in (g.dw1, g.db1, g.dw2, g.db2))
+        if sync:
+            self.sync_grads(g)
+        return g
+
+    def sync_grads(self, g):
+        """Replica-group SUM all-reduce in ascending expert id; gate grad over all GPUs."""
+        cnt = self.layer.replica_counts
+        local = self.layer.local_experts
+        li = {e: i for i, e in enumerate(local)}
+        for e in range(cnt.shape[0]):
+            grp = replica_gpus(cnt, e)
+            if len(grp) < 2:
+                continue
+            self.ex.sync_group(grp)
+            member = self.ex.rank in grp
+            flat = None
+            if member:
+                i = li[e]
+                flat = torch.cat([g.dw1[i].reshape(-1), g.db1[i], g.dw2[i].reshape(-1), g.db2[i]])
+            self.ex.all_reduce(flat, grp)  # non-members pass None
+            if not member:
+                continue
+            o = 0
+            for t in (g.dw1[i], g.db1[i], g.dw2[i], g.db2[i]):
+                n = t.numel()
+                t.copy_(flat[o:o + n].view_as(t))
+                o += n
+        self.ex.all_reduce(g.dwg, None)
+        return g

@@ -32,7 +32,7 @@ FIELDS = {
 
 PHASES = ["gate", "scan", "route", "dispatch", "ffn1_fwd", "ffn2_fwd", "combine_fwd",
           "combine_bwd", "ffn2_dgrad", "ffn1_dgrad", "ffn2_wgrad", "ffn1_wgrad", "bias_grad",
-          "unpermute", "gate_wgrad"]  # FM_PHASE_* order
+          "unpermute", "gate_wgrad", "relayout"]  # FM_PHASE_* order
 
 
 class _Config(C.Structure):

@@ -1,0 +1,150 @@
+"""Multi-GPU layer path on one B200: G virtual ranks (threads) drive the real
+phase kernels (gate, route over the all-gathered demand, dispatch into
+peer-major send buffers, relayout, expert FFN, combine, and the backward
+mirror) with an in-process loopback transport, then the replica-group
+gradient sync. Checked against the CPU oracle:
+
+* bit-exact: all-gathered TokenDemand, flows (= reference route()), every
+  rank's dispatch rows (canonical permutation), per-peer row counts;
+* bf16 tolerance (see test_layer_gpu.py): y and dx per rank equal the
+  single-GPU oracle on the same tokens (replicas hold identical weights);
+* after the SUM all-reduce over each replica group, every replica's weight
+  gradients equal the oracle's full-batch gradients (rel. error <= 1e-2).
+"""
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from oracle import layer as OL  # noqa: E402
+from paper_2304_03946_b200.distributed import (  # noqa: E402
+    DistributedMoELayer,
+    LoopbackHub,
+    collective_order_deadlock_free,
+)
+from paper_2304_03946_b200.layer import MoELayer  # noqa: E402
+
+from tests.test_layer_gpu import close_bf16, close_f32  # noqa: E402
+
+
+def run_ranks(G, fn):
+    errs, outs = [None] * G, [None] * G
+
+    def body(r):
+        try:
+            outs[r] = fn(r)
+        except BaseException as exc:  # surface in the main thread
+            errs[r] = exc
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for e in errs:
+        if e is not None:
+            raise e
+    return outs
+
+
+PLACEMENTS = {
+    # config-1 shape: 8 experts on 4 GPUs, expert 0 expanded onto GPUs 1 and 2
+    "cfg1_expanded": (8, 4, [(e, e % 4) for e in range(8)] + [(0, 1), (0, 2)]),
+    # hot expert replicated everywhere, two slots of expert 3 on GPU 0
+    "replicated": (8, 4, [(e, e % 4) for e in range(8)] + [(5, 0), (5, 2), (5, 3), (3, 0)]),
+    "two_gpus": (16, 2, [(e, e % 2) for e in range(16)] + [(1, 0), (2, 1)]),
+}
+
+
+@pytest.mark.parametrize("name", sorted(PLACEMENTS))
+def test_multigpu_loopback_parity(name):
+    N, G, pairs = PLACEMENTS[name]
+    k, d, f, T = 2, 256, 512, 600
+    cnt = np.zeros((N, G), np.int32)
+    for e, g in pairs:
+        cnt[e, g] += 1
+    assert collective_order_deadlock_free(cnt)
+    rng = np.random.default_rng(7)
+    p = 1.0 / np.arange(1, N + 1) ** 1.25
+    skew = np.log(p / p.sum())[rng.permutation(N)] + 3
+    X, wg, w1, b1, w2, b2 = OL.exact_inputs(rng, T * G, d, N, f, skew=skew)
+    dY = OL.bf16(rng.standard_normal((T * G, d)) * 0.5)
+    st = OL.forward(X, wg, w1, b1, w2, b2, k)  # full batch, single-GPU math
+    gr = OL.backward(st, dY)
+
+    hub = LoopbackHub(G)
+    bf = torch.bfloat16
+    dev = lambda a, dt=bf: torch.tensor(np.asarray(a), dtype=dt, device="cuda")
+
+    def rank_fn(r):
+        torch.cuda.set_device(0)
+        lay = MoELayer(N, k, d, f, replica_counts=cnt, num_gpus=G, rank=r, max_tokens=T)
+        loc = lay.local_experts
+        dl = DistributedMoELayer(lay, hub.endpoint(r))
+        xs = slice(r * T, (r + 1) * T)
+        y = dl.forward(dev(X[xs]), dev(wg), dev(w1[loc]), dev(b1[loc], torch.float32),
+                       dev(w2[loc]), dev(b2[loc], torch.float32))
+        g = dl.backward(dev(dY[xs]))
+        torch.cuda.synchronize()
+        idx = lay.read("topk_idx", T * k).reshape(T, k)
+        pos = lay.read("unit_pos", T * k).reshape(T, k)
+        flows = lay.read("flows", N * G * G).reshape(N, G, G)
+        D = dl.last_demand.cpu().numpy()
+        return dict(loc=loc, y=y.float().cpu().numpy(), idx=idx, pos=pos, flows=flows, D=D,
+                    send_rows=dl._st.send_rows, recv_rows=dl._st.recv_rows,
+                    dx=g.dx.float().cpu().numpy(), dw1=g.dw1.cpu().numpy(), dw2=g.dw2.cpu().numpy(),
+                    db1=g.db1.cpu().numpy(), db2=g.db2.cpu().numpy(), dwg=g.dwg.cpu().numpy())
+
+    outs = run_ranks(G, rank_fn)
+
+    # ---- routing state, bit-exact
+    hist = np.stack([OL.histogram(st["idx"][r * T:(r + 1) * T], N) for r in range(G)])  # [G, N]
+    flows_ref = oracle.Oracle().route(hist.T, cnt)
+    for r, o in enumerate(outs):
+        assert (o["D"] == hist).all(), "all-gathered demand differs"
+        assert (o["flows"] == flows_ref).all(), "flows differ from route()"
+        idx_r = st["idx"][r * T:(r + 1) * T]
+        assert (o["idx"] == idx_r).all()
+        rows, _ = OL.dispatch_rows(idx_r, OL.unit_ranks(idx_r, N), flows_ref, r, G, N)
+        assert (o["pos"] == rows).all(), f"rank {r}: dispatch rows differ"
+        assert o["send_rows"] == [int(flows_ref[:, r, dst].sum()) for dst in range(G)]
+        assert o["recv_rows"] == [int(flows_ref[:, src, r].sum()) for src in range(G)]
+
+    # ---- outputs and gradients
+    for r, o in enumerate(outs):
+        xs = slice(r * T, (r + 1) * T)
+        close_bf16(o["y"], st["y"][xs], f"y[rank {r}]")
+        close_bf16(o["dx"], gr["dx"][xs], f"dx[rank {r}]")
+        for i, e in enumerate(o["loc"]):
+            close_f32(o["dw1"][i], gr["dw1"][e], f"dw1[e{e}@{r}]")
+            close_f32(o["dw2"][i], gr["dw2"][e], f"dw2[e{e}@{r}]")
+            close_f32(o["db1"][i], gr["db1"][e], f"db1[e{e}@{r}]")
+            close_f32(o["db2"][i], gr["db2"][e], f"db2[e{e}@{r}]")
+        close_f32(o["dwg"], gr["dwg"], f"dwg[{r}]", tol=2e-2)
+
+
+def test_phase_api_single_gpu_matches_fused():
+    """G == 1 through the phase API (identity exchange) equals the fused step."""
+    N, k, d, f, T = 8, 2, 256, 256, 1000
+    rng = np.random.default_rng(11)
+    x, wg, w1, b1, w2, b2 = OL.exact_inputs(rng, T, d, N, f)
+    dy = OL.bf16(rng.standard_normal((T, d)))
+    bf = torch.bfloat16
+    dev = lambda a, dt=bf: torch.tensor(np.asarray(a), dtype=dt, device="cuda")
+    P = [dev(wg), dev(w1), dev(b1, torch.float32), dev(w2), dev(b2, torch.float32)]
+    fused = MoELayer(N, k, d, f, max_tokens=T)
+    y1 = fused.forward(dev(x), *P)
+    g1 = fused.backward(dev(dy))
+    hub = LoopbackHub(1)
+    phased = DistributedMoELayer(MoELayer(N, k, d, f, max_tokens=T), hub.endpoint(0))
+    y2 = phased.forward(dev(x), *P)
+    g2 = phased.backward(dev(dy))
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert torch.equal(g1.dx, g2.dx)
+    for a, b in [(g1.dw1, g2.dw1), (g1.dw2, g2.dw2), (g1.db1, g2.db1)]:
+        assert torch.allclose(a, b, rtol=1e-5, atol=1e-5)
