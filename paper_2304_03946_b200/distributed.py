@@ -143,9 +143,10 @@ class TorchExchange(Exchange):
                                     destroy=lambda pg: dist.destroy_process_group(pg))
 
     def all_gather(self, t):
-        out = torch.empty((self.world, *t.shape), dtype=t.dtype, device=t.device)
-        self.dist.all_gather_into_tensor(out, t.contiguous())
-        return out
+        flat = t.contiguous().reshape(-1)
+        out = torch.empty(self.world * flat.numel(), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out, flat)
+        return out.view(self.world, *t.shape)
 
     def all_to_all(self, out, inp, out_splits, in_splits):
         self.dist.all_to_all_single(out, inp, output_split_sizes=list(out_splits),
@@ -312,27 +313,32 @@ class DistributedMoELayer:
         return g
 
     def sync_grads(self, g):
-        """Replica-group SUM all-reduce in ascending expert id; gate grad over all GPUs."""
-        cnt = self.layer.replica_counts
-        local = self.layer.local_experts
-        li = {e: i for i, e in enumerate(local)}
-        for e in range(cnt.shape[0]):
-            grp = replica_gpus(cnt, e)
-            if len(grp) < 2:
-                continue
-            self.ex.sync_group(grp)
-            member = self.ex.rank in grp
-            flat = None
-            if member:
-                i = li[e]
-                flat = torch.cat([g.dw1[i].reshape(-1), g.db1[i], g.dw2[i].reshape(-1), g.db2[i]])
-            self.ex.all_reduce(flat, grp)  # non-members pass None
-            if not member:
-                continue
-            o = 0
-            for t in (g.dw1[i], g.db1[i], g.dw2[i], g.db2[i]):
-                n = t.numel()
-                t.copy_(flat[o:o + n].view_as(t))
-                o += n
-        self.ex.all_reduce(g.dwg, None)
-        return g
+        return sync_replica_grads(self.ex, self.layer.replica_counts, self.layer.local_experts, g)
+
+
+def sync_replica_grads(ex: Exchange, replica_counts, local_experts, g):
+    """Replica-group SUM all-reduce of each replicated expert's (dw1, db1, dw2,
+    db2), in ascending expert id on every rank (one flattened buffer per
+    expert), then the gate-weight gradient over all ranks."""
+    cnt = np.asarray(replica_counts)
+    li = {e: i for i, e in enumerate(local_experts)}
+    for e in range(cnt.shape[0]):
+        grp = replica_gpus(cnt, e)
+        if len(grp) < 2:
+            continue
+        ex.sync_group(grp)
+        member = ex.rank in grp
+        flat = None
+        if member:
+            i = li[e]
+            flat = torch.cat([g.dw1[i].reshape(-1), g.db1[i], g.dw2[i].reshape(-1), g.db2[i]])
+        ex.all_reduce(flat, grp)  # non-members pass None
+        if not member:
+            continue
+        o = 0
+        for t in (g.dw1[i], g.db1[i], g.dw2[i], g.db2[i]):
+            n = t.numel()
+            t.copy_(flat[o:o + n].view_as(t))
+            o += n
+    ex.all_reduce(g.dwg, None)
+    return g
