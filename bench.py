@@ -208,10 +208,103 @@ def run_reference_arm(args, world, rank):
 
 
 # ------------------------------------------------------------------ GPU arm
+CFG3 = dict(workload="BASELINE configs[2]: GPT-MoE layer, 64 experts top-1, d_model 1024, d_ff 4096, "
+            "65,536 tokens per GPU (weak scaling), drifting Zipf traffic",
+            N=64, k=1, d=1024, f=4096, T=65536, zipf=1.25)
+
+
+class FusedArm:
+    """configs[1] on one GPU: the fused single-GPU step (no host sync)."""
+
+    def __init__(self, cfg, dev, rank):
+        import torch
+
+        from paper_2304_03946_b200.layer import MoELayer
+
+        N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
+        self.layer = MoELayer(N, k, d, f, max_tokens=T)
+        p = self.layer.init_params(seed=1234)
+        logp = torch.tensor(zipf_log_popularity(N, cfg["zipf"], 42), dtype=torch.float32)
+        p["wg"][:, 0] = (logp * 2).to(p["wg"].dtype).to(dev)  # skew through the real gate
+        self.P = (p["wg"], p["w1"], p["b1"], p["w2"], p["b2"])
+        self.grads = None
+        self.N, self.G = N, 1
+        self.kernels_per_step = 9 + 8 + (2 if k > 1 else 1)
+
+    def step(self, x, dy):
+        self.layer.forward(x, *self.P)
+        self.grads = self.layer.backward(dy, self.grads)
+
+    def set_timing(self, on):
+        self.layer.set_timing(on)
+
+    def timing(self):
+        return self.layer.read_timing(), {}
+
+    def flows(self):
+        return self.layer.read("flows", self.N).reshape(self.N, 1, 1)
+
+    def hist(self):
+        return self.layer.read("hist", self.N)
+
+
+class DistArm:
+    """configs[2]: one process per GPU, NCCL all-to-all / all-reduce between phases."""
+
+    def __init__(self, cfg, dev, rank, world):
+        import torch
+
+        from paper_2304_03946_b200.distributed import DistributedMoELayer, LoopbackHub, TorchExchange
+        from paper_2304_03946_b200.layer import MoELayer
+
+        N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
+        G = world
+        slots = 2 * ((N + G - 1) // G)
+        cnt = np.zeros((N, G), np.int32)
+        cnt[np.arange(N), np.arange(N) % G] = 1  # Placement::initial (round robin)
+        self.layer = MoELayer(N, k, d, f, replica_counts=cnt, num_gpus=G, rank=rank, max_tokens=T,
+                              slots_per_gpu=slots)
+        ex = TorchExchange() if world > 1 else LoopbackHub(1).endpoint(0)
+        self.dl = DistributedMoELayer(self.layer, ex)
+        g = torch.Generator(device="cpu").manual_seed(1234)
+        wg = torch.randn(N, d, generator=g) * d**-0.5
+        wg[:, 0] = torch.tensor(zipf_log_popularity(N, cfg["zipf"], 42) * 2, dtype=torch.float32)
+        loc = self.layer.local_experts
+
+        def expert_params(e):  # identical on every replica: seeded by expert id
+            ge = torch.Generator(device="cpu").manual_seed(10_000 + e)
+            return (torch.randn(f, d, generator=ge) * d**-0.5, torch.randn(f, generator=ge) * 0.02,
+                    torch.randn(d, f, generator=ge) * f**-0.5, torch.randn(d, generator=ge) * 0.02)
+
+        ps = [expert_params(e) for e in loc]
+        st = lambda i: torch.stack([p[i] for p in ps]).to(dev)
+        bf = torch.bfloat16
+        self.P = (wg.to(bf).to(dev), st(0).to(bf), st(1).float(), st(2).to(bf), st(3).float())
+        self.N, self.G = N, G
+        self.kernels_per_step = 9 + 8 + (2 if k > 1 else 1) + 4 + 1  # + relayouts, transpose
+
+    def step(self, x, dy):
+        self.dl.forward(x, *self.P)
+        self.dl.backward(dy)
+
+    def set_timing(self, on):
+        self.layer.set_timing(on)
+        self.dl.set_timing(on)
+
+    def timing(self):
+        return self.layer.read_timing(), self.dl.read_timing()
+
+    def flows(self):
+        return self.layer.read("flows", self.N * self.G * self.G).reshape(self.N, self.G, self.G)
+
+    def hist(self):
+        return self.layer.read("hist", self.N)
+
+
 def run_ours(args, world, rank, local_rank):
     import torch
 
-    from paper_2304_03946_b200.layer import MoELayer
+    from paper_2304_03946_b200 import routing
 
     torch.cuda.set_device(local_rank)
     dist = None
@@ -219,36 +312,25 @@ def run_ours(args, world, rank, local_rank):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    cfg = dict(CFG2)
-    N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
     dev = torch.device("cuda", local_rank)
-    # Each rank runs the single-GPU layer on its own shard of tokens
-    # (replicas; the multi-GPU exchange path is exercised by the phase API).
-    layer = MoELayer(N, k, d, f, max_tokens=T)
-    params = layer.init_params(seed=1234)
+    multi = world > 1 or args.workload == "cfg3"
+    cfg = dict(CFG3 if multi else CFG2)
+    N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
+    arm = DistArm(cfg, dev, rank, world) if multi else FusedArm(cfg, dev, rank)
+
     gen = torch.Generator(device="cpu").manual_seed(100 + rank)
-    logp = torch.tensor(zipf_log_popularity(N, cfg["zipf"], 42), dtype=torch.float32)
-    params["wg"][:, 0] = (logp * 2).to(params["wg"].dtype).to(dev)  # skew through the gate
     x_host = torch.randn(T, d, generator=gen).to(torch.bfloat16)
     x_host[:, 0] = 0.5
     dy_host = (torch.randn(T, d, generator=gen) * 0.1).to(torch.bfloat16)
-    x = x_host.to(dev)
-    dy = dy_host.to(dev)
-    P = (params["wg"], params["w1"], params["b1"], params["w2"], params["b2"])
-    grads = None
+    x, dy = x_host.to(dev), dy_host.to(dev)
     stream = torch.cuda.current_stream()
 
-    def step():
-        nonlocal grads
-        layer.forward(x, *P)
-        grads = layer.backward(dy, grads)
-
     for _ in range(max(args.warmup, 3)):
-        step()
+        arm.step(x, dy)
     torch.cuda.synchronize()
 
-    # ---------------- device-timed region (value) with live per-phase timing
-    layer.set_timing(True)
+    # ---------------- device-timed region (value), live per-phase timing
+    arm.set_timing(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
@@ -256,21 +338,24 @@ def run_ours(args, world, rank, local_rank):
     with ClockSampler(local_rank) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            arm.step(x, dy)
         ev1.record(stream)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    phases = layer.read_timing()
-    layer.set_timing(False)
+    phases, comm = arm.timing()
+    arm.set_timing(False)
     if dist:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    hist = layer.read("hist", N)
-    units = int(hist.sum())
+    hist = arm.hist()
+    flows = arm.flows()
+    units = int(hist.sum())  # this GPU's demand units (T * k)
+    recv_units = int(flows[:, :, rank].sum())  # units this GPU's experts processed
+    balance = routing.balance_ratio(flows)
 
     # ---------------- e2e through the public API, pinned host inputs
     xh = [x_host.pin_memory(), torch.randn(T, d, generator=gen).to(torch.bfloat16).pin_memory()]
@@ -279,26 +364,23 @@ def run_ours(args, world, rank, local_rank):
     dyb = [torch.empty_like(dy), torch.empty_like(dy)]
     copy_stream = torch.cuda.Stream(device=dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
-    hist_host = None
 
     def e2e_run(n):
-        nonlocal grads, hist_host
         with torch.cuda.stream(copy_stream):
             xb[0].copy_(xh[0], non_blocking=True)
             dyb[0].copy_(dyh[0], non_blocking=True)
             copied[0].record(copy_stream)
         for i in range(n):
             cur, nxt = i % 2, (i + 1) % 2
-            if i + 1 < n:  # prefetch next step's inputs while this one computes
+            if i + 1 < n:  # prefetch the next step's inputs while this one computes
                 with torch.cuda.stream(copy_stream):
                     copy_stream.wait_stream(stream)
                     xb[nxt].copy_(xh[nxt], non_blocking=True)
                     dyb[nxt].copy_(dyh[nxt], non_blocking=True)
                     copied[nxt].record(copy_stream)
             stream.wait_event(copied[cur])
-            layer.forward(xb[cur], *P)
-            grads = layer.backward(dyb[cur], grads)
-            hist_host = layer.read("hist", N)  # host policy input, every step
+            arm.step(xb[cur], dyb[cur])
+            arm.hist()  # expert histogram to the host every step (placement-policy input)
 
     e2e_run(2)
     torch.cuda.synchronize()
@@ -324,20 +406,19 @@ def run_ours(args, world, rank, local_rank):
     gemm_names = ["ffn1_fwd", "ffn2_fwd", "ffn2_dgrad", "ffn1_dgrad", "ffn2_wgrad", "ffn1_wgrad"]
     gemm_ms = sum(phases[n][0] for n in gemm_names) / args.steps
     gemm_launches = sum(phases[n][1] for n in gemm_names) / args.steps
-    flop_step = 12.0 * units * d * f
-    achieved = flop_step / (gemm_ms * 1e-3) / 1e12
+    flop_step = 12.0 * recv_units * d * f  # algorithmic: real (unpadded) units on this GPU
+    achieved = flop_step / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
     traffic = None
     tp = ROOT / "profiles" / "gemm_traffic.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get("bytes_per_launch")
-    # HBM kernels: algorithmic bytes per step
-    hbm_bytes = {
+    hbm_bytes = {  # algorithmic bytes per step
         "gate": T * d * 2 + N * d * 2 + units * 12,
         "dispatch": T * d * 2 + units * d * 2 + units * 4,
         "combine_fwd": units * (d * 2 + 8) + T * d * 2,
         "combine_bwd": T * d * 2 + units * (d * 2 * 2 + 12),
         "unpermute": units * (d * 2 + 12) + T * d * 2,
-        "bias_grad": units * (f + d) * 2,
+        "relayout": 4 * recv_units * d * 2,
     }
     kernels = {}
     for name, (pms, n) in phases.items():
@@ -349,10 +430,12 @@ def run_ours(args, world, rank, local_rank):
             gbs = hbm_bytes[name] / (per * 1e-3) / 1e9
             ent.update({"achieved_GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3)})
         if name in gemm_names and per > 0:
-            tf = 2.0 * units * d * f / (per * 1e-3) / 1e12
+            tf = 2.0 * recv_units * d * f / (per * 1e-3) / 1e12
             ent.update({"achieved_TFLOPs": round(tf, 1), "frac_bf16": round(tf / peaks["bf16_sus"], 3)})
         kernels[name] = ent
-    kernels_per_step = 9 + 9 + (1 if k > 1 else 0)
+    for name, (cms, n) in comm.items():
+        kernels["comm_" + name] = {"ms_per_step": round(cms / args.steps, 4),
+                                   "calls_per_step": n / args.steps}
     line = {
         "metric": METRIC,
         "value": T * world / (ms_step * 1e-3),
@@ -365,16 +448,18 @@ def run_ours(args, world, rank, local_rank):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic (random-init weights of the configs[1] architecture; skew via the gate)",
-        "config": {"workload": cfg["workload"], "model": "MoE layer N16 k2 d1024 f4096",
+        "data": "synthetic (random-init weights of the configs architecture; Zipf skew via the gate)",
+        "config": {"workload": cfg["workload"],
+                   "model": f"MoE layer N{N} k{k} d{d} f{f}",
                    "global_batch": T * world, "tokens_per_gpu": T, "seq_len": None,
-                   "parallelism": "ep1" if world == 1 else f"replicas x{world}",
-                   "zipf": cfg["zipf"], "units_per_step": units,
-                   "expert_load_max_over_mean": float(hist.max() / hist.mean()),
+                   "parallelism": f"ep{world}" + ("+replicas" if multi else ""),
+                   "zipf": cfg["zipf"], "units_per_step_rank0": units,
+                   "expert_load_max_over_mean": float(hist.max() / max(hist.mean(), 1e-9)),
+                   "placement": "static (Placement::initial round robin)" if multi else "static",
                    "l2": "per-step working set > L2 (no flush)"},
         "e2e": {"value": T * world / (e2e_ms * 1e-3 / args.steps), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(2 * T * d * 2), "d2h_bytes_per_step": int(N * 8)},
-        "gpu_launches": kernels_per_step * args.steps,
+        "gpu_launches": arm.kernels_per_step * args.steps,
         "roofline": {"bound": "tensor", "kernel": "grouped_gemm (tcgen05, 6 launches/step)",
                      "achieved": round(achieved, 1), "peak": peaks["bf16_sus"],
                      "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_sus"], 4),
@@ -382,9 +467,9 @@ def run_ours(args, world, rank, local_rank):
                      "gemm_ms_per_step": round(gemm_ms, 4), "gemm_launches_per_step": gemm_launches},
         "kernels": kernels,
         "clocks": clocks.summary(),
-        "balance_ratio": 1.0,
+        "balance_ratio": balance,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not multi and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg)
         except Exception as exc:
@@ -401,6 +486,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default=None, choices=[None, "cfg2", "cfg3"],
+                    help="default: cfg2 at 1 GPU, cfg3 (multi-GPU phase path) at N > 1")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -239,6 +239,32 @@ class DistributedMoELayer:
             raise L.InvalidArgument("DistributedMoELayer: layer and exchange disagree on rank/world")
         self._st: StepBuffers | None = None
         self._saved = None
+        self._timing = False
+        self._marks: list[tuple[str, torch.cuda.Event, torch.cuda.Event]] = []
+
+    # CUDA-event timing of the exchanges (a2a, all-gather, all-reduce)
+    def set_timing(self, on: bool):
+        self._timing = on
+        self._marks = []
+
+    def read_timing(self) -> dict[str, tuple[float, int]]:
+        torch.cuda.synchronize()
+        out: dict[str, list] = {}
+        for name, a, b in self._marks:
+            v = out.setdefault(name, [0.0, 0])
+            v[0] += a.elapsed_time(b)
+            v[1] += 1
+        return {k: (v[0], v[1]) for k, v in out.items()}
+
+    def _x(self, name, fn, *args):
+        if not self._timing:
+            return fn(*args)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r = fn(*args)
+        b.record()
+        self._marks.append((name, a, b))
+        return r
 
     @property
     def replica_counts(self):
@@ -254,7 +280,7 @@ class DistributedMoELayer:
         stream = L.stream_ptr()
         hist = torch.empty(N, dtype=torch.int64, device=dev)
         self._call("fm_layer_gate", x.data_ptr(), T, wg.data_ptr(), hist.data_ptr(), stream)
-        gathered = self.ex.all_gather(hist)  # [G, N]
+        gathered = self._x("all_gather", self.ex.all_gather, hist)  # [G, N]
         G = lay.G
         send_rows = np.zeros(G, np.int32)
         recv_rows = np.zeros(G, np.int32)
@@ -267,10 +293,10 @@ class DistributedMoELayer:
         ret = torch.empty_like(recv)
         back = torch.empty_like(send)
         self._call("fm_layer_dispatch", x.data_ptr(), send.data_ptr(), stream)
-        self.ex.all_to_all(recv[: sum(recv_rows)], send[: T * k], recv_rows, send_rows)
+        self._x("a2a", self.ex.all_to_all, recv[: sum(recv_rows)], send[: T * k], recv_rows, send_rows)
         self._call("fm_layer_expert_forward", recv.data_ptr(), w1.data_ptr(), b1.data_ptr(),
                    w2.data_ptr(), b2.data_ptr(), ret.data_ptr(), stream)
-        self.ex.all_to_all(back[: T * k], ret[: sum(recv_rows)], send_rows, recv_rows)
+        self._x("a2a", self.ex.all_to_all, back[: T * k], ret[: sum(recv_rows)], send_rows, recv_rows)
         y = torch.empty(T, d, dtype=bf, device=dev)
         self._call("fm_layer_combine", back.data_ptr(), y.data_ptr(), stream)
         self._st = StepBuffers(send, recv, ret, back, send_rows, recv_rows)
@@ -299,17 +325,17 @@ class DistributedMoELayer:
         R = sum(st.recv_rows)
         self._call("fm_layer_combine_backward", dy.data_ptr(), st.back.data_ptr(), dsend.data_ptr(),
                    stream)
-        self.ex.all_to_all(drecv[:R], dsend[: T * k], st.recv_rows, st.send_rows)
+        self._x("a2a", self.ex.all_to_all, drecv[:R], dsend[: T * k], st.recv_rows, st.send_rows)
         self._call("fm_layer_expert_backward", drecv.data_ptr(), w1.data_ptr(), w2.data_ptr(),
                    g.dw1.data_ptr(), g.db1.data_ptr(), g.dw2.data_ptr(), g.db2.data_ptr(),
                    dret.data_ptr(), stream)
-        self.ex.all_to_all(dback[: T * k], dret[:R], st.send_rows, st.recv_rows)
+        self._x("a2a", self.ex.all_to_all, dback[: T * k], dret[:R], st.send_rows, st.recv_rows)
         self._call("fm_layer_unpermute_backward", dback.data_ptr(), st.send.data_ptr(),
                    wg.data_ptr(), g.dx.data_ptr(), g.dwg.data_ptr(), stream)
         if nl == 0:
             g.dw1, g.db1, g.dw2, g.db2 = (t[:0] for t in (g.dw1, g.db1, g.dw2, g.db2))
         if sync:
-            self.sync_grads(g)
+            self._x("grad_sync", self.sync_grads, g)
         return g
 
     def sync_grads(self, g):
