@@ -82,6 +82,13 @@ int fm_largest_remainder_round(const double* exact, int n, int64_t total, int64_
 int fm_static_ep_kept(const int64_t* demand_NG, int num_experts, int num_gpus,
                       double capacity_factor, int64_t* kept_NG, int64_t* dropped);
 
+/* Device port of the same rule, one thread per expert (explicit
+ * round-to-nearest double ops in the reference's order: bit-identical to the
+ * host). Device pointers; dropped (int64[1]) receives the total drop count. */
+int fm_static_ep_kept_device(const int64_t* demand_NG, int num_experts, int num_gpus,
+                             double capacity_factor, int64_t* kept_NG, int64_t* dropped,
+                             void* stream);
+
 /* ------------------------------------------------------------------------
  * Grouped expert GEMM on tcgen05 (test / building-block hook).
  * seg_start, seg_rows, tile_prefix are device int32 arrays describing the
@@ -139,10 +146,17 @@ int fm_layer_create(const fm_layer_config* cfg, const int32_t* replica_counts_NG
 int fm_layer_destroy(fm_layer* layer);
 /* Placement change (Expand / Shrink / Migrate applied, placement.hpp:92-104). */
 int fm_layer_set_placement(fm_layer* layer, const int32_t* replica_counts_NG);
+/* StaticEP mode (proj/src/baselines.cpp:81-131): capacity_factor > 0 and finite
+ * drops, each step, the units beyond fm_static_ep_kept's kept[e][g] on every
+ * source GPU — the LAST ones in the canonical unit order — before routing;
+ * dropped units contribute nothing to y (their gate gradient is kept).
+ * 0 or +inf disables drops (the FlexMoE mode, which never drops). */
+int fm_layer_set_capacity_factor(fm_layer* layer, double capacity_factor);
 int fm_layer_local_experts(const fm_layer* layer, int* num_local, int32_t* experts_out);
 
 /* Single-GPU (num_gpus == 1) fused step; no host synchronisation.
- * forward keeps what backward needs (routing, permuted activations). */
+ * forward keeps what backward needs (routing, permuted activations); x and
+ * the weights must stay valid until fm_layer_backward has been enqueued. */
 int fm_layer_forward(fm_layer* layer, const void* x, int num_tokens, const void* wg,
                      const void* w1, const float* b1, const void* w2, const float* b2, void* y,
                      void* stream);
@@ -204,6 +218,8 @@ int fm_layer_unpermute_backward(fm_layer* layer, const void* dback_buf, const vo
 #define FM_FIELD_DH 17          /* bf16 [rows,f] */
 #define FM_FIELD_DX_PERM 18     /* bf16 [rows,d] */
 #define FM_FIELD_ROUTE_STATUS 19 /* int32 [1] device route status */
+#define FM_FIELD_KEPT 20        /* int64 [N,G] StaticEP kept demand (capacity mode) */
+#define FM_FIELD_DROPPED 21     /* int64 [1]   units dropped this step (capacity mode) */
 int fm_layer_copy_out(fm_layer* layer, int field, void* host, size_t max_bytes, size_t* written);
 
 /* Per-phase CUDA-event timing on the launching stream (off by default).

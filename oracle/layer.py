@@ -102,29 +102,38 @@ def segments(flows, local_experts, me):
     return out
 
 
-def single_gpu_positions(idx, N):
-    """G == 1: X_perm row of each unit and the segment table."""
+def single_gpu_positions(idx, N, capacity_factor=0.0):
+    """G == 1: X_perm row of each unit (-1 = dropped) and the segment table.
+
+    With capacity_factor > 0 (StaticEP, baselines.cpp:89-122) the demand is
+    first cut to static_ep_kept (C oracle, pinned to the reference); the
+    units dropped are the last ones of each expert in canonical order."""
     ranks = unit_ranks(idx, N)
     hist = histogram(idx, N)
-    flows = Oracle().route(hist.reshape(N, 1), np.ones((N, 1), np.int32))
+    routed = hist.reshape(N, 1)
+    if capacity_factor > 0 and np.isfinite(capacity_factor):
+        routed, _ = Oracle().static_ep_kept(routed, capacity_factor)
+    flows = Oracle().route(routed, np.ones((N, 1), np.int32))
     segs = segments(flows, list(range(N)), 0)
     seg_start = np.array([s[0] for s in segs], np.int64)
-    pos = seg_start[idx] + ranks
+    keep = ranks < routed[idx, 0]
+    pos = np.where(keep, seg_start[idx] + ranks, -1)
     return pos, segs, flows, hist
 
 
-def forward(x, wg, w1, b1, w2, b2, k):
+def forward(x, wg, w1, b1, w2, b2, k, capacity_factor=0.0):
     """Single-GPU layer forward. Weights [N,...] in expert order. Returns a state dict."""
     x = np.asarray(x, np.float64)
     T, d = x.shape
     N = wg.shape[0]
     idx, w, logits = gate(x, wg, k)
-    pos, segs, flows, hist = single_gpu_positions(idx, N)
+    pos, segs, flows, hist = single_gpu_positions(idx, N, capacity_factor)
     rows = sum(s[2] for s in segs)
     f = w1.shape[1]
     x_perm = np.zeros((rows, d))
     for j in range(k):
-        x_perm[pos[:, j]] = x
+        kept = pos[:, j] >= 0
+        x_perm[pos[kept, j]] = x[kept]
     act = np.zeros((rows, f))
     y_perm = np.zeros((rows, d))
     for e, (s0, real, r) in enumerate(segs):
@@ -133,7 +142,9 @@ def forward(x, wg, w1, b1, w2, b2, k):
         seg = slice(s0, s0 + r)
         act[seg] = bf16(np.maximum(x_perm[seg] @ np.asarray(w1[e], np.float64).T + b1[e], 0.0))
         y_perm[seg] = bf16(act[seg] @ np.asarray(w2[e], np.float64).T + b2[e])
-    y = bf16(np.einsum("tk,tkd->td", w.astype(np.float32).astype(np.float64), y_perm[pos]))
+    live = (pos >= 0).astype(np.float64)  # dropped units contribute nothing
+    y = bf16(np.einsum("tk,tkd->td", w.astype(np.float32).astype(np.float64) * live,
+                       y_perm[np.maximum(pos, 0)]))
     return dict(x=x, wg=np.asarray(wg, np.float64), w1=w1, w2=w2, idx=idx, w=w, logits=logits,
                 pos=pos, segs=segs, flows=flows, hist=hist, x_perm=x_perm, act=act,
                 y_perm=y_perm, y=y, k=k)
@@ -148,9 +159,10 @@ def backward(st, dy):
     f = act.shape[1]
     wf = w.astype(np.float32).astype(np.float64)
     dy_perm = np.zeros_like(y_perm)
+    live = pos >= 0
     for j in range(k):
-        dy_perm[pos[:, j]] = bf16(wf[:, j : j + 1] * dy)
-    dw = np.einsum("td,tkd->tk", dy, y_perm[pos])
+        dy_perm[pos[live[:, j], j]] = bf16(wf[live[:, j], j : j + 1] * dy[live[:, j]])
+    dw = np.einsum("td,tkd->tk", dy, y_perm[np.maximum(pos, 0)]) * live
     dl = wf * (dw - (wf * dw).sum(axis=1, keepdims=True))
     dh = np.zeros((x_perm.shape[0], f))
     dx_perm = np.zeros_like(x_perm)
@@ -170,7 +182,7 @@ def backward(st, dy):
         db1[e] = dh[seg].sum(axis=0)
         db2[e] = dy_perm[seg].sum(axis=0)
     gate_in = np.einsum("tk,tkd->td", dl, st["wg"][idx]) if k > 1 else 0.0
-    dx = bf16(dx_perm[pos].sum(axis=1) + gate_in)
+    dx = bf16((dx_perm[np.maximum(pos, 0)] * live[:, :, None]).sum(axis=1) + gate_in)
     dwg = np.zeros((N, d))
     if k > 1:
         np.add.at(dwg, idx.reshape(-1), dl.reshape(-1, 1) * np.repeat(st["x"], k, axis=0))

@@ -177,8 +177,8 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
     const int e = idx[u];
     const int r = tile_base[static_cast<size_t>(tile) * N + e] + tile_rank[u];
     int row;
-    if (direct) {
-      row = p.seg_start[p.local_index[e]] + r;
+    if (direct) {  // G == 1: chunk_cnt[e] is the kept demand (all of it unless dropping)
+      row = r < p.chunk_cnt[e] ? p.seg_start[p.local_index[e]] + r : -1;
     } else {
       row = -1;
       for (int i = 0; i < G; ++i) {
@@ -191,9 +191,10 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
       }
     }
     if (lane == 0) {
-      pos_out[u] = row;
-      if (row_expert) row_expert[row] = e;
+      pos_out[u] = row;  // -1: dropped by the capacity rule (StaticEP)
+      if (row_expert && row >= 0) row_expert[row] = e;
     }
+    if (row < 0) continue;
     uint4* dst = reinterpret_cast<uint4*>(buf + static_cast<size_t>(row) * d);
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -313,10 +314,11 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(const __nv_bfloat16* _
     const bool two = j + 1 < k;
     const int p1 = __shfl_sync(0xffffffffu, my_pos, two ? j + 1 : j);
     const float w1 = __shfl_sync(0xffffffffu, my_w, two ? j + 1 : j);
-    load_row<VPL>(Y, p0, d, lane, q0);
-    if (two) load_row<VPL>(Y, p1, d, lane, q1);
-    axpy_row<VPL>(acc, q0, w0);
-    if (two) axpy_row<VPL>(acc, q1, w1);
+    const bool h0 = p0 >= 0, h1 = two && p1 >= 0;  // dropped units contribute nothing
+    if (h0) load_row<VPL>(Y, p0, d, lane, q0);
+    if (h1) load_row<VPL>(Y, p1, d, lane, q1);
+    if (h0) axpy_row<VPL>(acc, q0, w0);
+    if (h1) axpy_row<VPL>(acc, q1, w1);
   }
   store_row<VPL>(y, t, d, lane, acc);
 }
@@ -344,6 +346,10 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   for (int j = 0; j < k; ++j) {
     const int row = __shfl_sync(0xffffffffu, my_pos, j);
     const float wj = __shfl_sync(0xffffffffu, my_w, j);
+    if (row < 0) {  // dropped: no expert output, d(loss)/d(w_j) = 0
+      if (lane == j) my_dw = 0.0f;
+      continue;
+    }
     uint4 q[VPL];
     load_row<VPL>(Y, row, d, lane, q);
     uint4* dst = reinterpret_cast<uint4*>(dYbuf + static_cast<size_t>(row) * d);
@@ -370,7 +376,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   if (lane < k) {
     const float g_l = my_w * (my_dw - wdw);
     dl[static_cast<size_t>(t) * k + lane] = g_l;
-    if (dl_rows) dl_rows[my_pos] = g_l;
+    if (dl_rows && my_pos >= 0) dl_rows[my_pos] = g_l;
   }
 }
 
@@ -400,10 +406,11 @@ __global__ void __launch_bounds__(256) unpermute_bwd_kernel(
     const int p0 = __shfl_sync(0xffffffffu, my_pos, j);
     const int p1 = __shfl_sync(0xffffffffu, my_pos, two ? j + 1 : j);
     uint4 q0[VPL], q1[VPL];
-    load_row<VPL>(dXbuf, p0, d, lane, q0);
-    if (two) load_row<VPL>(dXbuf, p1, d, lane, q1);
-    axpy_row<VPL>(acc, q0, 1.0f);
-    if (two) axpy_row<VPL>(acc, q1, 1.0f);
+    const bool h0 = p0 >= 0, h1 = two && p1 >= 0;
+    if (h0) load_row<VPL>(dXbuf, p0, d, lane, q0);
+    if (h1) load_row<VPL>(dXbuf, p1, d, lane, q1);
+    if (h0) axpy_row<VPL>(acc, q0, 1.0f);
+    if (h1) axpy_row<VPL>(acc, q1, 1.0f);
   }
   if (gate_grad) {
     for (int j = 0; j < k; ++j) {
@@ -489,6 +496,30 @@ __global__ void gate_wgrad_kernel(const __nv_bfloat16* __restrict__ buf, const i
   }
 }
 
+// Gate-weight gradient of units dropped by the capacity rule (in no dispatch
+// row): dWg[e] += dl[u] * x[t], warp per token, f32 atomics.
+__global__ void dropped_gate_wgrad_kernel(const __nv_bfloat16* __restrict__ x,
+                                          const int32_t* __restrict__ pos,
+                                          const int32_t* __restrict__ idx,
+                                          const float* __restrict__ dl, int T, int d, int k,
+                                          float* __restrict__ dwg) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  for (int j = 0; j < k; ++j) {
+    const size_t u = static_cast<size_t>(t) * k + j;
+    if (pos[u] >= 0) continue;
+    const float g = dl[u];
+    float* out = dwg + static_cast<size_t>(idx[u]) * d;
+    const __nv_bfloat16* xr = x + static_cast<size_t>(t) * d;
+    for (int c = 2 * lane; c < d; c += 64) {
+      const uint32_t v = *reinterpret_cast<const uint32_t*>(xr + c);
+      atomicAdd(out + c, g * bf16lo(v));
+      atomicAdd(out + c + 1, g * bf16hi(v));
+    }
+  }
+}
+
 // demand[e][g] = gathered[g][e]  (all-gathered per-GPU histograms -> TokenDemand layout)
 __global__ void demand_transpose_kernel(const int64_t* __restrict__ gathered_GN, int N, int G,
                                         int64_t* __restrict__ demand_NG) {
@@ -521,6 +552,14 @@ void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int
   gate_wgrad_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(buf), rows_dev, rows_fixed,
                                          d, dl_rows, row_expert, dwg);
   FM_LAUNCH_CHECK("gate_wgrad_kernel");
+}
+
+void launch_dropped_gate_wgrad(const void* x, const int32_t* pos, const int32_t* idx, const float* dl,
+                               int T, int d, int k, float* dwg, cudaStream_t s) {
+  if (T <= 0) return;
+  dropped_gate_wgrad_kernel<<<(T + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), pos,
+                                                         idx, dl, T, d, k, dwg);
+  FM_LAUNCH_CHECK("dropped_gate_wgrad_kernel");
 }
 
 void launch_demand_transpose(const int64_t* gathered_GN, int N, int G, int64_t* demand_NG,

@@ -13,6 +13,7 @@
 // (placement.hpp:80-82). The experts hosted on this rank (count > 0) are the
 // local experts, in ascending id; their weights are packed in that order.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -54,6 +55,8 @@ void launch_segment_colsum(const void* buf, int cols, const float* row_w, const 
                            const int32_t* seg_out_index, float* out, int max_rows, cudaStream_t s);
 void launch_segment_tile_reduce(const float* partial, int cols, const PlanDev& p, int Nl, float* out,
                                 cudaStream_t s);
+void launch_dropped_gate_wgrad(const void* x, const int32_t* pos, const int32_t* idx, const float* dl,
+                               int T, int d, int k, float* dwg, cudaStream_t s);
 void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
@@ -183,6 +186,9 @@ class Layer {
     route_status_.reset(sizeof(int32_t));
     counts_.assign(static_cast<size_t>(N) * G, 0);
     host_counts_.assign(2 * G + 1, 0);
+    kept_.reset(sizeof(int64_t) * N * G);
+    dropped_.reset(sizeof(int64_t));
+    FM_CUDA(cudaMemset(dropped_.p, 0, sizeof(int64_t)));
   }
 
   void set_placement(const int32_t* counts_NG) {
@@ -323,15 +329,23 @@ class Layer {
       FM_CUDA(cudaMemcpyAsync(hist_out, hist_.p, sizeof(int64_t) * N, cudaMemcpyDeviceToDevice, s));
     timer_.end(s);
     cur_T_ = T;
+    saved_x_ = x;
     fused_state_ = false;
   }
 
-  // route() on the device over demand_ (already complete), then the plan.
+  // route() on the device over demand_ (already complete), then the plan. In
+  // StaticEP mode the demand first goes through the capacity-drop rule.
   void route_device(cudaStream_t s) {
     const int N = cfg_.num_experts, G = cfg_.num_gpus;
     timer_.begin(FM_PHASE_ROUTE, s);
-    route_counts_device(demand_.as<int64_t>(), counts_dev_.as<int32_t>(), N, G,
-                        flows_.as<int64_t>(), route_status_.as<int32_t>(), s);
+    const int64_t* routed = demand_.as<int64_t>();
+    if (drops_enabled()) {
+      static_ep_kept_device(demand_.as<int64_t>(), N, G, capacity_factor_, kept_.as<int64_t>(),
+                            dropped_.as<int64_t>(), s);
+      routed = kept_.as<int64_t>();
+    }
+    route_counts_device(routed, counts_dev_.as<int32_t>(), N, G, flows_.as<int64_t>(),
+                        route_status_.as<int32_t>(), s);
     launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s);
     timer_.end(s);
   }
@@ -472,9 +486,14 @@ class Layer {
     if (dwg) {
       timer_.begin(FM_PHASE_GATE_WGRAD, s);
       FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
-      if (gate_grad)
+      if (gate_grad) {
         launch_gate_wgrad(xrows, rows_dev, rows, rows, d, dl_rows_.as<float>(),
                           row_expert_.as<int32_t>(), dwg, s);
+        // units dropped by the capacity rule are in no dispatch row
+        if (drops_enabled())
+          launch_dropped_gate_wgrad(saved_x_, pos_.as<int32_t>(), topk_idx_.as<int32_t>(),
+                                    dl_.as<float>(), T, d, k, dwg, s);
+      }
       timer_.end(s);
     }
   }
@@ -527,6 +546,8 @@ class Layer {
       case FM_FIELD_DH: src = dh_.p; bytes = dh_.bytes; break;
       case FM_FIELD_DX_PERM: src = dx_perm_.p; bytes = dx_perm_.bytes; break;
       case FM_FIELD_ROUTE_STATUS: src = route_status_.p; bytes = 4; break;
+      case FM_FIELD_KEPT: src = kept_.p; bytes = 8ull * N * G; break;
+      case FM_FIELD_DROPPED: src = dropped_.p; bytes = 8; break;
       default: throw std::invalid_argument("fm_layer_copy_out: unknown field");
     }
     bytes = std::min(bytes, max_bytes);
@@ -536,6 +557,11 @@ class Layer {
   }
 
   size_t row_capacity() const { return row_cap_; }
+  bool drops_enabled() const { return capacity_factor_ > 0 && std::isfinite(capacity_factor_); }
+  void set_capacity_factor(double cf) {
+    if (!(cf >= 0)) throw std::invalid_argument("fm_layer: capacity_factor must be >= 0");
+    capacity_factor_ = cf;
+  }
   PhaseTimer& timer() { return timer_; }
 
  private:
@@ -551,6 +577,9 @@ class Layer {
   DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_, relu_mask_, tile_colsum_,
       row_expert_;
   std::vector<int32_t> host_counts_;
+  double capacity_factor_ = 0.0;  // 0 / inf: no drops (FlexMoE)
+  const void* saved_x_ = nullptr;  // gate input of the current step (must outlive backward)
+  DevBuf kept_, dropped_;
   int recv_total_ = 0, send_total_ = 0;
   bool fused_state_ = false;
   PlanDev plan_{};
@@ -585,6 +614,10 @@ int fm_layer_destroy(fm_layer* h) {
 
 int fm_layer_set_placement(fm_layer* h, const int32_t* replica_counts_NG) {
   return fm::guarded([&] { h->impl->set_placement(replica_counts_NG); });
+}
+
+int fm_layer_set_capacity_factor(fm_layer* h, double capacity_factor) {
+  return fm::guarded([&] { h->impl->set_capacity_factor(capacity_factor); });
 }
 
 int fm_layer_local_experts(const fm_layer* h, int* num_local, int32_t* experts) {

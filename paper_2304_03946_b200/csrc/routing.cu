@@ -47,7 +47,74 @@ __global__ void route_kernel(const int64_t* __restrict__ D, const int32_t* __res
   if (st != kRouteOk && status) atomicCAS(status, 0, st == kRouteNoReplica ? FM_ERR_INVALID_ARGUMENT : FM_ERR_LOGIC);
 }
 
+// StaticEP capacity drops on the device (baselines.cpp:89-122), one thread per
+// expert. The double arithmetic is spelled out with explicit round-to-nearest
+// intrinsics (no FMA contraction), in the reference's evaluation order:
+// cap = floor((cf * B) / N); exact[g] = (D[e][g] * cap) / load; then
+// largest-remainder rounding with a stable descending sort of the fractions.
+__global__ void static_ep_kept_kernel(const int64_t* __restrict__ D, int N, int G, double cf,
+                                      int64_t* __restrict__ kept, int64_t* __restrict__ dropped) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N) return;
+  int64_t tokens = 0;
+  for (int i = 0; i < N * G; ++i) tokens += D[i];
+  const int64_t cap =
+      static_cast<int64_t>(floor(__ddiv_rn(__dmul_rn(cf, static_cast<double>(tokens)), static_cast<double>(N))));
+  const int64_t* De = D + static_cast<size_t>(e) * G;
+  int64_t* Ke = kept + static_cast<size_t>(e) * G;
+  int64_t load = 0;
+  for (int g = 0; g < G; ++g) load += De[g];
+  int64_t drop = 0;
+  if (load <= cap) {
+    for (int g = 0; g < G; ++g) Ke[g] = De[g];
+  } else {
+    double frac[kMaxGpus];
+    int64_t out[kMaxGpus];
+    int order[kMaxGpus];
+    int64_t assigned = 0;
+    for (int g = 0; g < G; ++g) {
+      const double ex = __ddiv_rn(__dmul_rn(static_cast<double>(De[g]), static_cast<double>(cap)),
+                                  static_cast<double>(load));
+      const double fl = floor(ex);
+      out[g] = static_cast<int64_t>(fl);
+      frac[g] = __dsub_rn(ex, fl);
+      assigned += out[g];
+      int j = g - 1;
+      while (j >= 0 && frac[order[j]] < frac[g]) {
+        order[j + 1] = order[j];
+        --j;
+      }
+      order[j + 1] = g;
+    }
+    for (int64_t k = 0; assigned < cap; ++k, ++assigned) out[order[k % G]] += 1;
+    for (int64_t k = G; assigned > cap;) {
+      --k;
+      const int i = order[k % G];
+      if (out[i] > 0) {
+        out[i] -= 1;
+        --assigned;
+      }
+      if (k == 0) k = G;
+    }
+    for (int g = 0; g < G; ++g) {
+      const int64_t kg = out[g] < De[g] ? out[g] : De[g];
+      drop += De[g] - kg;
+      Ke[g] = kg;
+    }
+  }
+  if (dropped && drop) atomicAdd(reinterpret_cast<unsigned long long*>(dropped),
+                                 static_cast<unsigned long long>(drop));
+}
+
 }  // namespace
+
+void static_ep_kept_device(const int64_t* D, int N, int G, double cf, int64_t* kept,
+                           int64_t* dropped, cudaStream_t stream) {
+  if (N < 1 || G < 1 || G > kMaxGpus) throw std::invalid_argument("static_ep: bad dimensions");
+  if (dropped) FM_CUDA(cudaMemsetAsync(dropped, 0, sizeof(int64_t), stream));
+  static_ep_kept_kernel<<<(N + 127) / 128, 128, 0, stream>>>(D, N, G, cf, kept, dropped);
+  FM_LAUNCH_CHECK("static_ep_kept_kernel");
+}
 
 void route_counts_device(const int64_t* D, const int32_t* cnt, int N, int G, int64_t* flows,
                          int32_t* status, cudaStream_t stream) {
@@ -169,6 +236,15 @@ int fm_route_counts_device(const int64_t* demand_NG, const int32_t* replica_coun
   return fm::guarded([&] {
     fm::route_counts_device(demand_NG, replica_counts_NG, num_experts, num_gpus, flows_NGG,
                             status_dev, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fm_static_ep_kept_device(const int64_t* demand_NG, int num_experts, int num_gpus,
+                             double capacity_factor, int64_t* kept_NG, int64_t* dropped,
+                             void* stream) {
+  return fm::guarded([&] {
+    fm::static_ep_kept_device(demand_NG, num_experts, num_gpus, capacity_factor, kept_NG, dropped,
+                              static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -118,5 +118,7 @@ void route_counts_host(const int64_t* D, const int32_t* cnt, int N, int G, int64
 void route_counts_device(const int64_t* D, const int32_t* cnt, int N, int G, int64_t* flows,
                          int32_t* status, cudaStream_t stream);
 double balance_ratio_host(const int64_t* flows, int N, int G);
+void static_ep_kept_device(const int64_t* D, int N, int G, double cf, int64_t* kept,
+                           int64_t* dropped, cudaStream_t stream);
 
 }  // namespace fm

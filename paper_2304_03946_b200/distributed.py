@@ -300,14 +300,14 @@ class DistributedMoELayer:
         y = torch.empty(T, d, dtype=bf, device=dev)
         self._call("fm_layer_combine", back.data_ptr(), y.data_ptr(), stream)
         self._st = StepBuffers(send, recv, ret, back, send_rows, recv_rows)
-        self._saved = (T, wg, w1, w2)
+        self._saved = (T, wg, w1, w2, x)  # x: StaticEP backward re-reads dropped units
         self.last_demand = gathered
         return y
 
     def backward(self, dy, sync=True):
         from .layer import LayerGrads
 
-        T, wg, w1, w2 = self._saved
+        T, wg, w1, w2, _x = self._saved
         st = self._st
         lay = self.layer
         dev = dy.device

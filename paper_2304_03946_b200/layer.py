@@ -26,7 +26,8 @@ FIELDS = {
     "seg_rows": (9, np.int32), "totals": (10, np.int32), "send_rows": (11, np.int32),
     "recv_rows": (12, np.int32), "x_perm": (13, np.uint16), "act": (14, np.uint16),
     "y_perm": (15, np.uint16), "dy_perm": (16, np.uint16), "dh": (17, np.uint16),
-    "dx_perm": (18, np.uint16), "route_status": (19, np.int32),
+    "dx_perm": (18, np.uint16), "route_status": (19, np.int32), "kept": (20, np.int64),
+    "dropped": (21, np.int64),
 }
 
 
@@ -89,6 +90,11 @@ class MoELayer:
         L.check(L.lib().fm_layer_set_placement(self._h, cnt.ctypes.data))
         self.replica_counts = cnt.copy()
 
+    def set_capacity_factor(self, capacity_factor: float) -> None:
+        """StaticEP mode (baselines.cpp:81-131): > 0 drops units beyond capacity
+        (bit-exact with fm_static_ep_kept); 0 / inf = no drops (FlexMoE)."""
+        L.check(L.lib().fm_layer_set_capacity_factor(self._h, float(capacity_factor)))
+
     def init_params(self, seed=0, dtype=torch.bfloat16):
         """Random-init parameters of this layer's architecture (gate + local experts)."""
         g = torch.Generator(device="cpu").manual_seed(seed)
@@ -110,6 +116,7 @@ class MoELayer:
                                          b1.data_ptr(), w2.data_ptr(), b2.data_ptr(), y.data_ptr(),
                                          L.stream_ptr(stream)))
         self._saved = (T, x.device)
+        self._x_alive = x  # StaticEP backward re-reads the gate input of dropped units
         return y
 
     def backward(self, dy, grads: LayerGrads | None = None, stream=None) -> LayerGrads:

@@ -133,3 +133,63 @@ def test_layer_repeatable_and_deterministic_permutation():
     p2 = layer.read("unit_pos", T * k)
     assert (p1 == p2).all()
     assert torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("cf", [1.0, 1.25])
+def test_layer_static_ep_capacity_drops(cf):
+    """StaticEP mode: kept demand, dropped units and outputs vs the oracle
+    (whose static_ep_kept is pinned to the reference's run_static_ep)."""
+    import oracle
+
+    N, k, d, f, T = 8, 2, 256, 256, 3000
+    rng = np.random.default_rng(17)
+    p = 1.0 / np.arange(1, N + 1) ** 1.5
+    sk = np.log(p / p.sum())[rng.permutation(N)] + 3
+    x, wg, w1, b1, w2, b2 = OL.exact_inputs(rng, T, d, N, f, skew=sk)
+    st = OL.forward(x, wg, w1, b1, w2, b2, k, capacity_factor=cf)
+    dy = OL.bf16(rng.standard_normal((T, d)) * 0.5)
+    gr = OL.backward(st, dy)
+    kept_ref, dropped_ref = oracle.Oracle().static_ep_kept(st["hist"].reshape(N, 1), cf)
+    assert dropped_ref > 0
+
+    layer = MoELayer(N, k, d, f, max_tokens=T)
+    layer.set_capacity_factor(cf)
+    bf = torch.bfloat16
+    y = layer.forward(to_dev(x, bf), to_dev(wg, bf), to_dev(w1, bf), to_dev(b1, torch.float32),
+                      to_dev(w2, bf), to_dev(b2, torch.float32))
+    g = layer.backward(to_dev(dy, bf))
+    torch.cuda.synchronize()
+    assert (layer.read("kept", N).reshape(N, 1) == kept_ref).all()
+    assert layer.read("dropped", 1)[0] == dropped_ref
+    pos = layer.read("unit_pos", T * k).reshape(T, k)
+    assert (pos == st["pos"]).all(), "dropped / kept units differ"
+    assert ((pos < 0).sum()) == dropped_ref
+    close_bf16(y.float().cpu().numpy(), st["y"], "y")
+    close_bf16(g.dx.float().cpu().numpy(), gr["dx"], "dx")
+    close_f32(g.dw1.cpu().numpy(), gr["dw1"], "dw1")
+    close_f32(g.dw2.cpu().numpy(), gr["dw2"], "dw2")
+    close_f32(g.dwg.cpu().numpy(), gr["dwg"], "dwg", tol=2e-2)
+
+
+def test_static_ep_device_matches_reference_goldens():
+    """fm_static_ep_kept_device vs the reference's run_static_ep drop counts."""
+    import json
+    from pathlib import Path
+
+    from paper_2304_03946_b200 import _lib as L
+    from paper_2304_03946_b200 import routing
+
+    gold = json.loads((Path(__file__).parent / "golden" / "reference_golden.json").read_text())
+    for case in gold["static_ep"]:
+        for s, D in enumerate(case["trace"]):
+            D = np.array(D, np.int64)
+            N, G = D.shape
+            Dd = torch.tensor(D, device="cuda")
+            kept = torch.empty_like(Dd)
+            dropped = torch.zeros(1, dtype=torch.int64, device="cuda")
+            L.call("fm_static_ep_kept_device", Dd.data_ptr(), N, G, float(case["cf"]),
+                   kept.data_ptr(), dropped.data_ptr(), L.stream_ptr())
+            torch.cuda.synchronize()
+            kept_h, dropped_h = routing.static_ep_kept(D, case["cf"])
+            assert int(dropped.item()) == dropped_h == case["dropped"][s]
+            assert (kept.cpu().numpy() == kept_h).all()
