@@ -466,34 +466,60 @@ __global__ void segment_colsum_kernel(const __nv_bfloat16* __restrict__ buf, int
 __global__ void gate_wgrad_kernel(const __nv_bfloat16* __restrict__ buf, const int* __restrict__ rows_ptr,
                                   int rows_fixed, int d, const float* __restrict__ dl_rows,
                                   const int32_t* __restrict__ row_expert, float* __restrict__ dwg) {
+  // block: 256 rows x all d columns (blockDim = d/8); thread: one 16-B column
+  // vector. The expert sequence is uniform across the block, so flushes are
+  // block-wide: partial sums are transposed through smem and added with
+  // coalesced f32 atomics (one per column per run of an expert).
+  constexpr int kRows = 256, kBatch = 8;
+  extern __shared__ float flush_s[];  // [d]
   const int rows = rows_ptr ? *rows_ptr : rows_fixed;
-  const int r0 = blockIdx.x * 64;
+  const int r0 = blockIdx.x * kRows;
   if (r0 >= rows) return;
-  const int r1 = min(r0 + 64, rows);
-  const int c2 = (blockIdx.y * blockDim.x + threadIdx.x) * 2;
-  if (c2 >= d) return;
+  const int r1 = min(r0 + kRows, rows);
+  const int c8 = threadIdx.x * 8;
   int cur = -1;
-  float a0 = 0.0f, a1 = 0.0f;
-  for (int r = r0; r < r1; ++r) {
-    const int e = row_expert[r];
-    if (e != cur) {
-      if (cur >= 0) {
-        atomicAdd(dwg + static_cast<size_t>(cur) * d + c2, a0);
-        atomicAdd(dwg + static_cast<size_t>(cur) * d + c2 + 1, a1);
-      }
-      cur = e;
-      a0 = a1 = 0.0f;
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+  auto flush = [&]() {
+    if (cur < 0) return;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) flush_s[c8 + i] = acc[i];
+    __syncthreads();
+    float* o = dwg + static_cast<size_t>(cur) * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(o + c, flush_s[c]);
+    __syncthreads();
+  };
+  for (int rb = r0; rb < r1; rb += kBatch) {
+    int e[kBatch];
+    float g[kBatch];
+    uint4 v[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {  // all loads of the batch in flight together
+      const int r = min(rb + i, r1 - 1);
+      e[i] = __ldg(row_expert + r);
+      g[i] = __ldg(dl_rows + r);
+      v[i] = __ldg(reinterpret_cast<const uint4*>(buf + static_cast<size_t>(r) * d + c8));
     }
-    if (e < 0) continue;
-    const uint32_t v = *reinterpret_cast<const uint32_t*>(buf + static_cast<size_t>(r) * d + c2);
-    const float g = dl_rows[r];
-    a0 = fmaf(g, bf16lo(v), a0);
-    a1 = fmaf(g, bf16hi(v), a1);
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      if (rb + i >= r1) break;
+      if (e[i] != cur) {
+        flush();
+        cur = e[i];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = 0.0f;
+      }
+      if (e[i] < 0) continue;
+      const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        acc[2 * c] = fmaf(g[i], bf16lo(w[c]), acc[2 * c]);
+        acc[2 * c + 1] = fmaf(g[i], bf16hi(w[c]), acc[2 * c + 1]);
+      }
+    }
   }
-  if (cur >= 0) {
-    atomicAdd(dwg + static_cast<size_t>(cur) * d + c2, a0);
-    atomicAdd(dwg + static_cast<size_t>(cur) * d + c2 + 1, a1);
-  }
+  flush();
 }
 
 // Gate-weight gradient of units dropped by the capacity rule (in no dispatch
@@ -533,13 +559,24 @@ __global__ void demand_transpose_kernel(const int64_t* __restrict__ gathered_GN,
 // (fixed order: deterministic).
 __global__ void segment_tile_reduce_kernel(const float* __restrict__ partial, int cols, PlanDev p,
                                            float* __restrict__ out) {
+  // block: 32 columns x 8 tile lanes; lane j sums tiles t0+j, t0+j+8, ...; the
+  // eight partial sums are combined in fixed order (deterministic).
+  __shared__ float part[8][33];
   const int li = blockIdx.x;
-  const int col = blockIdx.y * blockDim.x + threadIdx.x;
-  if (col >= cols) return;
+  const int cx = threadIdx.x & 31, j = threadIdx.x >> 5;
+  const int col = blockIdx.y * 32 + cx;
   const int t0 = p.mtile_prefix[li], t1 = p.mtile_prefix[li + 1];
   float acc = 0.0f;
-  for (int t = t0; t < t1; ++t) acc += partial[static_cast<size_t>(t) * cols + col];
-  out[static_cast<size_t>(li) * cols + col] = acc;
+  if (col < cols)
+    for (int t = t0 + j; t < t1; t += 8) acc += __ldg(partial + static_cast<size_t>(t) * cols + col);
+  part[j][cx] = acc;
+  __syncthreads();
+  if (j == 0 && col < cols) {
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += part[i][cx];
+    out[static_cast<size_t>(li) * cols + col] = s;
+  }
 }
 
 }  // namespace
@@ -548,9 +585,9 @@ __global__ void segment_tile_reduce_kernel(const float* __restrict__ partial, in
 void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int max_rows, int d,
                        const float* dl_rows, const int32_t* row_expert, float* dwg, cudaStream_t s) {
   if (max_rows <= 0) return;
-  dim3 grid((max_rows + 63) / 64, (d / 2 + 255) / 256);
-  gate_wgrad_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(buf), rows_dev, rows_fixed,
-                                         d, dl_rows, row_expert, dwg);
+  gate_wgrad_kernel<<<(max_rows + 255) / 256, d / 8, d * 4, s>>>(static_cast<const __nv_bfloat16*>(buf),
+                                                           rows_dev, rows_fixed, d, dl_rows,
+                                                           row_expert, dwg);
   FM_LAUNCH_CHECK("gate_wgrad_kernel");
 }
 
@@ -571,7 +608,7 @@ void launch_demand_transpose(const int64_t* gathered_GN, int N, int G, int64_t* 
 void launch_segment_tile_reduce(const float* partial, int cols, const PlanDev& p, int Nl, float* out,
                                 cudaStream_t s) {
   if (Nl <= 0) return;
-  dim3 grid(Nl, (cols + 255) / 256);
+  dim3 grid(Nl, (cols + 31) / 32);
   segment_tile_reduce_kernel<<<grid, 256, 0, s>>>(partial, cols, p, out);
   FM_LAUNCH_CHECK("segment_tile_reduce_kernel");
 }

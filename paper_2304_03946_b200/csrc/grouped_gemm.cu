@@ -354,24 +354,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (!((mbits[c] >> i) & 1u)) v[i] = 0.0f;
-          if (args.colsum) {
-            // Column sums of the stored (bf16) values over this warp's 32 rows:
-            // transposed butterfly, lane l ends with column l of the chunk.
-            float cs[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) cs[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
-#pragma unroll
-            for (int sh = 16; sh >= 1; sh >>= 1) {
-              const bool up = (lane & sh) != 0;
-#pragma unroll
-              for (int i = 0; i < sh; ++i) {
-                const float send = up ? cs[i] : cs[i + sh];
-                const float keep = up ? cs[i + sh] : cs[i];
-                cs[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
-              }
-            }
-            colsum_s[(ab * 4 + q) * kBN + c * 32 + lane] = cs[0];
-          }
         }
         uint4 p[4];
 #pragma unroll
@@ -381,6 +363,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* buf = stage_begin();
         stage_row(buf, p);
         stage_commit(buf, col, tl.m0 + q * 32);
+        if (EPI == kEpiReluMask && args.colsum) {
+          // Column sums of the stored bf16 values over this warp's 32 rows, read
+          // back from the swizzled staging box: lanes 0-15 take rows 2i, lanes
+          // 16-31 rows 2i+1, two columns (one 32-bit word) each; conflict-free.
+          const int half = lane >> 4, pair = lane & 15;  // columns 2*pair, 2*pair+1
+          float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int r = 2 * i + half;
+            const int chunk = pair >> 2;  // 16-byte chunk holding this column pair
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(
+                buf + r * 64 + ((chunk ^ ((r >> 1) & 3)) << 4) + (pair & 3) * 4);
+            s0 += __uint_as_float(w << 16);
+            s1 += __uint_as_float(w & 0xFFFF0000u);
+          }
+          s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+          if (half == 0) {
+            float* dstc = colsum_s + (ab * 4 + q) * kBN + c * 32 + 2 * pair;
+            dstc[0] = s0;
+            dstc[1] = s1;
+          }
+        }
       };
       // TMEM reads double-buffered: chunk c+1 is in flight while c is processed.
       if (!empty_k) {
