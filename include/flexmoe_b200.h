@@ -90,6 +90,93 @@ int fm_static_ep_kept_device(const int64_t* demand_NG, int num_experts, int num_
                              void* stream);
 
 /* ------------------------------------------------------------------------
+ * Host placement scheduler — the consumer of the device histogram.
+ * Placements cross the ABI as the vExpert slot table slots_GE[g][s] = expert
+ * id or -1 (Placement::slot, placement.hpp:77), so slot-level ops are exact.
+ * ---------------------------------------------------------------------- */
+#define FM_MAX_GROUP 64
+/* ClusterTopology (proj/include/moesim/topology.hpp:27-94); all-reduce tables
+ * indexed by group size (entries below 2 unused). */
+typedef struct fm_cluster_profile {
+  int num_gpus;
+  int gpus_per_node;
+  int slots_per_gpu; /* vexperts_per_gpu */
+  double intra_node_bandwidth_bps;
+  double inter_node_bandwidth_bps;
+  double tps; /* tokens/s of one expert's fwd+bwd */
+  double expert_param_bytes;
+  double expert_state_bytes;
+  double token_bytes;
+  double allreduce_bps_intra[FM_MAX_GROUP + 1];
+  double allreduce_bps_inter[FM_MAX_GROUP + 1];
+} fm_cluster_profile;
+
+/* PlacementOp (placement.hpp:44-50): kind 0 Expand, 1 Shrink, 2 Migrate. */
+typedef struct fm_placement_op {
+  int kind;
+  int expert;
+  int gpu;
+  int a_gpu, a_slot, b_gpu, b_slot;
+} fm_placement_op;
+
+/* ClusterTopology::default_profile (topology.cpp:140-184). */
+int fm_profile_reference_default(int num_gpus, int slots_per_gpu, fm_cluster_profile* out);
+/* step_cost (cost_model.hpp:67 / cost_model.cpp:78-111): makespan and per-GPU
+ * {compute, a2a, sync} seconds of routing D on the placement. */
+int fm_step_cost(const int64_t* demand_NG, const int32_t* slots_GE, int num_experts,
+                 const fm_cluster_profile* profile, double* makespan, double* per_gpu_G3);
+/* make_scheduling_plan (policy.hpp:57 / policy.cpp:64-354). */
+int fm_make_scheduling_plan(const int64_t* demand_NG, const int32_t* slots_GE, int num_experts,
+                            const fm_cluster_profile* profile, int amortization_horizon,
+                            fm_placement_op* ops, int max_ops, int* n_ops);
+/* plan_migrations (policy.hpp:65 / policy.cpp:356-427). */
+int fm_plan_migrations(const int32_t* slots_GE, int num_experts, const fm_cluster_profile* profile,
+                       int amortization_horizon, fm_placement_op* ops, int max_ops, int* n_ops);
+/* Placement::apply (placement.hpp:104) on a slot table, in place; the implied
+ * TransferDescriptors (placement.hpp:31-35) as rows {src, dst, bytes}. */
+int fm_placement_apply(int32_t* slots_GE, int num_experts, const fm_cluster_profile* profile,
+                       const fm_placement_op* op, double* transfers_2x3, int* n_transfers);
+
+/* SimConfig (sim_engine.hpp:35-49). metric 0 MaxRatio / 1 Variance;
+ * policy_mode 0 Dynamic / 1 FixedInterval / 2 Static. */
+typedef struct fm_scheduler_config {
+  double threshold;
+  int metric;
+  int policy_mode;
+  int interval_steps;
+  int amortization_horizon;
+  double adjust_bandwidth_fraction;
+  int max_live_groups;
+  double group_creation_latency_s;
+} fm_scheduler_config;
+
+typedef struct fm_step_report {
+  double balance_ratio;
+  double metric_value;
+  double makespan_s; /* modelled, effective placement */
+  double adjust_s;
+  double adjust_bytes;
+  int group_misses;
+  int n_accepted; /* ops accepted into the adjustment queue (target placement) */
+  int n_applied;  /* ops that became effective at the start of this step */
+  int pending_ops;
+} fm_step_report;
+
+typedef struct fm_scheduler fm_scheduler;
+/* The Alg. 1 step driver (SimEngine::run_step, sim_engine.cpp:329-449):
+ * best-effort drain of the adjustment queue, route on the effective
+ * placement, trigger, policy loop on the target placement, one migration. */
+int fm_scheduler_create(const fm_cluster_profile* profile, const fm_scheduler_config* cfg,
+                        int num_experts, fm_scheduler** out);
+int fm_scheduler_destroy(fm_scheduler* s);
+int fm_scheduler_step(fm_scheduler* s, const int64_t* demand_NG, fm_step_report* out);
+/* which: 0 = ops accepted this step, 1 = ops applied (made effective) this step */
+int fm_scheduler_ops(fm_scheduler* s, int which, fm_placement_op* ops, int max_ops, int* n_ops);
+/* which: 0 = effective placement, 1 = target placement */
+int fm_scheduler_placement(fm_scheduler* s, int which, int32_t* slots_GE, int32_t* counts_NG);
+int fm_scheduler_reset(fm_scheduler* s, const int32_t* slots_GE);
+
+/* ------------------------------------------------------------------------
  * Grouped expert GEMM on tcgen05 (test / building-block hook).
  * seg_start, seg_rows, tile_prefix are device int32 arrays describing the
  * per-group token segments of the permuted buffers (rows multiple of 128).

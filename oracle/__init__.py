@@ -148,6 +148,12 @@ class Reference(_Base):
             C.c_int,
         ),
         "ref_time_route": ([_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P], C.c_int),
+        "ref_step_cost": ([_P, _P, C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
+        "ref_plan_migrations": ([_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
+        "ref_engine_detail": (
+            [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, C.c_int],
+            C.c_int,
+        ),
     }
 
     @staticmethod
@@ -208,6 +214,33 @@ class Reference(_Base):
         n = np.zeros(1, np.int32)
         self._check(self.lib.ref_make_scheduling_plan(_p(D), _p(cnt), N, G, slots, horizon, _p(ops), _p(n), 16))
         return ops[: n[0]]
+
+    def step_cost(self, D, cnt, slots):
+        D, cnt = _i64(D), _i32(cnt)
+        N, G = D.shape
+        mk = np.zeros(1)
+        per = np.zeros((G, 3))
+        self._check(self.lib.ref_step_cost(_p(D), _p(cnt), N, G, slots, _p(mk), _p(per)))
+        return float(mk[0]), per
+
+    def plan_migrations(self, cnt, slots, horizon=50):
+        cnt = _i32(cnt)
+        N, G = cnt.shape
+        ops = np.zeros((4, 7), np.int32)
+        n = np.zeros(1, np.int32)
+        self._check(self.lib.ref_plan_migrations(_p(cnt), N, G, slots, horizon, _p(ops), _p(n)))
+        return ops[: n[0]]
+
+    def engine_detail(self, trace, slots, policy_mode=0, interval=10, metric=0, max_ops=64):
+        trace = _i64(trace)
+        S, N, G = trace.shape
+        mk = np.zeros(S)
+        ab = np.zeros(S)
+        n = np.zeros(S, np.int32)
+        ops = np.zeros((S, max_ops, 7), np.int32)
+        self._check(self.lib.ref_engine_detail(_p(trace), S, N, G, slots, policy_mode, interval, metric,
+                                               _p(mk), _p(ab), _p(n), _p(ops), max_ops))
+        return mk, ab, [ops[s, : n[s]] for s in range(S)]
 
     def time_route(self, D, cnt, slots=None, iters=1000):
         D, cnt = _i64(D), _i32(cnt)

@@ -185,6 +185,78 @@ int ref_make_scheduling_plan(const int64_t* D, const int32_t* cnt, int N, int G,
   });
 }
 
+int ref_step_cost(const int64_t* D, const int32_t* cnt, int N, int G, int slots, double* makespan,
+                  double* per_gpu) {
+  return guarded([&] {
+    ClusterTopology topo = ClusterTopology::from_json(ClusterTopology::default_profile(G, slots));
+    TokenDemand d = to_demand(D, N, G);
+    Placement p = to_placement(cnt, N, G, slots);
+    StepCostBreakdown b = step_cost(d, p, route(d, p), topo);
+    *makespan = b.makespan_s;
+    for (int g = 0; g < G; ++g) {
+      per_gpu[3 * g] = b.per_gpu[g].compute_s;
+      per_gpu[3 * g + 1] = b.per_gpu[g].a2a_s;
+      per_gpu[3 * g + 2] = b.per_gpu[g].sync_s;
+    }
+  });
+}
+
+int ref_plan_migrations(const int32_t* cnt, int N, int G, int slots, int horizon, int32_t* ops,
+                        int* n_ops) {
+  return guarded([&] {
+    ClusterTopology topo = ClusterTopology::from_json(ClusterTopology::default_profile(G, slots));
+    PolicyConfig pc;
+    pc.amortization_horizon = horizon;
+    SchedulingPlan plan = plan_migrations(to_placement(cnt, N, G, slots), topo, pc);
+    int n = 0;
+    for (const PlacementOp& op : plan.ops) {
+      int32_t* o = ops + 7 * n++;
+      o[0] = static_cast<int>(op.kind);
+      o[1] = op.expert;
+      o[2] = op.gpu;
+      o[3] = op.a.gpu;
+      o[4] = op.a.slot;
+      o[5] = op.b.gpu;
+      o[6] = op.b.slot;
+    }
+    *n_ops = n;
+  });
+}
+
+// The engine with per-step detail: makespan, adjust bytes, accepted ops
+// [kind, expert, gpu, a.gpu, a.slot, b.gpu, b.slot] (up to max_ops per step).
+int ref_engine_detail(const int64_t* trace, int steps, int N, int G, int slots, int policy_mode,
+                      int interval, int metric, double* makespan, double* adjust_bytes,
+                      int32_t* n_ops, int32_t* ops, int max_ops) {
+  return guarded([&] {
+    std::vector<TokenDemand> tr = to_trace(trace, steps, N, G);
+    ClusterTopology topo = ClusterTopology::from_json(ClusterTopology::default_profile(G, slots));
+    SimConfig sc;
+    sc.policy_mode = static_cast<PolicyMode>(policy_mode);
+    sc.interval_steps = interval;
+    sc.metric = static_cast<BalanceMetric>(metric);
+    std::vector<StepReport> reps = run_simulation(tr, topo, sc);
+    for (int s = 0; s < steps; ++s) {
+      makespan[s] = reps[s].makespan_s;
+      adjust_bytes[s] = static_cast<double>(reps[s].adjust_bytes);
+      int n = 0;
+      for (const PlacementOp& op : reps[s].plan_applied) {
+        if (n >= max_ops) break;
+        int32_t* o = ops + (static_cast<size_t>(s) * max_ops + n) * 7;
+        o[0] = static_cast<int>(op.kind);
+        o[1] = op.expert;
+        o[2] = op.gpu;
+        o[3] = op.a.gpu;
+        o[4] = op.a.slot;
+        o[5] = op.b.gpu;
+        o[6] = op.b.slot;
+        ++n;
+      }
+      n_ops[s] = static_cast<int32_t>(reps[s].plan_applied.size());
+    }
+  });
+}
+
 // CPU-baseline timing of the reference's per-step count-level path:
 // `iters` calls of route() + balance_ratio() on the same inputs; returns
 // seconds per call.

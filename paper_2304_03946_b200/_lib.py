@@ -88,6 +88,17 @@ _SIGNATURES = {
     "fm_layer_backward": [_P] * 9,
     "fm_layer_copy_out": [_P, _I, _P, C.c_size_t, C.POINTER(C.c_size_t)],
     "fm_layer_set_timing": [_P, _I],
+    "fm_profile_reference_default": [_I, _I, _P],
+    "fm_step_cost": [_P, _P, _I, _P, _P, _P],
+    "fm_make_scheduling_plan": [_P, _P, _I, _P, _I, _P, _I, _P],
+    "fm_plan_migrations": [_P, _I, _P, _I, _P, _I, _P],
+    "fm_placement_apply": [_P, _I, _P, _P, _P, _P],
+    "fm_scheduler_create": [_P, _P, _I, _P],
+    "fm_scheduler_destroy": [_P],
+    "fm_scheduler_step": [_P, _P, _P],
+    "fm_scheduler_ops": [_P, _I, _P, _I, _P],
+    "fm_scheduler_placement": [_P, _I, _P, _P],
+    "fm_scheduler_reset": [_P, _P],
     "fm_layer_gate": [_P, _P, _I, _P, _P, _P],
     "fm_layer_route": [_P, _P, _P, _P, _P],
     "fm_layer_dispatch": [_P, _P, _P, _P],

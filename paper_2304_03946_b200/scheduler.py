@@ -1,0 +1,196 @@
+"""Host placement scheduler (C ABI in libflexmoe_b200.so).
+
+Mirrors the reference's policy layer on numpy arrays: the cluster profile
+(ClusterTopology), the vExpert slot table (Placement), step_cost,
+make_scheduling_plan, plan_migrations, Placement::apply, and the Alg. 1 step
+driver with its adjustment queue (SimEngine::run_step). It consumes the
+TokenDemand the device gate produces each step.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+
+MAX_GROUP = 64
+EXPAND, SHRINK, MIGRATE = 0, 1, 2
+
+
+class ClusterProfile(C.Structure):
+    _fields_ = [("num_gpus", C.c_int), ("gpus_per_node", C.c_int), ("slots_per_gpu", C.c_int),
+                ("intra_node_bandwidth_bps", C.c_double), ("inter_node_bandwidth_bps", C.c_double),
+                ("tps", C.c_double), ("expert_param_bytes", C.c_double),
+                ("expert_state_bytes", C.c_double), ("token_bytes", C.c_double),
+                ("allreduce_bps_intra", C.c_double * (MAX_GROUP + 1)),
+                ("allreduce_bps_inter", C.c_double * (MAX_GROUP + 1))]
+
+    @classmethod
+    def reference_default(cls, num_gpus, slots_per_gpu):
+        """ClusterTopology::default_profile (topology.cpp:140-184), A100-like."""
+        p = cls()
+        L.check(L.lib().fm_profile_reference_default(num_gpus, slots_per_gpu, C.byref(p)))
+        return p
+
+    @classmethod
+    def b200(cls, num_gpus, slots_per_gpu, tps, expert_param_bytes, expert_state_bytes, token_bytes,
+             link_bps=770e9, allreduce_bus_bps=725e9):
+        """One NVSwitch node of B200s: uniform peers (NVLink 5, measured 770 GB/s
+        per direction), all-reduce throughput from the measured bus bandwidth."""
+        p = cls()
+        p.num_gpus, p.gpus_per_node, p.slots_per_gpu = num_gpus, num_gpus, slots_per_gpu
+        p.intra_node_bandwidth_bps = link_bps
+        p.inter_node_bandwidth_bps = link_bps
+        p.tps, p.expert_param_bytes = tps, expert_param_bytes
+        p.expert_state_bytes, p.token_bytes = expert_state_bytes, token_bytes
+        for n in range(2, num_gpus + 1):  # algorithm bandwidth = bus bandwidth * n / (2(n-1))
+            p.allreduce_bps_intra[n] = allreduce_bus_bps * n / (2.0 * (n - 1))
+        return p
+
+
+class PlacementOp(C.Structure):
+    _fields_ = [("kind", C.c_int), ("expert", C.c_int), ("gpu", C.c_int), ("a_gpu", C.c_int),
+                ("a_slot", C.c_int), ("b_gpu", C.c_int), ("b_slot", C.c_int)]
+
+    def as_tuple(self):
+        return (self.kind, self.expert, self.gpu, self.a_gpu, self.a_slot, self.b_gpu, self.b_slot)
+
+
+class SchedulerConfig(C.Structure):
+    _fields_ = [("threshold", C.c_double), ("metric", C.c_int), ("policy_mode", C.c_int),
+                ("interval_steps", C.c_int), ("amortization_horizon", C.c_int),
+                ("adjust_bandwidth_fraction", C.c_double), ("max_live_groups", C.c_int),
+                ("group_creation_latency_s", C.c_double)]
+
+    @classmethod
+    def defaults(cls, **kw):
+        """SimConfig defaults (sim_engine.hpp:35-49)."""
+        c = cls(1.1, 0, 0, 10, 50, 0.5, 64, 0.005)
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+
+
+class StepReport(C.Structure):
+    _fields_ = [("balance_ratio", C.c_double), ("metric_value", C.c_double), ("makespan_s", C.c_double),
+                ("adjust_s", C.c_double), ("adjust_bytes", C.c_double), ("group_misses", C.c_int),
+                ("n_accepted", C.c_int), ("n_applied", C.c_int), ("pending_ops", C.c_int)]
+
+
+def slots_from_counts(counts, slots_per_gpu):
+    """Placement::from_counts slot fill (placement.cpp:74-107): per GPU, experts
+    ascending, each taking its count of consecutive slots."""
+    cnt = np.asarray(counts, np.int32)
+    N, G = cnt.shape
+    slots = -np.ones((G, slots_per_gpu), np.int32)
+    for g in range(G):
+        s = 0
+        for e in range(N):
+            for _ in range(cnt[e, g]):
+                slots[g, s] = e
+                s += 1
+    return slots
+
+
+def counts_from_slots(slots, num_experts):
+    slots = np.asarray(slots)
+    G = slots.shape[0]
+    cnt = np.zeros((num_experts, G), np.int32)
+    for g in range(G):
+        for e in slots[g]:
+            if e >= 0:
+                cnt[e, g] += 1
+    return cnt
+
+
+def _ops(buf, n):
+    return [buf[i].as_tuple() for i in range(n.value)]
+
+
+def step_cost(D, slots, prof: ClusterProfile):
+    D = np.ascontiguousarray(D, np.int64)
+    slots = np.ascontiguousarray(slots, np.int32)
+    mk = C.c_double()
+    per = np.zeros((prof.num_gpus, 3))
+    L.check(L.lib().fm_step_cost(D.ctypes.data, slots.ctypes.data, D.shape[0], C.byref(prof),
+                                 C.byref(mk), per.ctypes.data))
+    return mk.value, per
+
+
+def make_scheduling_plan(D, slots, prof: ClusterProfile, horizon=50):
+    D = np.ascontiguousarray(D, np.int64)
+    slots = np.ascontiguousarray(slots, np.int32)
+    buf = (PlacementOp * 16)()
+    n = C.c_int()
+    L.check(L.lib().fm_make_scheduling_plan(D.ctypes.data, slots.ctypes.data, D.shape[0], C.byref(prof),
+                                            horizon, buf, 16, C.byref(n)))
+    return _ops(buf, n)
+
+
+def plan_migrations(slots, num_experts, prof: ClusterProfile, horizon=50):
+    slots = np.ascontiguousarray(slots, np.int32)
+    buf = (PlacementOp * 4)()
+    n = C.c_int()
+    L.check(L.lib().fm_plan_migrations(slots.ctypes.data, num_experts, C.byref(prof), horizon, buf, 4,
+                                       C.byref(n)))
+    return _ops(buf, n)
+
+
+def apply_op(slots, num_experts, prof: ClusterProfile, op):
+    """Returns (new slot table, transfers [(src, dst, bytes)])."""
+    s = np.ascontiguousarray(slots, np.int32).copy()
+    o = PlacementOp(*op)
+    t = np.zeros((2, 3))
+    n = C.c_int()
+    L.check(L.lib().fm_placement_apply(s.ctypes.data, num_experts, C.byref(prof), C.byref(o),
+                                       t.ctypes.data, C.byref(n)))
+    return s, [(int(a), int(b), float(c)) for a, b, c in t[: n.value]]
+
+
+@dataclass
+class StepResult:
+    report: StepReport
+    accepted: list
+    applied: list
+
+
+class Scheduler:
+    """SimEngine::run_step driver over device-produced demand."""
+
+    def __init__(self, prof: ClusterProfile, num_experts: int, cfg: SchedulerConfig | None = None):
+        self.prof, self.N = prof, num_experts
+        self.cfg = cfg or SchedulerConfig.defaults()
+        h = C.c_void_p()
+        L.check(L.lib().fm_scheduler_create(C.byref(prof), C.byref(self.cfg), num_experts, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            L.lib().fm_scheduler_destroy(self._h)
+            self._h = None
+
+    def step(self, D) -> StepResult:
+        D = np.ascontiguousarray(D, np.int64)
+        rep = StepReport()
+        L.check(L.lib().fm_scheduler_step(self._h, D.ctypes.data, C.byref(rep)))
+        return StepResult(rep, self._ops(0, rep.n_accepted), self._ops(1, rep.n_applied))
+
+    def _ops(self, which, n):
+        buf = (PlacementOp * max(n, 1))()
+        got = C.c_int()
+        L.check(L.lib().fm_scheduler_ops(self._h, which, buf, max(n, 1), C.byref(got)))
+        return _ops(buf, got)
+
+    def placement(self, which="effective"):
+        G, E = self.prof.num_gpus, self.prof.slots_per_gpu
+        slots = np.zeros((G, E), np.int32)
+        counts = np.zeros((self.N, G), np.int32)
+        L.check(L.lib().fm_scheduler_placement(self._h, 0 if which == "effective" else 1,
+                                               slots.ctypes.data, counts.ctypes.data))
+        return slots, counts
+
+    def reset(self, slots):
+        s = np.ascontiguousarray(slots, np.int32)
+        L.check(L.lib().fm_scheduler_reset(self._h, s.ctypes.data))
