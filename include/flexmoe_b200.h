@@ -170,6 +170,12 @@ int fm_scheduler_create(const fm_cluster_profile* profile, const fm_scheduler_co
                         int num_experts, fm_scheduler** out);
 int fm_scheduler_destroy(fm_scheduler* s);
 int fm_scheduler_step(fm_scheduler* s, const int64_t* demand_NG, fm_step_report* out);
+/* The same step in two halves, for a runtime that routes on the device in
+ * between: begin = best-effort drain (ops whose transfers completed become
+ * effective; switch the layer's placement before routing), finish = the rest
+ * on the step's demand. begin + finish == step. */
+int fm_scheduler_begin_step(fm_scheduler* s, fm_step_report* out);
+int fm_scheduler_finish_step(fm_scheduler* s, const int64_t* demand_NG, fm_step_report* out);
 /* which: 0 = ops accepted this step, 1 = ops applied (made effective) this step */
 int fm_scheduler_ops(fm_scheduler* s, int which, fm_placement_op* ops, int max_ops, int* n_ops);
 /* which: 0 = effective placement, 1 = target placement */

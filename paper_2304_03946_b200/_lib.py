@@ -96,6 +96,8 @@ _SIGNATURES = {
     "fm_scheduler_create": [_P, _P, _I, _P],
     "fm_scheduler_destroy": [_P],
     "fm_scheduler_step": [_P, _P, _P],
+    "fm_scheduler_begin_step": [_P, _P],
+    "fm_scheduler_finish_step": [_P, _P, _P],
     "fm_scheduler_ops": [_P, _I, _P, _I, _P],
     "fm_scheduler_placement": [_P, _I, _P, _P],
     "fm_scheduler_reset": [_P, _P],

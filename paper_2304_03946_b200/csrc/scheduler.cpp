@@ -666,11 +666,24 @@ double Scheduler::trigger(const std::vector<int64_t>& flows, int N) const {
 }
 
 StepOutcome Scheduler::step(const std::vector<int64_t>& D) {
-  const int N = effective_.experts(), G = effective_.gpus();
-  StepOutcome out;
+  begin_step();
+  return finish_step(D);
+}
+
+const StepOutcome& Scheduler::begin_step() {
   // 1. transfers that overlapped the previous step land (best-effort budget)
-  out.applied = queue_.drain(cfg_.adjust_bandwidth_fraction * prev_makespan_, prof_, effective_,
-                             out.adjust_bytes, out.adjust_seconds);
+  cur_ = StepOutcome{};
+  cur_.applied = queue_.drain(cfg_.adjust_bandwidth_fraction * prev_makespan_, prof_, effective_,
+                              cur_.adjust_bytes, cur_.adjust_seconds);
+  begun_ = true;
+  return cur_;
+}
+
+StepOutcome Scheduler::finish_step(const std::vector<int64_t>& D) {
+  if (!begun_) throw std::logic_error("scheduler: finish_step without begin_step");
+  begun_ = false;
+  const int N = effective_.experts(), G = effective_.gpus();
+  StepOutcome out = cur_;
   // 2. the step on the effective placement
   const std::vector<int64_t> flows = flows_for(D, effective_);
   StepTime st = step_time(D, effective_, flows, prof_);

@@ -188,6 +188,11 @@ class Scheduler {
  public:
   Scheduler(const ClusterProfile& prof, const SchedulerConfig& cfg, int num_experts);
   StepOutcome step(const std::vector<int64_t>& D);
+  // step() in two halves: the drain (ops that become effective at the step
+  // boundary, before the device routes) and the rest, once the step's
+  // demand is known.
+  const StepOutcome& begin_step();
+  StepOutcome finish_step(const std::vector<int64_t>& D);
   const SlotPlacement& effective() const { return effective_; }
   const SlotPlacement& target() const { return target_; }
   const TransferQueue& queue() const { return queue_; }
@@ -202,6 +207,8 @@ class Scheduler {
   GroupLru lru_;
   double prev_makespan_ = 0;
   int step_ = 0;
+  StepOutcome cur_;
+  bool begun_ = false;
 };
 
 }  // namespace sched

@@ -170,6 +170,38 @@ int fm_scheduler_step(fm_scheduler* h, const int64_t* D, fm_step_report* out) {
   });
 }
 
+int fm_scheduler_begin_step(fm_scheduler* h, fm_step_report* out) {
+  return fm::guarded([&] {
+    const StepOutcome& o = h->s->begin_step();
+    h->last = o;
+    if (out) {
+      std::memset(out, 0, sizeof(*out));
+      out->adjust_s = o.adjust_seconds;
+      out->adjust_bytes = o.adjust_bytes;
+      out->n_applied = static_cast<int>(o.applied.size());
+      out->pending_ops = static_cast<int>(h->s->queue().size());
+    }
+  });
+}
+
+int fm_scheduler_finish_step(fm_scheduler* h, const int64_t* D, fm_step_report* out) {
+  return fm::guarded([&] {
+    const int N = h->s->effective().experts(), G = h->s->effective().gpus();
+    h->last = h->s->finish_step(demand(D, N, G));
+    if (out) {
+      out->balance_ratio = h->last.balance_ratio;
+      out->metric_value = h->last.metric_value;
+      out->makespan_s = h->last.makespan;
+      out->adjust_s = h->last.adjust_seconds;
+      out->adjust_bytes = h->last.adjust_bytes;
+      out->group_misses = h->last.group_misses;
+      out->n_accepted = static_cast<int>(h->last.accepted.size());
+      out->n_applied = static_cast<int>(h->last.applied.size());
+      out->pending_ops = static_cast<int>(h->s->queue().size());
+    }
+  });
+}
+
 int fm_scheduler_ops(fm_scheduler* h, int which, fm_placement_op* ops, int max_ops, int* n_ops) {
   return fm::guarded([&] {
     copy_ops(which == 0 ? h->last.accepted : h->last.applied, ops, max_ops, n_ops);

@@ -177,6 +177,19 @@ class Scheduler:
         L.check(L.lib().fm_scheduler_step(self._h, D.ctypes.data, C.byref(rep)))
         return StepResult(rep, self._ops(0, rep.n_accepted), self._ops(1, rep.n_applied))
 
+    def begin_step(self) -> list:
+        """Drain half: returns the ops that became effective at this boundary."""
+        rep = StepReport()
+        L.check(L.lib().fm_scheduler_begin_step(self._h, C.byref(rep)))
+        self._begin = rep
+        return self._ops(1, rep.n_applied)
+
+    def finish_step(self, D) -> StepResult:
+        D = np.ascontiguousarray(D, np.int64)
+        rep = StepReport()
+        L.check(L.lib().fm_scheduler_finish_step(self._h, D.ctypes.data, C.byref(rep)))
+        return StepResult(rep, self._ops(0, rep.n_accepted), self._ops(1, rep.n_applied))
+
     def _ops(self, which, n):
         buf = (PlacementOp * max(n, 1))()
         got = C.c_int()

@@ -144,3 +144,16 @@ def test_engine_matches_reference(case):
         n_ops += len(r.accepted)
     if mode != 2:
         assert n_ops > 0
+
+
+def test_split_step_equals_step():
+    tr = oracle.Oracle().generate_trace(16, 4, 16384, zipf=1.5, seed=3, steps=40)
+    a = S.Scheduler(S.ClusterProfile.reference_default(4, 8), 16)
+    b = S.Scheduler(S.ClusterProfile.reference_default(4, 8), 16)
+    for s in range(40):
+        ra = a.step(tr[s])
+        applied = b.begin_step()
+        rb = b.finish_step(tr[s])
+        assert applied == ra.applied == rb.applied
+        assert ra.accepted == rb.accepted
+        assert ra.report.makespan_s == rb.report.makespan_s
