@@ -129,6 +129,11 @@ class Exchange:
         """Called on EVERY rank, in ascending expert id, for every replica group
         (group creation is collective over the world in torch.distributed)."""
 
+    def p2p(self, sends: list, recvs: list) -> None:
+        """Point-to-point copies: sends [(dst, tensor)], recvs [(src, tensor)],
+        matched per (src, dst) pair in list order. Called by every rank."""
+        raise NotImplementedError
+
 
 class TorchExchange(Exchange):
     """torch.distributed transport (NCCL on B200 / NVLink; gloo on CPU)."""
@@ -154,6 +159,13 @@ class TorchExchange(Exchange):
 
     def sync_group(self, group):
         self.groups.touch(group)
+
+    def p2p(self, sends, recvs):
+        ops = [self.dist.P2POp(self.dist.isend, t.contiguous(), dst) for dst, t in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, t, src) for src, t in recvs]
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
 
     def all_reduce(self, t, group):
         if group is None:
@@ -205,6 +217,18 @@ class LoopbackExchange(Exchange):
     def sync_group(self, group):
         if self.rank == 0:
             self.hub.groups.touch(group)
+
+    def p2p(self, sends, recvs):
+        allsends = self._swap(sends)
+        inbox: dict[int, list] = {}
+        for src in range(self.world):
+            inbox[src] = [t for dst, t in allsends[src] if dst == self.rank]
+        taken: dict[int, int] = {}
+        for src, t in recvs:
+            i = taken.get(src, 0)
+            t.copy_(inbox[src][i])
+            taken[src] = i + 1
+        self._swap(None)  # senders keep their tensors alive until copied
 
     def all_reduce(self, t, group):
         members = range(self.world) if group is None else group
