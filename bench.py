@@ -249,47 +249,66 @@ class FusedArm:
 
 
 class DistArm:
-    """configs[2]: one process per GPU, NCCL all-to-all / all-reduce between phases."""
+    """configs[2]: one process per GPU, NCCL all-to-all / all-reduce between phases,
+    drifting Zipf traffic, dynamic expand/shrink/migrate by the host scheduler with
+    peer-to-peer migration of expert state inside the timed region."""
 
     def __init__(self, cfg, dev, rank, world):
         import torch
 
-        from paper_2304_03946_b200.distributed import DistributedMoELayer, LoopbackHub, TorchExchange
-        from paper_2304_03946_b200.layer import MoELayer
+        from paper_2304_03946_b200 import scheduler as S
+        from paper_2304_03946_b200.distributed import LoopbackHub, TorchExchange
+        from paper_2304_03946_b200.runtime import FlexMoERuntime
 
         N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
         G = world
-        slots = 2 * ((N + G - 1) // G)
-        cnt = np.zeros((N, G), np.int32)
-        cnt[np.arange(N), np.arange(N) % G] = 1  # Placement::initial (round robin)
-        self.layer = MoELayer(N, k, d, f, replica_counts=cnt, num_gpus=G, rank=rank, max_tokens=T,
-                              slots_per_gpu=slots)
+        slots = 2 * ((N + G - 1) // G)  # vExpert budget 2*ceil(N/G) (moesim.cpp:141-146)
+        params = 2 * d * f + d + f
+        # B200 profile: NVLink 5 link / NCCL bus bandwidth (B200_PROFILING.md), expert
+        # throughput from the grouped GEMM (12*d*f FLOP per unit at ~1.2 PFLOP/s),
+        # f32 gradients, 14 B/param of state (bf16 + f32 master + Adam m, v).
+        prof = S.ClusterProfile.b200(G, slots, tps=1.2e15 / (12.0 * d * f),
+                                     expert_param_bytes=4.0 * params,
+                                     expert_state_bytes=14.0 * params, token_bytes=2.0 * d)
         ex = TorchExchange() if world > 1 else LoopbackHub(1).endpoint(0)
-        self.dl = DistributedMoELayer(self.layer, ex)
         g = torch.Generator(device="cpu").manual_seed(1234)
         wg = torch.randn(N, d, generator=g) * d**-0.5
-        wg[:, 0] = torch.tensor(zipf_log_popularity(N, cfg["zipf"], 42) * 2, dtype=torch.float32)
-        loc = self.layer.local_experts
-
-        def expert_params(e):  # identical on every replica: seeded by expert id
-            ge = torch.Generator(device="cpu").manual_seed(10_000 + e)
-            return (torch.randn(f, d, generator=ge) * d**-0.5, torch.randn(f, generator=ge) * 0.02,
-                    torch.randn(d, f, generator=ge) * f**-0.5, torch.randn(d, generator=ge) * 0.02)
-
-        ps = [expert_params(e) for e in loc]
-        st = lambda i: torch.stack([p[i] for p in ps]).to(dev)
-        bf = torch.bfloat16
-        self.P = (wg.to(bf).to(dev), st(0).to(bf), st(1).float(), st(2).to(bf), st(3).float())
+        self.logp = zipf_log_popularity(N, cfg["zipf"], 42)
+        wg[:, 0] = torch.tensor(self.logp * 2, dtype=torch.float32)
+        self.rt = FlexMoERuntime(N, k, d, f, ex, prof, max_tokens=T, gate_weight=wg, optimizer=False)
+        self.layer, self.dl = self.rt.layer, self.rt.dl
+        self.drift = np.random.default_rng(42)  # same walk on every rank
         self.N, self.G = N, G
         self.kernels_per_step = 9 + 8 + (2 if k > 1 else 1) + 4 + 1  # + relayouts, transpose
+        self.reset_stats()
+
+    def reset_stats(self):
+        self.mig_bytes = 0
+        self.mig_ms = 0.0
+        self.applied = 0
+        self.accepted = 0
+        self.ratios = []
 
     def step(self, x, dy):
-        self.dl.forward(x, *self.P)
-        self.dl.backward(dy)
+        import torch
+
+        # drifting popularity (workload.cpp:164-170: p *= exp(U[-0.02, 0.02]), renormalised),
+        # applied through the gate's skew column
+        self.logp = self.logp + self.drift.uniform(-0.02, 0.02, self.N)
+        self.logp -= np.log(np.exp(self.logp).sum())
+        self.rt.wg[:, 0] = torch.tensor(self.logp * 2, dtype=torch.float32).to(self.rt.wg)
+        out = self.rt.step(x, dy)
+        self.mig_bytes += out.migration_bytes
+        self.mig_ms += out.migration_ms
+        self.applied += len(out.applied)
+        self.accepted += len(out.accepted)
+        self.ratios.append(out.balance_ratio)
 
     def set_timing(self, on):
         self.layer.set_timing(on)
         self.dl.set_timing(on)
+        if on:
+            self.reset_stats()
 
     def timing(self):
         return self.layer.read_timing(), self.dl.read_timing()
@@ -299,6 +318,15 @@ class DistArm:
 
     def hist(self):
         return self.layer.read("hist", self.N)
+
+    def summary(self, steps):
+        return {"placement": "dynamic (host scheduler: expand/shrink/migrate, B200 profile)",
+                "balance_ratio_mean": float(np.mean(self.ratios)) if self.ratios else None,
+                "balance_ratio_last": self.ratios[-1] if self.ratios else None,
+                "ops_accepted": self.accepted, "ops_applied": self.applied,
+                "migration_bytes_per_step": self.mig_bytes / steps,
+                "migration_ms_per_step": self.mig_ms / steps,
+                "replica_counts": self.rt.history[-1].replica_counts.tolist() if self.rt.history else None}
 
 
 def run_ours(args, world, rank, local_rank):
@@ -345,6 +373,7 @@ def run_ours(args, world, rank, local_rank):
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     phases, comm = arm.timing()
+    dyn = arm.summary(args.steps) if multi else None
     arm.set_timing(False)
     if dist:
         t = torch.tensor([ms], device=dev)
@@ -455,7 +484,7 @@ def run_ours(args, world, rank, local_rank):
                    "parallelism": f"ep{world}" + ("+replicas" if multi else ""),
                    "zipf": cfg["zipf"], "units_per_step_rank0": units,
                    "expert_load_max_over_mean": float(hist.max() / max(hist.mean(), 1e-9)),
-                   "placement": "static (Placement::initial round robin)" if multi else "static",
+                   "placement": "dynamic" if multi else "static",
                    "l2": "per-step working set > L2 (no flush)"},
         "e2e": {"value": T * world / (e2e_ms * 1e-3 / args.steps), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(2 * T * d * 2), "d2h_bytes_per_step": int(N * 8)},
@@ -469,6 +498,8 @@ def run_ours(args, world, rank, local_rank):
         "clocks": clocks.summary(),
         "balance_ratio": balance,
     }
+    if multi:
+        line["dynamic_placement"] = dyn
     if world == 1 and not multi and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg)

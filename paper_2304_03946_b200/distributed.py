@@ -311,6 +311,9 @@ class DistributedMoELayer:
         self._call("fm_layer_route", gathered.data_ptr(), send_rows.ctypes.data, recv_rows.ctypes.data,
                    stream)
         send_rows, recv_rows = send_rows.tolist(), recv_rows.tolist()
+        # fm_layer_route synchronised the stream: the demand is final, take the
+        # host copy for the placement scheduler now (no extra sync later)
+        self.last_demand_host = gathered.cpu().numpy().T.copy()  # TokenDemand [N][G]
         bf = torch.bfloat16
         send = torch.empty(max(T * k, 1), d, dtype=bf, device=dev)
         recv = torch.empty(max(sum(recv_rows), 1), d, dtype=bf, device=dev)

@@ -178,7 +178,7 @@ class FlexMoERuntime:
         mig_bytes, mig_ms = self._apply(applied) if applied else (0, 0.0)
         w1, b1, w2, b2 = self.packed
         y = self.dl.forward(x, self.wg, w1, b1, w2, b2)
-        D = self.dl.last_demand.cpu().numpy().T.copy()  # TokenDemand [N][G]
+        D = self.dl.last_demand_host  # TokenDemand [N][G], copied when routing synchronised
         grads = self.dl.backward(dy)
         if self.optimizer and self.layer.local_experts:
             self.store.adam_step(self.layer.local_experts, grads)
