@@ -198,6 +198,10 @@ int fm_scheduler_reset(fm_scheduler* s, const int32_t* slots_GE);
 #define FM_GEMM_DGRAD 3           /* C[rows,N] = A[rows,K] W_g[K,N]                  bf16 */
 #define FM_GEMM_WGRAD 4           /* C[g][M_w,N] = A[seg_g, M_w]^T B[seg_g, N]       f32  */
 
+/* Tile shape of the grouped GEMM: 1 = 128x256 per CTA, 2 = CTA pairs
+ * (tcgen05 cta_group::2, 256x256 per pair), 0 = automatic (default). */
+int fm_set_gemm_cta_group(int cta_group);
+
 int fm_grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
                     const void* aux, const int32_t* seg_start, const int32_t* seg_rows,
                     const int32_t* tile_prefix, int num_groups, int total_rows, int M_w, int N,

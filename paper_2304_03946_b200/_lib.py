@@ -80,6 +80,7 @@ _SIGNATURES = {
     "fm_static_ep_kept_device": [_P, _I, _I, C.c_double, _P, _P, _P],
     "fm_layer_set_capacity_factor": [_P, C.c_double],
     "fm_grouped_gemm": [_I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P],
+    "fm_set_gemm_cta_group": [_I],
     "fm_layer_create": [_P, _P, C.POINTER(_P)],
     "fm_layer_destroy": [_P],
     "fm_layer_set_placement": [_P, _P],

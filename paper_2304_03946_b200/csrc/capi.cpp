@@ -71,6 +71,7 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
                   cudaStream_t stream);
+void set_gemm_cta_group(int cg);
 
 }  // namespace fm
 
@@ -79,6 +80,10 @@ extern "C" {
 const char* fm_last_error(void) { return fm::g_last_error.c_str(); }
 
 const char* fm_version(void) { return "flexmoe_b200 0.1 (sm_100a)"; }
+
+int fm_set_gemm_cta_group(int cta_group) {
+  return fm::guarded([&] { fm::set_gemm_cta_group(cta_group); });
+}
 
 int fm_grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
                     const void* aux, const int32_t* seg_start, const int32_t* seg_rows,

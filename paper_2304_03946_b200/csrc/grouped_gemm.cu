@@ -17,7 +17,8 @@
 //   warp 1  : MMA issuer   (one elected lane), 128x256x16 UMMA, f32 in TMEM
 //   warp 2  : TMEM allocator (512 columns = two 128x256 f32 accumulators)
 //   warps 4-7: epilogue — tcgen05.ld, bias / ReLU / ReLU-mask, store.
-// Smem ring: 4 stages x (A 16 KB + B 32 KB).
+// Smem ring: 4 stages x (A 16 KB + B 32 KB) for single CTAs; 6 x (16 + 16 KB)
+// per CTA for CTA pairs (cta_group::2, 256x256 tiles).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -28,13 +29,10 @@
 namespace fm {
 namespace gemm {
 
-constexpr int kBM = 128;
-constexpr int kBN = 256;
+constexpr int kBM = 128;  // rows per CTA (one TMEM lane per row)
+constexpr int kBN = 256;  // output columns per tile
 constexpr int kBK = 64;
-constexpr int kStages = 4;
 constexpr int kABytes = kBM * kBK * 2;
-constexpr int kBBytes = kBN * kBK * 2;
-constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 256;
 constexpr int kTmemCols = 512;
 // Epilogue staging: per epilogue warp two 32-row x 64-byte buffers (SWIZZLE_64B
@@ -42,9 +40,21 @@ constexpr int kTmemCols = 512;
 constexpr int kStageOutBytes = 32 * 64;
 constexpr int kOutBytes = 4 * 2 * kStageOutBytes;
 constexpr int kMaxGroups = 256;
-constexpr int kSmemBytes =
-    kStages * kStageBytes + kOutBytes + 1024 + 256 + 2 * kBN * 4 + 2 * 4 * kBN * 4 + kMaxGroups * 4;
 constexpr uint32_t kMnChunkBytes = kBK * 128;  // one 64-wide MN chunk of a stage (8 KB)
+
+// CG = CTAs per MMA: 1 (128x256 tile per CTA) or 2 (CTA pair, 256x256 tile,
+// cta_group::2: each CTA stages its 128 rows of A and half of B's 256 columns,
+// the leader issues the MMA, each CTA holds its 128 rows of the accumulator).
+template <int CG>
+struct Cfg {
+  static constexpr int kBNc = kBN / CG;              // B rows (N) staged per CTA
+  static constexpr int kBBytes = kBNc * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = CG == 1 ? 4 : 6;
+  static constexpr int kTileM = kBM * CG;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kOutBytes + 1024 + 512 + 2 * kBN * 4 +
+                                    2 * 4 * kBN * 4 + 2 * kMaxGroups * 4;
+};
 
 enum Schedule { kRows = 0, kWgrad = 1 };
 enum Epilogue { kEpiBiasRelu = 0, kEpiBias = 1, kEpiReluMask = 2, kEpiNone = 3, kEpiF32 = 4 };
@@ -67,42 +77,71 @@ struct Args {
 
 struct Tile {
   int group;
-  int m0;      // kRows: token row; kWgrad: output row
+  int m0;      // this CTA's first row (kRows: token row; kWgrad: output row)
   int n0;
   int k_row0;  // kWgrad: first token row of the reduction
   int num_kb;
-  int mtile;   // kRows: global 128-row tile index (for per-tile column partials)
+  int mtile;   // kRows: global 128-row tile index of this CTA's rows
+  bool valid;  // this CTA's 128 rows lie inside the group (CG == 2 tail half)
 };
 
-template <int SCHED>
-__device__ __forceinline__ int total_tiles(const Args& a) {
-  if (SCHED == kRows) return __ldg(a.tile_prefix + a.num_groups) * (a.N / kBN);
-  return a.num_groups * (a.M_w / kBM) * (a.N / kBN);
+// Per-kernel schedule tables in smem: kWgrad walks groups longest-reduction-
+// first (LPT) so long tiles start in the first waves; kRows with CG == 2
+// needs the prefix of 256-row tile pairs per group.
+template <int SCHED, int CG>
+__device__ __forceinline__ void build_tables(const Args& a, int* order_s, int* pair_prefix_s) {
+  if (SCHED == kWgrad) {
+    for (int i = threadIdx.x; i < a.num_groups; i += blockDim.x) {
+      const int ri = __ldg(a.seg_rows + i);
+      int rank = 0;
+      for (int j = 0; j < a.num_groups; ++j) {
+        const int rj = __ldg(a.seg_rows + j);
+        rank += (rj > ri) || (rj == ri && j < i);
+      }
+      order_s[rank] = i;
+    }
+  } else if (CG == 2 && threadIdx.x == 0) {
+    int acc = 0;
+    for (int g = 0; g < a.num_groups; ++g) {
+      pair_prefix_s[g] = acc;
+      acc += (__ldg(a.tile_prefix + g + 1) - __ldg(a.tile_prefix + g) + 1) / 2;
+    }
+    pair_prefix_s[a.num_groups] = acc;
+  }
 }
 
-// kWgrad walks groups longest-reduction-first (LPT): `order` lists group ids by
-// descending token count, so the long tiles start in the first waves and the
-// tail of the persistent schedule is made of the short ones.
-template <int SCHED>
-__device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g, const int* order) {
+template <int SCHED, int CG>
+__device__ __forceinline__ int total_tiles(const Args& a, const int* pair_prefix_s) {
+  const int n_tiles = a.N / kBN;
+  if (SCHED == kRows) return (CG == 1 ? __ldg(a.tile_prefix + a.num_groups) : pair_prefix_s[a.num_groups]) * n_tiles;
+  return a.num_groups * (a.M_w / Cfg<CG>::kTileM) * n_tiles;
+}
+
+template <int SCHED, int CG>
+__device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g, const int* order,
+                                            const int* pair_prefix_s, int rank) {
   Tile tl;
   const int n_tiles = a.N / kBN;
+  tl.valid = true;
   if (SCHED == kRows) {
-    while (__ldg(a.tile_prefix + g + 1) * n_tiles <= t) ++g;
-    const int local = t - __ldg(a.tile_prefix + g) * n_tiles;
+    const int* pre = CG == 1 ? a.tile_prefix : pair_prefix_s;
+    while ((CG == 1 ? __ldg(pre + g + 1) : pre[g + 1]) * n_tiles <= t) ++g;
+    const int local = t - (CG == 1 ? __ldg(pre + g) : pre[g]) * n_tiles;
+    const int m_local = (local / n_tiles) * CG + rank;  // this CTA's 128-row tile in the group
     tl.group = g;
-    tl.mtile = __ldg(a.tile_prefix + g) + local / n_tiles;
-    tl.m0 = __ldg(a.seg_start + g) + (local / n_tiles) * kBM;
+    tl.mtile = __ldg(a.tile_prefix + g) + m_local;
+    tl.valid = tl.mtile < __ldg(a.tile_prefix + g + 1);
+    tl.m0 = __ldg(a.seg_start + g) + m_local * kBM;
     tl.n0 = (local % n_tiles) * kBN;
     tl.k_row0 = 0;
     tl.num_kb = a.K / kBK;
   } else {
-    const int per_group = (a.M_w / kBM) * n_tiles;
+    const int per_group = (a.M_w / Cfg<CG>::kTileM) * n_tiles;
     const int slot = t / per_group;
     const int local = t - slot * per_group;
     g = order[slot];
     tl.group = g;
-    tl.m0 = (local / n_tiles) * kBM;
+    tl.m0 = (local / n_tiles) * Cfg<CG>::kTileM + rank * kBM;
     tl.n0 = (local % n_tiles) * kBN;
     tl.k_row0 = __ldg(a.seg_start + g);
     tl.num_kb = __ldg(a.seg_rows + g) / kBK;
@@ -116,94 +155,94 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int SCHED, bool A_MN, bool B_MN, int EPI>
+template <int SCHED, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const Args args) {
+  using C = Cfg<CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + kStages * kABytes;
-  uint8_t* smem_out = smem + kStages * kStageBytes;  // 1024-aligned
+  uint8_t* smem_b = smem + C::kStages * kABytes;
+  uint8_t* smem_out = smem + C::kStages * C::kStageBytes;  // 1024-aligned
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_out + kOutBytes);
-  uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* empty_bar = full_bar + C::kStages;
+  uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  // [tmem holder | bias 2x256 f32 | colsum 2x4x256 f32 | group order 256 | pair prefix 257]
+  float* bias_s = reinterpret_cast<float*>(tmem_holder + 4);
+  float* colsum_s = bias_s + 2 * kBN;
+  int* order_s = reinterpret_cast<int*>(colsum_s + 8 * kBN);
+  int* pair_prefix_s = order_s + kMaxGroups;
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
-  // [tmem holder | bias 2x256 f32 | colsum 2x4x256 f32 | group order 256 i32]
-  int* order_s = reinterpret_cast<int*>(reinterpret_cast<float*>(tmem_holder + 4) + 2 * kBN + 8 * kBN);
-  if (SCHED == kWgrad) {
-    for (int i = threadIdx.x; i < args.num_groups; i += blockDim.x) {
-      const int ri = __ldg(args.seg_rows + i);
-      int rank = 0;
-      for (int j = 0; j < args.num_groups; ++j) {
-        const int rj = __ldg(args.seg_rows + j);
-        rank += (rj > ri) || (rj == ri && j < i);
-      }
-      order_s[rank] = i;
-    }
-  }
+  const int rank = CG == 2 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x / CG, num_clusters = gridDim.x / CG;
+  build_tables<SCHED, CG>(args, order_s, pair_prefix_s);
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&map_a);
     ptx::tma_prefetch_desc(&map_b);
     ptx::tma_prefetch_desc(&map_c);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull_bar[b], 1);
-      ptx::mbar_init(&tempty_bar[b], 128);
+      ptx::mbar_init(&tempty_bar[b], 128 * CG);  // both CTAs' epilogues release the pair's TMEM
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_holder, kTmemCols);
+  if (warp == 2) ptx::tmem_alloc_cg<CG>(tmem_holder, kTmemCols);
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int ntiles = total_tiles<SCHED>(args);
+  const int ntiles = total_tiles<SCHED, CG>(args, pair_prefix_s);
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
+    // ------------------------------------------------------------ producer (every CTA)
     if (lane == 0) {
+      // CG == 2: both CTAs' loads complete on the leader's full barrier
+      const uint32_t lead_full = CG == 2 ? ptx::mapa(ptx::smem_u32(full_bar), 0) : 0;
       int stage = 0;
       uint32_t phase = 0;
       int g = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const Tile tl = decode_tile<SCHED>(args, t, g, order_s);
+      for (int t = cluster; t < ntiles; t += num_clusters) {
+        const Tile tl = decode_tile<SCHED, CG>(args, t, g, order_s, pair_prefix_s, rank);
         const int b_row_base = tl.group * args.b_rows_per_group;
+        const int n_cta = tl.n0 + rank * C::kBNc;  // this CTA's slice of B
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
+          if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes * CG);
           uint8_t* sa = smem_a + stage * kABytes;
-          uint8_t* sb = smem_b + stage * kBBytes;
+          uint8_t* sb = smem_b + stage * C::kBBytes;
           const int k0 = kb * kBK;
+          auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+            if (CG == 1) ptx::tma_load_2d(dst, m, &full_bar[stage], c0, c1);
+            else ptx::tma_load_2d_2sm(dst, m, lead_full + stage * 8, c0, c1);
+          };
           if (!A_MN) {
-            ptx::tma_load_2d(sa, &map_a, &full_bar[stage], k0, tl.m0);
+            load(sa, &map_a, k0, tl.m0);
           } else {
 #pragma unroll
-            for (int j = 0; j < kBM / 64; ++j)
-              ptx::tma_load_2d(sa + j * kMnChunkBytes, &map_a, &full_bar[stage], tl.m0 + j * 64,
-                               tl.k_row0 + k0);
+            for (int j = 0; j < kBM / 64; ++j) load(sa + j * kMnChunkBytes, &map_a, tl.m0 + j * 64, tl.k_row0 + k0);
           }
           if (!B_MN) {
-            ptx::tma_load_2d(sb, &map_b, &full_bar[stage], k0, b_row_base + tl.n0);
+            load(sb, &map_b, k0, b_row_base + n_cta);
           } else {
             const int krow = (SCHED == kRows) ? b_row_base + k0 : tl.k_row0 + k0;
 #pragma unroll
-            for (int j = 0; j < kBN / 64; ++j)
-              ptx::tma_load_2d(sb + j * kMnChunkBytes, &map_b, &full_bar[stage], tl.n0 + j * 64,
-                               krow);
+            for (int j = 0; j < C::kBNc / 64; ++j) load(sb + j * kMnChunkBytes, &map_b, n_cta + j * 64, krow);
           }
-          if (++stage == kStages) {
+          if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -211,9 +250,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBM, kBN, A_MN, B_MN);
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::kTileM, kBN, A_MN, B_MN);
       constexpr uint32_t a_lbo = A_MN ? kMnChunkBytes : 16;
       constexpr uint32_t b_lbo = B_MN ? kMnChunkBytes : 16;
       // Advance per UMMA_K=16 step: 32 B inside a K-major swizzle row,
@@ -224,8 +263,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int g = 0;
       int iter = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
-        const Tile tl = decode_tile<SCHED>(args, t, g, order_s);
+      for (int t = cluster; t < ntiles; t += num_clusters, ++iter) {
+        const Tile tl = decode_tile<SCHED, CG>(args, t, g, order_s, pair_prefix_s, rank);
         const int ab = iter & 1;
         ptx::mbar_wait(&tempty_bar[ab], ((iter >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
@@ -234,37 +273,40 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
-          const uint32_t sb = ptx::smem_u32(smem_b + stage * kBBytes);
+          const uint32_t sb = ptx::smem_u32(smem_b + stage * C::kBBytes);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t da = ptx::umma_desc_sw128(sa + k * a_kstep, a_lbo, 1024);
             const uint64_t db = ptx::umma_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
-            ptx::mma_bf16_ss(d_tmem, da, db, idesc, (kb | k) != 0);
+            if (CG == 1) ptx::mma_bf16_ss(d_tmem, da, db, idesc, (kb | k) != 0);
+            else ptx::mma_bf16_ss_pair(d_tmem, da, db, idesc, (kb | k) != 0);
           }
-          ptx::mma_commit(&empty_bar[stage]);
-          if (++stage == kStages) {
+          if (CG == 1) ptx::mma_commit(&empty_bar[stage]);
+          else ptx::mma_commit_pair(&empty_bar[stage], 0x3);
+          if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit(&tfull_bar[ab]);
+        if (CG == 1) ptx::mma_commit(&tfull_bar[ab]);
+        else ptx::mma_commit_pair(&tfull_bar[ab], 0x3);
       }
     }
   } else if (warp >= 4) {
-    // ------------------------------------------------------------ epilogue
+    // ------------------------------------------------------------ epilogue (every CTA)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
     const int et = static_cast<int>(threadIdx.x) - 128;  // 0..127 among epilogue threads
-    float* bias_s = reinterpret_cast<float*>(tmem_holder + 4);  // [2][kBN]
-    float* colsum_s = bias_s + 2 * kBN;                          // [2][4 warps][kBN]
     constexpr bool kBias = (EPI == kEpiBiasRelu || EPI == kEpiBias);
     const int mask_ld = args.N / 32;  // mask words per token row
     uint8_t* warp_out = smem_out + q * 2 * kStageOutBytes;
+    // release of the accumulator goes to the leader's barrier
+    const uint32_t lead_tempty = CG == 2 ? ptx::mapa(ptx::smem_u32(tempty_bar), 0) : 0;
     uint32_t out_seq = 0;
     int g = 0;
     int iter = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
-      const Tile tl = decode_tile<SCHED>(args, t, g, order_s);
+    for (int t = cluster; t < ntiles; t += num_clusters, ++iter) {
+      const Tile tl = decode_tile<SCHED, CG>(args, t, g, order_s, pair_prefix_s, rank);
       const int ab = iter & 1;
       // Everything that does not depend on the accumulator is fetched before
       // waiting on it: the tile's bias slice (to smem) and the ReLU mask bits.
@@ -276,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::named_bar_sync(1, 128);
       }
       uint32_t mbits[kBN / 32];
-      if (EPI == kEpiReluMask) {
+      if (EPI == kEpiReluMask && tl.valid) {
         const uint4* mp = reinterpret_cast<const uint4*>(
             args.mask + static_cast<size_t>(tl.m0 + row) * mask_ld + tl.n0 / 32);
         const uint4 m0 = __ldg(mp), m1 = __ldg(mp + 1);
@@ -387,25 +429,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       };
-      // TMEM reads double-buffered: chunk c+1 is in flight while c is processed.
-      if (!empty_k) {
-        ptx::tmem_ld_32x32b_x32(t_row, ra);
-        ptx::tmem_ld_wait_regs(ra);
-      }
-#pragma unroll
-      for (int c = 0; c < kBN / 32; c += 2) {
-        if (!empty_k) ptx::tmem_ld_32x32b_x32(t_row + (c + 1) * 32, rb);
-        process(c, ra);
+      if (tl.valid) {
+        // TMEM reads double-buffered: chunk c+1 is in flight while c is processed.
         if (!empty_k) {
-          ptx::tmem_ld_wait_regs(rb);
-          if (c + 2 < kBN / 32) ptx::tmem_ld_32x32b_x32(t_row + (c + 2) * 32, ra);
+          ptx::tmem_ld_32x32b_x32(t_row, ra);
+          ptx::tmem_ld_wait_regs(ra);
         }
-        process(c + 1, rb);
-        if (!empty_k && c + 2 < kBN / 32) ptx::tmem_ld_wait_regs(ra);
+#pragma unroll
+        for (int c = 0; c < kBN / 32; c += 2) {
+          if (!empty_k) ptx::tmem_ld_32x32b_x32(t_row + (c + 1) * 32, rb);
+          process(c, ra);
+          if (!empty_k) {
+            ptx::tmem_ld_wait_regs(rb);
+            if (c + 2 < kBN / 32) ptx::tmem_ld_32x32b_x32(t_row + (c + 2) * 32, ra);
+          }
+          process(c + 1, rb);
+          if (!empty_k && c + 2 < kBN / 32) ptx::tmem_ld_wait_regs(ra);
+        }
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty_bar[ab]);
-      if (EPI == kEpiReluMask && args.colsum) {
+      if (CG == 1 || leader) ptx::mbar_arrive(&tempty_bar[ab]);
+      else ptx::mbar_arrive_cluster(lead_tempty + ab * 8);
+      if (EPI == kEpiReluMask && args.colsum && tl.valid) {
         // combine the four warps in a fixed order (deterministic), one row per tile
         ptx::named_bar_sync(2, 128);
         const float* cs = colsum_s + ab * 4 * kBN;
@@ -416,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           dst[col] = ((cs[col] + cs[kBN + col]) + cs[2 * kBN + col]) + cs[3 * kBN + col];
         }
       }
-      if (EPI == kEpiBiasRelu && args.mask) {
+      if (EPI == kEpiBiasRelu && args.mask && tl.valid) {
         uint4* mp = reinterpret_cast<uint4*>(args.mask + static_cast<size_t>(tl.m0 + row) * mask_ld +
                                              tl.n0 / 32);
         mp[0] = make_uint4(relu_bits[0], relu_bits[1], relu_bits[2], relu_bits[3]);
@@ -428,29 +473,57 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) ptx::cluster_sync(); else __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, kTmemCols);
+    ptx::tmem_dealloc_cg<CG>(tmem_base, kTmemCols);
   }
 }
 
-template <int SCHED, bool A_MN, bool B_MN, int EPI>
-void launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Args& args,
-            cudaStream_t stream) {
-  auto kern = grouped_gemm_kernel<SCHED, A_MN, B_MN, EPI>;
+template <int SCHED, bool A_MN, bool B_MN, int EPI, int CG>
+void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Args& args,
+               cudaStream_t stream) {
+  using C = Cfg<CG>;
+  auto kern = grouped_gemm_kernel<SCHED, A_MN, B_MN, EPI, CG>;
   static bool configured = false;
   if (!configured) {
-    FM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    FM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
     configured = true;
   }
-  int grid = num_sms();
-  if (SCHED == kWgrad) grid = std::min(grid, std::max(1, args.num_groups * (args.M_w / kBM) * (args.N / kBN)));
-  kern<<<grid, kThreads, kSmemBytes, stream>>>(ma, mb, mc, args);
-  FM_LAUNCH_CHECK("grouped_gemm_kernel");
+  int grid = num_sms() / CG * CG;
+  if (SCHED == kWgrad)
+    grid = std::min(grid, CG * std::max(1, args.num_groups * (args.M_w / C::kTileM) * (args.N / kBN)));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FM_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, args));
+}
+
+// CTA-pair tiles unless overridden (FM_GEMM_CTA_GROUP / fm_set_gemm_cta_group)
+int g_cta_group = 0;  // 0 = auto
+
+template <int SCHED, bool A_MN, bool B_MN, int EPI>
+void launch(const CUtensorMap* maps1, const CUtensorMap* maps2, const Args& args, int cg,
+            cudaStream_t stream) {
+  if (cg == 2) launch_cg<SCHED, A_MN, B_MN, EPI, 2>(maps2[0], maps2[1], maps2[2], args, stream);
+  else launch_cg<SCHED, A_MN, B_MN, EPI, 1>(maps1[0], maps1[1], maps1[2], args, stream);
 }
 
 }  // namespace gemm
+
+void set_gemm_cta_group(int cg) {
+  if (cg != 0 && cg != 1 && cg != 2) throw std::invalid_argument("gemm cta group must be 0, 1 or 2");
+  gemm::g_cta_group = cg;
+}
 
 // Host entry used by the layer and by the C-ABI test hook.
 void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
@@ -475,48 +548,59 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
   a.ldc = N;
   a.bias = bias;
   a.mask = static_cast<uint32_t*>(const_cast<void*>(aux));
+  // CTA pairs for the token-row GEMMs when groups are large enough that the
+  // odd 128-row tail of each group (computed, not stored) is cheap; always for
+  // wgrad (M_w is a multiple of 256).
+  int cg = g_cta_group;
+  if (cg == 0) {
+    if (variant == FM_GEMM_WGRAD) cg = (M_w % 256 == 0) ? 2 : 1;
+    else cg = (total_rows / num_groups >= 2048) ? 2 : 1;
+  }
+  if (variant == FM_GEMM_WGRAD && M_w % (kBM * cg) != 0) cg = 1;
+  CUtensorMap m1[3], m2[3];
   switch (variant) {
     case FM_GEMM_FWD_BIAS_RELU:
     case FM_GEMM_FWD_BIAS: {
       if (K % kBK != 0) throw std::invalid_argument("grouped_gemm: K must be a multiple of 64");
       // A [rows, K] K-major; B = W_g [N, K] K-major, groups stacked.
-      CUtensorMap ma = make_tmap_bf16(A, K, total_rows, K, 64, kBM);
-      CUtensorMap mb = make_tmap_bf16(B, K, static_cast<uint64_t>(num_groups) * N, K, 64, kBN);
-      CUtensorMap mc = make_tmap_2d(C, false, N, total_rows, N, 32, 32, 64);
+      m1[0] = m2[0] = make_tmap_bf16(A, K, total_rows, K, 64, kBM);
+      m1[1] = make_tmap_bf16(B, K, static_cast<uint64_t>(num_groups) * N, K, 64, kBN);
+      m2[1] = make_tmap_bf16(B, K, static_cast<uint64_t>(num_groups) * N, K, 64, kBN / 2);
+      m1[2] = m2[2] = make_tmap_2d(C, false, N, total_rows, N, 32, 32, 64);
       a.b_rows_per_group = N;
       if (variant == FM_GEMM_FWD_BIAS_RELU)
-        launch<kRows, false, false, kEpiBiasRelu>(ma, mb, mc, a, stream);
+        launch<kRows, false, false, kEpiBiasRelu>(m1, m2, a, cg, stream);
       else
-        launch<kRows, false, false, kEpiBias>(ma, mb, mc, a, stream);
+        launch<kRows, false, false, kEpiBias>(m1, m2, a, cg, stream);
       break;
     }
     case FM_GEMM_DGRAD_RELU_MASK:
     case FM_GEMM_DGRAD: {
       if (K % kBK != 0) throw std::invalid_argument("grouped_gemm: K must be a multiple of 64");
       // A [rows, K] K-major; B = W_g viewed [K, N] (N contiguous) -> MN-major.
-      CUtensorMap ma = make_tmap_bf16(A, K, total_rows, K, 64, kBM);
-      CUtensorMap mb = make_tmap_bf16(B, N, static_cast<uint64_t>(num_groups) * K, N, 64, kBK);
-      CUtensorMap mc = make_tmap_2d(C, false, N, total_rows, N, 32, 32, 64);
+      m1[0] = m2[0] = make_tmap_bf16(A, K, total_rows, K, 64, kBM);
+      m1[1] = m2[1] = make_tmap_bf16(B, N, static_cast<uint64_t>(num_groups) * K, N, 64, kBK);
+      m1[2] = m2[2] = make_tmap_2d(C, false, N, total_rows, N, 32, 32, 64);
       a.b_rows_per_group = K;
       if (variant == FM_GEMM_DGRAD_RELU_MASK) {
         if (!aux) throw std::invalid_argument("grouped_gemm: relu-mask dgrad needs the ReLU bit mask");
         // `bias` doubles as the optional per-tile column-sum output here
         a.colsum = const_cast<float*>(bias);
         a.bias = nullptr;
-        launch<kRows, false, true, kEpiReluMask>(ma, mb, mc, a, stream);
+        launch<kRows, false, true, kEpiReluMask>(m1, m2, a, cg, stream);
       } else {
-        launch<kRows, false, true, kEpiNone>(ma, mb, mc, a, stream);
+        launch<kRows, false, true, kEpiNone>(m1, m2, a, cg, stream);
       }
       break;
     }
     case FM_GEMM_WGRAD: {
       if (M_w % kBM != 0) throw std::invalid_argument("grouped_gemm: M_w must be a multiple of 128");
       // A = tokens x M_w (M contiguous) -> MN-major; B = tokens x N -> MN-major.
-      CUtensorMap ma = make_tmap_bf16(A, M_w, total_rows, M_w, 64, kBK);
-      CUtensorMap mb = make_tmap_bf16(B, N, total_rows, N, 64, kBK);
-      CUtensorMap mc = make_tmap_2d(C, true, N, static_cast<uint64_t>(num_groups) * M_w, N, 16, 32, 64);
+      m1[0] = m2[0] = make_tmap_bf16(A, M_w, total_rows, M_w, 64, kBK);
+      m1[1] = m2[1] = make_tmap_bf16(B, N, total_rows, N, 64, kBK);
+      m1[2] = m2[2] = make_tmap_2d(C, true, N, static_cast<uint64_t>(num_groups) * M_w, N, 16, 32, 64);
       a.b_rows_per_group = 0;
-      launch<kWgrad, true, true, kEpiF32>(ma, mb, mc, a, stream);
+      launch<kWgrad, true, true, kEpiF32>(m1, m2, a, cg, stream);
       break;
     }
     default:

@@ -12,6 +12,14 @@ pytestmark = pytest.mark.gpu
 from paper_2304_03946_b200 import _lib as L  # noqa: E402
 
 
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"], autouse=True)
+def cta_group(request):
+    """Every GEMM test runs with single-CTA 128x256 tiles and CTA-pair 256x256 tiles."""
+    L.call("fm_set_gemm_cta_group", request.param)
+    yield request.param
+    L.call("fm_set_gemm_cta_group", 0)
+
+
 def _segments(rows_per_group, device):
     pad = [((r + 127) // 128) * 128 for r in rows_per_group]
     start = [0]
@@ -55,7 +63,7 @@ def _setup(rows, d_in, d_out, seed=0):
     return pad, start, tiles, total, A, i32
 
 
-@pytest.mark.parametrize("rows", [[200, 0, 77, 512], [1000]])
+@pytest.mark.parametrize("rows", [[200, 0, 77, 512], [1000], [128, 384, 130, 0, 900]])
 @pytest.mark.parametrize("relu", [True, False])
 def test_fwd(rows, relu):
     K, N = 512, 768
