@@ -33,25 +33,29 @@ constexpr int kBM = 128;  // rows per CTA (one TMEM lane per row)
 constexpr int kBN = 256;  // output columns per tile
 constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;
-constexpr int kThreads = 256;
 constexpr int kTmemCols = 512;
 // Epilogue staging: per epilogue warp two 32-row x 64-byte buffers (SWIZZLE_64B
-// TMA store boxes): 4 warps x 2 x 2 KB.
+// TMA store boxes).
 constexpr int kStageOutBytes = 32 * 64;
-constexpr int kOutBytes = 4 * 2 * kStageOutBytes;
 constexpr int kMaxGroups = 256;
 constexpr uint32_t kMnChunkBytes = kBK * 128;  // one 64-wide MN chunk of a stage (8 KB)
 
 // CG = CTAs per MMA: 1 (128x256 tile per CTA) or 2 (CTA pair, 256x256 tile,
 // cta_group::2: each CTA stages its 128 rows of A and half of B's 256 columns,
 // the leader issues the MMA, each CTA holds its 128 rows of the accumulator).
+// Epilogue warps EW: 4 (one per TMEM lane quarter, all 256 columns) or 8 (two
+// per quarter, 128 columns each) — the CTA-pair kernel has the smem for the
+// second set, which doubles the epilogue's latency hiding.
 template <int CG>
 struct Cfg {
   static constexpr int kBNc = kBN / CG;              // B rows (N) staged per CTA
   static constexpr int kBBytes = kBNc * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = CG == 1 ? 4 : 6;
+  static constexpr int kStages = CG == 1 ? 4 : 5;
   static constexpr int kTileM = kBM * CG;
+  static constexpr int kEW = CG == 1 ? 4 : 8;
+  static constexpr int kThreads = 128 + 32 * kEW;
+  static constexpr int kOutBytes = kEW * 2 * kStageOutBytes;
   static constexpr int kSmemBytes = kStages * kStageBytes + kOutBytes + 1024 + 512 + 2 * kBN * 4 +
                                     2 * 4 * kBN * 4 + 2 * kMaxGroups * 4;
 };
@@ -156,7 +160,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 
 template <int SCHED, bool A_MN, bool B_MN, int EPI, int CG>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const Args args) {
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + C::kStages * kABytes;
   uint8_t* smem_out = smem + C::kStages * C::kStageBytes;  // 1024-aligned
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_out + kOutBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_out + C::kOutBytes);
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull_bar[b], 1);
-      ptx::mbar_init(&tempty_bar[b], 128 * CG);  // both CTAs' epilogues release the pair's TMEM
+      ptx::mbar_init(&tempty_bar[b], C::kEW * CG);  // one arrive per epilogue warp, both CTAs
     }
     ptx::fence_mbar_init();
   }
@@ -294,12 +298,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (every CTA)
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    constexpr int kEpiThreads = 32 * C::kEW;
+    constexpr int kChunks = (kBN / 32) / (C::kEW / 4);  // 32-column chunks per warp
+    const int ew = static_cast<int>(warp) - 4;          // epilogue warp 0..EW-1
+    const int q = warp & 3;                             // TMEM lane quarter this warp may access
+    const int col0 = (ew >> 2) * kChunks * 32;          // this warp's first column in the tile
     const int row = q * 32 + lane;
-    const int et = static_cast<int>(threadIdx.x) - 128;  // 0..127 among epilogue threads
+    const int et = static_cast<int>(threadIdx.x) - 128;  // index among epilogue threads
     constexpr bool kBias = (EPI == kEpiBiasRelu || EPI == kEpiBias);
     const int mask_ld = args.N / 32;  // mask words per token row
-    uint8_t* warp_out = smem_out + q * 2 * kStageOutBytes;
+    uint8_t* warp_out = smem_out + ew * 2 * kStageOutBytes;
     // release of the accumulator goes to the leader's barrier
     const uint32_t lead_tempty = CG == 2 ? ptx::mapa(ptx::smem_u32(tempty_bar), 0) : 0;
     uint32_t out_seq = 0;
@@ -313,24 +321,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* bs = bias_s + ab * kBN;
       if (kBias) {
         const float* bp = args.bias + static_cast<size_t>(tl.group) * args.N + tl.n0;
-        bs[et] = __ldg(bp + et);
-        bs[et + 128] = __ldg(bp + et + 128);
-        ptx::named_bar_sync(1, 128);
+        for (int i = et; i < kBN; i += kEpiThreads) bs[i] = __ldg(bp + i);
+        ptx::named_bar_sync(1, kEpiThreads);
       }
-      uint32_t mbits[kBN / 32];
+      uint32_t mbits[kChunks];
       if (EPI == kEpiReluMask && tl.valid) {
         const uint4* mp = reinterpret_cast<const uint4*>(
-            args.mask + static_cast<size_t>(tl.m0 + row) * mask_ld + tl.n0 / 32);
-        const uint4 m0 = __ldg(mp), m1 = __ldg(mp + 1);
-        mbits[0] = m0.x; mbits[1] = m0.y; mbits[2] = m0.z; mbits[3] = m0.w;
-        mbits[4] = m1.x; mbits[5] = m1.y; mbits[6] = m1.z; mbits[7] = m1.w;
+            args.mask + static_cast<size_t>(tl.m0 + row) * mask_ld + (tl.n0 + col0) / 32);
+#pragma unroll
+        for (int i = 0; i < kChunks / 4; ++i) {
+          const uint4 m = __ldg(mp + i);
+          mbits[4 * i] = m.x; mbits[4 * i + 1] = m.y; mbits[4 * i + 2] = m.z; mbits[4 * i + 3] = m.w;
+        }
       }
       ptx::mbar_wait(&tfull_bar[ab], (iter >> 1) & 1);
       ptx::tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + ab * kBN;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + ab * kBN + col0;
       const bool empty_k = tl.num_kb == 0;
       uint32_t ra[32], rb[32];
-      uint32_t relu_bits[kBN / 32];
+      uint32_t relu_bits[kChunks];
       // Output staging: this warp's 32 rows x 64 B go to a swizzled smem box
       // (SWIZZLE_64B: 16-byte chunk j of row r sits at chunk j ^ ((r >> 1) & 3)),
       // then one lane issues the TMA store. Two buffers per warp alternate.
@@ -356,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       // chunk c of 32 columns: bias / activation / mask, convert, store
       auto process = [&](int c, uint32_t (&r)[32]) {
-        const int col = tl.n0 + c * 32;
+        const int col = tl.n0 + col0 + c * 32;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = empty_k ? 0.0f : __uint_as_float(r[i]);
@@ -381,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (kBias) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += bs[c * 32 + i];
+          for (int i = 0; i < 32; ++i) v[i] += bs[col0 + c * 32 + i];
         }
         if (EPI == kEpiBiasRelu) {
           uint32_t bits = 0;
@@ -423,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
           s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
           if (half == 0) {
-            float* dstc = colsum_s + (ab * 4 + q) * kBN + c * 32 + 2 * pair;
+            float* dstc = colsum_s + (ab * 4 + q) * kBN + col0 + c * 32 + 2 * pair;
             dstc[0] = s0;
             dstc[1] = s1;
           }
@@ -436,36 +445,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_ld_wait_regs(ra);
         }
 #pragma unroll
-        for (int c = 0; c < kBN / 32; c += 2) {
+        for (int c = 0; c < kChunks; c += 2) {
           if (!empty_k) ptx::tmem_ld_32x32b_x32(t_row + (c + 1) * 32, rb);
           process(c, ra);
           if (!empty_k) {
             ptx::tmem_ld_wait_regs(rb);
-            if (c + 2 < kBN / 32) ptx::tmem_ld_32x32b_x32(t_row + (c + 2) * 32, ra);
+            if (c + 2 < kChunks) ptx::tmem_ld_32x32b_x32(t_row + (c + 2) * 32, ra);
           }
           process(c + 1, rb);
-          if (!empty_k && c + 2 < kBN / 32) ptx::tmem_ld_wait_regs(ra);
+          if (!empty_k && c + 2 < kChunks) ptx::tmem_ld_wait_regs(ra);
         }
       }
+      // release the accumulator: one arrive per warp once all its TMEM reads are done
       ptx::tc_fence_before();
-      if (CG == 1 || leader) ptx::mbar_arrive(&tempty_bar[ab]);
-      else ptx::mbar_arrive_cluster(lead_tempty + ab * 8);
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 1 || leader) ptx::mbar_arrive(&tempty_bar[ab]);
+        else ptx::mbar_arrive_cluster(lead_tempty + ab * 8);
+      }
       if (EPI == kEpiReluMask && args.colsum && tl.valid) {
-        // combine the four warps in a fixed order (deterministic), one row per tile
-        ptx::named_bar_sync(2, 128);
+        // combine the four row quarters in a fixed order (deterministic)
+        ptx::named_bar_sync(2, kEpiThreads);
         const float* cs = colsum_s + ab * 4 * kBN;
         float* dst = args.colsum + static_cast<size_t>(tl.mtile) * args.N + tl.n0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = et + h * 128;
+        for (int col = et; col < kBN; col += kEpiThreads)
           dst[col] = ((cs[col] + cs[kBN + col]) + cs[2 * kBN + col]) + cs[3 * kBN + col];
-        }
       }
       if (EPI == kEpiBiasRelu && args.mask && tl.valid) {
         uint4* mp = reinterpret_cast<uint4*>(args.mask + static_cast<size_t>(tl.m0 + row) * mask_ld +
-                                             tl.n0 / 32);
-        mp[0] = make_uint4(relu_bits[0], relu_bits[1], relu_bits[2], relu_bits[3]);
-        mp[1] = make_uint4(relu_bits[4], relu_bits[5], relu_bits[6], relu_bits[7]);
+                                             (tl.n0 + col0) / 32);
+#pragma unroll
+        for (int i = 0; i < kChunks / 4; ++i)
+          mp[i] = make_uint4(relu_bits[4 * i], relu_bits[4 * i + 1], relu_bits[4 * i + 2],
+                             relu_bits[4 * i + 3]);
       }
     }
     if (lane == 0) ptx::bulk_wait<0>();  // all output stores complete before exit
@@ -495,7 +507,7 @@ void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
     grid = std::min(grid, CG * std::max(1, args.num_groups * (args.M_w / C::kTileM) * (args.N / kBN)));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
