@@ -270,7 +270,9 @@ class DistArm:
         prof = S.ClusterProfile.b200(G, slots, tps=1.2e15 / (12.0 * d * f),
                                      expert_param_bytes=4.0 * params,
                                      expert_state_bytes=14.0 * params, token_bytes=2.0 * d)
-        ex = TorchExchange() if world > 1 else LoopbackHub(1).endpoint(0)
+        import torch.distributed as tdist
+
+        ex = TorchExchange() if tdist.is_initialized() else LoopbackHub(1).endpoint(0)
         g = torch.Generator(device="cpu").manual_seed(1234)
         wg = torch.randn(N, d, generator=g) * d**-0.5
         self.logp = zipf_log_popularity(N, cfg["zipf"], 42)
@@ -336,7 +338,7 @@ def run_ours(args, world, rank, local_rank):
 
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    if world > 1 or "RANK" in os.environ:  # launched by torchrun: NCCL transport even at N=1
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))

@@ -199,3 +199,22 @@ def test_dispatch_layout_gloo():
                         exp.extend((s, u) for u in units[lo:lo + c])
                     lo += c
             assert got == exp, (me, e)
+
+
+def _p2p_body(rank, world):
+    """Migration transport: batched send/recv pairs matched per (src, dst) in order."""
+    ex = TorchExchange()
+    a = torch.full((4, 3), float(rank + 1))
+    b = torch.arange(5, dtype=torch.float32) + 10 * rank
+    sends = [(1 - rank, a), (1 - rank, b)]
+    ra, rb = torch.empty(4, 3), torch.empty(5)
+    ex.p2p(sends, [(1 - rank, ra), (1 - rank, rb)])
+    ex.p2p([], [])  # empty rounds are legal (every rank calls p2p every step)
+    return ra, rb
+
+
+@pytest.mark.timeout(300)
+def test_p2p_migration_transport_gloo():
+    (ra0, rb0), (ra1, rb1) = _spawn(_p2p_body)
+    assert torch.equal(ra0, torch.full((4, 3), 2.0)) and torch.equal(ra1, torch.full((4, 3), 1.0))
+    assert torch.equal(rb0, torch.arange(5.0) + 10) and torch.equal(rb1, torch.arange(5.0))
