@@ -172,7 +172,9 @@ def run_reference_arm(args, world, rank):
         return
     import oracle
 
-    cfg = dict(CFG2)
+    # the same workload our arm runs at this N (configs[1] at 1 GPU, configs[2..4] otherwise)
+    multi = world > 1 or args.workload in WORKLOADS
+    cfg = dict(WORKLOADS[args.workload or "cfg3"] if multi else CFG2)
     # whole run bounded to ~2 minutes of host work: per-step sample sized to it
     budget = max(0.25, 120.0 / max(1, args.steps + args.warmup))
     t_small, hist = cpu_layer_sample(cfg, 256)
@@ -193,7 +195,8 @@ def run_reference_arm(args, world, rank):
     kind = "port"
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": cfg.get("scaling", "weak"), "vs_baseline": None,
+            "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": cfg["workload"], "tokens_per_step_sampled": tokens,
                        "global_batch": cfg["T"], "parallelism": "cpu"},
@@ -210,7 +213,16 @@ def run_reference_arm(args, world, rank):
 # ------------------------------------------------------------------ GPU arm
 CFG3 = dict(workload="BASELINE configs[2]: GPT-MoE layer, 64 experts top-1, d_model 1024, d_ff 4096, "
             "65,536 tokens per GPU (weak scaling), drifting Zipf traffic",
-            N=64, k=1, d=1024, f=4096, T=65536, zipf=1.25)
+            N=64, k=1, d=1024, f=4096, T=65536, zipf=1.25, policy_mode=0, interval=10, scaling="weak")
+CFG4 = dict(workload="BASELINE configs[3]: BERT-MoE layer, 32 experts top-2, d_model 768, d_ff 3072, "
+            "65,536 tokens per GPU, expand/shrink/migrate every 100 steps with P2P weight+optimizer "
+            "migration", N=32, k=2, d=768, f=3072, T=65536, zipf=1.25, policy_mode=1, interval=100,
+            scaling="weak")
+CFG5 = dict(workload="BASELINE configs[4]: Swin-MoE-scale layer, 128 experts top-1, d_model 1024, "
+            "d_ff 4096, 256K tokens in total (strong scaling), severe imbalance (Zipf 2.0), migration "
+            "cost included", N=128, k=1, d=1024, f=4096, T=262144, zipf=2.0, policy_mode=0, interval=10,
+            scaling="strong")
+WORKLOADS = {"cfg3": CFG3, "cfg4": CFG4, "cfg5": CFG5}
 
 
 class FusedArm:
@@ -277,7 +289,9 @@ class DistArm:
         wg = torch.randn(N, d, generator=g) * d**-0.5
         self.logp = zipf_log_popularity(N, cfg["zipf"], 42)
         wg[:, 0] = torch.tensor(self.logp * 2, dtype=torch.float32)
-        self.rt = FlexMoERuntime(N, k, d, f, ex, prof, max_tokens=T, gate_weight=wg, optimizer=False)
+        sched_cfg = S.SchedulerConfig.defaults(policy_mode=cfg["policy_mode"], interval_steps=cfg["interval"])
+        self.rt = FlexMoERuntime(N, k, d, f, ex, prof, sched_cfg=sched_cfg, max_tokens=T, gate_weight=wg,
+                                 optimizer=False)
         self.layer, self.dl = self.rt.layer, self.rt.dl
         self.drift = np.random.default_rng(42)  # same walk on every rank
         self.N, self.G = N, G
@@ -343,8 +357,10 @@ def run_ours(args, world, rank, local_rank):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)
-    multi = world > 1 or args.workload == "cfg3"
-    cfg = dict(CFG3 if multi else CFG2)
+    multi = world > 1 or args.workload in WORKLOADS
+    cfg = dict(WORKLOADS[args.workload or "cfg3"] if multi else CFG2)
+    if cfg.get("scaling") == "strong":  # fixed total tokens, split over the GPUs
+        cfg["T"] = cfg["T"] // world
     N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
     arm = DistArm(cfg, dev, rank, world) if multi else FusedArm(cfg, dev, rank)
 
@@ -476,7 +492,7 @@ def run_ours(args, world, rank, local_rank):
         "warmup": args.warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": cfg.get("scaling", "weak"),
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights of the configs architecture; Zipf skew via the gate)",
@@ -519,8 +535,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default=None, choices=[None, "cfg2", "cfg3"],
-                    help="default: cfg2 at 1 GPU, cfg3 (multi-GPU phase path) at N > 1")
+    ap.add_argument("--workload", default=None, choices=[None, "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="default: cfg2 at 1 GPU, cfg3 (multi-GPU runtime) at N > 1; "
+                         "cfg3-5 run the multi-GPU runtime at any N")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
