@@ -38,6 +38,7 @@ constexpr int kTmemCols = 512;
 // TMA store boxes).
 constexpr int kStageOutBytes = 32 * 64;
 constexpr int kMaxGroups = 256;
+constexpr int kTableInts = kMaxGroups + 4;  // one smem schedule table (groups + 1, padded)
 constexpr uint32_t kMnChunkBytes = kBK * 128;  // one 64-wide MN chunk of a stage (8 KB)
 
 // CG = CTAs per MMA: 1 (128x256 tile per CTA) or 2 (CTA pair, 256x256 tile,
@@ -57,7 +58,7 @@ struct Cfg {
   static constexpr int kThreads = 128 + 32 * kEW;
   static constexpr int kOutBytes = kEW * 2 * kStageOutBytes;
   static constexpr int kSmemBytes = kStages * kStageBytes + kOutBytes + 1024 + 512 + 2 * kBN * 4 +
-                                    2 * 4 * kBN * 4 + 2 * kMaxGroups * 4;
+                                    2 * 4 * kBN * 4 + 4 * kTableInts * 4;
 };
 
 enum Schedule { kRows = 0, kWgrad = 1 };
@@ -89,11 +90,28 @@ struct Tile {
   bool valid;  // this CTA's 128 rows lie inside the group (CG == 2 tail half)
 };
 
-// Per-kernel schedule tables in smem: kWgrad walks groups longest-reduction-
-// first (LPT) so long tiles start in the first waves; kRows with CG == 2
-// needs the prefix of 256-row tile pairs per group.
+// Per-kernel schedule tables in smem, so that no tile decode touches global
+// memory (the producer runs only a few stages ahead of the tensor pipe; a
+// dependent L2 round trip at every tile boundary shows up as an MMA bubble).
+//   order_s   kWgrad: groups longest-reduction-first (LPT), so long tiles
+//             start in the first waves; kb_s: k-blocks per LPT slot
+//   pair_s    kRows CG == 2: prefix of 256-row tile pairs per group
+//   tp_s      kRows: tile_prefix;  ss_s: seg_start
+struct Tables {
+  int* order_s;
+  int* pair_s;
+  int* tp_s;
+  int* ss_s;
+};
+
 template <int SCHED, int CG>
-__device__ __forceinline__ void build_tables(const Args& a, int* order_s, int* pair_prefix_s) {
+__device__ __forceinline__ void build_tables(const Args& a, const Tables& tb) {
+  int* order_s = tb.order_s;
+  int* pair_prefix_s = tb.pair_s;
+  int* kb_s = tb.tp_s;
+  for (int i = threadIdx.x; i < a.num_groups; i += blockDim.x) tb.ss_s[i] = __ldg(a.seg_start + i);
+  if (SCHED == kRows)
+    for (int i = threadIdx.x; i <= a.num_groups; i += blockDim.x) tb.tp_s[i] = __ldg(a.tile_prefix + i);
   if (SCHED == kWgrad) {
     for (int i = threadIdx.x; i < a.num_groups; i += blockDim.x) {
       const int ri = __ldg(a.seg_rows + i);
@@ -103,6 +121,7 @@ __device__ __forceinline__ void build_tables(const Args& a, int* order_s, int* p
         rank += (rj > ri) || (rj == ri && j < i);
       }
       order_s[rank] = i;
+      kb_s[rank] = ri / kBK;  // k-blocks of the slot's group (the MMA issuer's only input)
     }
   } else if (CG == 2 && threadIdx.x == 0) {
     int acc = 0;
@@ -115,27 +134,26 @@ __device__ __forceinline__ void build_tables(const Args& a, int* order_s, int* p
 }
 
 template <int SCHED, int CG>
-__device__ __forceinline__ int total_tiles(const Args& a, const int* pair_prefix_s) {
+__device__ __forceinline__ int total_tiles(const Args& a, const Tables& tb) {
   const int n_tiles = a.N / kBN;
-  if (SCHED == kRows) return (CG == 1 ? __ldg(a.tile_prefix + a.num_groups) : pair_prefix_s[a.num_groups]) * n_tiles;
+  if (SCHED == kRows) return (CG == 1 ? tb.tp_s : tb.pair_s)[a.num_groups] * n_tiles;
   return a.num_groups * (a.M_w / Cfg<CG>::kTileM) * n_tiles;
 }
 
 template <int SCHED, int CG>
-__device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g, const int* order,
-                                            const int* pair_prefix_s, int rank) {
+__device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g, const Tables& tb, int rank) {
   Tile tl;
   const int n_tiles = a.N / kBN;
   tl.valid = true;
   if (SCHED == kRows) {
-    const int* pre = CG == 1 ? a.tile_prefix : pair_prefix_s;
-    while ((CG == 1 ? __ldg(pre + g + 1) : pre[g + 1]) * n_tiles <= t) ++g;
-    const int local = t - (CG == 1 ? __ldg(pre + g) : pre[g]) * n_tiles;
+    const int* pre = CG == 1 ? tb.tp_s : tb.pair_s;
+    while (pre[g + 1] * n_tiles <= t) ++g;
+    const int local = t - pre[g] * n_tiles;
     const int m_local = (local / n_tiles) * CG + rank;  // this CTA's 128-row tile in the group
     tl.group = g;
-    tl.mtile = __ldg(a.tile_prefix + g) + m_local;
-    tl.valid = tl.mtile < __ldg(a.tile_prefix + g + 1);
-    tl.m0 = __ldg(a.seg_start + g) + m_local * kBM;
+    tl.mtile = tb.tp_s[g] + m_local;
+    tl.valid = tl.mtile < tb.tp_s[g + 1];
+    tl.m0 = tb.ss_s[g] + m_local * kBM;
     tl.n0 = (local % n_tiles) * kBN;
     tl.k_row0 = 0;
     tl.num_kb = a.K / kBK;
@@ -143,12 +161,12 @@ __device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g, const 
     const int per_group = (a.M_w / Cfg<CG>::kTileM) * n_tiles;
     const int slot = t / per_group;
     const int local = t - slot * per_group;
-    g = order[slot];
+    g = tb.order_s[slot];
     tl.group = g;
     tl.m0 = (local / n_tiles) * Cfg<CG>::kTileM + rank * kBM;
     tl.n0 = (local % n_tiles) * kBN;
-    tl.k_row0 = __ldg(a.seg_start + g);
-    tl.num_kb = __ldg(a.seg_rows + g) / kBK;
+    tl.k_row0 = tb.ss_s[g];
+    tl.num_kb = tb.tp_s[slot];  // kb_s
     tl.mtile = 0;
   }
   return tl;
@@ -176,18 +194,19 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  // [tmem holder | bias 2x256 f32 | colsum 2x4x256 f32 | group order 256 | pair prefix 257]
+  // [tmem holder | bias 2x256 f32 | colsum 2x4x256 f32 | 4 schedule tables]
   float* bias_s = reinterpret_cast<float*>(tmem_holder + 4);
   float* colsum_s = bias_s + 2 * kBN;
-  int* order_s = reinterpret_cast<int*>(colsum_s + 8 * kBN);
-  int* pair_prefix_s = order_s + kMaxGroups;
+  int* tables_s = reinterpret_cast<int*>(colsum_s + 8 * kBN);
+  const Tables tb{tables_s, tables_s + kTableInts, tables_s + 2 * kTableInts, tables_s + 3 * kTableInts};
+  const int* kb_s = tb.tp_s;  // kWgrad: k-blocks per LPT slot
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
   const int rank = CG == 2 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
   const bool leader = rank == 0;
   const int cluster = blockIdx.x / CG, num_clusters = gridDim.x / CG;
-  build_tables<SCHED, CG>(args, order_s, pair_prefix_s);
+  build_tables<SCHED, CG>(args, tb);
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&map_a);
@@ -209,7 +228,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int ntiles = total_tiles<SCHED, CG>(args, pair_prefix_s);
+  const int ntiles = total_tiles<SCHED, CG>(args, tb);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer (every CTA)
@@ -220,7 +239,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       uint32_t phase = 0;
       int g = 0;
       for (int t = cluster; t < ntiles; t += num_clusters) {
-        const Tile tl = decode_tile<SCHED, CG>(args, t, g, order_s, pair_prefix_s, rank);
+        const Tile tl = decode_tile<SCHED, CG>(args, t, g, tb, rank);
         const int b_row_base = tl.group * args.b_rows_per_group;
         const int n_cta = tl.n0 + rank * C::kBNc;  // this CTA's slice of B
         for (int kb = 0; kb < tl.num_kb; ++kb) {
@@ -265,15 +284,17 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       constexpr uint32_t b_kstep = B_MN ? 16 * 128 : 32;
       int stage = 0;
       uint32_t phase = 0;
-      int g = 0;
       int iter = 0;
+      // The issuer only needs each tile's k-block count (no tile decode, no
+      // global loads between tiles: any gap here is a tensor-pipe bubble).
+      const int per_group = SCHED == kWgrad ? (args.M_w / C::kTileM) * (args.N / kBN) : 1;
       for (int t = cluster; t < ntiles; t += num_clusters, ++iter) {
-        const Tile tl = decode_tile<SCHED, CG>(args, t, g, order_s, pair_prefix_s, rank);
+        const int num_kb = SCHED == kRows ? args.K / kBK : kb_s[t / per_group];
         const int ab = iter & 1;
         ptx::mbar_wait(&tempty_bar[ab], ((iter >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + ab * kBN;
-        for (int kb = 0; kb < tl.num_kb; ++kb) {
+        for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
@@ -314,7 +335,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     int g = 0;
     int iter = 0;
     for (int t = cluster; t < ntiles; t += num_clusters, ++iter) {
-      const Tile tl = decode_tile<SCHED, CG>(args, t, g, order_s, pair_prefix_s, rank);
+      const Tile tl = decode_tile<SCHED, CG>(args, t, g, tb, rank);
       const int ab = iter & 1;
       // Everything that does not depend on the accumulator is fetched before
       // waiting on it: the tile's bias slice (to smem) and the ReLU mask bits.
@@ -358,7 +379,9 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
+#ifndef FM_DEBUG_NO_STORE
           ptx::tma_store_2d(&map_c, buf, x, y);
+#endif
           ptx::bulk_commit();
         }
         ++out_seq;
