@@ -45,7 +45,11 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+// KT = top_k (compile-time: the insertion network is KT slots deep, not 8).
+// Two CTAs per SM: the per-tile chain (TMA -> MMA -> top-k epilogue) is
+// latency-bound, a second resident CTA overlaps it (measured: 1.3x over one).
+template <int KT>
+__global__ void __launch_bounds__(kThreads, 2)
     gate_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                 const Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
-    const int k = a.top_k;
+    constexpr int k = KT;
     uint32_t* my_mask = masks + q * a.Npad;
     int iter = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
@@ -148,10 +152,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(&tfull_bar[ab], (iter >> 1) & 1);
       ptx::tc_fence_after();
 
-      float best_v[kMaxTopK];
-      int best_e[kMaxTopK];
+      float best_v[KT];
+      int best_e[KT];
 #pragma unroll
-      for (int j = 0; j < kMaxTopK; ++j) {
+      for (int j = 0; j < KT; ++j) {
         best_v[j] = -INFINITY;
         best_e[j] = -1;
       }
@@ -169,8 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // while ids ascend keeps the lower id ahead on ties.
           if (e < a.N) {
 #pragma unroll
-            for (int j = kMaxTopK - 1; j >= 0; --j) {
-              if (j >= k) continue;
+            for (int j = KT - 1; j >= 0; --j) {
               const bool beats_prev = j > 0 && (best_e[j - 1] < 0 || v > best_v[j - 1]);
               const bool beats_cur = best_e[j] < 0 || v > best_v[j];
               if (beats_prev) {
@@ -189,33 +192,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_arrive(&tempty_bar[ab]);
 
       // softmax over the kept logits (k = 1 gives weight 1)
-      float wsum = 0.0f, wexp[kMaxTopK];
+      float wsum = 0.0f, wexp[KT];
 #pragma unroll
-      for (int j = 0; j < kMaxTopK; ++j) {
-        wexp[j] = (j < k) ? expf(best_v[j] - best_v[0]) : 0.0f;
+      for (int j = 0; j < KT; ++j) {
+        wexp[j] = expf(best_v[j] - best_v[0]);
         wsum += wexp[j];
       }
 
       // warp-aggregated histogram: one bit per (lane, expert) in this warp's mask row
       if (valid) {
 #pragma unroll
-        for (int j = 0; j < kMaxTopK; ++j)
-          if (j < k) atomicOr(&my_mask[best_e[j]], 1u << lane);
+        for (int j = 0; j < KT; ++j) atomicOr(&my_mask[best_e[j]], 1u << lane);
       }
       named_bar_sync(1, 128);  // all four masks of this tile are final
       if (valid) {
         const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-        for (int j = 0; j < kMaxTopK; ++j) {
-          if (j < k) {
-            const int e = best_e[j];
-            int rank = __popc(masks[q * a.Npad + e] & lt);
-            for (int w = 0; w < q; ++w) rank += __popc(masks[w * a.Npad + e]);
-            const size_t u = static_cast<size_t>(t) * k + j;
-            a.topk_idx[u] = e;
-            a.topk_w[u] = wexp[j] / wsum;
-            a.tile_rank[u] = rank;
-          }
+        for (int j = 0; j < KT; ++j) {
+          const int e = best_e[j];
+          int rank = __popc(masks[q * a.Npad + e] & lt);
+          for (int w = 0; w < q; ++w) rank += __popc(masks[w * a.Npad + e]);
+          const size_t u = static_cast<size_t>(t) * k + j;
+          a.topk_idx[u] = e;
+          a.topk_w[u] = wexp[j] / wsum;
+          a.tile_rank[u] = rank;
         }
       }
       const int et = q * 32 + lane;
@@ -252,20 +252,34 @@ void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, 
   if (T <= 0) return;
   const int Npad = ((N + 31) / 32) * 32;
   const int stage_bytes0 = kABytes + Npad * kBK * 2;
-  const int stages = std::max(2, std::min(kMaxStages, (200 * 1024) / stage_bytes0));
+  // two CTAs per SM when both TMEM double-buffers fit (2 x 2 x Npad <= 512 columns)
+  const int kCtasPerSm = Npad <= 128 ? 2 : 1;
+  const int stages = std::max(2, std::min(kMaxStages, (200 * 1024 / kCtasPerSm) / stage_bytes0));
   Args a{T, N, Npad, d, top_k, stages, topk_idx, topk_w, tile_rank, tile_counts};
   CUtensorMap mx = make_tmap_bf16(x, d, T, d, 64, kTM);
   CUtensorMap mw = make_tmap_bf16(wg, d, N, d, 64, Npad);
   const int stage_bytes = kABytes + Npad * kBK * 2;
   const int smem = 1024 + stages * stage_bytes + 2 * kMaxStages * 8 + 64 + 4 * Npad * 4;
-  static int configured_smem = 0;
-  if (smem > configured_smem) {
-    FM_CUDA(cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured_smem = smem;
-  }
   const int tiles = gate_num_tiles(T);
-  const int grid = std::min(tiles, num_sms());
-  gate_kernel<<<grid, kThreads, smem, stream>>>(mx, mw, a);
+  const int grid = std::min(tiles, kCtasPerSm * num_sms());
+  auto launch = [&](auto kernel) {
+    static int configured_smem[kMaxTopK + 1] = {};
+    if (smem > configured_smem[top_k]) {
+      FM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      configured_smem[top_k] = smem;
+    }
+    kernel<<<grid, kThreads, smem, stream>>>(mx, mw, a);
+  };
+  switch (top_k) {
+    case 1: launch(gate_kernel<1>); break;
+    case 2: launch(gate_kernel<2>); break;
+    case 3: launch(gate_kernel<3>); break;
+    case 4: launch(gate_kernel<4>); break;
+    case 5: launch(gate_kernel<5>); break;
+    case 6: launch(gate_kernel<6>); break;
+    case 7: launch(gate_kernel<7>); break;
+    default: launch(gate_kernel<8>); break;
+  }
   FM_LAUNCH_CHECK("gate_kernel");
 }
 
