@@ -183,6 +183,27 @@ int fm_scheduler_placement(fm_scheduler* s, int which, int32_t* slots_GE, int32_
 int fm_scheduler_reset(fm_scheduler* s, const int32_t* slots_GE);
 
 /* ------------------------------------------------------------------------
+ * Trace export / replay. The reference's TokenDemand
+ * trace file "step,expert,gpu,tokens" (one line per non-zero cell, sorted by
+ * (step, expert, gpu)); device gate histograms recorded here replay in the
+ * reference engine/CLI and reference traces drive this framework.
+ * demand_SNG: [step][expert][gpu] int64, host memory.
+ * ---------------------------------------------------------------------- */
+
+/* Replaces `save_trace(std::span<const TokenDemand>, const std::string&)`
+ * (proj/include/moesim/workload.hpp:79, impl proj/src/workload.cpp:175-192).
+ * step_ids: the TokenDemand.step of each entry (NULL = 0, 1, ...). */
+int fm_trace_save(const char* path, const int64_t* demand_SNG, const int32_t* step_ids, int num_steps,
+                  int num_experts, int num_gpus);
+/* Replaces `load_trace(path)` / `load_trace(path, num_experts, num_gpus)`
+ * (workload.hpp:82-86, workload.cpp:194-341): num_experts = num_gpus = 0 infers
+ * the dimensions from the largest ids. Call with demand_SNG = NULL to get the
+ * sizes, then with a buffer of `capacity` >= steps*N*G cells. Malformed files:
+ * FM_ERR_RUNTIME with the reference's "<path>:<line>: <what>" messages. */
+int fm_trace_load(const char* path, int num_experts, int num_gpus, int64_t* demand_SNG, int64_t capacity,
+                  int* num_steps, int* num_experts_out, int* num_gpus_out);
+
+/* ------------------------------------------------------------------------
  * Grouped expert GEMM on tcgen05 (test / building-block hook).
  * seg_start, seg_rows, tile_prefix are device int32 arrays describing the
  * per-group token segments of the permuted buffers (rows multiple of 128).

@@ -139,6 +139,8 @@ class Reference(_Base):
             C.c_int,
         ),
         "ref_static_ep": ([_P, C.c_int, C.c_int, C.c_int, C.c_double, _P, _P], C.c_int),
+        "ref_save_trace": ([C.c_char_p, _P, C.c_int, C.c_int, C.c_int], C.c_int),
+        "ref_load_trace": ([C.c_char_p, C.c_int, C.c_int, _P, C.c_int64, _P], C.c_int),
         "ref_engine_run": (
             [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P],
             C.c_int,
@@ -187,6 +189,18 @@ class Reference(_Base):
     def generate_trace(self, N, G, tokens_per_step, zipf=1.25, drift=0.02, seed=42, steps=1):
         out = np.zeros((steps, N, G), np.int64)
         self._check(self.lib.ref_generate_trace(N, G, int(tokens_per_step), float(zipf), float(drift), int(seed), steps, _p(out)))
+        return out
+
+    def save_trace(self, trace, path):
+        trace = _i64(trace)
+        S, N, G = trace.shape
+        self._check(self.lib.ref_save_trace(str(path).encode(), _p(trace), S, N, G))
+
+    def load_trace(self, path, N=0, G=0):
+        dims = np.zeros(3, np.int32)
+        self._check(self.lib.ref_load_trace(str(path).encode(), N, G, None, 0, _p(dims)))
+        out = np.zeros(tuple(int(v) for v in dims), np.int64)
+        self._check(self.lib.ref_load_trace(str(path).encode(), N, G, _p(out), out.size, _p(dims)))
         return out
 
     def static_ep(self, trace, cf=1.0):

@@ -118,6 +118,26 @@ int ref_generate_trace(int N, int G, int64_t tokens, double zipf, double drift, 
   });
 }
 
+// Trace file I/O through the reference's save_trace / load_trace.
+int ref_save_trace(const char* path, const int64_t* trace, int steps, int N, int G) {
+  return guarded([&] { save_trace(to_trace(trace, steps, N, G), path); });
+}
+
+// N = G = 0: load_trace(path) (inferred dimensions); dims = {steps, N, G};
+// out (capacity cells, may be NULL) receives [steps][N][G].
+int ref_load_trace(const char* path, int N, int G, int64_t* out, int64_t capacity, int32_t* dims) {
+  return guarded([&] {
+    std::vector<TokenDemand> tr = (N == 0 && G == 0) ? load_trace(path) : load_trace(path, N, G);
+    dims[0] = static_cast<int32_t>(tr.size());
+    dims[1] = tr.front().num_experts;
+    dims[2] = tr.front().num_gpus;
+    const size_t cells = static_cast<size_t>(dims[1]) * dims[2];
+    if (!out || static_cast<int64_t>(cells * tr.size()) > capacity) return;
+    for (size_t s = 0; s < tr.size(); ++s)
+      std::memcpy(out + s * cells, tr[s].demand.data(), sizeof(int64_t) * cells);
+  });
+}
+
 // StaticEP baseline through the reference's run_baseline: per-step dropped
 // tokens and balance ratio (of the post-drop routing).
 int ref_static_ep(const int64_t* trace, int steps, int N, int G, double cf, int64_t* dropped,

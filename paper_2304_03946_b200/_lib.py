@@ -77,6 +77,8 @@ _SIGNATURES = {
     "fm_balance_ratio": [_P, _I, _I, _DP],
     "fm_largest_remainder_round": [_P, _I, C.c_int64, _P],
     "fm_static_ep_kept": [_P, _I, _I, C.c_double, _P, _I64P],
+    "fm_trace_save": [C.c_char_p, _P, _P, _I, _I, _I],
+    "fm_trace_load": [C.c_char_p, _I, _I, _P, C.c_int64, _P, _P, _P],
     "fm_static_ep_kept_device": [_P, _I, _I, C.c_double, _P, _P, _P],
     "fm_layer_set_capacity_factor": [_P, C.c_double],
     "fm_grouped_gemm": [_I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P],

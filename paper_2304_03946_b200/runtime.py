@@ -107,13 +107,16 @@ class RuntimeStep:
     migration_bytes: int = 0
     migration_ms: float = 0.0
     replica_counts: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    makespan_s: float = 0.0  # modelled step time on the effective placement (Eq. 5)
+    adjust_bytes: float = 0.0
 
 
 class FlexMoERuntime:
     def __init__(self, num_experts, top_k, d_model, d_ff, exchange: Exchange, profile: S.ClusterProfile,
                  sched_cfg: S.SchedulerConfig | None = None, max_tokens=65536, gate_weight=None,
-                 lr=1e-4, optimizer=True):
+                 lr=1e-4, optimizer=True, recorder=None):
         self.N, self.k, self.d, self.f = num_experts, top_k, d_model, d_ff
+        self.recorder = recorder  # trace.TraceRecorder: per-step device TokenDemand export
         self.ex = exchange
         self.rank, self.G = exchange.rank, exchange.world
         self.prof = profile
@@ -179,6 +182,8 @@ class FlexMoERuntime:
         w1, b1, w2, b2 = self.packed
         y = self.dl.forward(x, self.wg, w1, b1, w2, b2)
         D = self.dl.last_demand_host  # TokenDemand [N][G], copied when routing synchronised
+        if self.recorder is not None:
+            self.recorder.record(D)
         grads = self.dl.backward(dy)
         if self.optimizer and self.layer.local_experts:
             self.store.adam_step(self.layer.local_experts, grads)
@@ -186,6 +191,7 @@ class FlexMoERuntime:
         res = self.sched.finish_step(D)
         out = RuntimeStep(y=y, balance_ratio=res.report.balance_ratio, applied=applied,
                           accepted=res.accepted, migration_bytes=mig_bytes, migration_ms=mig_ms,
-                          replica_counts=S.counts_from_slots(self.slots, self.N).sum(axis=1))
+                          replica_counts=S.counts_from_slots(self.slots, self.N).sum(axis=1),
+                          makespan_s=res.report.makespan_s, adjust_bytes=res.report.adjust_bytes)
         self.history.append(out)
         return out
