@@ -183,6 +183,53 @@ int fm_scheduler_placement(fm_scheduler* s, int which, int32_t* slots_GE, int32_
 int fm_scheduler_reset(fm_scheduler* s, const int32_t* slots_GE);
 
 /* ------------------------------------------------------------------------
+ * Comparison baselines, one step at a time:
+ * replaces `run_baseline(trace, topo, BaselineConfig, SimConfig)`
+ * (proj/include/moesim/baselines.hpp, impl proj/src/baselines.cpp:81-276).
+ *   FM_BASELINE_STATIC_EP         round-robin placement, capacity drops
+ *   FM_BASELINE_FULL_REPLICATE    hottest `replicate_top` experts shadowed on
+ *                                 every GPU, re-derived from each step's demand
+ *   FM_BASELINE_STRICT_REBALANCE  loads rewritten to B/G per GPU (count level)
+ * Each step returns the reference's StepReport fields, the placement it ran
+ * on (FullReplicate runs for real on the device runtime with it), the routed
+ * demand (post-drop / rebalanced) and its flows.
+ * ---------------------------------------------------------------------- */
+#define FM_BASELINE_STATIC_EP 0
+#define FM_BASELINE_FULL_REPLICATE 1
+#define FM_BASELINE_STRICT_REBALANCE 2
+
+typedef struct fm_baseline_config {
+  int kind;
+  double capacity_factor; /* StaticEP; +inf = unlimited */
+  int replicate_top;      /* FullReplicate */
+  int metric;             /* 0 max ratio, 1 variance */
+  int max_live_groups;
+  double group_creation_latency_s;
+} fm_baseline_config;
+
+typedef struct fm_baseline_report {
+  double balance_ratio; /* baselines.cpp:31-40: max*G/sum, 1.0 when empty */
+  double metric_value;
+  double makespan_s;
+  double slot_utilization;
+  int group_misses;
+  int64_t tokens_total; /* pre-drop */
+  int64_t tokens_dropped;
+  int64_t tokens_reassigned;
+} fm_baseline_report;
+
+typedef struct fm_baseline fm_baseline;
+int fm_baseline_create(const fm_cluster_profile* profile, const fm_baseline_config* cfg, int num_experts,
+                       fm_baseline** out);
+int fm_baseline_destroy(fm_baseline* b);
+/* Any of counts_NG (int32 [N][G]), routed_demand_NG (int64 [N][G]) and
+ * flows_NGG (int64 [N][G][G]) may be NULL. */
+int fm_baseline_step(fm_baseline* b, const int64_t* demand_NG, fm_baseline_report* out, int32_t* counts_NG,
+                     int64_t* routed_demand_NG, int64_t* flows_NGG);
+/* The placement of the last step (slots_GE int32 [G][slots]). */
+int fm_baseline_placement(fm_baseline* b, int32_t* slots_GE, int32_t* counts_NG, int* slots_per_gpu);
+
+/* ------------------------------------------------------------------------
  * Trace export / replay. The reference's TokenDemand
  * trace file "step,expert,gpu,tokens" (one line per non-zero cell, sorted by
  * (step, expert, gpu)); device gate histograms recorded here replay in the

@@ -139,6 +139,7 @@ class Reference(_Base):
             C.c_int,
         ),
         "ref_static_ep": ([_P, C.c_int, C.c_int, C.c_int, C.c_double, _P, _P], C.c_int),
+        "ref_baseline_run": ([C.c_int, _P] + [C.c_int] * 4 + [C.c_double, C.c_int, C.c_int] + [_P] * 8, C.c_int),
         "ref_save_trace": ([C.c_char_p, _P, C.c_int, C.c_int, C.c_int], C.c_int),
         "ref_load_trace": ([C.c_char_p, C.c_int, C.c_int, _P, C.c_int64, _P], C.c_int),
         "ref_engine_run": (
@@ -201,6 +202,19 @@ class Reference(_Base):
         self._check(self.lib.ref_load_trace(str(path).encode(), N, G, None, 0, _p(dims)))
         out = np.zeros(tuple(int(v) for v in dims), np.int64)
         self._check(self.lib.ref_load_trace(str(path).encode(), N, G, _p(out), out.size, _p(dims)))
+        return out
+
+    def baseline_run(self, kind, trace, slots, cf=1.0, replicate_top=1, metric=0):
+        trace = _i64(trace)
+        S, N, G = trace.shape
+        out = dict(ratio=np.zeros(S), metric=np.zeros(S), makespan=np.zeros(S),
+                   misses=np.zeros(S, np.int32), dropped=np.zeros(S, np.int64),
+                   reassigned=np.zeros(S, np.int64), util=np.zeros(S), replicas=np.zeros((S, N), np.int32))
+        self._check(self.lib.ref_baseline_run(int(kind), _p(trace), S, N, G, int(slots), float(cf),
+                                              int(replicate_top), int(metric),
+                                              *[_p(out[k]) for k in ("ratio", "metric", "makespan", "misses",
+                                                                     "dropped", "reassigned", "util",
+                                                                     "replicas")]))
         return out
 
     def static_ep(self, trace, cf=1.0):

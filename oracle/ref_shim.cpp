@@ -158,6 +158,36 @@ int ref_static_ep(const int64_t* trace, int steps, int N, int G, double cf, int6
   });
 }
 
+// Any baseline through run_baseline on the default profile (slots per GPU
+// given): per-step ratio, metric, makespan, group misses, dropped,
+// reassigned, slot utilization and replica counts [steps][N].
+int ref_baseline_run(int kind, const int64_t* trace, int steps, int N, int G, int slots, double cf,
+                     int replicate_top, int metric, double* ratio, double* metric_value,
+                     double* makespan, int32_t* misses, int64_t* dropped, int64_t* reassigned,
+                     double* util, int32_t* replicas) {
+  return guarded([&] {
+    std::vector<TokenDemand> tr = to_trace(trace, steps, N, G);
+    ClusterTopology topo = ClusterTopology::from_json(ClusterTopology::default_profile(G, slots));
+    BaselineConfig b;
+    b.kind = static_cast<BaselineKind>(kind);
+    b.capacity_factor = cf;
+    b.replicate_top = replicate_top;
+    SimConfig sc;
+    sc.metric = static_cast<BalanceMetric>(metric);
+    std::vector<StepReport> reps = run_baseline(tr, topo, b, sc);
+    for (int s = 0; s < steps; ++s) {
+      ratio[s] = reps[s].balance_ratio;
+      metric_value[s] = reps[s].metric_value;
+      makespan[s] = reps[s].makespan_s;
+      misses[s] = reps[s].group_cache_misses;
+      dropped[s] = reps[s].tokens_dropped;
+      reassigned[s] = reps[s].tokens_reassigned;
+      util[s] = reps[s].slot_utilization;
+      for (int e = 0; e < N; ++e) replicas[static_cast<size_t>(s) * N + e] = reps[s].replica_counts[e];
+    }
+  });
+}
+
 // The dynamic engine (SimEngine::run) on a trace with the default profile
 // (slots per GPU given): per-step balance ratio, replica counts [steps][N],
 // and totals of applied Expand / Shrink / Migrate ops.

@@ -104,6 +104,10 @@ _SIGNATURES = {
     "fm_scheduler_ops": [_P, _I, _P, _I, _P],
     "fm_scheduler_placement": [_P, _I, _P, _P],
     "fm_scheduler_reset": [_P, _P],
+    "fm_baseline_create": [_P, _P, _I, _P],
+    "fm_baseline_destroy": [_P],
+    "fm_baseline_step": [_P, _P, _P, _P, _P, _P],
+    "fm_baseline_placement": [_P, _P, _P, _P],
     "fm_layer_gate": [_P, _P, _I, _P, _P, _P],
     "fm_layer_route": [_P, _P, _P, _P, _P],
     "fm_layer_dispatch": [_P, _P, _P, _P],

@@ -70,6 +70,12 @@ struct fm_scheduler {
   StepOutcome last;
 };
 
+namespace fm {
+namespace sched {
+ClusterProfile profile_from_c(const fm_cluster_profile* c) { return to_profile(c); }
+}  // namespace sched
+}  // namespace fm
+
 extern "C" {
 
 int fm_profile_reference_default(int num_gpus, int slots_per_gpu, fm_cluster_profile* out) {

@@ -297,7 +297,12 @@ class DistributedMoELayer:
     def _call(self, name, *args):
         L.check(getattr(L.lib(), name)(self.layer._h, *args))
 
-    def forward(self, x, wg, w1, b1, w2, b2):
+    def forward(self, x, wg, w1, b1, w2, b2, on_demand=None):
+        """on_demand(D [N][G] host) -> None | (w1, b1, w2, b2): called once the
+        step's TokenDemand is all-gathered and before routing; it may switch
+        the layer's placement (a per-step placement such as FullReplicate's
+        shadows, baselines.cpp:143-156) and return the operands of the new
+        local experts."""
         lay, d, N, k = self.layer, self.layer.d, self.layer.N, self.layer.k
         T = x.shape[0]
         dev = x.device
@@ -305,6 +310,10 @@ class DistributedMoELayer:
         hist = torch.empty(N, dtype=torch.int64, device=dev)
         self._call("fm_layer_gate", x.data_ptr(), T, wg.data_ptr(), hist.data_ptr(), stream)
         gathered = self._x("all_gather", self.ex.all_gather, hist)  # [G, N]
+        if on_demand is not None:
+            new = on_demand(gathered.cpu().numpy().T.copy())
+            if new is not None:
+                w1, b1, w2, b2 = new
         G = lay.G
         send_rows = np.zeros(G, np.int32)
         recv_rows = np.zeros(G, np.int32)

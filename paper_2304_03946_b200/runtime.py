@@ -195,3 +195,109 @@ class FlexMoERuntime:
                           makespan_s=res.report.makespan_s, adjust_bytes=res.report.adjust_bytes)
         self.history.append(out)
         return out
+
+
+class BaselineRuntime:
+    """The paper's comparison systems on the device,
+    driven by the same gate histogram as FlexMoERuntime
+    (proj/src/baselines.cpp:81-161):
+
+    * StaticEP (DeepSpeed-like): round-robin placement, the layer in capacity
+      mode drops over-capacity units on the device (the device port of the
+      reference's drop rule) — `host.demand` is the reference's kept demand;
+    * FullReplicate (FasterMoE-like shadowing): each step, after the demand
+      is all-gathered, the hottest `replicate_top` experts are shadowed on
+      every GPU: the owner (round-robin home, e % G) sends the bf16 weights +
+      f32 biases peer-to-peer, the shadows' gradients are SUM-reduced within
+      the replica group, and only the owner keeps optimizer state and steps.
+
+    Every rank runs the same host baseline on the same demand: placements
+    agree without a broadcast. `step()` returns the reference's StepReport
+    fields (`host`) next to the device outputs."""
+
+    def __init__(self, num_experts, top_k, d_model, d_ff, exchange: Exchange, profile: S.ClusterProfile,
+                 cfg: S.BaselineConfig, max_tokens=65536, gate_weight=None, lr=1e-4, optimizer=True):
+        if cfg.kind not in (S.STATIC_EP, S.FULL_REPLICATE):
+            raise ValueError("BaselineRuntime runs StaticEP or FullReplicate (StrictRebalance rewrites "
+                             "the gate's demand: count level only, scheduler.Baseline)")
+        self.N, self.k, self.d, self.f = num_experts, top_k, d_model, d_ff
+        self.ex, self.rank, self.G = exchange, exchange.rank, exchange.world
+        self.cfg = cfg
+        self.base = S.Baseline(profile, num_experts, cfg)
+        _, counts = self.base.placement()
+        self.home = np.arange(num_experts) % self.G  # round-robin owner (placement.cpp:52-68)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        slots = int(np.asarray(counts).sum(axis=0).max()) + (cfg.replicate_top if cfg.kind == S.FULL_REPLICATE else 0)
+        self.layer = MoELayer(num_experts, top_k, d_model, d_ff, replica_counts=counts, num_gpus=self.G,
+                              rank=self.rank, max_tokens=max_tokens, slots_per_gpu=slots)
+        if cfg.kind == S.STATIC_EP:
+            self.layer.set_capacity_factor(cfg.capacity_factor)
+        self.dl = DistributedMoELayer(self.layer, exchange)
+        self.store = ExpertStore(d_model, d_ff, dev, lr=lr)
+        self.owned = [e for e in range(num_experts) if self.home[e] == self.rank]
+        for e in self.owned:
+            self.store.create(e)
+        if gate_weight is None:
+            g = torch.Generator(device="cpu").manual_seed(7)
+            gate_weight = torch.randn(num_experts, d_model, generator=g) * d_model**-0.5
+        self.wg = gate_weight.to(dev).to(torch.bfloat16)
+        self.optimizer = optimizer
+        self.history: list = []
+
+    def _params(self, e):
+        m = self.store.master[e]
+        return [m["w1"].to(torch.bfloat16), m["b1"], m["w2"].to(torch.bfloat16), m["b2"]]
+
+    def _shadow(self, counts):
+        """Switch to this step's placement; owners send the shadows' weights."""
+        self.layer.set_placement(counts)
+        local = self.layer.local_experts
+        sends, recvs, got, nbytes = [], [], {}, 0
+        for e in range(self.N):  # ascending expert id on every rank: P2P pairs match in order
+            h = int(self.home[e])
+            for g in np.nonzero(counts[e] > 0)[0].tolist():
+                if g == h:
+                    continue
+                if h == self.rank:
+                    ts = self._params(e)
+                    sends += [(g, t) for t in ts]
+                    nbytes += sum(t.numel() * t.element_size() for t in ts)
+                if g == self.rank:
+                    got[e] = [torch.empty(self.f, self.d, dtype=torch.bfloat16, device=self.device),
+                              torch.empty(self.f, device=self.device),
+                              torch.empty(self.d, self.f, dtype=torch.bfloat16, device=self.device),
+                              torch.empty(self.d, device=self.device)]
+                    recvs += [(h, t) for t in got[e]]
+        self.ex.p2p(sends, recvs)
+        if not local:
+            z = torch.zeros(1, device=self.device)
+            return (z.to(torch.bfloat16), z, z.to(torch.bfloat16), z), nbytes
+        ps = [got[e] if e in got else self._params(e) for e in local]
+        return tuple(torch.stack([p[i] for p in ps]) for i in range(4)), nbytes
+
+    def step(self, x, dy):
+        info = {}
+
+        def on_demand(D):
+            res = self.base.step(D)
+            info["host"], info["D"] = res, D
+            if self.cfg.kind == S.FULL_REPLICATE:
+                ops, info["shadow_bytes"] = self._shadow(res.counts)
+                return ops
+            return None
+
+        packed = self.store.pack(self.owned) if self.cfg.kind == S.STATIC_EP else (None,) * 4
+        y = self.dl.forward(x, self.wg, *packed, on_demand=on_demand)
+        grads = self.dl.backward(dy)  # SUM over each replica group (shadows included)
+        local = self.layer.local_experts
+        if self.optimizer and self.owned:
+            idx = torch.tensor([local.index(e) for e in self.owned], device=self.device)
+            from .layer import LayerGrads
+            sub = LayerGrads(dx=grads.dx, dwg=grads.dwg, dw1=grads.dw1[idx], db1=grads.db1[idx],
+                             dw2=grads.dw2[idx], db2=grads.db2[idx])
+            self.store.adam_step(self.owned, sub)
+        out = dict(y=y, grads=grads, host=info["host"], demand=info["D"],
+                   shadow_bytes=info.get("shadow_bytes", 0), local=list(local))
+        self.history.append(out)
+        return out

@@ -207,3 +207,72 @@ class Scheduler:
     def reset(self, slots):
         s = np.ascontiguousarray(slots, np.int32)
         L.check(L.lib().fm_scheduler_reset(self._h, s.ctypes.data))
+
+
+# ---------------------------------------------------------------- baselines
+STATIC_EP, FULL_REPLICATE, STRICT_REBALANCE = 0, 1, 2
+BASELINES = {"static-ep": STATIC_EP, "full-replicate": FULL_REPLICATE, "strict-rebalance": STRICT_REBALANCE}
+
+
+class BaselineConfig(C.Structure):
+    """BaselineConfig (proj/include/moesim/baselines.hpp) + the SimConfig
+    fields a baseline step uses."""
+
+    _fields_ = [("kind", C.c_int), ("capacity_factor", C.c_double), ("replicate_top", C.c_int),
+                ("metric", C.c_int), ("max_live_groups", C.c_int), ("group_creation_latency_s", C.c_double)]
+
+    @classmethod
+    def make(cls, kind, capacity_factor=1.0, replicate_top=1, metric=0, max_live_groups=64,
+             group_creation_latency_s=0.005):
+        kind = BASELINES[kind] if isinstance(kind, str) else int(kind)
+        return cls(kind, float(capacity_factor), int(replicate_top), int(metric), int(max_live_groups),
+                   float(group_creation_latency_s))
+
+
+class BaselineReport(C.Structure):
+    _fields_ = [("balance_ratio", C.c_double), ("metric_value", C.c_double), ("makespan_s", C.c_double),
+                ("slot_utilization", C.c_double), ("group_misses", C.c_int), ("tokens_total", C.c_int64),
+                ("tokens_dropped", C.c_int64), ("tokens_reassigned", C.c_int64)]
+
+
+@dataclass
+class BaselineStep:
+    report: BaselineReport
+    counts: np.ndarray   # [N][G] placement the step ran on
+    demand: np.ndarray   # [N][G] routed demand (post-drop / rebalanced)
+    flows: np.ndarray    # [N][G][G]
+
+
+class Baseline:
+    """run_baseline (baselines.cpp:81-276), one step at a time over
+    device-produced demand: StaticEP, FullReplicate, StrictRebalance."""
+
+    def __init__(self, prof: ClusterProfile, num_experts: int, cfg: BaselineConfig):
+        self.prof, self.N, self.cfg = prof, num_experts, cfg
+        h = C.c_void_p()
+        L.check(L.lib().fm_baseline_create(C.byref(prof), C.byref(cfg), num_experts, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            L.lib().fm_baseline_destroy(self._h)
+            self._h = None
+
+    def step(self, D) -> BaselineStep:
+        D = np.ascontiguousarray(D, np.int64)
+        G = self.prof.num_gpus
+        rep = BaselineReport()
+        counts = np.zeros((self.N, G), np.int32)
+        demand = np.zeros((self.N, G), np.int64)
+        flows = np.zeros((self.N, G, G), np.int64)
+        L.check(L.lib().fm_baseline_step(self._h, D.ctypes.data, C.byref(rep), counts.ctypes.data,
+                                         demand.ctypes.data, flows.ctypes.data))
+        return BaselineStep(rep, counts, demand, flows)
+
+    def placement(self):
+        e = C.c_int()
+        L.check(L.lib().fm_baseline_placement(self._h, None, None, C.byref(e)))
+        slots = np.zeros((self.prof.num_gpus, e.value), np.int32)
+        counts = np.zeros((self.N, self.prof.num_gpus), np.int32)
+        L.check(L.lib().fm_baseline_placement(self._h, slots.ctypes.data, counts.ctypes.data, C.byref(e)))
+        return slots, counts
