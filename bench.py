@@ -260,6 +260,15 @@ class FusedArm:
         return self.layer.read("hist", self.N)
 
 
+def measured_tps(N, k, d, f):
+    """(TPS, source): the committed B200 measurement for this model shape, if any."""
+    for path in sorted(Path(__file__).resolve().parent.glob("profiles/b200_profile_*.json")):
+        m = json.loads(path.read_text())["measurement"]
+        if m["model"] == {"num_experts": N, "top_k": k, "d_model": d, "d_ff": f}:
+            return float(m["tps"]), f"measured ({path.name})"
+    return 1.2e15 / (12.0 * d * f), "assumed 1.2 PFLOP/s grouped GEMM"
+
+
 class DistArm:
     """configs[2]: one process per GPU, NCCL all-to-all / all-reduce between phases,
     drifting Zipf traffic, dynamic expand/shrink/migrate by the host scheduler with
@@ -275,13 +284,13 @@ class DistArm:
         N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
         G = world
         slots = 2 * ((N + G - 1) // G)  # vExpert budget 2*ceil(N/G) (moesim.cpp:141-146)
-        params = 2 * d * f + d + f
-        # B200 profile: NVLink 5 link / NCCL bus bandwidth (B200_PROFILING.md), expert
-        # throughput from the grouped GEMM (12*d*f FLOP per unit at ~1.2 PFLOP/s),
-        # f32 gradients, 14 B/param of state (bf16 + f32 master + Adam m, v).
-        prof = S.ClusterProfile.b200(G, slots, tps=1.2e15 / (12.0 * d * f),
-                                     expert_param_bytes=4.0 * params,
-                                     expert_state_bytes=14.0 * params, token_bytes=2.0 * d)
+        # B200 profile (paper_2304_03946_b200/profile.py): NVLink 5 link / NCCL bus
+        # bandwidth (B200_PROFILING.md), f32 gradients, 14 B/param of state, and the
+        # per-GPU TPS MEASURED on a B200 for this model shape (profiles/b200_profile_*.json;
+        # without one, the grouped GEMM's 12*d*f FLOP per unit at 1.2 PFLOP/s).
+        from paper_2304_03946_b200.profile import b200_profile
+        self.tps, self.tps_source = measured_tps(N, k, d, f)
+        prof = b200_profile(G, slots, self.tps, d, f)
         import torch.distributed as tdist
 
         ex = TorchExchange() if tdist.is_initialized() else LoopbackHub(1).endpoint(0)
@@ -337,6 +346,7 @@ class DistArm:
 
     def summary(self, steps):
         return {"placement": "dynamic (host scheduler: expand/shrink/migrate, B200 profile)",
+                "profile_tps": self.tps, "profile_tps_source": self.tps_source,
                 "balance_ratio_mean": float(np.mean(self.ratios)) if self.ratios else None,
                 "balance_ratio_last": self.ratios[-1] if self.ratios else None,
                 "ops_accepted": self.accepted, "ops_applied": self.applied,

@@ -140,6 +140,7 @@ class Reference(_Base):
         ),
         "ref_static_ep": ([_P, C.c_int, C.c_int, C.c_int, C.c_double, _P, _P], C.c_int),
         "ref_baseline_run": ([C.c_int, _P] + [C.c_int] * 4 + [C.c_double, C.c_int, C.c_int] + [_P] * 8, C.c_int),
+        "ref_topology_load": ([C.c_char_p, _P, _P, _P, _P], C.c_int),
         "ref_save_trace": ([C.c_char_p, _P, C.c_int, C.c_int, C.c_int], C.c_int),
         "ref_load_trace": ([C.c_char_p, C.c_int, C.c_int, _P, C.c_int64, _P], C.c_int),
         "ref_engine_run": (
@@ -191,6 +192,12 @@ class Reference(_Base):
         out = np.zeros((steps, N, G), np.int64)
         self._check(self.lib.ref_generate_trace(N, G, int(tokens_per_step), float(zipf), float(drift), int(seed), steps, _p(out)))
         return out
+
+    def topology_load(self, path):
+        ints, dbl = np.zeros(3, np.int32), np.zeros(6)
+        intra, inter = np.zeros(65), np.zeros(65)
+        self._check(self.lib.ref_topology_load(str(path).encode(), _p(ints), _p(dbl), _p(intra), _p(inter)))
+        return ints, dbl, intra, inter
 
     def save_trace(self, trace, path):
         trace = _i64(trace)

@@ -7,6 +7,7 @@
 // by bench.py's reference arm for the count-level CPU path timing.
 // No reference source is copied: this file only calls the public API in
 // proj/include/moesim/*.hpp.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -135,6 +136,39 @@ int ref_load_trace(const char* path, int N, int G, int64_t* out, int64_t capacit
     if (!out || static_cast<int64_t>(cells * tr.size()) > capacity) return;
     for (size_t s = 0; s < tr.size(); ++s)
       std::memcpy(out + s * cells, tr[s].demand.data(), sizeof(int64_t) * cells);
+  });
+}
+
+// ClusterTopology::from_file: ints {num_gpus, gpus_per_node, vexperts};
+// dbl {intra_bw, inter_bw, tps, param_bytes, state_bytes, token_bytes};
+// intra/inter bps by group size (65 entries each, 0 = absent).
+int ref_topology_load(const char* path, int32_t* ints, double* dbl, double* intra, double* inter) {
+  return guarded([&] {
+    ClusterTopology t = ClusterTopology::from_file(path);
+    ints[0] = t.num_gpus();
+    ints[1] = t.gpus_per_node();
+    ints[2] = t.vexperts_per_gpu();
+    dbl[0] = t.intra_node_bandwidth();
+    dbl[1] = t.inter_node_bandwidth();
+    dbl[2] = t.tps();
+    dbl[3] = t.expert_param_bytes();
+    dbl[4] = t.expert_state_bytes();
+    dbl[5] = t.token_bytes();
+    for (int n = 0; n <= 64; ++n) intra[n] = inter[n] = 0;
+    std::vector<GpuId> grp;
+    for (int n = 2; n <= t.num_gpus() && n <= 64; ++n) {
+      grp.clear();
+      for (int g = 0; g < n; ++g) grp.push_back(g);
+      if (!t.spans_nodes(grp)) intra[n] = t.group_bps(grp);
+      std::vector<GpuId> wide;  // same size across nodes (first GPU of each node, then fill)
+      if (t.num_gpus() > t.gpus_per_node()) {
+        for (int g = 0; g < t.num_gpus() && static_cast<int>(wide.size()) < n; g += t.gpus_per_node())
+          wide.push_back(g);
+        for (int g = 0; g < t.num_gpus() && static_cast<int>(wide.size()) < n; ++g)
+          if (std::find(wide.begin(), wide.end(), g) == wide.end()) wide.push_back(g);
+        if (wide.size() == static_cast<size_t>(n) && t.spans_nodes(wide)) inter[n] = t.group_bps(wide);
+      }
+    }
   });
 }
 

@@ -35,6 +35,41 @@ class ClusterProfile(C.Structure):
         return p
 
     @classmethod
+    def from_json(cls, cfg):
+        """ClusterTopology::from_json / from_file (topology.cpp:64-138): a dict,
+        a JSON string or a path."""
+        import json
+        import os
+        if isinstance(cfg, (str, bytes, os.PathLike)) and not str(cfg).lstrip().startswith("{"):
+            try:
+                with open(cfg) as fh:
+                    cfg = json.load(fh)
+            except OSError:
+                raise L.FlexMoEError(f"cannot open topology config: {os.fspath(cfg)}") from None
+        elif isinstance(cfg, (str, bytes)):
+            cfg = json.loads(cfg)
+        return _profile_from_json(cls, cfg)
+
+    def to_json(self) -> dict:
+        """ClusterTopology::to_json (topology.cpp:222-255)."""
+        G, gpn = self.num_gpus, self.gpus_per_node
+        cfg = {"num_gpus": G, "gpus_per_node": gpn, "vexperts_per_gpu": self.slots_per_gpu,
+               "intra_node_bandwidth_bps": self.intra_node_bandwidth_bps, "tps": self.tps,
+               "expert_param_bytes": self.expert_param_bytes, "expert_state_bytes": self.expert_state_bytes,
+               "token_bytes": self.token_bytes}
+        if self.inter_node_bandwidth_bps > 0:
+            cfg["inter_node_bandwidth_bps"] = self.inter_node_bandwidth_bps
+        bps = {}
+        max_intra = min(gpn, G)
+        if max_intra >= 2:
+            bps["intra"] = {str(n): self.allreduce_bps_intra[n] for n in range(2, max_intra + 1)}
+        if G > gpn:
+            bps["inter"] = {str(n): self.allreduce_bps_inter[n] for n in range(2, G + 1)}
+        if bps:
+            cfg["allreduce_bps"] = bps
+        return cfg
+
+    @classmethod
     def b200(cls, num_gpus, slots_per_gpu, tps, expert_param_bytes, expert_state_bytes, token_bytes,
              link_bps=770e9, allreduce_bus_bps=725e9):
         """One NVSwitch node of B200s: uniform peers (NVLink 5, measured 770 GB/s
@@ -48,6 +83,83 @@ class ClusterProfile(C.Structure):
         for n in range(2, num_gpus + 1):  # algorithm bandwidth = bus bandwidth * n / (2(n-1))
             p.allreduce_bps_intra[n] = allreduce_bus_bps * n / (2.0 * (n - 1))
         return p
+
+
+def _topology_error(msg):
+    return L.InvalidArgument("topology config: " + msg)
+
+
+def _positive(cfg, key):
+    if key not in cfg:
+        raise _topology_error(f"missing field '{key}'")
+    v = float(cfg[key])
+    if not v > 0:
+        raise _topology_error(f"non-positive {key}")
+    return v
+
+
+def _bps_table(table, max_size, span):
+    out = [0.0] * (max_size + 1)
+    for n in range(2, max_size + 1):
+        key = str(n)
+        if key not in table:
+            raise _topology_error(f"allreduce_bps.{span} missing entry for group size {key}")
+        v = float(table[key])
+        if not v > 0:
+            raise _topology_error(f"non-positive allreduce_bps.{span}[{key}]")
+        if n > 2 and v > out[n - 1]:
+            raise _topology_error(f"allreduce_bps.{span} must be non-increasing in group size")
+        out[n] = v
+    return out
+
+
+def _profile_from_json(cls, cfg):
+    """ClusterTopology::from_json (topology.cpp:64-128): same fields, checks
+    and messages."""
+    for key in ("num_gpus", "gpus_per_node", "vexperts_per_gpu"):
+        if key not in cfg:
+            raise _topology_error(f"missing field '{key}'")
+    G, gpn, E = int(cfg["num_gpus"]), int(cfg["gpus_per_node"]), int(cfg["vexperts_per_gpu"])
+    if G < 1:
+        raise _topology_error("num_gpus must be >= 1")
+    if gpn < 1 or G % gpn != 0:
+        raise _topology_error("num_gpus must be a positive multiple of gpus_per_node")
+    if E < 1:
+        raise _topology_error("vexperts_per_gpu must be >= 1")
+    if G > MAX_GROUP:
+        raise L.InvalidArgument(f"profile: at most {MAX_GROUP} GPUs")
+    p = cls()
+    p.num_gpus, p.gpus_per_node, p.slots_per_gpu = G, gpn, E
+    p.intra_node_bandwidth_bps = _positive(cfg, "intra_node_bandwidth_bps")
+    p.tps = _positive(cfg, "tps")
+    p.expert_param_bytes = _positive(cfg, "expert_param_bytes")
+    p.expert_state_bytes = _positive(cfg, "expert_state_bytes")
+    p.token_bytes = _positive(cfg, "token_bytes")
+    multi = G > gpn
+    if multi or "inter_node_bandwidth_bps" in cfg:
+        p.inter_node_bandwidth_bps = _positive(cfg, "inter_node_bandwidth_bps")
+    if G >= 2:
+        if "allreduce_bps" not in cfg:
+            raise _topology_error("missing field 'allreduce_bps'")
+        tables = cfg["allreduce_bps"]
+        max_intra = min(gpn, G)
+        intra = inter = None
+        if max_intra >= 2:
+            if "intra" not in tables:
+                raise _topology_error("missing allreduce_bps.intra")
+            intra = _bps_table(tables["intra"], max_intra, "intra")
+            for n, v in enumerate(intra):
+                p.allreduce_bps_intra[n] = v
+        if multi:
+            if "inter" not in tables:
+                raise _topology_error("missing allreduce_bps.inter")
+            inter = _bps_table(tables["inter"], G, "inter")
+            for n in range(2, max_intra + 1):
+                if inter[n] > intra[n]:
+                    raise _topology_error(f"inter-node bps exceeds intra-node bps for group size {n}")
+            for n, v in enumerate(inter):
+                p.allreduce_bps_inter[n] = v
+    return p
 
 
 class PlacementOp(C.Structure):
