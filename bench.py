@@ -309,7 +309,7 @@ class DistArm:
 
     def reset_stats(self):
         self.mig_bytes = 0
-        self.mig_ms = 0.0
+        self.mig0 = self.rt.migration_stats()
         self.applied = 0
         self.accepted = 0
         self.ratios = []
@@ -324,7 +324,6 @@ class DistArm:
         self.rt.wg[:, 0] = torch.tensor(self.logp * 2, dtype=torch.float32).to(self.rt.wg)
         out = self.rt.step(x, dy)
         self.mig_bytes += out.migration_bytes
-        self.mig_ms += out.migration_ms
         self.applied += len(out.applied)
         self.accepted += len(out.accepted)
         self.ratios.append(out.balance_ratio)
@@ -351,7 +350,9 @@ class DistArm:
                 "balance_ratio_last": self.ratios[-1] if self.ratios else None,
                 "ops_accepted": self.accepted, "ops_applied": self.applied,
                 "migration_bytes_per_step": self.mig_bytes / steps,
-                "migration_ms_per_step": self.mig_ms / steps,
+                "migration_copy_ms_per_step": (self.rt.migration_stats()["copy_ms"] - self.mig0["copy_ms"]) / steps,
+                "migration_transport": "P2P cudaMemcpyAsync of pool slots on a side stream (CUDA IPC), "
+                                       "overlapped with gate/routing/dispatch",
                 "replica_counts": self.rt.history[-1].replica_counts.tolist() if self.rt.history else None}
 
 

@@ -410,6 +410,75 @@ int fm_layer_copy_out(fm_layer* layer, int field, void* host, size_t max_bytes, 
 int fm_layer_set_timing(fm_layer* layer, int enable);
 int fm_layer_read_timing(fm_layer* layer, double* ms_by_phase, int* launches_by_phase);
 
+/* ------------------------------------------------------------------------
+ * Expert state pool and peer-to-peer migration (one per GPU).
+ *
+ * The reference models a placement change as TransferDescriptor{src, dst,
+ * bytes} (proj/include/moesim/placement.hpp:31-35, produced by
+ * Placement::expand/migrate, placement.cpp:143-232) drained by the adjustment
+ * queue (sim_engine.cpp:124-262); bytes = expert_state_bytes (topology.cpp:177).
+ * Here the state really moves: every hosted expert owns one slot of a
+ * cudaMalloc'd pool holding its f32 master parameters and Adam moments,
+ *   slot = [ master | m | v ], each P = 2*f*d + f + d floats laid out
+ *          [ w1 (f,d) | b1 (f) | w2 (d,f) | b2 (d) ],
+ * and a transfer is a cudaMemcpyAsync of one slot from a peer GPU's pool
+ * (CUDA IPC, NVLink / NVSwitch) on the pool's side stream, issued by the
+ * receiving GPU. The bf16 working copy is re-derived from the master on
+ * arrival (bit-identical to the source's, which rounds the same floats).
+ * The copies overlap the gate / routing / dispatch of the step; the compute
+ * stream waits for them (fm_pool_wait_ready) only before the expert FFN.
+ *
+ * Ordering contract: a source slot may be pulled during the step in which
+ * the placement changed; it must not be written before every peer has passed
+ * that step's expert FFN (any later full-world collective orders it), and a
+ * slot vacated in step s is reused no earlier than step s+1.
+ * ---------------------------------------------------------------------- */
+typedef struct fm_expert_pool fm_expert_pool;
+
+/* Adam hyper-parameters of fm_pool_adam (bias-corrected, step >= 1). */
+typedef struct fm_adam_config {
+  float lr;
+  float beta1;
+  float beta2;
+  float eps;
+  int step;
+} fm_adam_config;
+
+/* `slots` expert slots on the current device, `world` peer pools addressable. */
+int fm_pool_create(int slots, int d_model, int d_ff, int world, fm_expert_pool** out);
+int fm_pool_destroy(fm_expert_pool* pool);
+/* P (floats per tensor set) and the slot stride in bytes (>= 12*P, 256-aligned). */
+int fm_pool_info(const fm_expert_pool* pool, int64_t* params_per_expert, int64_t* slot_bytes);
+/* Device address of slot `slot` (master at +0, m at +4P bytes, v at +8P). */
+int fm_pool_slot_ptr(fm_expert_pool* pool, int slot, void** dev_ptr);
+/* cudaIpcMemHandle_t of the pool allocation (64 bytes) and its import on a peer
+ * process; fm_pool_link_peer links a pool of the same process instead. */
+int fm_pool_ipc_handle(fm_expert_pool* pool, void* handle64);
+int fm_pool_open_peer(fm_expert_pool* pool, int peer, const void* handle64);
+int fm_pool_link_peer(fm_expert_pool* pool, int peer, fm_expert_pool* peer_pool);
+/* Pull expert states: moves_n3[i] = {dst_slot (local), peer, src_slot (peer's)};
+ * whole slots (12*P bytes each) copied peer -> local on the side stream after
+ * everything already enqueued on `stream`. Then the bf16/f32 operand packing of
+ * the `num_local` experts in `local_slots` (ascending expert id) into w1 [n,f,d]
+ * bf16, b1 [n,f] f32, w2 [n,d,f] bf16, b2 [n,d] f32 (device) runs on the side
+ * stream too; fm_pool_wait_ready makes a stream wait for both. */
+int fm_pool_migrate(fm_expert_pool* pool, const int32_t* moves_n3, int num_moves,
+                    const int32_t* local_slots, int num_local, void* w1, float* b1, void* w2,
+                    float* b2, void* stream);
+int fm_pool_wait_ready(fm_expert_pool* pool, void* stream);
+/* Packing alone, on `stream`. */
+int fm_pool_pack(fm_expert_pool* pool, const int32_t* local_slots, int num_local, void* w1, float* b1,
+                 void* w2, float* b2, void* stream);
+/* Fused Adam on the local experts (slot i <- grads [i] of dw1 [n,f,d], db1 [n,f],
+ * dw2 [n,d,f], db2 [n,d] f32) that also refreshes the packed operands. */
+int fm_pool_adam(fm_expert_pool* pool, const int32_t* local_slots, int num_local, const float* dw1,
+                 const float* db1, const float* dw2, const float* db2, const fm_adam_config* cfg,
+                 void* w1, float* b1, void* w2, float* b2, void* stream);
+/* Totals over all fm_pool_migrate calls so far: side-stream copy time (CUDA
+ * events around each batch of copies; synchronises on the last one), bytes
+ * pulled, slots pulled. */
+int fm_pool_migration_stats(fm_expert_pool* pool, double* copy_ms, int64_t* bytes, int64_t* copies);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

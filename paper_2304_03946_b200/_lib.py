@@ -117,6 +117,18 @@ _SIGNATURES = {
     "fm_layer_expert_backward": [_P] * 10,
     "fm_layer_unpermute_backward": [_P] * 7,
     "fm_layer_read_timing": [_P, _P, _P],
+    "fm_pool_create": [_I, _I, _I, _I, C.POINTER(_P)],
+    "fm_pool_destroy": [_P],
+    "fm_pool_info": [_P, _P, _P],
+    "fm_pool_slot_ptr": [_P, _I, C.POINTER(_P)],
+    "fm_pool_ipc_handle": [_P, _P],
+    "fm_pool_open_peer": [_P, _I, _P],
+    "fm_pool_link_peer": [_P, _I, _P],
+    "fm_pool_migrate": [_P, _P, _I, _P, _I, _P, _P, _P, _P, _P],
+    "fm_pool_wait_ready": [_P, _P],
+    "fm_pool_pack": [_P, _P, _I, _P, _P, _P, _P, _P],
+    "fm_pool_adam": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "fm_pool_migration_stats": [_P, _P, _P, _P],
 }
 _RESTYPES = {"fm_last_error": C.c_char_p, "fm_version": C.c_char_p}
 

@@ -134,6 +134,11 @@ class Exchange:
         matched per (src, dst) pair in list order. Called by every rank."""
         raise NotImplementedError
 
+    def share_pool(self, pool) -> None:
+        """Map every peer's ExpertPool into `pool` (collective): CUDA IPC handles
+        across processes, plain pointers in one process."""
+        raise NotImplementedError
+
 
 class TorchExchange(Exchange):
     """torch.distributed transport (NCCL on B200 / NVLink; gloo on CPU)."""
@@ -166,6 +171,13 @@ class TorchExchange(Exchange):
         if ops:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
+
+    def share_pool(self, pool):
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, pool.ipc_handle())
+        for peer, h in enumerate(handles):
+            if peer != self.rank:
+                pool.open_peer(peer, h)
 
     def all_reduce(self, t, group):
         if group is None:
@@ -229,6 +241,11 @@ class LoopbackExchange(Exchange):
             t.copy_(inbox[src][i])
             taken[src] = i + 1
         self._swap(None)  # senders keep their tensors alive until copied
+
+    def share_pool(self, pool):
+        for peer, other in enumerate(self._swap(pool)):
+            if peer != self.rank:
+                pool.link_peer(peer, other)
 
     def all_reduce(self, t, group):
         members = range(self.world) if group is None else group
@@ -297,12 +314,14 @@ class DistributedMoELayer:
     def _call(self, name, *args):
         L.check(getattr(L.lib(), name)(self.layer._h, *args))
 
-    def forward(self, x, wg, w1, b1, w2, b2, on_demand=None):
+    def forward(self, x, wg, w1, b1, w2, b2, on_demand=None, before_experts=None):
         """on_demand(D [N][G] host) -> None | (w1, b1, w2, b2): called once the
         step's TokenDemand is all-gathered and before routing; it may switch
         the layer's placement (a per-step placement such as FullReplicate's
         shadows, baselines.cpp:143-156) and return the operands of the new
-        local experts."""
+        local experts. before_experts(): called right before the expert FFN
+        is enqueued (the runtime makes the stream wait for migrated expert
+        state there, so the copies overlap gate, routing and dispatch)."""
         lay, d, N, k = self.layer, self.layer.d, self.layer.N, self.layer.k
         T = x.shape[0]
         dev = x.device
@@ -330,6 +349,8 @@ class DistributedMoELayer:
         back = torch.empty_like(send)
         self._call("fm_layer_dispatch", x.data_ptr(), send.data_ptr(), stream)
         self._x("a2a", self.ex.all_to_all, recv[: sum(recv_rows)], send[: T * k], recv_rows, send_rows)
+        if before_experts is not None:
+            before_experts()
         self._call("fm_layer_expert_forward", recv.data_ptr(), w1.data_ptr(), b1.data_ptr(),
                    w2.data_ptr(), b2.data_ptr(), ret.data_ptr(), stream)
         self._x("a2a", self.ex.all_to_all, back[: T * k], ret[: sum(recv_rows)], send_rows, recv_rows)

@@ -44,8 +44,10 @@ def expert_param_bytes(d, f):
 
 
 def expert_state_bytes(d, f):
-    """bf16 weights + f32 master + Adam m/v: 14 B per parameter."""
-    return 14.0 * (2 * d * f + d + f)
+    """f32 master + Adam m/v: 12 B per parameter — what an ExpertPool slot
+    transfer moves (pool.py; the bf16 working copy of SURVEY.md §8d's 14 B is
+    re-derived from the master on arrival instead of being copied)."""
+    return 12.0 * (2 * d * f + d + f)
 
 
 def _column(N, units, zipf):

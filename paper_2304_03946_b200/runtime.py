@@ -14,13 +14,16 @@ Per training step on every rank (one process per GPU):
 Every rank runs the same deterministic scheduler on the same all-gathered
 demand, so placements agree without any broadcast.
 
-Expert state moved per transfer = bf16 weights + f32 master weights + Adam
-m/v (14 bytes per parameter); the peer copies use the
-exchange's P2P path (NCCL send/recv over NVLink with torch.distributed).
+Expert state lives in a per-GPU ExpertPool (pool.py, csrc/expert_pool.cu):
+f32 master weights + Adam m/v, 12 bytes per parameter (the bf16 working copy
+is re-derived on arrival, so the 14 B/param of SURVEY.md §8d shrink to 12).
+A transfer is a peer-to-peer cudaMemcpyAsync of one slot, pulled by the
+receiving GPU on the pool's side stream (CUDA IPC mapping of the source's
+pool); the compute stream waits for it only before the expert FFN, so the
+copy overlaps the gate, the demand all-gather, routing and the dispatch.
 """
 from __future__ import annotations
 
-import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -29,74 +32,7 @@ import torch
 from . import scheduler as S
 from .distributed import DistributedMoELayer, Exchange
 from .layer import MoELayer
-
-_TENSORS = ("w1", "b1", "w2", "b2")
-
-
-class ExpertStore:
-    """Parameters and Adam state of the experts hosted on this GPU."""
-
-    def __init__(self, d, f, device, lr=1e-4, betas=(0.9, 0.999), eps=1e-8):
-        self.d, self.f, self.device = d, f, device
-        self.lr, self.betas, self.eps = lr, betas, eps
-        self.master: dict[int, dict[str, torch.Tensor]] = {}  # f32
-        self.m: dict[int, dict[str, torch.Tensor]] = {}
-        self.v: dict[int, dict[str, torch.Tensor]] = {}
-        self.t = 0
-
-    @staticmethod
-    def init_expert(e, d, f):
-        g = torch.Generator(device="cpu").manual_seed(10_000 + e)  # identical on every rank
-        return {"w1": torch.randn(f, d, generator=g) * d**-0.5, "b1": torch.randn(f, generator=g) * 0.02,
-                "w2": torch.randn(d, f, generator=g) * f**-0.5, "b2": torch.randn(d, generator=g) * 0.02}
-
-    def create(self, e):
-        p = self.init_expert(e, self.d, self.f)
-        self.master[e] = {k: v.to(self.device) for k, v in p.items()}
-        self.m[e] = {k: torch.zeros_like(v) for k, v in self.master[e].items()}
-        self.v[e] = {k: torch.zeros_like(v) for k, v in self.master[e].items()}
-
-    def state(self, e) -> list[torch.Tensor]:
-        """The tensors that make up expert e's model state, in a fixed order."""
-        return [self.master[e][k] for k in _TENSORS] + [self.m[e][k] for k in _TENSORS] + \
-               [self.v[e][k] for k in _TENSORS]
-
-    def empty_state(self, e):
-        shapes = {"w1": (self.f, self.d), "b1": (self.f,), "w2": (self.d, self.f), "b2": (self.d,)}
-        self.master[e] = {k: torch.empty(s, device=self.device) for k, s in shapes.items()}
-        self.m[e] = {k: torch.empty(s, device=self.device) for k, s in shapes.items()}
-        self.v[e] = {k: torch.empty(s, device=self.device) for k, s in shapes.items()}
-        return self.state(e)
-
-    def drop(self, e):
-        for d_ in (self.master, self.m, self.v):
-            d_.pop(e, None)
-
-    def state_bytes(self, e) -> int:
-        return sum(t.numel() * t.element_size() for t in self.state(e)) + \
-            sum(self.master[e][k].numel() * 2 for k in ("w1", "w2"))  # + the bf16 working copy
-
-    def pack(self, local):
-        """Layer operands for the local experts (ascending id): bf16 weights, f32 biases."""
-        if not local:
-            z = torch.zeros(1, device=self.device)
-            return z.to(torch.bfloat16), z, z.to(torch.bfloat16), z
-        st = lambda k: torch.stack([self.master[e][k] for e in local])
-        return st("w1").to(torch.bfloat16), st("b1"), st("w2").to(torch.bfloat16), st("b2")
-
-    @torch.no_grad()
-    def adam_step(self, local, grads):
-        """One Adam step per local expert from the (replica-summed) gradients."""
-        self.t += 1
-        b1, b2 = self.betas
-        c1, c2 = 1 - b1**self.t, 1 - b2**self.t
-        for i, e in enumerate(local):
-            for k, gk in zip(_TENSORS, (grads.dw1[i], grads.db1[i], grads.dw2[i], grads.db2[i])):
-                m, v, w = self.m[e][k], self.v[e][k], self.master[e][k]
-                m.mul_(b1).add_(gk, alpha=1 - b1)
-                v.mul_(b2).addcmul_(gk, gk, value=1 - b2)
-                w.addcdiv_(m / c1, (v / c2).sqrt_().add_(self.eps), value=-self.lr)
-
+from .pool import ExpertStore, SlotAllocator, apply_placement_change
 
 @dataclass
 class RuntimeStep:
@@ -104,8 +40,7 @@ class RuntimeStep:
     balance_ratio: float
     applied: list
     accepted: list
-    migration_bytes: int = 0
-    migration_ms: float = 0.0
+    migration_bytes: int = 0  # expert state pulled by this GPU this step (copies run async)
     replica_counts: np.ndarray = field(default_factory=lambda: np.zeros(0))
     makespan_s: float = 0.0  # modelled step time on the effective placement (Eq. 5)
     adjust_bytes: float = 0.0
@@ -127,9 +62,20 @@ class FlexMoERuntime:
         self.layer = MoELayer(num_experts, top_k, d_model, d_ff, replica_counts=counts, num_gpus=self.G,
                               rank=self.rank, max_tokens=max_tokens, slots_per_gpu=profile.slots_per_gpu)
         self.dl = DistributedMoELayer(self.layer, exchange)
-        self.store = ExpertStore(d_model, d_ff, dev, lr=lr)
+        # every rank tracks every rank's slot table (same ops, same order): a
+        # receiver knows the source's slot without a round trip. A GPU hosts at
+        # most E experts; vacated slots stay readable for one step -> 2E slots.
+        E = profile.slots_per_gpu
+        self.slot_dir = [SlotAllocator(2 * E) for _ in range(self.G)]
+        self.store = ExpertStore(d_model, d_ff, dev, capacity=2 * E, world=self.G, max_local=E, lr=lr,
+                                 allocator=self.slot_dir[self.rank])
+        for g in range(self.G):
+            for e in range(num_experts):
+                if counts[e, g] > 0:
+                    self.slot_dir[g].host(e)
         for e in self.layer.local_experts:
             self.store.create(e)
+        exchange.share_pool(self.store.pool)
         if gate_weight is None:
             g = torch.Generator(device="cpu").manual_seed(7)
             gate_weight = torch.randn(num_experts, d_model, generator=g) * d_model**-0.5
@@ -139,58 +85,45 @@ class FlexMoERuntime:
         self.history: list[RuntimeStep] = []
 
     # ------------------------------------------------------------ migrations
-    def _moves(self, old_counts, new_counts):
-        """(expert, src, dst) state copies: every GPU that newly hosts an expert
-        receives it from the lowest-id GPU that hosted it before (a holder of
-        the up-to-date state). Identical on every rank, so sends and receives
-        pair up without negotiation."""
-        moves = []
-        for e in range(self.N):
-            holders = np.nonzero(old_counts[e] > 0)[0]
-            for g in np.nonzero((new_counts[e] > 0) & (old_counts[e] == 0))[0]:
-                moves.append((e, int(holders[0]), int(g)))
-        return moves
-
     def _apply(self, ops):
-        """Make `ops` effective on this rank: move expert states, re-pack."""
+        """Make `ops` effective on this rank: update every rank's slot table,
+        pull the states this GPU newly hosts from their sources' pools on the
+        side stream, re-pack the local operands there too. Returns the bytes
+        this GPU pulls; the copies complete asynchronously (the step's expert
+        FFN waits for them)."""
         old_counts = S.counts_from_slots(self.slots, self.N)
         for op in ops:  # Placement::apply in queue order (sim_engine.cpp:256-260)
             self.slots, _ = S.apply_op(self.slots, self.N, self.prof, op)
         counts = S.counts_from_slots(self.slots, self.N)
+        pulls = [(ds, src, ss) for _, src, ss, dst, ds in apply_placement_change(self.slot_dir, old_counts, counts)
+                 if dst == self.rank]
         new_local = [e for e in range(self.N) if counts[e, self.rank] > 0]
-        t0 = time.perf_counter()
-        sends, recvs, nbytes = [], [], 0
-        for e, src, dst in self._moves(old_counts, counts):
-            if src == self.rank:
-                sends += [(dst, t) for t in self.store.state(e)]
-                nbytes += sum(t.numel() * t.element_size() for t in self.store.state(e))
-            if dst == self.rank:
-                recvs += [(src, t) for t in self.store.empty_state(e)]
-        self.ex.p2p(sends, recvs)
-        old_local = set(np.nonzero(old_counts[:, self.rank] > 0)[0].tolist())
-        for e in old_local - set(new_local):
-            self.store.drop(e)
         self.layer.set_placement(counts)
-        self.packed = self.store.pack(new_local)
-        torch.cuda.synchronize()
-        return nbytes, (time.perf_counter() - t0) * 1e3
+        self.store.pool.migrate(pulls, self.store.slots(new_local), self.store.packed(max(1, len(new_local))))
+        self.packed = self.store.packed(max(1, len(new_local)))
+        return len(pulls) * self.store.pool.state_bytes
+
+    def migration_stats(self) -> dict:
+        """Side-stream copy time, bytes and slots pulled by this GPU so far."""
+        ms, nbytes, copies = self.store.pool.migration_stats()
+        return {"copy_ms": ms, "bytes": nbytes, "copies": copies}
 
     # ------------------------------------------------------------ one step
     def step(self, x, dy) -> RuntimeStep:
         applied = self.sched.begin_step()
-        mig_bytes, mig_ms = self._apply(applied) if applied else (0, 0.0)
+        mig_bytes = self._apply(applied) if applied else 0
         w1, b1, w2, b2 = self.packed
-        y = self.dl.forward(x, self.wg, w1, b1, w2, b2)
+        y = self.dl.forward(x, self.wg, w1, b1, w2, b2,
+                            before_experts=lambda: self.store.pool.wait_ready())
         D = self.dl.last_demand_host  # TokenDemand [N][G], copied when routing synchronised
         if self.recorder is not None:
             self.recorder.record(D)
         grads = self.dl.backward(dy)
         if self.optimizer and self.layer.local_experts:
-            self.store.adam_step(self.layer.local_experts, grads)
-            self.packed = self.store.pack(self.layer.local_experts)
+            self.store.adam_step(self.layer.local_experts, grads)  # refreshes self.packed in place
         res = self.sched.finish_step(D)
         out = RuntimeStep(y=y, balance_ratio=res.report.balance_ratio, applied=applied,
-                          accepted=res.accepted, migration_bytes=mig_bytes, migration_ms=mig_ms,
+                          accepted=res.accepted, migration_bytes=mig_bytes,
                           replica_counts=S.counts_from_slots(self.slots, self.N).sum(axis=1),
                           makespan_s=res.report.makespan_s, adjust_bytes=res.report.adjust_bytes)
         self.history.append(out)
@@ -234,8 +167,8 @@ class BaselineRuntime:
         if cfg.kind == S.STATIC_EP:
             self.layer.set_capacity_factor(cfg.capacity_factor)
         self.dl = DistributedMoELayer(self.layer, exchange)
-        self.store = ExpertStore(d_model, d_ff, dev, lr=lr)
         self.owned = [e for e in range(num_experts) if self.home[e] == self.rank]
+        self.store = ExpertStore(d_model, d_ff, dev, capacity=max(1, len(self.owned)), lr=lr)
         for e in self.owned:
             self.store.create(e)
         if gate_weight is None:
