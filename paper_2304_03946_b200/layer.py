@@ -116,7 +116,11 @@ class MoELayer:
                                          b1.data_ptr(), w2.data_ptr(), b2.data_ptr(), y.data_ptr(),
                                          L.stream_ptr(stream)))
         self._saved = (T, x.device)
-        self._x_alive = x  # StaticEP backward re-reads the gate input of dropped units
+        # the native step keeps raw pointers to x (StaticEP backward re-reads the
+        # gate input of dropped units) and to wg, w1, w2 (dgrad / gate backward):
+        # hold the tensors until backward is enqueued, or the caching allocator
+        # may hand their memory to the gradient buffers (fm_layer_forward contract)
+        self._alive = (x, wg, w1, b1, w2, b2)
         return y
 
     def backward(self, dy, grads: LayerGrads | None = None, stream=None) -> LayerGrads:
@@ -131,6 +135,7 @@ class MoELayer:
                                           grads.dwg.data_ptr(), grads.dw1.data_ptr(),
                                           grads.db1.data_ptr(), grads.dw2.data_ptr(),
                                           grads.db2.data_ptr(), L.stream_ptr(stream)))
+        self._alive = None  # enqueued: later allocations are stream-ordered after it
         return grads
 
     # ---------------------------------------------------------------- timing
