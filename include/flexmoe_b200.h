@@ -428,10 +428,13 @@ int fm_layer_read_timing(fm_layer* layer, double* ms_by_phase, int* launches_by_
  * The copies overlap the gate / routing / dispatch of the step; the compute
  * stream waits for them (fm_pool_wait_ready) only before the expert FFN.
  *
- * Ordering contract: a source slot may be pulled during the step in which
- * the placement changed; it must not be written before every peer has passed
- * that step's expert FFN (any later full-world collective orders it), and a
- * slot vacated in step s is reused no earlier than step s+1.
+ * Ordering contract: the receiver enqueues the pull after a collective that
+ * every source joins only once its previous optimizer update is enqueued (the
+ * runtime uses the step's demand all-gather), so it reads the state the
+ * source starts the step with; the source must not write the slot before
+ * every peer has passed that step's expert FFN (any later full-world
+ * collective orders it); a slot vacated in step s is reused no earlier than
+ * step s+1.
  * ---------------------------------------------------------------------- */
 typedef struct fm_expert_pool fm_expert_pool;
 

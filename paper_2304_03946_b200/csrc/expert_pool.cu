@@ -10,7 +10,8 @@
 // NVLink on its side stream. The bf16 operands of the expert GEMMs are
 // re-derived from the master on the same stream, so the compute stream only
 // waits (fm_pool_wait_ready) right before the expert FFN: the copies overlap
-// the gate, the histogram all-gather, routing and the dispatch all-to-all.
+// routing and the dispatch all-to-all (they are issued after the demand
+// all-gather, see the ordering contract in include/flexmoe_b200.h).
 //
 // Kernels: `pack` (master -> bf16 weights / f32 biases, ascending local
 // order) and a fused Adam that updates master/m/v in place and writes the

@@ -314,14 +314,18 @@ class DistributedMoELayer:
     def _call(self, name, *args):
         L.check(getattr(L.lib(), name)(self.layer._h, *args))
 
-    def forward(self, x, wg, w1, b1, w2, b2, on_demand=None, before_experts=None):
+    def forward(self, x, wg, w1, b1, w2, b2, on_demand=None, before_experts=None, after_gather=None):
         """on_demand(D [N][G] host) -> None | (w1, b1, w2, b2): called once the
         step's TokenDemand is all-gathered and before routing; it may switch
         the layer's placement (a per-step placement such as FullReplicate's
         shadows, baselines.cpp:143-156) and return the operands of the new
-        local experts. before_experts(): called right before the expert FFN
-        is enqueued (the runtime makes the stream wait for migrated expert
-        state there, so the copies overlap gate, routing and dispatch)."""
+        local experts. after_gather(): called right after the demand
+        all-gather is enqueued — the first point of the step that every GPU
+        passes only after finishing its previous step (optimizer update
+        included); the runtime starts expert-state pulls there.
+        before_experts(): called right before the expert FFN is enqueued (the
+        runtime makes the stream wait for the pulls there, so the copies
+        overlap routing and dispatch)."""
         lay, d, N, k = self.layer, self.layer.d, self.layer.N, self.layer.k
         T = x.shape[0]
         dev = x.device
@@ -329,6 +333,8 @@ class DistributedMoELayer:
         hist = torch.empty(N, dtype=torch.int64, device=dev)
         self._call("fm_layer_gate", x.data_ptr(), T, wg.data_ptr(), hist.data_ptr(), stream)
         gathered = self._x("all_gather", self.ex.all_gather, hist)  # [G, N]
+        if after_gather is not None:
+            after_gather()
         if on_demand is not None:
             new = on_demand(gathered.cpu().numpy().T.copy())
             if new is not None:

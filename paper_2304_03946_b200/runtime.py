@@ -19,8 +19,9 @@ f32 master weights + Adam m/v, 12 bytes per parameter (the bf16 working copy
 is re-derived on arrival, so the 14 B/param of SURVEY.md §8d shrink to 12).
 A transfer is a peer-to-peer cudaMemcpyAsync of one slot, pulled by the
 receiving GPU on the pool's side stream (CUDA IPC mapping of the source's
-pool); the compute stream waits for it only before the expert FFN, so the
-copy overlaps the gate, the demand all-gather, routing and the dispatch.
+pool), issued once the step's demand all-gather is enqueued; the compute
+stream waits for it only before the expert FFN, so the copy overlaps routing
+and the dispatch all-to-all.
 """
 from __future__ import annotations
 
@@ -86,11 +87,16 @@ class FlexMoERuntime:
 
     # ------------------------------------------------------------ migrations
     def _apply(self, ops):
-        """Make `ops` effective on this rank: update every rank's slot table,
-        pull the states this GPU newly hosts from their sources' pools on the
-        side stream, re-pack the local operands there too. Returns the bytes
-        this GPU pulls; the copies complete asynchronously (the step's expert
-        FFN waits for them)."""
+        """Make `ops` effective on this rank: update every rank's slot table and
+        the layer's placement. Returns (bytes this GPU pulls, a callable that
+        enqueues the pulls of the states it newly hosts and the operand
+        re-pack on the pool's side stream).
+
+        The pulls are issued after the step's demand all-gather: a source GPU
+        joins that collective only after its previous step's optimizer update,
+        so the pulled state is the one the source starts this step with. The
+        source's next update comes after this step's gradient all-reduces,
+        which the receiver joins only after its expert FFN waited for the pull."""
         old_counts = S.counts_from_slots(self.slots, self.N)
         for op in ops:  # Placement::apply in queue order (sim_engine.cpp:256-260)
             self.slots, _ = S.apply_op(self.slots, self.N, self.prof, op)
@@ -99,9 +105,13 @@ class FlexMoERuntime:
                  if dst == self.rank]
         new_local = [e for e in range(self.N) if counts[e, self.rank] > 0]
         self.layer.set_placement(counts)
-        self.store.pool.migrate(pulls, self.store.slots(new_local), self.store.packed(max(1, len(new_local))))
         self.packed = self.store.packed(max(1, len(new_local)))
-        return len(pulls) * self.store.pool.state_bytes
+        local_slots = self.store.slots(new_local)
+
+        def issue():
+            self.store.pool.migrate(pulls, local_slots, self.store.packed(max(1, len(new_local))))
+
+        return len(pulls) * self.store.pool.state_bytes, issue
 
     def migration_stats(self) -> dict:
         """Side-stream copy time, bytes and slots pulled by this GPU so far."""
@@ -111,9 +121,9 @@ class FlexMoERuntime:
     # ------------------------------------------------------------ one step
     def step(self, x, dy) -> RuntimeStep:
         applied = self.sched.begin_step()
-        mig_bytes = self._apply(applied) if applied else 0
+        mig_bytes, issue = self._apply(applied) if applied else (0, None)
         w1, b1, w2, b2 = self.packed
-        y = self.dl.forward(x, self.wg, w1, b1, w2, b2,
+        y = self.dl.forward(x, self.wg, w1, b1, w2, b2, after_gather=issue,
                             before_experts=lambda: self.store.pool.wait_ready())
         D = self.dl.last_demand_host  # TokenDemand [N][G], copied when routing synchronised
         if self.recorder is not None:
