@@ -241,7 +241,7 @@ class FusedArm:
         self.P = (p["wg"], p["w1"], p["b1"], p["w2"], p["b2"])
         self.grads = None
         self.N, self.G = N, 1
-        self.kernels_per_step = 9 + 8 + (2 if k > 1 else 1)
+        self.kernels_per_step = 9 + 8 + 1  # dWg rides on the bias-gradient tile sums
 
     def step(self, x, dy):
         self.layer.forward(x, *self.P)
@@ -476,6 +476,9 @@ def run_ours(args, world, rank, local_rank):
         "combine_fwd": units * (d * 2 + 8) + T * d * 2,
         "combine_bwd": T * d * 2 + units * (d * 2 * 2 + 12),
         "unpermute": units * (d * 2 + 12) + T * d * 2,
+        # fused path: per-tile column sums of dY_perm (db2) and dl-weighted X_perm (dWg)
+        # + the db1/db2/dWg partial reduces
+        "bias_grad": (units * (2 * d * 2 + 4) + 4 * (units // 128) * (f + 2 * d) * 2) if not multi else None,
         "relayout": 4 * recv_units * d * 2,
     }
     kernels = {}
@@ -484,7 +487,7 @@ def run_ours(args, world, rank, local_rank):
             continue
         per = pms / args.steps
         ent = {"ms_per_step": round(per, 4), "launches_per_step": n / args.steps}
-        if name in hbm_bytes and per > 0:
+        if hbm_bytes.get(name) and per > 0:
             gbs = hbm_bytes[name] / (per * 1e-3) / 1e9
             ent.update({"achieved_GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3)})
         if name in gemm_names and per > 0:

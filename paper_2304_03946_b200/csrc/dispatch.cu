@@ -424,41 +424,6 @@ __global__ void __launch_bounds__(256) unpermute_bwd_kernel(
   store_row<VPL>(dx, t, d, lane, acc);
 }
 
-// Column sums per 128-row block of a segmented [rows, cols] bf16 buffer,
-// accumulated (f32 atomics) into out[segment][cols]; optionally row-weighted
-// (weights per row, f32), which gives the gate-weight gradient when the
-// weights are dl_rows and the buffer is the dispatched activations.
-__global__ void segment_colsum_kernel(const __nv_bfloat16* __restrict__ buf, int cols,
-                                      const float* __restrict__ row_w, PlanDev p, int Nl,
-                                      const int32_t* __restrict__ seg_out_index,
-                                      float* __restrict__ out) {
-  const int rb = blockIdx.x;  // 128-row block
-  const int total = p.totals[0];
-  const int r0 = rb * kRowAlign;
-  if (r0 >= total) return;
-  int lo = 0, hi = Nl;  // segment with seg_start <= r0 (segments are 128-aligned)
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (p.seg_start[mid] <= r0) lo = mid; else hi = mid;
-  }
-  // skip empty segments that share the same start
-  while (lo + 1 < Nl && p.seg_start[lo + 1] <= r0) ++lo;
-  const int seg_end = p.seg_start[lo] + p.seg_real[lo];
-  const int rend = min(r0 + kRowAlign, seg_end);
-  const int c2 = (blockIdx.y * blockDim.x + threadIdx.x) * 2;
-  if (c2 >= cols || r0 >= rend) return;
-  float a0 = 0.0f, a1 = 0.0f;
-  for (int r = r0; r < rend; ++r) {
-    const uint32_t v = *reinterpret_cast<const uint32_t*>(buf + static_cast<size_t>(r) * cols + c2);
-    const float s = row_w ? row_w[r] : 1.0f;
-    a0 += s * bf16lo(v);
-    a1 += s * bf16hi(v);
-  }
-  const int oi = seg_out_index ? seg_out_index[lo] : lo;
-  atomicAdd(out + static_cast<size_t>(oi) * cols + c2, a0);
-  atomicAdd(out + static_cast<size_t>(oi) * cols + c2 + 1, a1);
-}
-
 // Gate-weight gradient: dWg[e][:] += sum over dispatch rows r with
 // row_expert[r] == e of dl_rows[r] * buf[r][:]. Rows of one expert are
 // contiguous runs (segments / send chunks), so each block accumulates a run
@@ -555,27 +520,90 @@ __global__ void demand_transpose_kernel(const int64_t* __restrict__ gathered_GN,
   demand_NG[i] = gathered_GN[static_cast<size_t>(g) * N + e];
 }
 
-// out[li][col] = sum over the 128-row tiles of segment li of partial[tile][col]
-// (fixed order: deterministic).
-__global__ void segment_tile_reduce_kernel(const float* __restrict__ partial, int cols, PlanDev p,
-                                           float* __restrict__ out) {
+// Per-128-row-tile column sums of permuted activations (expert segments are
+// 128-row aligned, so a tile belongs to one expert): partial[tile][c] =
+// sum over the tile's real rows r of w[r] * buf[r][c] (w = 1 when row_w is
+// null). Job 0 / 1 in blockIdx.y (e.g. dWg from X_perm with dl per row, db2
+// from dY_perm). Thread = 8 columns (16-byte loads), 8 rows in flight.
+// Plain stores, then segment_tile_reduce: deterministic, no atomics.
+struct TileSumJob {
+  const __nv_bfloat16* buf;
+  const float* row_w;
+  float* partial;  // [tiles][cols]
+};
+
+__global__ void __launch_bounds__(256) segment_tile_colsum_kernel(TileSumJob j0, TileSumJob j1, int cols,
+                                                                  PlanDev p, int Nl) {
+  const TileSumJob jb = blockIdx.y == 0 ? j0 : j1;
+  const int tile = blockIdx.x;
+  if (tile >= p.mtile_prefix[Nl]) return;
+  int lo = 0, hi = Nl;  // segment li with mtile_prefix[li] <= tile < mtile_prefix[li + 1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (p.mtile_prefix[mid] <= tile) lo = mid; else hi = mid;
+  }
+  while (lo + 1 < Nl && p.mtile_prefix[lo + 1] <= tile) ++lo;  // skip empty segments
+  const int r0 = tile * kRowAlign;
+  const int r1 = min(r0 + kRowAlign, p.seg_start[lo] + p.seg_real[lo]);  // pad rows carry nothing
+  const int c8 = threadIdx.x * 8;
+  if (c8 >= cols) return;
+  float acc[8] = {};
+  constexpr int kB = 8;
+  for (int rb = r0; rb < r1; rb += kB) {
+    uint4 v[kB];
+    float w[kB];
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int r = min(rb + i, r1 - 1);
+      v[i] = __ldg(reinterpret_cast<const uint4*>(jb.buf + static_cast<size_t>(r) * cols + c8));
+      w[i] = rb + i < r1 ? (jb.row_w ? __ldg(jb.row_w + r) : 1.0f) : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const uint32_t q[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        acc[2 * c] = fmaf(w[i], bf16lo(q[c]), acc[2 * c]);
+        acc[2 * c + 1] = fmaf(w[i], bf16hi(q[c]), acc[2 * c + 1]);
+      }
+    }
+  }
+  float4* dst = reinterpret_cast<float4*>(jb.partial + static_cast<size_t>(tile) * cols + c8);
+  dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+// out[oi(li)][col] = sum over the 128-row tiles of segment li of partial[tile][col]
+// (fixed order: deterministic); oi = out_index[li] (null: li). Up to three
+// jobs in blockIdx.z.
+struct TileReduceJob {
+  const float* partial;
+  int cols;
+  const int32_t* out_index;
+  float* out;
+};
+
+__global__ void segment_tile_reduce_kernel(TileReduceJob j0, TileReduceJob j1, TileReduceJob j2, PlanDev p) {
+  const TileReduceJob jb = blockIdx.z == 0 ? j0 : (blockIdx.z == 1 ? j1 : j2);
   // block: 32 columns x 8 tile lanes; lane j sums tiles t0+j, t0+j+8, ...; the
   // eight partial sums are combined in fixed order (deterministic).
   __shared__ float part[8][33];
   const int li = blockIdx.x;
   const int cx = threadIdx.x & 31, j = threadIdx.x >> 5;
   const int col = blockIdx.y * 32 + cx;
+  if (blockIdx.y * 32 >= jb.cols) return;
   const int t0 = p.mtile_prefix[li], t1 = p.mtile_prefix[li + 1];
   float acc = 0.0f;
-  if (col < cols)
-    for (int t = t0 + j; t < t1; t += 8) acc += __ldg(partial + static_cast<size_t>(t) * cols + col);
+  if (col < jb.cols)
+    for (int t = t0 + j; t < t1; t += 8) acc += __ldg(jb.partial + static_cast<size_t>(t) * jb.cols + col);
   part[j][cx] = acc;
   __syncthreads();
-  if (j == 0 && col < cols) {
+  if (j == 0 && col < jb.cols) {
     float s = 0.0f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) s += part[i][cx];
-    out[static_cast<size_t>(li) * cols + col] = s;
+    const int oi = jb.out_index ? jb.out_index[li] : li;
+    jb.out[static_cast<size_t>(oi) * jb.cols + col] = s;
   }
 }
 
@@ -605,11 +633,40 @@ void launch_demand_transpose(const int64_t* gathered_GN, int N, int G, int64_t* 
   FM_LAUNCH_CHECK("demand_transpose_kernel");
 }
 
-void launch_segment_tile_reduce(const float* partial, int cols, const PlanDev& p, int Nl, float* out,
-                                cudaStream_t s) {
+// Column sums per 128-row tile of up to two permuted buffers (null buf: job off).
+void launch_segment_tile_colsum(const void* buf0, const float* w0, float* partial0, const void* buf1,
+                                const float* w1, float* partial1, int cols, const PlanDev& p, int Nl,
+                                int max_tiles, cudaStream_t s) {
+  if (Nl <= 0 || max_tiles <= 0 || (!buf0 && !buf1)) return;
+  if (cols % 8 != 0 || cols > 8 * 256) throw std::invalid_argument("segment tile colsum: cols % 8 == 0, <= 2048");
+  TileSumJob j[2] = {{static_cast<const __nv_bfloat16*>(buf0), w0, partial0},
+                     {static_cast<const __nv_bfloat16*>(buf1), w1, partial1}};
+  const int nj = (buf0 ? 1 : 0) + (buf1 ? 1 : 0);
+  if (!buf0) j[0] = j[1];
+  const int threads = ((cols / 8 + 31) / 32) * 32;
+  segment_tile_colsum_kernel<<<dim3(max_tiles, nj), threads, 0, s>>>(j[0], j[1], cols, p, Nl);
+  FM_LAUNCH_CHECK("segment_tile_colsum_kernel");
+}
+
+// Up to three reductions of per-tile partials into per-segment rows (null out: off).
+void launch_segment_tile_reduce(const float* partial0, int cols0, const int32_t* idx0, float* out0,
+                                const float* partial1, int cols1, const int32_t* idx1, float* out1,
+                                const float* partial2, int cols2, const int32_t* idx2, float* out2,
+                                const PlanDev& p, int Nl, cudaStream_t s) {
   if (Nl <= 0) return;
-  dim3 grid(Nl, (cols + 31) / 32);
-  segment_tile_reduce_kernel<<<grid, 256, 0, s>>>(partial, cols, p, out);
+  TileReduceJob all[3] = {{partial0, cols0, idx0, out0}, {partial1, cols1, idx1, out1},
+                          {partial2, cols2, idx2, out2}};
+  TileReduceJob use[3];
+  int n = 0, maxc = 0;
+  for (const auto& j : all)
+    if (j.out) {
+      use[n++] = j;
+      maxc = std::max(maxc, j.cols);
+    }
+  if (n == 0) return;
+  for (int i = n; i < 3; ++i) use[i] = use[0];
+  dim3 grid(Nl, (maxc + 31) / 32, n);
+  segment_tile_reduce_kernel<<<grid, 256, 0, s>>>(use[0], use[1], use[2], p);
   FM_LAUNCH_CHECK("segment_tile_reduce_kernel");
 }
 
@@ -709,13 +766,5 @@ void launch_unpermute_bwd(const void* dXbuf, const int32_t* pos, const int32_t* 
   FM_LAUNCH_CHECK("unpermute_bwd_kernel");
 }
 
-void launch_segment_colsum(const void* buf, int cols, const float* row_w, const PlanDev& p, int Nl,
-                           const int32_t* seg_out_index, float* out, int max_rows, cudaStream_t s) {
-  if (max_rows <= 0 || Nl <= 0) return;
-  dim3 grid((max_rows + kRowAlign - 1) / kRowAlign, (cols / 2 + 255) / 256);
-  segment_colsum_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(buf), cols, row_w, p,
-                                              Nl, seg_out_index, out);
-  FM_LAUNCH_CHECK("segment_colsum_kernel");
-}
 
 }  // namespace fm

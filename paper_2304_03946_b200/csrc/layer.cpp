@@ -51,10 +51,13 @@ void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const
 void launch_unpermute_bwd(const void* dXbuf, const int32_t* pos, const int32_t* idx, const float* dl,
                           const void* wg, int T, int d, int k, bool gate_grad, void* dx,
                           cudaStream_t s);
-void launch_segment_colsum(const void* buf, int cols, const float* row_w, const PlanDev& p, int Nl,
-                           const int32_t* seg_out_index, float* out, int max_rows, cudaStream_t s);
-void launch_segment_tile_reduce(const float* partial, int cols, const PlanDev& p, int Nl, float* out,
-                                cudaStream_t s);
+void launch_segment_tile_colsum(const void* buf0, const float* w0, float* partial0, const void* buf1,
+                                const float* w1, float* partial1, int cols, const PlanDev& p, int Nl,
+                                int max_tiles, cudaStream_t s);
+void launch_segment_tile_reduce(const float* partial0, int cols0, const int32_t* idx0, float* out0,
+                                const float* partial1, int cols1, const int32_t* idx1, float* out1,
+                                const float* partial2, int cols2, const int32_t* idx2, float* out2,
+                                const PlanDev& p, int Nl, cudaStream_t s);
 void launch_dropped_gate_wgrad(const void* x, const int32_t* pos, const int32_t* idx, const float* dl,
                                int T, int d, int k, float* dwg, cudaStream_t s);
 void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
@@ -273,6 +276,7 @@ class Layer {
     row_expert_.reset(4 * row_cap_);
     relu_mask_.reset(4 * row_cap_ * (f / 32));
     tile_colsum_.reset(4 * (row_cap_ / 128) * f);
+    tile_sum_.reset(4 * 2 * (row_cap_ / 128) * d);  // per-tile db2 / dWg partials
   }
 
   // ------------------------------------------------------------ fused single-GPU step
@@ -284,10 +288,10 @@ class Layer {
     gate(x, T, wg, nullptr, s);
     route_device(s);
     timer_.begin(FM_PHASE_DISPATCH, s);
-    launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), row_expert_.as<int32_t>(), s);
+    launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);
     launch_dispatch(x, T, cfg_.d_model, cfg_.top_k, cfg_.num_experts, 1, 0, true,
                     topk_idx_.as<int32_t>(), tile_rank_.as<int32_t>(), tile_base_.as<int32_t>(),
-                    plan_, pos_.as<int32_t>(), x_perm_.p, row_expert_.as<int32_t>(), s);
+                    plan_, pos_.as<int32_t>(), x_perm_.p, nullptr, s);
     timer_.end(s);
     expert_forward(w1, b1, w2, b2, s);
     combine(y_perm_.p, y, s);
@@ -306,9 +310,12 @@ class Layer {
     timer_.begin(FM_PHASE_COMBINE_BWD, s);
     launch_zero_pad(dy_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);
     timer_.end(s);
-    expert_backward(saved_w1_, saved_w2_, dw1, db1, dw2, db2, s);
+    // the dispatched units' share of dWg = per-tile column sums of X_perm
+    // weighted by dl per row, reduced with db1 / db2 (dropped units: below)
+    const bool dwg_tiles = dwg && cfg_.top_k > 1 && nl() > 0;
+    expert_backward(saved_w1_, saved_w2_, dw1, db1, dw2, db2, s, dwg_tiles ? dwg : nullptr);
     unpermute_backward(dx_perm_.p, x_perm_.p, plan_.totals, static_cast<int>(row_cap_), saved_wg_, dx,
-                       dwg, s);
+                       dwg, s, dwg_tiles);
   }
 
   // ------------------------------------------------------------ phases
@@ -416,8 +423,10 @@ class Layer {
     timer_.end(s);
   }
 
+  // dwg_tiles (fused path): also the gate-weight gradient of the dispatched
+  // units, from X_perm and dl per dispatch row, in the same tile passes.
   void expert_backward(const void* w1, const void* w2, float* dw1, float* db1, float* dw2,
-                       float* db2, cudaStream_t s) {
+                       float* db2, cudaStream_t s, float* dwg_tiles = nullptr) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0) return;
     const int rows = static_cast<int>(row_cap_);
@@ -445,12 +454,19 @@ class Layer {
                    plan_.seg_rows, nullptr, Nl, rows, f, d, 0, s);
       timer_.end(s);
     }
+    // bias / gate-weight gradients: per-128-row-tile column sums (db1's come from
+    // the dgrad epilogue; dY_perm's and the dl-weighted X_perm's here), then one
+    // fixed-order reduce per segment (deterministic, no atomics)
     timer_.begin(FM_PHASE_BIAS_GRAD, s);
-    if (db1) launch_segment_tile_reduce(tile_colsum_.as<float>(), f, plan_, Nl, db1, s);
-    if (db2) {
-      FM_CUDA(cudaMemsetAsync(db2, 0, sizeof(float) * Nl * d, s));
-      launch_segment_colsum(dy_perm_.p, d, nullptr, plan_, Nl, nullptr, db2, rows, s);
-    }
+    const int max_tiles = static_cast<int>(row_cap_ / 128);
+    float* part_db2 = tile_sum_.as<float>();
+    float* part_dwg = part_db2 + static_cast<size_t>(max_tiles) * d;
+    launch_segment_tile_colsum(dwg_tiles ? x_perm_.p : nullptr, dl_rows_.as<float>(), part_dwg,
+                               db2 ? dy_perm_.p : nullptr, nullptr, part_db2, d, plan_, Nl, max_tiles, s);
+    if (dwg_tiles)  // experts hosted nowhere keep a zero row
+      FM_CUDA(cudaMemsetAsync(dwg_tiles, 0, sizeof(float) * cfg_.num_experts * d, s));
+    launch_segment_tile_reduce(tile_colsum_.as<float>(), f, nullptr, db1, part_db2, d, nullptr, db2, part_dwg, d,
+                               local_expert_dev_, dwg_tiles, plan_, Nl, s);
     timer_.end(s);
   }
 
@@ -475,8 +491,10 @@ class Layer {
   // dx and the gate weight gradient. dback: dX rows in dispatch order;
   // xrows: the dispatched activations in the same order (X_perm or the send
   // buffer); rows_dev / rows: how many of them.
+  // dwg_done: the dispatched units' share of dWg is already in dwg (fused
+  // path, tile sums); only the units dropped by the capacity rule remain.
   void unpermute_backward(const void* dback, const void* xrows, const int* rows_dev, int rows,
-                          const void* wg, void* dx, float* dwg, cudaStream_t s) {
+                          const void* wg, void* dx, float* dwg, cudaStream_t s, bool dwg_done = false) {
     const int T = cur_T_, d = cfg_.d_model, k = cfg_.top_k, N = cfg_.num_experts;
     const bool gate_grad = k > 1;
     timer_.begin(FM_PHASE_UNPERMUTE, s);
@@ -485,10 +503,11 @@ class Layer {
     timer_.end(s);
     if (dwg) {
       timer_.begin(FM_PHASE_GATE_WGRAD, s);
-      FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
+      if (!dwg_done) FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
       if (gate_grad) {
-        launch_gate_wgrad(xrows, rows_dev, rows, rows, d, dl_rows_.as<float>(),
-                          row_expert_.as<int32_t>(), dwg, s);
+        if (!dwg_done)
+          launch_gate_wgrad(xrows, rows_dev, rows, rows, d, dl_rows_.as<float>(),
+                            row_expert_.as<int32_t>(), dwg, s);
         // units dropped by the capacity rule are in no dispatch row
         if (drops_enabled())
           launch_dropped_gate_wgrad(saved_x_, pos_.as<int32_t>(), topk_idx_.as<int32_t>(),
@@ -575,7 +594,7 @@ class Layer {
   DevBuf topk_idx_, topk_w_, tile_rank_, pos_, dl_, tile_counts_, tile_base_, hist_, demand_,
       flows_, counts_dev_, route_status_, plan_mem_;
   DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_, relu_mask_, tile_colsum_,
-      row_expert_;
+      row_expert_, tile_sum_;
   std::vector<int32_t> host_counts_;
   double capacity_factor_ = 0.0;  // 0 / inf: no drops (FlexMoE)
   const void* saved_x_ = nullptr;  // gate input of the current step (must outlive backward)
