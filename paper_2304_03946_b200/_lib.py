@@ -157,6 +157,15 @@ def lib() -> C.CDLL:
     return _lib
 
 
+def release(destroy_fn: str, handle) -> None:
+    """Calls `destroy_fn(handle)` unless the handle is empty or the library is
+    already gone (interpreter shutdown clears module globals before __del__)."""
+    lib_ = _lib
+    if lib_ is None or handle is None or not handle.value:
+        return
+    getattr(lib_, destroy_fn)(handle)
+
+
 def exported_symbols() -> list[str]:
     return sorted(set(_SIGNATURES) | set(_RESTYPES))
 

@@ -72,10 +72,11 @@ class MoELayer:
         self._saved = None
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            L.lib().fm_layer_destroy(h)
-            self._h = None
+        try:
+            L.release("fm_layer_destroy", getattr(self, "_h", None))
+        except (TypeError, AttributeError):  # interpreter shutdown
+            pass
+        self._h = None
 
     # ---------------------------------------------------------------- placement
     @property

@@ -55,10 +55,11 @@ class ExpertPool:
         self._peers = []  # keep linked pools alive
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            L.lib().fm_pool_destroy(h)
-            self._h = None
+        try:
+            L.release("fm_pool_destroy", getattr(self, "_h", None))
+        except (TypeError, AttributeError):  # interpreter shutdown
+            pass
+        self._h = None
 
     @property
     def state_bytes(self) -> int:

@@ -279,9 +279,11 @@ class Scheduler:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
-            L.lib().fm_scheduler_destroy(self._h)
-            self._h = None
+        try:
+            L.release("fm_scheduler_destroy", getattr(self, "_h", None))
+        except (TypeError, AttributeError):  # interpreter shutdown
+            pass
+        self._h = None
 
     def step(self, D) -> StepResult:
         D = np.ascontiguousarray(D, np.int64)
@@ -366,9 +368,11 @@ class Baseline:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
-            L.lib().fm_baseline_destroy(self._h)
-            self._h = None
+        try:
+            L.release("fm_baseline_destroy", getattr(self, "_h", None))
+        except (TypeError, AttributeError):  # interpreter shutdown
+            pass
+        self._h = None
 
     def step(self, D) -> BaselineStep:
         D = np.ascontiguousarray(D, np.int64)
