@@ -195,12 +195,14 @@ def exact_inputs(rng, T, d, N, f, skew=None):
     (|j| <= 8), so every logit is a multiple of 2^-9 with |logit| <= d/8 and is
     computed exactly in f32 in any order -> top-k comparable bit for bit.
     `skew` (log-popularity per expert) is added through a constant feature
-    column, quantised to multiples of 1/64, as in the bench's Zipf gate."""
+    column, quantised to multiples of 1/64 and then to bf16 (|v| >= 4 keeps
+    only 1/32 steps), as in the bench's Zipf gate: the device multiplies the
+    bf16 value, so the oracle must too."""
     x = rng.integers(-8, 9, size=(T, d)) / 8.0
     wg = rng.integers(-8, 9, size=(N, d)) / 64.0
     if skew is not None:
         x[:, 0] = 1.0
-        wg[:, 0] = np.clip(np.round(np.asarray(skew) * 64) / 64, -8, 8)
+        wg[:, 0] = bf16(np.clip(np.round(np.asarray(skew) * 64) / 64, -8, 8))
     w1 = bf16(rng.standard_normal((N, f, d)) * d**-0.5)
     w2 = bf16(rng.standard_normal((N, d, f)) * f**-0.5)
     b1 = (rng.standard_normal((N, f)) * 0.1).astype(np.float32).astype(np.float64)

@@ -55,6 +55,12 @@ CASES = [
     (16, 2, 512, 768, 777, "zipf"),
     (64, 1, 256, 256, 3000, "zipf"),
     (32, 4, 256, 512, 129, None),
+    # edge cases: the maximum expert count and top-k, BERT-MoE dims (configs[3]),
+    # one token, a ragged sub-warp token count
+    (256, 8, 256, 256, 1500, "zipf"),
+    (16, 2, 768, 3072, 2048, "zipf"),
+    (8, 2, 256, 256, 1, None),
+    (8, 1, 256, 256, 31, None),
 ]
 
 
