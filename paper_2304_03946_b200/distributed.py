@@ -407,8 +407,10 @@ class DistributedMoELayer:
 
 def sync_replica_grads(ex: Exchange, replica_counts, local_experts, g):
     """Replica-group SUM all-reduce of each replicated expert's (dw1, db1, dw2,
-    db2), in ascending expert id on every rank (one flattened buffer per
-    expert), then the gate-weight gradient over all ranks."""
+    db2), in ascending expert id on every rank, then the gate-weight gradient
+    over all ranks. In place and copy-free: each expert's gradient is four
+    contiguous slices of the layer's gradient arrays (dw1[i] is [f, d] etc.),
+    reduced where they lie (NCCL runs them back to back on its stream)."""
     cnt = np.asarray(replica_counts)
     li = {e: i for i, e in enumerate(local_experts)}
     for e in range(cnt.shape[0]):
@@ -416,18 +418,12 @@ def sync_replica_grads(ex: Exchange, replica_counts, local_experts, g):
         if len(grp) < 2:
             continue
         ex.sync_group(grp)
-        member = ex.rank in grp
-        flat = None
-        if member:
+        if ex.rank in grp:
             i = li[e]
-            flat = torch.cat([g.dw1[i].reshape(-1), g.db1[i], g.dw2[i].reshape(-1), g.db2[i]])
-        ex.all_reduce(flat, grp)  # non-members pass None
-        if not member:
-            continue
-        o = 0
-        for t in (g.dw1[i], g.db1[i], g.dw2[i], g.db2[i]):
-            n = t.numel()
-            t.copy_(flat[o:o + n].view_as(t))
-            o += n
+            for t in (g.dw1[i], g.db1[i], g.dw2[i], g.db2[i]):
+                ex.all_reduce(t, grp)
+        else:  # non-members take part in the same calls (loopback rendezvous)
+            for _ in range(4):
+                ex.all_reduce(None, grp)
     ex.all_reduce(g.dwg, None)
     return g
