@@ -362,6 +362,42 @@ int fm_layer_expert_backward(fm_layer* layer, const void* drecv_buf, const void*
 int fm_layer_unpermute_backward(fm_layer* layer, const void* dback_buf, const void* send_buf,
                                 const void* wg, void* dx, float* dwg, void* stream);
 
+/* Peer-to-peer transport (the B200-native alternative to the all-to-alls
+ * above). fm_layer_enable_p2p allocates one exchange arena per
+ * GPU (X_perm, Y_perm, dY_perm, dX_perm, dl rows and arrival flags, sized for
+ * route()'s worst case) that every peer maps: CUDA IPC handles
+ * (fm_layer_p2p_handle / fm_layer_p2p_open_peer) across processes, or
+ * fm_layer_p2p_link_peer between layers of one process. Token rows then
+ * cross NVLink inside the kernels that produce or consume them:
+ *   fm_layer_gate            (as above; advances the exchange epoch)
+ *   host: all-gather hist_out -> gathered [G][N]
+ *   fm_layer_route_p2p       route() + plan incl. every peer's X_perm layout (no host sync)
+ *   fm_layer_dispatch_p2p    x rows -> the expert GPUs' X_perm; flags
+ *   fm_layer_expert_forward_p2p   wait for all sources, FFN, flag "Y ready"
+ *   fm_layer_combine_p2p     wait, y = sum_j w_j Y rows read from the expert GPUs
+ *   fm_layer_combine_backward_p2p  dY rows (+ gate dl) -> the expert GPUs' dY_perm; flags
+ *   fm_layer_expert_backward_p2p   wait, dgrad, flag "dX ready", weight grads; dwg gets this
+ *                            GPU's share of the gate-weight gradient (sum it over all GPUs)
+ *   fm_layer_unpermute_backward_p2p  wait, dx from dX rows read from the expert GPUs
+ * Waits are device-side (flags in the arena, monotonic epochs) and bounded:
+ * after ~20 s a wait gives up and fm_layer_p2p_status reports it. Slots are
+ * reused across steps only after the next step's demand all-gather, which
+ * every GPU joins after finishing the previous step. */
+int fm_layer_enable_p2p(fm_layer* layer);
+int fm_layer_p2p_handle(fm_layer* layer, void* handle64);
+int fm_layer_p2p_open_peer(fm_layer* layer, int peer, const void* handle64);
+int fm_layer_p2p_link_peer(fm_layer* layer, int peer, fm_layer* peer_layer);
+int fm_layer_p2p_status(fm_layer* layer, int* timed_out);
+int fm_layer_route_p2p(fm_layer* layer, const int64_t* gathered_hist_GN, void* stream);
+int fm_layer_dispatch_p2p(fm_layer* layer, const void* x, void* stream);
+int fm_layer_expert_forward_p2p(fm_layer* layer, const void* w1, const float* b1, const void* w2,
+                                const float* b2, void* stream);
+int fm_layer_combine_p2p(fm_layer* layer, void* y, void* stream);
+int fm_layer_combine_backward_p2p(fm_layer* layer, const void* dy, void* stream);
+int fm_layer_expert_backward_p2p(fm_layer* layer, const void* w1, const void* w2, float* dw1, float* db1,
+                                 float* dw2, float* db2, float* dwg, void* stream);
+int fm_layer_unpermute_backward_p2p(fm_layer* layer, const void* wg, void* dx, float* dwg, void* stream);
+
 /* Introspection (synchronous device->host copy, for tests / metrics). */
 #define FM_FIELD_TOPK_IDX 0     /* int32 [T,k] */
 #define FM_FIELD_TOPK_W 1       /* f32   [T,k] */
@@ -405,7 +441,7 @@ int fm_layer_copy_out(fm_layer* layer, int field, void* host, size_t max_bytes, 
 #define FM_PHASE_BIAS_GRAD 12   /* db1, db2 */
 #define FM_PHASE_UNPERMUTE 13   /* dx gather + gate input grad */
 #define FM_PHASE_GATE_WGRAD 14  /* dWg */
-#define FM_PHASE_RELAYOUT 15    /* a2a order <-> expert segments (multi-GPU) */
+#define FM_PHASE_RELAYOUT 15    /* multi-GPU: a2a order <-> expert segments, or P2P arrival waits */
 #define FM_NUM_PHASES 16
 int fm_layer_set_timing(fm_layer* layer, int enable);
 int fm_layer_read_timing(fm_layer* layer, double* ms_by_phase, int* launches_by_phase);

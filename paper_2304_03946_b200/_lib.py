@@ -117,6 +117,18 @@ _SIGNATURES = {
     "fm_layer_expert_backward": [_P] * 10,
     "fm_layer_unpermute_backward": [_P] * 7,
     "fm_layer_read_timing": [_P, _P, _P],
+    "fm_layer_enable_p2p": [_P],
+    "fm_layer_p2p_handle": [_P, _P],
+    "fm_layer_p2p_open_peer": [_P, _I, _P],
+    "fm_layer_p2p_link_peer": [_P, _I, _P],
+    "fm_layer_p2p_status": [_P, _P],
+    "fm_layer_route_p2p": [_P, _P, _P],
+    "fm_layer_dispatch_p2p": [_P, _P, _P],
+    "fm_layer_expert_forward_p2p": [_P] * 6,
+    "fm_layer_combine_p2p": [_P, _P, _P],
+    "fm_layer_combine_backward_p2p": [_P, _P, _P],
+    "fm_layer_expert_backward_p2p": [_P] * 9,
+    "fm_layer_unpermute_backward_p2p": [_P] * 5,
     "fm_pool_create": [_I, _I, _I, _I, C.POINTER(_P)],
     "fm_pool_destroy": [_P],
     "fm_pool_info": [_P, _P, _P],

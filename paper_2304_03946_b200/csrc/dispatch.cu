@@ -87,7 +87,8 @@ __global__ void expert_scan_kernel(const int32_t* __restrict__ tile_counts, int 
 // One block. Turns flows[e][src][dst] into the offsets every later kernel
 // uses (see PlanDev in layer_plan.h).
 __global__ void plan_kernel(const int64_t* __restrict__ flows, int N, int G, int me,
-                            const int32_t* __restrict__ local_expert, int Nl, PlanDev p) {
+                            const int32_t* __restrict__ local_expert, int Nl, PlanDev p,
+                            const int32_t* __restrict__ counts) {
   extern __shared__ int32_t sf[];  // flows as int32 [N][G][G]
   const int nflow = N * G * G;
   for (int i = threadIdx.x; i < nflow; i += blockDim.x) sf[i] = static_cast<int32_t>(flows[i]);
@@ -149,6 +150,28 @@ __global__ void plan_kernel(const int64_t* __restrict__ flows, int N, int G, int
     p.recv_chunk_off[G * Nl] = roff;
     p.totals[2] = roff;  // units received
   }
+  // P2P: where (e, me)'s units start in every destination's X_perm. Every GPU
+  // lays out its segments the same way (hosted experts ascending, 128-row
+  // padded, sources ascending inside a segment), so each source computes its
+  // destinations' layouts from the shared flows and replica counts.
+  if (p.peer_row && counts) {
+    for (int dst = threadIdx.x; dst < G; dst += blockDim.x) {
+      int start = 0;
+      for (int e = 0; e < N; ++e) {
+        if (counts[e * G + dst] <= 0) {
+          p.peer_row[e * G + dst] = -1;
+          continue;
+        }
+        int real = 0, before = 0;
+        for (int s = 0; s < G; ++s) {
+          real += FL(e, s, dst);
+          if (s < me) before += FL(e, s, dst);
+        }
+        p.peer_row[e * G + dst] = start + before;
+        start += (real + kRowAlign - 1) / kRowAlign * kRowAlign;
+      }
+    }
+  }
 #undef FL
 }
 
@@ -161,7 +184,7 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
                                 const int32_t* __restrict__ tile_rank,
                                 const int32_t* __restrict__ tile_base, PlanDev p,
                                 int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf,
-                                int32_t* __restrict__ row_expert) {
+                                int32_t* __restrict__ row_expert, const P2P pp) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -176,7 +199,7 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
     const int u = t * k + j;
     const int e = idx[u];
     const int r = tile_base[static_cast<size_t>(tile) * N + e] + tile_rank[u];
-    int row;
+    int row, to = -1;
     if (direct) {  // G == 1: chunk_cnt[e] is the kept demand (all of it unless dropping)
       row = r < p.chunk_cnt[e] ? p.seg_start[p.local_index[e]] + r : -1;
     } else {
@@ -185,17 +208,21 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
         const int dst = (i == 0) ? me : (i <= me ? i - 1 : i);
         const int lo = p.chunk_lo[e * G + dst];
         if (r < lo + p.chunk_cnt[e * G + dst]) {
-          row = p.send_off[e * G + dst] + (r - lo);
+          // P2P: straight into the destination's X_perm; else the send buffer
+          row = pp.unit_dst ? p.peer_row[e * G + dst] + (r - lo) : p.send_off[e * G + dst] + (r - lo);
+          to = dst;
           break;
         }
       }
     }
     if (lane == 0) {
       pos_out[u] = row;  // -1: dropped by the capacity rule (StaticEP)
+      if (pp.unit_dst) pp.unit_dst[u] = row >= 0 ? to : -1;
       if (row_expert && row >= 0) row_expert[row] = e;
     }
     if (row < 0) continue;
-    uint4* dst = reinterpret_cast<uint4*>(buf + static_cast<size_t>(row) * d);
+    __nv_bfloat16* out = pp.unit_dst ? reinterpret_cast<__nv_bfloat16*>(pp.base[to] + pp.x_off) : buf;
+    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d);
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       if (lane + 32 * i < nvec) dst[lane + 32 * i] = v[i];
@@ -258,12 +285,38 @@ __device__ __forceinline__ void unit_meta(const int32_t* __restrict__ pos, const
   }
 }
 
+// Lane j < k: destination GPU of the token's unit j (-1 without P2P).
+__device__ __forceinline__ int unit_dst_of(const P2P& pp, size_t base, int k, int lane) {
+  return (pp.unit_dst && lane < k) ? pp.unit_dst[base + lane] : -1;
+}
+
+// Row buffer of unit with destination `to`: the peer's arena region, or the
+// local buffer (single GPU / NCCL layouts).
+template <class T>
+__device__ __forceinline__ T* peer_rows(const P2P& pp, int64_t off, int to, T* local) {
+  return to >= 0 ? reinterpret_cast<T*>(pp.base[to] + off) : local;
+}
+
 template <int VPL>
 __device__ __forceinline__ void load_row(const __nv_bfloat16* __restrict__ base, size_t row, int d,
                                          int lane, uint4 (&q)[VPL]) {
   const uint4* src = reinterpret_cast<const uint4*>(base + row * static_cast<size_t>(d));
 #pragma unroll
   for (int i = 0; i < VPL; ++i) q[i] = __ldg(src + lane + 32 * i);
+}
+// Rows written by another GPU in this step: L2-coherent loads, no L1 reuse.
+template <int VPL>
+__device__ __forceinline__ void load_row_cg(const __nv_bfloat16* base, size_t row, int d, int lane,
+                                            uint4 (&q)[VPL]) {
+  const uint4* src = reinterpret_cast<const uint4*>(base + row * static_cast<size_t>(d));
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) q[i] = __ldcg(src + lane + 32 * i);
+}
+template <int VPL>
+__device__ __forceinline__ void load_unit_row(const P2P& pp, int64_t off, int to, const __nv_bfloat16* local,
+                                              size_t row, int d, int lane, uint4 (&q)[VPL]) {
+  if (to >= 0) load_row_cg<VPL>(reinterpret_cast<const __nv_bfloat16*>(pp.base[to] + off), row, d, lane, q);
+  else load_row<VPL>(local, row, d, lane, q);
 }
 
 template <int VPL>
@@ -290,11 +343,12 @@ __device__ __forceinline__ void store_row(__nv_bfloat16* __restrict__ base, size
 }
 
 // y[t] = sum_j w[t,j] * Y[pos[t,j]]  (Eq. 4), f32 accumulation.
+// P2P: Y rows are read where the expert ran (NVLink loads from the peer's Y_perm).
 template <int VPL>
-__global__ void __launch_bounds__(256) combine_fwd_kernel(const __nv_bfloat16* __restrict__ Y,
+__global__ void __launch_bounds__(256) combine_fwd_kernel(const __nv_bfloat16* __restrict__ Yl,
                                                           const int32_t* __restrict__ pos,
                                                           const float* __restrict__ w, int T, int k,
-                                                          __nv_bfloat16* __restrict__ y) {
+                                                          __nv_bfloat16* __restrict__ y, const P2P pp) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -302,6 +356,7 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(const __nv_bfloat16* _
   int my_pos;
   float my_w;
   unit_meta(pos, w, static_cast<size_t>(t) * k, k, lane, my_pos, my_w);
+  const int my_to = unit_dst_of(pp, static_cast<size_t>(t) * k, k, lane);
   float acc[VPL][8];
 #pragma unroll
   for (int i = 0; i < VPL; ++i)
@@ -314,9 +369,11 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(const __nv_bfloat16* _
     const bool two = j + 1 < k;
     const int p1 = __shfl_sync(0xffffffffu, my_pos, two ? j + 1 : j);
     const float w1 = __shfl_sync(0xffffffffu, my_w, two ? j + 1 : j);
+    const int to0 = __shfl_sync(0xffffffffu, my_to, j);
+    const int to1 = __shfl_sync(0xffffffffu, my_to, two ? j + 1 : j);
     const bool h0 = p0 >= 0, h1 = two && p1 >= 0;  // dropped units contribute nothing
-    if (h0) load_row<VPL>(Y, p0, d, lane, q0);
-    if (h1) load_row<VPL>(Y, p1, d, lane, q1);
+    if (h0) load_unit_row<VPL>(pp, pp.y_off, to0, Yl, p0, d, lane, q0);
+    if (h1) load_unit_row<VPL>(pp, pp.y_off, to1, Yl, p1, d, lane, q1);
     if (h0) axpy_row<VPL>(acc, q0, w0);
     if (h1) axpy_row<VPL>(acc, q1, w1);
   }
@@ -328,11 +385,13 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(const __nv_bfloat16* _
 //   dw_j       = <dy[t], Y[pos]>
 //   dl_j       = w_j * (dw_j - sum_i w_i dw_i)   (softmax over the kept logits)
 // dl is written per unit and, when dl_rows != null, per dispatch row.
+// P2P: Y rows are read from the expert's GPU, the dY row (and dl for the
+// host's gate-weight gradient) is written straight into its dY_perm / dl rows.
 template <int VPL>
 __global__ void __launch_bounds__(256) combine_bwd_kernel(
-    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Y,
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Yl,
     const int32_t* __restrict__ pos, const float* __restrict__ w, int T, int k,
-    __nv_bfloat16* __restrict__ dYbuf, float* __restrict__ dl, float* __restrict__ dl_rows) {
+    __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P pp) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -340,6 +399,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   int my_pos;
   float my_w;
   unit_meta(pos, w, static_cast<size_t>(t) * k, k, lane, my_pos, my_w);
+  const int my_to = unit_dst_of(pp, static_cast<size_t>(t) * k, k, lane);
   uint4 g[VPL];
   load_row<VPL>(dy, t, d, lane, g);
   float my_dw = 0.0f;  // lane j keeps dw_j
@@ -350,9 +410,10 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
       if (lane == j) my_dw = 0.0f;
       continue;
     }
+    const int to = __shfl_sync(0xffffffffu, my_to, j);
     uint4 q[VPL];
-    load_row<VPL>(Y, row, d, lane, q);
-    uint4* dst = reinterpret_cast<uint4*>(dYbuf + static_cast<size_t>(row) * d);
+    load_unit_row<VPL>(pp, pp.y_off, to, Yl, row, d, lane, q);
+    uint4* dst = reinterpret_cast<uint4*>(peer_rows(pp, pp.dy_off, to, dYl) + static_cast<size_t>(row) * d);
     float dot = 0.0f;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
@@ -376,17 +437,19 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   if (lane < k) {
     const float g_l = my_w * (my_dw - wdw);
     dl[static_cast<size_t>(t) * k + lane] = g_l;
+    float* dl_rows = peer_rows(pp, pp.dl_off, my_to, dl_rows_l);
     if (dl_rows && my_pos >= 0) dl_rows[my_pos] = g_l;
   }
 }
 
 // dx[t] = sum_j dXbuf[pos[t,j]] + sum_j dl[t,j] * Wg[idx[t,j], :]
+// P2P: dX rows are read from the expert's GPU (NVLink loads from its dX_perm).
 template <int VPL>
 __global__ void __launch_bounds__(256) unpermute_bwd_kernel(
-    const __nv_bfloat16* __restrict__ dXbuf, const int32_t* __restrict__ pos,
+    const __nv_bfloat16* __restrict__ dXl, const int32_t* __restrict__ pos,
     const int32_t* __restrict__ idx, const float* __restrict__ dl,
     const __nv_bfloat16* __restrict__ wg, int T, int k, int gate_grad,
-    __nv_bfloat16* __restrict__ dx) {
+    __nv_bfloat16* __restrict__ dx, const P2P pp) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -396,6 +459,7 @@ __global__ void __launch_bounds__(256) unpermute_bwd_kernel(
   unit_meta(pos, gate_grad ? dl : nullptr, static_cast<size_t>(t) * k, k, lane, my_pos, my_dl);
   unit_meta(idx, nullptr, static_cast<size_t>(t) * k, k, lane, my_e, my_dl);
   if (gate_grad && lane < k) my_dl = __ldg(dl + static_cast<size_t>(t) * k + lane);
+  const int my_to = unit_dst_of(pp, static_cast<size_t>(t) * k, k, lane);
   float acc[VPL][8];
 #pragma unroll
   for (int i = 0; i < VPL; ++i)
@@ -405,10 +469,12 @@ __global__ void __launch_bounds__(256) unpermute_bwd_kernel(
     const bool two = j + 1 < k;
     const int p0 = __shfl_sync(0xffffffffu, my_pos, j);
     const int p1 = __shfl_sync(0xffffffffu, my_pos, two ? j + 1 : j);
+    const int to0 = __shfl_sync(0xffffffffu, my_to, j);
+    const int to1 = __shfl_sync(0xffffffffu, my_to, two ? j + 1 : j);
     uint4 q0[VPL], q1[VPL];
     const bool h0 = p0 >= 0, h1 = two && p1 >= 0;
-    if (h0) load_row<VPL>(dXbuf, p0, d, lane, q0);
-    if (h1) load_row<VPL>(dXbuf, p1, d, lane, q1);
+    if (h0) load_unit_row<VPL>(pp, pp.dx_off, to0, dXl, p0, d, lane, q0);
+    if (h1) load_unit_row<VPL>(pp, pp.dx_off, to1, dXl, p1, d, lane, q1);
     if (h0) axpy_row<VPL>(acc, q0, 1.0f);
     if (h1) axpy_row<VPL>(acc, q1, 1.0f);
   }
@@ -609,6 +675,40 @@ __global__ void segment_tile_reduce_kernel(TileReduceJob j0, TileReduceJob j1, T
 
 }  // namespace
 
+// ----------------------------------------------------------------- P2P flags
+// Arrival flags live in every GPU's arena: flags[slot][src] = last epoch in
+// which `src` completed exchange `slot` towards this GPU. Epochs only grow, so
+// nothing is ever reset and a stale flag can never satisfy a newer wait.
+__global__ void p2p_signal_kernel(const P2P pp, int G, int me, int slot, unsigned long long epoch) {
+  const int dst = threadIdx.x;
+  if (dst >= G) return;
+  __threadfence_system();  // this stream's earlier writes (kernels before) are visible first
+  unsigned long long* f =
+      reinterpret_cast<unsigned long long*>(pp.base[dst] + pp.flag_off) + slot * kMaxPeers + me;
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+}
+
+// Waits until every source has signalled `epoch` in `slot` (bounded: after
+// ~20 s it records a timeout in *err and gives up instead of hanging).
+__global__ void p2p_wait_kernel(const unsigned long long* flags, int G, int slot, unsigned long long epoch,
+                                int* err) {
+  const int src = threadIdx.x;
+  if (src >= G) return;
+  const unsigned long long* f = flags + slot * kMaxPeers + src;
+  unsigned long long t0, now, v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+    if (v >= epoch) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - t0 > 20000000000ull) {
+      atomicExch(err, 1);
+      break;
+    }
+    __nanosleep(256);
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int max_rows, int d,
                        const float* dl_rows, const int32_t* row_expert, float* dwg, cudaStream_t s) {
@@ -677,7 +777,7 @@ void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_
 }
 
 void launch_plan(const int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
-                 const PlanDev& p, cudaStream_t s) {
+                 const PlanDev& p, cudaStream_t s, const int32_t* counts) {
   const int smem = N * G * G * 4;
   if (smem > 200 * 1024) throw std::invalid_argument("plan: N*G*G too large");
   static int configured = 0;
@@ -685,20 +785,21 @@ void launch_plan(const int64_t* flows, int N, int G, int me, const int32_t* loca
     FM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = smem;
   }
-  plan_kernel<<<1, 256, smem, s>>>(flows, N, G, me, local_expert, Nl, p);
+  plan_kernel<<<1, 256, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts);
   FM_LAUNCH_CHECK("plan_kernel");
 }
 
 void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
                      const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
                      const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
-                     cudaStream_t s) {
+                     cudaStream_t s, const P2P* pp) {
+  const P2P none{};
   if (d % 8 != 0 || d > 2048) throw std::invalid_argument("dispatch: d_model must be a multiple of 8, <= 2048");
   if (T <= 0) return;
   const int warps = 8;
   dispatch_kernel<<<(T + warps - 1) / warps, warps * 32, 0, s>>>(
       static_cast<const __nv_bfloat16*>(x), T, d, k, N, G, me, direct ? 1 : 0, idx, tile_rank,
-      tile_base, p, pos, static_cast<__nv_bfloat16*>(buf), row_expert);
+      tile_base, p, pos, static_cast<__nv_bfloat16*>(buf), row_expert, pp ? *pp : none);
   FM_LAUNCH_CHECK("dispatch_kernel");
 }
 
@@ -730,41 +831,55 @@ void launch_relayout(void* recv, void* perm, int d, int G, int Nl, const PlanDev
   }
 
 void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T, int d, int k,
-                        void* y, cudaStream_t s) {
+                        void* y, cudaStream_t s, const P2P* pp) {
+  const P2P none{};
   if (T <= 0) return;
   if (d % 256 != 0) throw std::invalid_argument("combine: d_model must be a multiple of 256");
   const int warps = 8;
   const int grid = (T + warps - 1) / warps;
   FM_VPL_DISPATCH(d, (combine_fwd_kernel<V><<<grid, warps * 32, 0, s>>>(
                          static_cast<const __nv_bfloat16*>(Y), pos, w, T, k,
-                         static_cast<__nv_bfloat16*>(y))));
+                         static_cast<__nv_bfloat16*>(y), pp ? *pp : none)));
   FM_LAUNCH_CHECK("combine_fwd_kernel");
 }
 
 void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const float* w, int T,
-                        int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s) {
+                        int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s, const P2P* pp) {
+  const P2P none{};
   if (T <= 0) return;
   if (k > 32) throw std::invalid_argument("combine_bwd: top_k <= 32");
   const int warps = 8;
   const int grid = (T + warps - 1) / warps;
   FM_VPL_DISPATCH(d, (combine_bwd_kernel<V><<<grid, warps * 32, 0, s>>>(
                          static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(Y),
-                         pos, w, T, k, static_cast<__nv_bfloat16*>(dYbuf), dl, dl_rows)));
+                         pos, w, T, k, static_cast<__nv_bfloat16*>(dYbuf), dl, dl_rows, pp ? *pp : none)));
   FM_LAUNCH_CHECK("combine_bwd_kernel");
 }
 
 void launch_unpermute_bwd(const void* dXbuf, const int32_t* pos, const int32_t* idx, const float* dl,
                           const void* wg, int T, int d, int k, bool gate_grad, void* dx,
-                          cudaStream_t s) {
+                          cudaStream_t s, const P2P* pp) {
+  const P2P none{};
   if (T <= 0) return;
   const int warps = 8;
   const int grid = (T + warps - 1) / warps;
   FM_VPL_DISPATCH(d, (unpermute_bwd_kernel<V><<<grid, warps * 32, 0, s>>>(
                          static_cast<const __nv_bfloat16*>(dXbuf), pos, idx, dl,
                          static_cast<const __nv_bfloat16*>(wg), T, k, gate_grad ? 1 : 0,
-                         static_cast<__nv_bfloat16*>(dx))));
+                         static_cast<__nv_bfloat16*>(dx), pp ? *pp : none)));
   FM_LAUNCH_CHECK("unpermute_bwd_kernel");
 }
 
+
+void launch_p2p_signal(const P2P& pp, int G, int me, int slot, unsigned long long epoch, cudaStream_t s) {
+  p2p_signal_kernel<<<1, 64, 0, s>>>(pp, G, me, slot, epoch);
+  FM_LAUNCH_CHECK("p2p_signal_kernel");
+}
+
+void launch_p2p_wait(const void* local_flags, int G, int slot, unsigned long long epoch, int* err,
+                     cudaStream_t s) {
+  p2p_wait_kernel<<<1, 64, 0, s>>>(static_cast<const unsigned long long*>(local_flags), G, slot, epoch, err);
+  FM_LAUNCH_CHECK("p2p_wait_kernel");
+}
 
 }  // namespace fm

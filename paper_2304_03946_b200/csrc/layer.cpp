@@ -32,11 +32,11 @@ void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, 
 void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_t* tile_base,
                         int64_t* hist, int64_t* demand_NG, int G, int me, cudaStream_t s);
 void launch_plan(const int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
-                 const PlanDev& p, cudaStream_t s);
+                 const PlanDev& p, cudaStream_t s, const int32_t* counts = nullptr);
 void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
                      const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
                      const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
-                     cudaStream_t s);
+                     cudaStream_t s, const P2P* pp = nullptr);
 void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, int32_t* row_expert, cudaStream_t s);
 void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int max_rows, int d,
                        const float* dl_rows, const int32_t* row_expert, float* dwg, cudaStream_t s);
@@ -45,12 +45,12 @@ void launch_demand_transpose(const int64_t* gathered_GN, int N, int G, int64_t* 
 void launch_relayout(void* recv, void* perm, int d, int G, int Nl, const PlanDev& p, int max_rows,
                      int dir, cudaStream_t s);
 void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T, int d, int k,
-                        void* y, cudaStream_t s);
+                        void* y, cudaStream_t s, const P2P* pp = nullptr);
 void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const float* w, int T,
-                        int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s);
+                        int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s, const P2P* pp = nullptr);
 void launch_unpermute_bwd(const void* dXbuf, const int32_t* pos, const int32_t* idx, const float* dl,
                           const void* wg, int T, int d, int k, bool gate_grad, void* dx,
-                          cudaStream_t s);
+                          cudaStream_t s, const P2P* pp = nullptr);
 void launch_segment_tile_colsum(const void* buf0, const float* w0, float* partial0, const void* buf1,
                                 const float* w1, float* partial1, int cols, const PlanDev& p, int Nl,
                                 int max_tiles, cudaStream_t s);
@@ -58,6 +58,9 @@ void launch_segment_tile_reduce(const float* partial0, int cols0, const int32_t*
                                 const float* partial1, int cols1, const int32_t* idx1, float* out1,
                                 const float* partial2, int cols2, const int32_t* idx2, float* out2,
                                 const PlanDev& p, int Nl, cudaStream_t s);
+void launch_p2p_signal(const P2P& pp, int G, int me, int slot, unsigned long long epoch, cudaStream_t s);
+void launch_p2p_wait(const void* local_flags, int G, int slot, unsigned long long epoch, int* err,
+                     cudaStream_t s);
 void launch_dropped_gate_wgrad(const void* x, const int32_t* pos, const int32_t* idx, const float* dl,
                                int T, int d, int k, float* dwg, cudaStream_t s);
 void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
@@ -70,17 +73,25 @@ namespace {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool owned = true;  // false: a view into another allocation (the P2P arena)
   void reset(size_t n) {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     bytes = 0;
+    owned = true;
     if (n) {
       FM_CUDA(cudaMalloc(&p, n));
       bytes = n;
     }
   }
+  void view(void* ptr, size_t n) {
+    if (p && owned) cudaFree(p);
+    p = ptr;
+    bytes = n;
+    owned = false;
+  }
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
   }
   template <class T>
   T* as() const {
@@ -225,7 +236,7 @@ class Layer {
     const int Nl = static_cast<int>(local_.size());
     // plan arrays: one int32 allocation
     const size_t n_plan = 3 * N * G + 2 * G + N + 3 * Nl + (Nl + 1) + (G * Nl + 1) + G * Nl + 4 +
-                          Nl /*local_expert*/;
+                          Nl /*local_expert*/ + N * G /*peer_row*/;
     plan_mem_.reset(sizeof(int32_t) * n_plan);
     int32_t* q = plan_mem_.as<int32_t>();
     auto take = [&](size_t n) {
@@ -247,6 +258,8 @@ class Layer {
     plan_.recv_chunk_dst = take(G * Nl);
     plan_.totals = take(4);
     local_expert_dev_ = take(Nl);
+    peer_row_mem_ = take(N * G);
+    plan_.peer_row = p2p_ ? peer_row_mem_ : nullptr;
     std::vector<int32_t> li(N, -1);
     for (int i = 0; i < Nl; ++i) li[local_[i]] = i;
     FM_CUDA(cudaMemcpy(plan_.local_index, li.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
@@ -266,13 +279,15 @@ class Layer {
     if (rows <= row_cap_) return;
     const size_t d = cfg_.d_model, f = cfg_.d_ff;
     row_cap_ = std::max<size_t>(rows, 128);
-    x_perm_.reset(2 * row_cap_ * d);
+    if (!p2p_) {  // with P2P these live in the shared arena, sized for the worst case
+      x_perm_.reset(2 * row_cap_ * d);
+      y_perm_.reset(2 * row_cap_ * d);
+      dy_perm_.reset(2 * row_cap_ * d);
+      dx_perm_.reset(2 * row_cap_ * d);
+      dl_rows_.reset(4 * row_cap_);
+    }
     act_.reset(2 * row_cap_ * f);
-    y_perm_.reset(2 * row_cap_ * d);
-    dy_perm_.reset(2 * row_cap_ * d);
     dh_.reset(2 * row_cap_ * f);
-    dx_perm_.reset(2 * row_cap_ * d);
-    dl_rows_.reset(4 * row_cap_);
     row_expert_.reset(4 * row_cap_);
     relu_mask_.reset(4 * row_cap_ * (f / 32));
     tile_colsum_.reset(4 * (row_cap_ / 128) * f);
@@ -338,6 +353,7 @@ class Layer {
     cur_T_ = T;
     saved_x_ = x;
     fused_state_ = false;
+    if (p2p_) ++epoch_;  // one exchange epoch per step, the same on every GPU
   }
 
   // route() on the device over demand_ (already complete), then the plan. In
@@ -353,7 +369,8 @@ class Layer {
     }
     route_counts_device(routed, counts_dev_.as<int32_t>(), N, G, flows_.as<int64_t>(),
                         route_status_.as<int32_t>(), s);
-    launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s);
+    launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s,
+                p2p_ ? counts_dev_.as<int32_t>() : nullptr);
     timer_.end(s);
   }
 
@@ -425,10 +442,15 @@ class Layer {
 
   // dwg_tiles (fused path): also the gate-weight gradient of the dispatched
   // units, from X_perm and dl per dispatch row, in the same tile passes.
+  // signal_dx (P2P): tell the sources dX_perm is complete right after the
+  // FFN1 dgrad, so their un-permute overlaps this GPU's weight gradients.
   void expert_backward(const void* w1, const void* w2, float* dw1, float* db1, float* dw2,
-                       float* db2, cudaStream_t s, float* dwg_tiles = nullptr) {
+                       float* db2, cudaStream_t s, float* dwg_tiles = nullptr, bool signal_dx = false) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
-    if (Nl == 0) return;
+    if (Nl == 0) {
+      if (signal_dx) p2p_signal(3, s);
+      return;
+    }
     const int rows = static_cast<int>(row_cap_);
     // dA = dY . W2 masked by relu'(H) -> dH [rows, f]; db1 partials per 128-row tile
     timer_.begin(FM_PHASE_FFN2_DGRAD, s);
@@ -441,6 +463,7 @@ class Layer {
     grouped_gemm(FM_GEMM_DGRAD, dh_.p, w1, dx_perm_.p, nullptr, nullptr, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s);
     timer_.end(s);
+    if (signal_dx) p2p_signal(3, s);
     // dW2[li] = dY^T . act  [d, f];  dW1[li] = dH^T . X  [f, d]
     if (dw2) {
       timer_.begin(FM_PHASE_FFN2_WGRAD, s);
@@ -517,6 +540,141 @@ class Layer {
     }
   }
 
+  // ------------------------------------------------------------ P2P transport
+  // Token rows move over NVLink inside the kernels that produce / consume
+  // them (no staging buffers, no all-to-all, no relayout): dispatch writes
+  // x rows into the expert GPU's X_perm, combine reads Y rows from the expert
+  // GPU's Y_perm, combine_bwd writes dY rows (and dl) into its dY_perm,
+  // un-permute reads dX rows from its dX_perm. Arrival flags order them.
+  void enable_p2p() {
+    if (p2p_) return;
+    const size_t N = cfg_.num_experts, G = cfg_.num_gpus, T = cfg_.max_tokens, k = cfg_.top_k;
+    const size_t d = cfg_.d_model;
+    if (G > static_cast<size_t>(kMaxPeers)) throw std::invalid_argument("fm_layer_enable_p2p: at most 64 GPUs");
+    // worst case of route(): every unit of every GPU lands here, plus padding
+    const size_t rows = round_up(G * T * k + N * 127, 128);
+    auto al = [](size_t b) { return round_up(b, 256); };
+    const size_t rb = al(2 * rows * d);
+    pp_ = P2P{};
+    pp_.x_off = 0;
+    pp_.y_off = rb;
+    pp_.dy_off = 2 * rb;
+    pp_.dx_off = 3 * rb;
+    pp_.dl_off = 4 * rb;
+    pp_.flag_off = 4 * rb + al(4 * rows);
+    const size_t bytes = pp_.flag_off + al(sizeof(unsigned long long) * kP2PSlots * kMaxPeers);
+    arena_.reset(bytes);
+    FM_CUDA(cudaMemset(arena_.p, 0, bytes));
+    char* a = arena_.as<char>();
+    p2p_ = true;
+    x_perm_.view(a + pp_.x_off, 2 * rows * d);
+    y_perm_.view(a + pp_.y_off, 2 * rows * d);
+    dy_perm_.view(a + pp_.dy_off, 2 * rows * d);
+    dx_perm_.view(a + pp_.dx_off, 2 * rows * d);
+    dl_rows_.view(a + pp_.dl_off, 4 * rows);
+    row_cap_ = 0;
+    ensure_rows(rows);  // the local per-row buffers at the same capacity
+    unit_dst_.reset(sizeof(int32_t) * T * k);
+    p2p_err_.reset(sizeof(int));
+    FM_CUDA(cudaMemset(p2p_err_.p, 0, sizeof(int)));
+    pp_.unit_dst = unit_dst_.as<int32_t>();
+    peer_ipc_.assign(G, false);
+    pp_.base[cfg_.rank] = a;
+    plan_.peer_row = peer_row_mem_;
+  }
+  void p2p_handle(void* out64) {
+    require_p2p();
+    cudaIpcMemHandle_t h;
+    FM_CUDA(cudaIpcGetMemHandle(&h, arena_.p));
+    std::memcpy(out64, &h, sizeof(h));
+  }
+  void p2p_open_peer(int peer, const void* handle64) {
+    require_p2p();
+    check_peer(peer);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    void* ptr = nullptr;
+    FM_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    close_peer(peer);
+    pp_.base[peer] = static_cast<char*>(ptr);
+    peer_ipc_[peer] = true;
+  }
+  void p2p_link_peer(int peer, Layer& other) {
+    require_p2p();
+    check_peer(peer);
+    if (!other.p2p_ || other.arena_.bytes != arena_.bytes)
+      throw std::invalid_argument("fm_layer_p2p_link_peer: peer layer has a different P2P arena");
+    close_peer(peer);
+    pp_.base[peer] = other.arena_.as<char>();
+  }
+  int p2p_status() {
+    if (!p2p_) return 0;
+    int e = 0;
+    FM_CUDA(cudaMemcpy(&e, p2p_err_.p, sizeof(int), cudaMemcpyDeviceToHost));
+    return e;
+  }
+  void route_p2p(const int64_t* gathered_GN, cudaStream_t s) {
+    require_linked();
+    launch_demand_transpose(gathered_GN, cfg_.num_experts, cfg_.num_gpus, demand_.as<int64_t>(), s);
+    route_device(s);  // flows + plan incl. every destination's X_perm rows; no host sync
+  }
+  void dispatch_p2p(const void* x, cudaStream_t s) {
+    timer_.begin(FM_PHASE_DISPATCH, s);
+    launch_dispatch(x, cur_T_, cfg_.d_model, cfg_.top_k, cfg_.num_experts, cfg_.num_gpus, cfg_.rank, false,
+                    topk_idx_.as<int32_t>(), tile_rank_.as<int32_t>(), tile_base_.as<int32_t>(), plan_,
+                    pos_.as<int32_t>(), nullptr, nullptr, s, &pp_);
+    timer_.end(s);
+    p2p_signal(0, s);
+  }
+  void expert_forward_p2p(const void* w1, const float* b1, const void* w2, const float* b2, cudaStream_t s) {
+    launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);  // own pad rows only
+    p2p_wait(0, s);
+    expert_forward(w1, b1, w2, b2, s);
+    p2p_signal(1, s);
+  }
+  void combine_p2p(void* y, cudaStream_t s) {
+    p2p_wait(1, s);
+    timer_.begin(FM_PHASE_COMBINE_FWD, s);
+    launch_combine_fwd(y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), cur_T_, cfg_.d_model, cfg_.top_k, y, s,
+                       &pp_);
+    timer_.end(s);
+  }
+  void combine_backward_p2p(const void* dy, cudaStream_t s) {
+    const bool gate_grad = cfg_.top_k > 1;
+    timer_.begin(FM_PHASE_COMBINE_BWD, s);
+    launch_combine_bwd(dy, y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), cur_T_, cfg_.d_model, cfg_.top_k,
+                       dy_perm_.p, dl_.as<float>(), gate_grad ? dl_rows_.as<float>() : nullptr, s, &pp_);
+    timer_.end(s);
+    p2p_signal(2, s);
+  }
+  // dwg (optional) receives this GPU's share of the gate-weight gradient: its
+  // hosted units (dl-weighted X_perm tile sums), to be summed over all GPUs.
+  void expert_backward_p2p(const void* w1, const void* w2, float* dw1, float* db1, float* dw2, float* db2,
+                           float* dwg, cudaStream_t s) {
+    launch_zero_pad(dy_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);
+    p2p_wait(2, s);
+    const bool dwg_tiles = dwg && cfg_.top_k > 1 && nl() > 0;
+    if (dwg && !dwg_tiles)
+      FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * cfg_.num_experts * cfg_.d_model, s));
+    expert_backward(w1, w2, dw1, db1, dw2, db2, s, dwg_tiles ? dwg : nullptr, /*signal_dx=*/true);
+  }
+  void unpermute_backward_p2p(const void* wg, void* dx, float* dwg, cudaStream_t s) {
+    const int T = cur_T_, d = cfg_.d_model, k = cfg_.top_k;
+    const bool gate_grad = k > 1;
+    p2p_wait(3, s);
+    timer_.begin(FM_PHASE_UNPERMUTE, s);
+    launch_unpermute_bwd(dx_perm_.p, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(), wg, T, d, k,
+                         gate_grad, dx, s, &pp_);
+    timer_.end(s);
+    if (dwg && gate_grad && drops_enabled()) {  // dropped units are in no X_perm: add them here
+      timer_.begin(FM_PHASE_GATE_WGRAD, s);
+      launch_dropped_gate_wgrad(saved_x_, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(), T, d, k,
+                                dwg, s);
+      timer_.end(s);
+    }
+  }
+  bool p2p() const { return p2p_; }
+
   // phase wrappers (G >= 1)
   void ph_expert_forward(const void* recv_buf, const void* w1, const float* b1, const void* w2,
                          const float* b2, void* ret_buf, cudaStream_t s) {
@@ -589,7 +747,47 @@ class Layer {
       throw std::invalid_argument("fm_layer: token count exceeds max_tokens");
   }
 
+  void require_p2p() const {
+    if (!p2p_) throw std::logic_error("fm_layer: P2P transport not enabled (fm_layer_enable_p2p)");
+  }
+  void require_linked() const {
+    require_p2p();
+    for (int g = 0; g < cfg_.num_gpus; ++g)
+      if (!pp_.base[g]) throw std::logic_error("fm_layer: P2P peer " + std::to_string(g) + " is not mapped");
+  }
+  void check_peer(int peer) const {
+    if (peer < 0 || peer >= cfg_.num_gpus || peer == cfg_.rank)
+      throw std::out_of_range("fm_layer: P2P peer out of range");
+  }
+  void close_peer(int peer) {
+    if (peer_ipc_[peer] && pp_.base[peer]) cudaIpcCloseMemHandle(pp_.base[peer]);
+    peer_ipc_[peer] = false;
+    pp_.base[peer] = nullptr;
+  }
+  void p2p_signal(int slot, cudaStream_t s) {
+    launch_p2p_signal(pp_, cfg_.num_gpus, cfg_.rank, slot, epoch_, s);
+  }
+  void p2p_wait(int slot, cudaStream_t s) {
+    timer_.begin(FM_PHASE_RELAYOUT, s);
+    launch_p2p_wait(arena_.as<char>() + pp_.flag_off, cfg_.num_gpus, slot, epoch_, p2p_err_.as<int>(), s);
+    timer_.end(s);
+  }
+
+ public:
+  ~Layer() {
+    if (p2p_)
+      for (int g = 0; g < cfg_.num_gpus; ++g)
+        if (peer_ipc_[g] && pp_.base[g]) cudaIpcCloseMemHandle(pp_.base[g]);
+  }
+
+ private:
   fm_layer_config cfg_;
+  bool p2p_ = false;
+  DevBuf arena_, unit_dst_, p2p_err_;
+  P2P pp_{};
+  std::vector<bool> peer_ipc_;
+  unsigned long long epoch_ = 0;
+  int32_t* peer_row_mem_ = nullptr;
   std::vector<int32_t> counts_, local_;
   DevBuf topk_idx_, topk_w_, tile_rank_, pos_, dl_, tile_counts_, tile_base_, hist_, demand_,
       flows_, counts_dev_, route_status_, plan_mem_;
@@ -710,6 +908,70 @@ int fm_layer_unpermute_backward(fm_layer* h, const void* dback_buf, const void* 
   return fm::guarded([&] {
     h->impl->ph_unpermute_backward(dback_buf, send_buf, wg, dx, dwg, static_cast<cudaStream_t>(stream));
   });
+}
+
+int fm_layer_enable_p2p(fm_layer* h) {
+  return fm::guarded([&] { h->impl->enable_p2p(); });
+}
+
+int fm_layer_p2p_handle(fm_layer* h, void* handle64) {
+  return fm::guarded([&] {
+    if (!handle64) throw std::invalid_argument("fm_layer_p2p_handle: null handle");
+    h->impl->p2p_handle(handle64);
+  });
+}
+
+int fm_layer_p2p_open_peer(fm_layer* h, int peer, const void* handle64) {
+  return fm::guarded([&] {
+    if (!handle64) throw std::invalid_argument("fm_layer_p2p_open_peer: null handle");
+    h->impl->p2p_open_peer(peer, handle64);
+  });
+}
+
+int fm_layer_p2p_link_peer(fm_layer* h, int peer, fm_layer* other) {
+  return fm::guarded([&] {
+    if (!other) throw std::invalid_argument("fm_layer_p2p_link_peer: null peer layer");
+    h->impl->p2p_link_peer(peer, *other->impl);
+  });
+}
+
+int fm_layer_p2p_status(fm_layer* h, int* timed_out) {
+  return fm::guarded([&] {
+    if (!timed_out) throw std::invalid_argument("fm_layer_p2p_status: null output");
+    *timed_out = h->impl->p2p_status();
+  });
+}
+
+int fm_layer_route_p2p(fm_layer* h, const int64_t* gathered_hist_GN, void* stream) {
+  return fm::guarded([&] { h->impl->route_p2p(gathered_hist_GN, static_cast<cudaStream_t>(stream)); });
+}
+
+int fm_layer_dispatch_p2p(fm_layer* h, const void* x, void* stream) {
+  return fm::guarded([&] { h->impl->dispatch_p2p(x, static_cast<cudaStream_t>(stream)); });
+}
+
+int fm_layer_expert_forward_p2p(fm_layer* h, const void* w1, const float* b1, const void* w2, const float* b2,
+                                void* stream) {
+  return fm::guarded([&] { h->impl->expert_forward_p2p(w1, b1, w2, b2, static_cast<cudaStream_t>(stream)); });
+}
+
+int fm_layer_combine_p2p(fm_layer* h, void* y, void* stream) {
+  return fm::guarded([&] { h->impl->combine_p2p(y, static_cast<cudaStream_t>(stream)); });
+}
+
+int fm_layer_combine_backward_p2p(fm_layer* h, const void* dy, void* stream) {
+  return fm::guarded([&] { h->impl->combine_backward_p2p(dy, static_cast<cudaStream_t>(stream)); });
+}
+
+int fm_layer_expert_backward_p2p(fm_layer* h, const void* w1, const void* w2, float* dw1, float* db1, float* dw2,
+                                 float* db2, float* dwg, void* stream) {
+  return fm::guarded([&] {
+    h->impl->expert_backward_p2p(w1, w2, dw1, db1, dw2, db2, dwg, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fm_layer_unpermute_backward_p2p(fm_layer* h, const void* wg, void* dx, float* dwg, void* stream) {
+  return fm::guarded([&] { h->impl->unpermute_backward_p2p(wg, dx, dwg, static_cast<cudaStream_t>(stream)); });
 }
 
 int fm_layer_set_timing(fm_layer* h, int enable) {

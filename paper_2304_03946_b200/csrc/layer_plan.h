@@ -21,6 +21,21 @@ struct PlanDev {
   int32_t* recv_chunk_off;  // [G*Nl+1] a2a receive-buffer offset of (src, li)
   int32_t* recv_chunk_dst;  // [G*Nl]  X_perm row of that chunk's first row
   int32_t* totals;          // [4]     padded rows, units sent, units received
+  int32_t* peer_row;        // [N][G]  P2P: X_perm row on dst of (e, me)'s first unit (null otherwise)
+};
+
+// Peer-to-peer transport: every GPU's exchange arena holds its
+// X_perm, Y_perm, dY_perm, dX_perm (bf16 rows), dl per X_perm row (f32) and
+// the arrival flags, at the same offsets on every GPU; base[g] is GPU g's
+// arena as mapped in this process (CUDA IPC, or the pointer itself in one
+// process). Units carry their destination GPU in unit_dst; null unit_dst
+// means the single-GPU / NCCL layouts (local buffers only).
+constexpr int kMaxPeers = 64;
+constexpr int kP2PSlots = 4;  // 0 rows dispatched, 1 Y ready, 2 dY rows pushed, 3 dX ready
+struct P2P {
+  char* base[kMaxPeers];
+  int64_t x_off, y_off, dy_off, dx_off, dl_off, flag_off;  // byte offsets inside an arena
+  int32_t* unit_dst;                                       // [T*k] destination GPU (-1: dropped)
 };
 
 }  // namespace fm

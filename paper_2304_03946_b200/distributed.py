@@ -139,6 +139,16 @@ class Exchange:
         across processes, plain pointers in one process."""
         raise NotImplementedError
 
+    def share_layer(self, layer) -> None:
+        """Map every peer's P2P exchange arena into `layer` (collective)."""
+        raise NotImplementedError
+
+    def fence(self) -> None:
+        """Before a device-side arrival wait: every rank's preceding signals must
+        be enqueued. Separate GPUs need nothing; ranks sharing one device
+        stream (loopback) rendezvous on the host so no wait is queued ahead of
+        the signal it waits for."""
+
 
 class TorchExchange(Exchange):
     """torch.distributed transport (NCCL on B200 / NVLink; gloo on CPU)."""
@@ -178,6 +188,13 @@ class TorchExchange(Exchange):
         for peer, h in enumerate(handles):
             if peer != self.rank:
                 pool.open_peer(peer, h)
+
+    def share_layer(self, layer):
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, layer.p2p_handle())
+        for peer, h in enumerate(handles):
+            if peer != self.rank:
+                layer.p2p_open_peer(peer, h)
 
     def all_reduce(self, t, group):
         if group is None:
@@ -247,6 +264,14 @@ class LoopbackExchange(Exchange):
             if peer != self.rank:
                 pool.link_peer(peer, other)
 
+    def share_layer(self, layer):
+        for peer, other in enumerate(self._swap(layer)):
+            if peer != self.rank:
+                layer.p2p_link_peer(peer, other)
+
+    def fence(self):
+        self.hub.barrier.wait()
+
     def all_reduce(self, t, group):
         members = range(self.world) if group is None else group
         allv = self._swap(t.clone() if (t is not None and self.rank in members) else None)
@@ -271,13 +296,24 @@ class StepBuffers:
 class DistributedMoELayer:
     """FlexMoE layer on one GPU of G, driving fm_layer_* phases around `exchange`."""
 
-    def __init__(self, layer, exchange: Exchange):
+    def __init__(self, layer, exchange: Exchange, transport: str = "nccl"):
+        """transport "nccl": dispatch / combine and their backward mirrors are
+        all-to-alls of staging buffers (plus relayouts). "p2p": token rows
+        cross NVLink inside the dispatch / combine / un-permute kernels,
+        straight between the token's GPU and its expert GPU's permuted
+        buffers (CUDA IPC-mapped arenas, device-side arrival flags)."""
         from .layer import MoELayer
 
         assert isinstance(layer, MoELayer)
         self.layer, self.ex = layer, exchange
         if layer.G != exchange.world or layer.rank != exchange.rank:
             raise L.InvalidArgument("DistributedMoELayer: layer and exchange disagree on rank/world")
+        if transport not in ("nccl", "p2p"):
+            raise L.InvalidArgument(f"DistributedMoELayer: unknown transport {transport!r}")
+        self.transport = transport
+        if transport == "p2p":
+            layer.enable_p2p()
+            exchange.share_layer(layer)
         self._st: StepBuffers | None = None
         self._saved = None
         self._timing = False
@@ -335,6 +371,8 @@ class DistributedMoELayer:
         gathered = self._x("all_gather", self.ex.all_gather, hist)  # [G, N]
         if after_gather is not None:
             after_gather()
+        if self.transport == "p2p":
+            return self._forward_p2p(x, T, wg, w1, b1, w2, b2, gathered, on_demand, before_experts)
         if on_demand is not None:
             new = on_demand(gathered.cpu().numpy().T.copy())
             if new is not None:
@@ -367,9 +405,60 @@ class DistributedMoELayer:
         self.last_demand = gathered
         return y
 
+    def _forward_p2p(self, x, T, wg, w1, b1, w2, b2, gathered, on_demand, before_experts):
+        stream = L.stream_ptr()
+        self.last_demand_host = gathered.cpu().numpy().T.copy()  # TokenDemand [N][G] (policy input)
+        if on_demand is not None:
+            new = on_demand(self.last_demand_host.copy())
+            if new is not None:
+                w1, b1, w2, b2 = new
+        self._call("fm_layer_route_p2p", gathered.data_ptr(), stream)
+        self._call("fm_layer_dispatch_p2p", x.data_ptr(), stream)
+        self.ex.fence()
+        if before_experts is not None:
+            before_experts()
+        self._call("fm_layer_expert_forward_p2p", w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(),
+                   stream)
+        self.ex.fence()
+        y = torch.empty(T, self.layer.d, dtype=torch.bfloat16, device=x.device)
+        self._call("fm_layer_combine_p2p", y.data_ptr(), stream)
+        self._st = None
+        self._saved = (T, wg, w1, w2, x)
+        self.last_demand = gathered
+        return y
+
+    def _backward_p2p(self, dy, sync):
+        from .layer import LayerGrads
+
+        T, wg, w1, w2, _x = self._saved
+        lay, dev, stream = self.layer, dy.device, L.stream_ptr()
+        nl = len(lay.local_experts)
+        k, d, f, N = lay.k, lay.d, lay.f, lay.N
+        z = lambda *s: torch.empty(*s, device=dev, dtype=torch.float32)
+        g = LayerGrads(dx=torch.empty(T, d, device=dev, dtype=torch.bfloat16), dwg=z(N, d),
+                       dw1=z(max(nl, 1), f, d), db1=z(max(nl, 1), f), dw2=z(max(nl, 1), d, f),
+                       db2=z(max(nl, 1), d))
+        self._call("fm_layer_combine_backward_p2p", dy.data_ptr(), stream)
+        self.ex.fence()
+        self._call("fm_layer_expert_backward_p2p", w1.data_ptr(), w2.data_ptr(), g.dw1.data_ptr(),
+                   g.db1.data_ptr(), g.dw2.data_ptr(), g.db2.data_ptr(), g.dwg.data_ptr(), stream)
+        self.ex.fence()
+        self._call("fm_layer_unpermute_backward_p2p", wg.data_ptr(), g.dx.data_ptr(), g.dwg.data_ptr(), stream)
+        if nl == 0:
+            g.dw1, g.db1, g.dw2, g.db2 = (t[:0] for t in (g.dw1, g.db1, g.dw2, g.db2))
+        if sync:  # dwg holds this GPU's share: the all-GPU sum below completes it
+            self._x("grad_sync", self.sync_grads, g)
+        return g
+
+    def p2p_timed_out(self) -> bool:
+        """True if a device-side P2P arrival wait gave up (synchronises)."""
+        return self.layer.p2p_status() != 0
+
     def backward(self, dy, sync=True):
         from .layer import LayerGrads
 
+        if self.transport == "p2p":
+            return self._backward_p2p(dy, sync)
         T, wg, w1, w2, _x = self._saved
         st = self._st
         lay = self.layer

@@ -139,6 +139,29 @@ class MoELayer:
         self._alive = None  # enqueued: later allocations are stream-ordered after it
         return grads
 
+    # ---------------------------------------------------------------- P2P transport
+    def enable_p2p(self) -> None:
+        """Allocate the exchange arena for the peer-to-peer transport."""
+        L.check(L.lib().fm_layer_enable_p2p(self._h))
+
+    def p2p_handle(self) -> bytes:
+        buf = (C.c_char * 64)()
+        L.check(L.lib().fm_layer_p2p_handle(self._h, buf))
+        return bytes(buf)
+
+    def p2p_open_peer(self, peer: int, handle: bytes) -> None:
+        buf = (C.c_char * 64).from_buffer_copy(handle)
+        L.check(L.lib().fm_layer_p2p_open_peer(self._h, peer, buf))
+
+    def p2p_link_peer(self, peer: int, other: "MoELayer") -> None:
+        L.check(L.lib().fm_layer_p2p_link_peer(self._h, peer, other._h))
+        self._p2p_peers = getattr(self, "_p2p_peers", []) + [other]  # keep the peer arena alive
+
+    def p2p_status(self) -> int:
+        st = C.c_int(0)
+        L.check(L.lib().fm_layer_p2p_status(self._h, C.byref(st)))
+        return st.value
+
     # ---------------------------------------------------------------- timing
     def set_timing(self, enable: bool) -> None:
         L.check(L.lib().fm_layer_set_timing(self._h, 1 if enable else 0))

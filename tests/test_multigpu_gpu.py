@@ -60,8 +60,35 @@ PLACEMENTS = {
 }
 
 
+def p2p_rows(idx, flows, me, G, N, cnt):
+    """P2P: row of each unit in its destination GPU's X_perm (that GPU's padded
+    expert segments, sources ascending inside a segment, then rank)."""
+    ranks = OL.unit_ranks(idx, N)
+    starts = {}
+    for dst in range(G):
+        local = [e for e in range(N) if cnt[e, dst] > 0]
+        for e, (s0, _, _) in zip(local, OL.segments(flows, local, dst)):
+            starts[(e, dst)] = s0 + int(flows[e, :me, dst].sum())
+    order = [me] + [g for g in range(G) if g != me]
+    rows = np.zeros(idx.shape, np.int64)
+    for t in range(idx.shape[0]):
+        for j in range(idx.shape[1]):
+            e, r, lo = idx[t, j], ranks[t, j], 0
+            for dst in order:
+                c = flows[e, me, dst]
+                if r < lo + c:
+                    rows[t, j] = starts[(e, dst)] + r - lo
+                    break
+                lo += c
+    return rows
+
+
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
 @pytest.mark.parametrize("name", sorted(PLACEMENTS))
-def test_multigpu_loopback_parity(name):
+def test_multigpu_loopback_parity(name, transport):
+    """transport "nccl": staging buffers + all-to-alls (loopback copies here);
+    "p2p": rows written / read directly in the peers' permuted buffers inside
+    the dispatch / combine / un-permute kernels, device-side arrival flags."""
     N, G, pairs = PLACEMENTS[name]
     k, d, f, T = 2, 256, 512, 600
     cnt = np.zeros((N, G), np.int32)
@@ -84,7 +111,7 @@ def test_multigpu_loopback_parity(name):
         torch.cuda.set_device(0)
         lay = MoELayer(N, k, d, f, replica_counts=cnt, num_gpus=G, rank=r, max_tokens=T)
         loc = lay.local_experts
-        dl = DistributedMoELayer(lay, hub.endpoint(r))
+        dl = DistributedMoELayer(lay, hub.endpoint(r), transport=transport)
         xs = slice(r * T, (r + 1) * T)
         y = dl.forward(dev(X[xs]), dev(wg), dev(w1[loc]), dev(b1[loc], torch.float32),
                        dev(w2[loc]), dev(b2[loc], torch.float32))
@@ -94,8 +121,11 @@ def test_multigpu_loopback_parity(name):
         pos = lay.read("unit_pos", T * k).reshape(T, k)
         flows = lay.read("flows", N * G * G).reshape(N, G, G)
         D = dl.last_demand.cpu().numpy()
+        if transport == "p2p":
+            assert not dl.p2p_timed_out(), "a P2P arrival wait timed out"
+        st_ = dl._st
         return dict(loc=loc, y=y.float().cpu().numpy(), idx=idx, pos=pos, flows=flows, D=D,
-                    send_rows=dl._st.send_rows, recv_rows=dl._st.recv_rows,
+                    send_rows=st_.send_rows if st_ else None, recv_rows=st_.recv_rows if st_ else None,
                     dx=g.dx.float().cpu().numpy(), dw1=g.dw1.cpu().numpy(), dw2=g.dw2.cpu().numpy(),
                     db1=g.db1.cpu().numpy(), db2=g.db2.cpu().numpy(), dwg=g.dwg.cpu().numpy())
 
@@ -109,6 +139,10 @@ def test_multigpu_loopback_parity(name):
         assert (o["flows"] == flows_ref).all(), "flows differ from route()"
         idx_r = st["idx"][r * T:(r + 1) * T]
         assert (o["idx"] == idx_r).all()
+        if transport == "p2p":
+            rows = p2p_rows(idx_r, flows_ref, r, G, N, cnt)
+            assert (o["pos"] == rows).all(), f"rank {r}: X_perm rows on the expert GPUs differ"
+            continue
         rows, _ = OL.dispatch_rows(idx_r, OL.unit_ranks(idx_r, N), flows_ref, r, G, N)
         assert (o["pos"] == rows).all(), f"rank {r}: dispatch rows differ"
         assert o["send_rows"] == [int(flows_ref[:, r, dst].sum()) for dst in range(G)]
