@@ -299,12 +299,16 @@ class DistArm:
         self.logp = zipf_log_popularity(N, cfg["zipf"], 42)
         wg[:, 0] = torch.tensor(self.logp * 2, dtype=torch.float32)
         sched_cfg = S.SchedulerConfig.defaults(policy_mode=cfg["policy_mode"], interval_steps=cfg["interval"])
+        self.transport = cfg.get("transport", "p2p")
         self.rt = FlexMoERuntime(N, k, d, f, ex, prof, sched_cfg=sched_cfg, max_tokens=T, gate_weight=wg,
-                                 optimizer=False)
+                                 optimizer=False, transport=self.transport)
         self.layer, self.dl = self.rt.layer, self.rt.dl
         self.drift = np.random.default_rng(42)  # same walk on every rank
         self.N, self.G = N, G
-        self.kernels_per_step = 9 + 8 + (2 if k > 1 else 1) + 4 + 1  # + relayouts, transpose
+        if self.transport == "p2p":  # fwd 14 (incl. 2 signals, 2 waits), bwd 13 (incl. 2 signals, 2 waits)
+            self.kernels_per_step = 27
+        else:
+            self.kernels_per_step = 9 + 8 + (2 if k > 1 else 1) + 4 + 1  # + relayouts, transpose
         self.reset_stats()
 
     def reset_stats(self):
@@ -345,6 +349,9 @@ class DistArm:
 
     def summary(self, steps):
         return {"placement": "dynamic (host scheduler: expand/shrink/migrate, B200 profile)",
+                "token_transport": ("P2P: rows written/read in the expert GPU's permuted buffers inside "
+                                    "dispatch/combine/un-permute (CUDA IPC, NVLink), device-side flags")
+                if self.transport == "p2p" else "NCCL all-to-all of staging buffers",
                 "profile_tps": self.tps, "profile_tps_source": self.tps_source,
                 "balance_ratio_mean": float(np.mean(self.ratios)) if self.ratios else None,
                 "balance_ratio_last": self.ratios[-1] if self.ratios else None,
@@ -370,6 +377,7 @@ def run_ours(args, world, rank, local_rank):
     dev = torch.device("cuda", local_rank)
     multi = world > 1 or args.workload in WORKLOADS
     cfg = dict(WORKLOADS[args.workload or "cfg3"] if multi else CFG2)
+    cfg["transport"] = args.transport
     if cfg.get("scaling") == "strong":  # fixed total tokens, split over the GPUs
         cfg["T"] = cfg["T"] // world
     N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
@@ -549,6 +557,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="multi-GPU token transport (configs[2..4] workloads)")
     ap.add_argument("--workload", default=None, choices=[None, "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="default: cfg2 at 1 GPU, cfg3 (multi-GPU runtime) at N > 1; "
                          "cfg3-5 run the multi-GPU runtime at any N")

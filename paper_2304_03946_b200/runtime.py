@@ -50,7 +50,7 @@ class RuntimeStep:
 class FlexMoERuntime:
     def __init__(self, num_experts, top_k, d_model, d_ff, exchange: Exchange, profile: S.ClusterProfile,
                  sched_cfg: S.SchedulerConfig | None = None, max_tokens=65536, gate_weight=None,
-                 lr=1e-4, optimizer=True, recorder=None):
+                 lr=1e-4, optimizer=True, recorder=None, transport="p2p"):
         self.N, self.k, self.d, self.f = num_experts, top_k, d_model, d_ff
         self.recorder = recorder  # trace.TraceRecorder: per-step device TokenDemand export
         self.ex = exchange
@@ -62,7 +62,7 @@ class FlexMoERuntime:
         self.device = dev
         self.layer = MoELayer(num_experts, top_k, d_model, d_ff, replica_counts=counts, num_gpus=self.G,
                               rank=self.rank, max_tokens=max_tokens, slots_per_gpu=profile.slots_per_gpu)
-        self.dl = DistributedMoELayer(self.layer, exchange)
+        self.dl = DistributedMoELayer(self.layer, exchange, transport=transport)
         # every rank tracks every rank's slot table (same ops, same order): a
         # receiver knows the source's slot without a round trip. A GPU hosts at
         # most E experts; vacated slots stay readable for one step -> 2E slots.
@@ -159,7 +159,8 @@ class BaselineRuntime:
     fields (`host`) next to the device outputs."""
 
     def __init__(self, num_experts, top_k, d_model, d_ff, exchange: Exchange, profile: S.ClusterProfile,
-                 cfg: S.BaselineConfig, max_tokens=65536, gate_weight=None, lr=1e-4, optimizer=True):
+                 cfg: S.BaselineConfig, max_tokens=65536, gate_weight=None, lr=1e-4, optimizer=True,
+                 transport="p2p"):
         if cfg.kind not in (S.STATIC_EP, S.FULL_REPLICATE):
             raise ValueError("BaselineRuntime runs StaticEP or FullReplicate (StrictRebalance rewrites "
                              "the gate's demand: count level only, scheduler.Baseline)")
@@ -176,7 +177,7 @@ class BaselineRuntime:
                               rank=self.rank, max_tokens=max_tokens, slots_per_gpu=slots)
         if cfg.kind == S.STATIC_EP:
             self.layer.set_capacity_factor(cfg.capacity_factor)
-        self.dl = DistributedMoELayer(self.layer, exchange)
+        self.dl = DistributedMoELayer(self.layer, exchange, transport=transport)
         self.owned = [e for e in range(num_experts) if self.home[e] == self.rank]
         self.store = ExpertStore(d_model, d_ff, dev, capacity=max(1, len(self.owned)), lr=lr)
         for e in self.owned:

@@ -21,7 +21,8 @@ from tests.test_layer_gpu import close_bf16  # noqa: E402
 from tests.test_multigpu_gpu import run_ranks  # noqa: E402
 
 
-def test_runtime_dynamic_placement_loopback():
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_runtime_dynamic_placement_loopback(transport):
     N, k, d, f, T, G, E, steps = 8, 2, 256, 256, 512, 4, 4, 10
     hub = LoopbackHub(G)
     gen = torch.Generator(device="cpu").manual_seed(0)
@@ -36,7 +37,7 @@ def test_runtime_dynamic_placement_loopback():
     def rank_fn(r):
         torch.cuda.set_device(0)
         rt = FlexMoERuntime(N, k, d, f, hub.endpoint(r), S.ClusterProfile.reference_default(G, E),
-                            max_tokens=T, gate_weight=wg, lr=1e-3)
+                            max_tokens=T, gate_weight=wg, lr=1e-3, transport=transport)
         x, dy = xs[r].cuda(), dys[r].cuda()
         hist = []
         for s in range(steps):
