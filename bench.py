@@ -322,10 +322,19 @@ class DistArm:
         import torch
 
         # drifting popularity (workload.cpp:164-170: p *= exp(U[-0.02, 0.02]), renormalised),
-        # applied through the gate's skew column
-        self.logp = self.logp + self.drift.uniform(-0.02, 0.02, self.N)
-        self.logp -= np.log(np.exp(self.logp).sum())
-        self.rt.wg[:, 0] = torch.tensor(self.logp * 2, dtype=torch.float32).to(self.rt.wg)
+        # applied through the gate's skew column. The walk is host-side and
+        # independent of the device, so it is generated 256 steps at a time and
+        # staged on the device once (no per-step pageable copy / host sync).
+        if not getattr(self, "_walk", None) or self._walk_i == self._walk[1].shape[0]:
+            cols = []
+            for _ in range(256):
+                self.logp = self.logp + self.drift.uniform(-0.02, 0.02, self.N)
+                self.logp -= np.log(np.exp(self.logp).sum())
+                cols.append(self.logp * 2)
+            dev_walk = torch.tensor(np.stack(cols), dtype=torch.float32).to(self.rt.wg.device).to(self.rt.wg.dtype)
+            self._walk, self._walk_i = (None, dev_walk), 0
+        self.rt.wg[:, 0] = self._walk[1][self._walk_i]
+        self._walk_i += 1
         out = self.rt.step(x, dy)
         self.mig_bytes += out.migration_bytes
         self.applied += len(out.applied)
