@@ -36,7 +36,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2304_03946_b200 import scheduler as S  # noqa: E402
 from paper_2304_03946_b200.distributed import LoopbackHub  # noqa: E402
 from paper_2304_03946_b200.profile import b200_profile  # noqa: E402
-from paper_2304_03946_b200.runtime import FlexMoERuntime  # noqa: E402
+from paper_2304_03946_b200.runtime import BaselineRuntime, FlexMoERuntime  # noqa: E402
 
 
 def zipf_logp(N, s, seed):
@@ -46,11 +46,14 @@ def zipf_logp(N, s, seed):
 
 
 def run(mode, N, k, d, f, T, G, steps, zipf, transport):
+    """mode: "static" / "dynamic" (FlexMoERuntime; policy frozen or FlexMoE's),
+    "static-ep" (DeepSpeed-like capacity 1.0, drops), "full-replicate"
+    (FasterMoE-like shadowing of the hottest expert) — BaselineRuntime."""
     hub = LoopbackHub(G)
     E = 2 * -(-N // G)
     prof = b200_profile(G, E, tps=2.0e7, d=d, f=f)
-    policy = {"dynamic": 0, "static": 2}[mode]
-    cfg = S.SchedulerConfig.defaults(policy_mode=policy)
+    baseline = mode in ("static-ep", "full-replicate")
+    cfg = S.SchedulerConfig.defaults(policy_mode={"dynamic": 0, "static": 2}.get(mode, 2))
     g = torch.Generator(device="cpu").manual_seed(1234)
     wg0 = torch.randn(N, d, generator=g) * d**-0.5
     logp0 = zipf_logp(N, zipf, 42)
@@ -64,8 +67,13 @@ def run(mode, N, k, d, f, T, G, steps, zipf, transport):
     def rank_fn(r):
         try:
             torch.cuda.set_device(0)
-            rt = FlexMoERuntime(N, k, d, f, hub.endpoint(r), prof, sched_cfg=cfg, max_tokens=T,
-                                gate_weight=wg0.clone(), lr=1e-4, transport=transport)
+            if baseline:
+                rt = BaselineRuntime(N, k, d, f, hub.endpoint(r), prof,
+                                     S.BaselineConfig.make(mode, capacity_factor=1.0, replicate_top=1),
+                                     max_tokens=T, gate_weight=wg0.clone(), lr=1e-4, transport=transport)
+            else:
+                rt = FlexMoERuntime(N, k, d, f, hub.endpoint(r), prof, sched_cfg=cfg, max_tokens=T,
+                                    gate_weight=wg0.clone(), lr=1e-4, transport=transport)
             x, dy = xs[r].cuda(), dys[r].cuda()
             walk = np.random.default_rng(42)  # the same drift on every rank
             logp = logp0.copy()
@@ -77,12 +85,18 @@ def run(mode, N, k, d, f, T, G, steps, zipf, transport):
                 st = rt.step(x, dy)
                 flows = rt.layer.read("flows", N * G * G).reshape(N, G, G)
                 recv = flows.sum(axis=1).sum(axis=0)  # per-GPU received units
+                if baseline:
+                    rep = st["host"].report
+                    out.append({"step": s, "balance_ratio": float(recv.max() / recv.mean()),
+                                "tokens_dropped": int(rep.tokens_dropped), "tokens_total": int(rep.tokens_total),
+                                "applied": [], "shadow_bytes": int(st["shadow_bytes"])})
+                    continue
                 out.append({"step": s, "balance_ratio": float(recv.max() / recv.mean()),
                             "scheduler_ratio": st.balance_ratio, "applied": [list(o) for o in st.applied],
                             "pulled_bytes": int(st.migration_bytes),
                             "replicas": [int(c) for c in st.replica_counts]})
             torch.cuda.synchronize()
-            mig = rt.migration_stats()
+            mig = {"bytes": 0, "copy_ms": 0.0, "copies": 0} if baseline else rt.migration_stats()
             rec[r] = {"steps": out, "migration": mig}
         except BaseException as exc:
             errs[r] = exc
@@ -109,6 +123,10 @@ def run(mode, N, k, d, f, T, G, steps, zipf, transport):
         "expert_state_pulled_bytes": sum(rec[r]["migration"]["bytes"] for r in range(G)),
         "expert_state_copy_ms": sum(rec[r]["migration"]["copy_ms"] for r in range(G)),
         "slots_pulled": sum(rec[r]["migration"]["copies"] for r in range(G)),
+        "tokens_dropped_fraction": (sum(s.get("tokens_dropped", 0) for s in steps0) /
+                                    max(1, sum(s.get("tokens_total", 0) for s in steps0))) if baseline else 0.0,
+        "shadow_bytes_per_step_per_rank": (float(np.mean([np.mean([s.get("shadow_bytes", 0) for s in rec[r]["steps"]])
+                                                          for r in range(G)])) if baseline else 0.0),
         "decisions_identical_on_all_ranks": all(
             [s["applied"] for s in rec[r]["steps"]] == [s["applied"] for s in steps0] for r in range(G)),
         "per_step": steps0,
@@ -126,7 +144,8 @@ def main():
            "workload": {"experts": N, "top_k": k, "d_model": d, "d_ff": f, "tokens_per_gpu": T, "gpus_virtual": G,
                         "zipf": zipf, "drift": "p *= exp(U[-0.02, 0.02]) per step (workload.cpp:164-170)",
                         "transport": "p2p", "steps": a.steps},
-           "runs": [run(m, N, k, d, f, T, G, a.steps, zipf, "p2p") for m in ("static", "dynamic")]}
+           "runs": [run(m, N, k, d, f, T, G, a.steps, zipf, "p2p")
+                    for m in ("static", "static-ep", "full-replicate", "dynamic")]}
     Path(a.out).write_text(json.dumps(res, indent=1))
     for r in res["runs"]:
         print(json.dumps({kk: v for kk, v in r.items() if kk != "per_step"}))
