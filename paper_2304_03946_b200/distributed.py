@@ -344,6 +344,16 @@ class DistributedMoELayer:
         return r
 
     @property
+    def last_demand_host(self) -> np.ndarray:
+        """This step's all-gathered TokenDemand D[e][g] on the host (waits for
+        its copy if it is still in flight)."""
+        if getattr(self, "_demand_event", None) is not None:
+            self._demand_event.synchronize()
+            self._demand_host = self._demand_pinned.numpy().T.copy()
+            self._demand_event = None
+        return self._demand_host
+
+    @property
     def replica_counts(self):
         return self.layer.replica_counts
 
@@ -385,7 +395,8 @@ class DistributedMoELayer:
         send_rows, recv_rows = send_rows.tolist(), recv_rows.tolist()
         # fm_layer_route synchronised the stream: the demand is final, take the
         # host copy for the placement scheduler now (no extra sync later)
-        self.last_demand_host = gathered.cpu().numpy().T.copy()  # TokenDemand [N][G]
+        self._demand_host = gathered.cpu().numpy().T.copy()  # TokenDemand [N][G]
+        self._demand_event = None
         bf = torch.bfloat16
         send = torch.empty(max(T * k, 1), d, dtype=bf, device=dev)
         recv = torch.empty(max(sum(recv_rows), 1), d, dtype=bf, device=dev)
@@ -407,11 +418,18 @@ class DistributedMoELayer:
 
     def _forward_p2p(self, x, T, wg, w1, b1, w2, b2, gathered, on_demand, before_experts):
         stream = L.stream_ptr()
-        self.last_demand_host = gathered.cpu().numpy().T.copy()  # TokenDemand [N][G] (policy input)
-        if on_demand is not None:
-            new = on_demand(self.last_demand_host.copy())
+        if on_demand is not None:  # a per-step placement needs the demand before routing
+            self._demand_host = gathered.cpu().numpy().T.copy()
+            self._demand_event = None
+            new = on_demand(self._demand_host.copy())
             if new is not None:
                 w1, b1, w2, b2 = new
+        else:  # no host sync in the step: the policy's copy lands asynchronously
+            if getattr(self, "_demand_pinned", None) is None or self._demand_pinned.shape != gathered.shape:
+                self._demand_pinned = torch.empty(gathered.shape, dtype=gathered.dtype, pin_memory=True)
+            self._demand_pinned.copy_(gathered, non_blocking=True)
+            self._demand_event = torch.cuda.Event()
+            self._demand_event.record()
         self._call("fm_layer_route_p2p", gathered.data_ptr(), stream)
         self._call("fm_layer_dispatch_p2p", x.data_ptr(), stream)
         self.ex.fence()

@@ -125,10 +125,10 @@ class FlexMoERuntime:
         w1, b1, w2, b2 = self.packed
         y = self.dl.forward(x, self.wg, w1, b1, w2, b2, after_gather=issue,
                             before_experts=lambda: self.store.pool.wait_ready())
-        D = self.dl.last_demand_host  # TokenDemand [N][G], copied when routing synchronised
+        grads = self.dl.backward(dy)
+        D = self.dl.last_demand_host  # TokenDemand [N][G] (its host copy overlapped the step)
         if self.recorder is not None:
             self.recorder.record(D)
-        grads = self.dl.backward(dy)
         if self.optimizer and self.layer.local_experts:
             self.store.adam_step(self.layer.local_experts, grads)  # refreshes self.packed in place
         res = self.sched.finish_step(D)
