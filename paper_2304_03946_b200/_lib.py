@@ -10,7 +10,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "libflexmoe_b200.so"
+import os
+
+# FLEXMOE_B200_LIB: load another build of the same library (A/B measurements)
+_LIB_PATH = Path(os.environ.get("FLEXMOE_B200_LIB") or Path(__file__).resolve().parent / "libflexmoe_b200.so")
 
 FM_OK = 0
 FM_ERR_INVALID_ARGUMENT = 1

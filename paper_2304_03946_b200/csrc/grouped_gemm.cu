@@ -52,11 +52,15 @@ struct Cfg {
   static constexpr int kBNc = kBN / CG;              // B rows (N) staged per CTA
   static constexpr int kBBytes = kBNc * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = CG == 1 ? 4 : 5;
+  // CTA pairs: 6 stages (~2.2 us of MMA work in flight at power-capped clocks,
+  // enough to cover TMA load latency while the epilogue's stores share the
+  // TMA unit), paid for with one output staging buffer per epilogue warp.
+  static constexpr int kStages = CG == 1 ? 4 : 6;
+  static constexpr int kOutBufs = CG == 1 ? 2 : 1;
   static constexpr int kTileM = kBM * CG;
   static constexpr int kEW = CG == 1 ? 4 : 8;
   static constexpr int kThreads = 128 + 32 * kEW;
-  static constexpr int kOutBytes = kEW * 2 * kStageOutBytes;
+  static constexpr int kOutBytes = kEW * kOutBufs * kStageOutBytes;
   static constexpr int kSmemBytes = kStages * kStageBytes + kOutBytes + 1024 + 512 + 2 * kBN * 4 +
                                     2 * 4 * kBN * 4 + 4 * kTableInts * 4;
 };
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     const int et = static_cast<int>(threadIdx.x) - 128;  // index among epilogue threads
     constexpr bool kBias = (EPI == kEpiBiasRelu || EPI == kEpiBias);
     const int mask_ld = args.N / 32;  // mask words per token row
-    uint8_t* warp_out = smem_out + ew * 2 * kStageOutBytes;
+    uint8_t* warp_out = smem_out + ew * C::kOutBufs * kStageOutBytes;
     // release of the accumulator goes to the leader's barrier
     const uint32_t lead_tempty = CG == 2 ? ptx::mapa(ptx::smem_u32(tempty_bar), 0) : 0;
     uint32_t out_seq = 0;
@@ -365,8 +369,11 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       // (SWIZZLE_64B: 16-byte chunk j of row r sits at chunk j ^ ((r >> 1) & 3)),
       // then one lane issues the TMA store. Two buffers per warp alternate.
       auto stage_begin = [&]() -> uint8_t* {
-        uint8_t* buf = warp_out + (out_seq & 1) * kStageOutBytes;
-        if (lane == 0) ptx::bulk_wait_read<1>();  // the store that last used `buf` has read it
+        uint8_t* buf = warp_out + (C::kOutBufs == 2 ? (out_seq & 1) : 0) * kStageOutBytes;
+        if (lane == 0) {  // the store that last used `buf` has read it
+          if (C::kOutBufs == 2) ptx::bulk_wait_read<1>();
+          else ptx::bulk_wait_read<0>();
+        }
         __syncwarp();
         return buf;
       };
