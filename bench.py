@@ -241,7 +241,9 @@ class FusedArm:
         self.P = (p["wg"], p["w1"], p["b1"], p["w2"], p["b2"])
         self.grads = None
         self.N, self.G = N, 1
-        self.kernels_per_step = 9 + 8 + 1  # dWg rides on the bias-gradient tile sums
+        # fwd: gate, scan, route+plan, dispatch(+pads), ffn1, ffn2, combine = 7;
+        # bwd: combine_bwd(+pads), 4 GEMMs, tile sums, reduce, unpermute = 8
+        self.kernels_per_step = 7 + 8
 
     def step(self, x, dy):
         self.layer.forward(x, *self.P)
@@ -305,10 +307,10 @@ class DistArm:
         self.layer, self.dl = self.rt.layer, self.rt.dl
         self.drift = np.random.default_rng(42)  # same walk on every rank
         self.N, self.G = N, G
-        if self.transport == "p2p":  # fwd 14 (incl. 2 signals, 2 waits), bwd 13 (incl. 2 signals, 2 waits)
-            self.kernels_per_step = 27
-        else:
-            self.kernels_per_step = 9 + 8 + (2 if k > 1 else 1) + 4 + 1  # + relayouts, transpose
+        if self.transport == "p2p":  # fwd 13 (incl. 2 signals, 2 waits), bwd 13 (incl. 2 signals, 2 waits)
+            self.kernels_per_step = 26
+        else:  # + demand transpose, staging relayouts / pad zeroing, run-based gate wgrad
+            self.kernels_per_step = 8 + 13 + (1 if k > 1 else 0)
         self.reset_stats()
 
     def reset_stats(self):

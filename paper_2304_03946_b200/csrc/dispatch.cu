@@ -19,6 +19,7 @@
 
 #include "fm_internal.h"
 #include "layer_plan.h"
+#include "routing.cuh"
 
 namespace fm {
 namespace {
@@ -86,11 +87,27 @@ __global__ void expert_scan_kernel(const int32_t* __restrict__ tile_counts, int 
 // ----------------------------------------------------------------- plan
 // One block. Turns flows[e][src][dst] into the offsets every later kernel
 // uses (see PlanDev in layer_plan.h).
-__global__ void plan_kernel(const int64_t* __restrict__ flows, int N, int G, int me,
+// With `demand` set, the block first runs route() itself (Alg. 3, one thread
+// per expert: split_expert_demand, the same routine as fm_route_counts) and
+// writes the flows — route + plan in one launch, no kernel boundary between.
+__global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
                             const int32_t* __restrict__ local_expert, int Nl, PlanDev p,
-                            const int32_t* __restrict__ counts) {
+                            const int32_t* __restrict__ counts, const int64_t* __restrict__ demand,
+                            int32_t* __restrict__ status) {
   extern __shared__ int32_t sf[];  // flows as int32 [N][G][G]
   const int nflow = N * G * G;
+  if (demand) {
+    if (threadIdx.x == 0 && status) *status = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+      int64_t* fe = flows + static_cast<size_t>(e) * G * G;
+      for (int i = 0; i < G * G; ++i) fe[i] = 0;
+      const int st = split_expert_demand(e, demand, counts, G, flows);
+      if (st != kRouteOk && status)
+        atomicCAS(status, 0, st == kRouteNoReplica ? FM_ERR_INVALID_ARGUMENT : FM_ERR_LOGIC);
+    }
+    __syncthreads();  // the block's global flow writes are visible to all its threads
+  }
   for (int i = threadIdx.x; i < nflow; i += blockDim.x) sf[i] = static_cast<int32_t>(flows[i]);
   __syncthreads();
 #define FL(e, s, d) sf[((e) * G + (s)) * G + (d)]
@@ -154,7 +171,7 @@ __global__ void plan_kernel(const int64_t* __restrict__ flows, int N, int G, int
   // lays out its segments the same way (hosted experts ascending, 128-row
   // padded, sources ascending inside a segment), so each source computes its
   // destinations' layouts from the shared flows and replica counts.
-  if (p.peer_row && counts) {
+  if (p.peer_row) {
     for (int dst = threadIdx.x; dst < G; dst += blockDim.x) {
       int start = 0;
       for (int e = 0; e < N; ++e) {
@@ -175,6 +192,23 @@ __global__ void plan_kernel(const int64_t* __restrict__ flows, int N, int G, int
 #undef FL
 }
 
+// Zero the padding rows of segment li: [seg_start + real, seg_start + rows)
+// (part `part` of `parts` blocks on it); optionally mark them as carrying no
+// expert (row_expert = -1).
+constexpr int kPadParts = 4;
+__device__ __forceinline__ void zero_pad_segment(__nv_bfloat16* __restrict__ buf, int d, const PlanDev& p, int li,
+                                                 int part, int parts, int32_t* __restrict__ row_expert) {
+  const int first = p.seg_start[li] + p.seg_real[li];
+  const int last = p.seg_start[li] + p.seg_rows[li];
+  if (row_expert && part == 0)
+    for (int r = first + threadIdx.x; r < last; r += blockDim.x) row_expert[r] = -1;
+  const int nvec = d / 8;
+  const size_t begin = static_cast<size_t>(first) * nvec, end = static_cast<size_t>(last) * nvec;
+  uint4* b = reinterpret_cast<uint4*>(buf);
+  for (size_t i = begin + part * blockDim.x + threadIdx.x; i < end; i += static_cast<size_t>(parts) * blockDim.x)
+    b[i] = make_uint4(0, 0, 0, 0);
+}
+
 // ----------------------------------------------------------------- dispatch
 // Warp per token: resolve each unit's row in the dispatch buffer and copy the
 // token's activations there (k copies). When `direct` (G == 1), the dispatch
@@ -184,7 +218,13 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
                                 const int32_t* __restrict__ tile_rank,
                                 const int32_t* __restrict__ tile_base, PlanDev p,
                                 int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf,
-                                int32_t* __restrict__ row_expert, const P2P pp) {
+                                int32_t* __restrict__ row_expert, const P2P pp, int tok_blocks,
+                                __nv_bfloat16* __restrict__ pad_buf, int Nl) {
+  if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero pad_buf's padding rows
+    const int b = blockIdx.x - tok_blocks;
+    zero_pad_segment(pad_buf, d, p, b / kPadParts, b % kPadParts, kPadParts, row_expert);
+    return;
+  }
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -229,22 +269,11 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
   }
 }
 
-// Zero the padding rows of each segment: [seg_start + real, seg_start + rows);
-// optionally mark them as carrying no expert (row_expert = -1).
 __global__ void zero_pad_kernel(__nv_bfloat16* __restrict__ buf, int d, PlanDev p, int Nl,
                                 int32_t* __restrict__ row_expert) {
   const int li = blockIdx.y;
   if (li >= Nl) return;
-  const int first = p.seg_start[li] + p.seg_real[li];
-  const int last = p.seg_start[li] + p.seg_rows[li];
-  if (row_expert && blockIdx.x == 0)
-    for (int r = first + threadIdx.x; r < last; r += blockDim.x) row_expert[r] = -1;
-  const int nvec = d / 8;
-  const size_t begin = static_cast<size_t>(first) * nvec, end = static_cast<size_t>(last) * nvec;
-  uint4* b = reinterpret_cast<uint4*>(buf);
-  for (size_t i = begin + blockIdx.x * blockDim.x + threadIdx.x; i < end;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x)
-    b[i] = make_uint4(0, 0, 0, 0);
+  zero_pad_segment(buf, d, p, li, blockIdx.x, gridDim.x, row_expert);
 }
 
 // a2a receive buffer (src-major, expert-minor) <-> X_perm segments.
@@ -391,7 +420,13 @@ template <int VPL>
 __global__ void __launch_bounds__(256) combine_bwd_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Yl,
     const int32_t* __restrict__ pos, const float* __restrict__ w, int T, int k,
-    __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P pp) {
+    __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P pp,
+    int tok_blocks, PlanDev pad_plan) {
+  if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero dYl's padding rows
+    const int b = blockIdx.x - tok_blocks;
+    zero_pad_segment(dYl, VPL * 256, pad_plan, b / kPadParts, b % kPadParts, kPadParts, nullptr);
+    return;
+  }
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -776,8 +811,10 @@ void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_
   FM_LAUNCH_CHECK("expert_scan_kernel");
 }
 
-void launch_plan(const int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
-                 const PlanDev& p, cudaStream_t s, const int32_t* counts) {
+void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
+                 const PlanDev& p, cudaStream_t s, const int32_t* counts, const int64_t* demand,
+                 int32_t* status) {
+  if (demand && (N > 256 || G > kMaxGpus)) throw std::invalid_argument("route: bad dimensions");
   const int smem = N * G * G * 4;
   if (smem > 200 * 1024) throw std::invalid_argument("plan: N*G*G too large");
   static int configured = 0;
@@ -785,27 +822,30 @@ void launch_plan(const int64_t* flows, int N, int G, int me, const int32_t* loca
     FM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = smem;
   }
-  plan_kernel<<<1, 256, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts);
+  plan_kernel<<<1, 256, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status);
   FM_LAUNCH_CHECK("plan_kernel");
 }
 
 void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
                      const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
                      const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
-                     cudaStream_t s, const P2P* pp) {
+                     cudaStream_t s, const P2P* pp, void* pad_buf, int Nl) {
   const P2P none{};
   if (d % 8 != 0 || d > 2048) throw std::invalid_argument("dispatch: d_model must be a multiple of 8, <= 2048");
-  if (T <= 0) return;
   const int warps = 8;
-  dispatch_kernel<<<(T + warps - 1) / warps, warps * 32, 0, s>>>(
+  const int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
+  const int pad_blocks = pad_buf ? Nl * kPadParts : 0;
+  if (tok_blocks + pad_blocks == 0) return;
+  dispatch_kernel<<<tok_blocks + pad_blocks, warps * 32, 0, s>>>(
       static_cast<const __nv_bfloat16*>(x), T, d, k, N, G, me, direct ? 1 : 0, idx, tile_rank,
-      tile_base, p, pos, static_cast<__nv_bfloat16*>(buf), row_expert, pp ? *pp : none);
+      tile_base, p, pos, static_cast<__nv_bfloat16*>(buf), row_expert, pp ? *pp : none, tok_blocks,
+      static_cast<__nv_bfloat16*>(pad_buf), Nl);
   FM_LAUNCH_CHECK("dispatch_kernel");
 }
 
 void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, int32_t* row_expert, cudaStream_t s) {
   if (Nl <= 0) return;
-  dim3 grid(4, Nl);
+  dim3 grid(kPadParts, Nl);
   zero_pad_kernel<<<grid, 256, 0, s>>>(static_cast<__nv_bfloat16*>(buf), d, p, Nl, row_expert);
   FM_LAUNCH_CHECK("zero_pad_kernel");
 }
@@ -844,15 +884,19 @@ void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T
 }
 
 void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const float* w, int T,
-                        int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s, const P2P* pp) {
+                        int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s, const P2P* pp,
+                        const PlanDev* pad_plan, int Nl) {
   const P2P none{};
-  if (T <= 0) return;
   if (k > 32) throw std::invalid_argument("combine_bwd: top_k <= 32");
   const int warps = 8;
-  const int grid = (T + warps - 1) / warps;
-  FM_VPL_DISPATCH(d, (combine_bwd_kernel<V><<<grid, warps * 32, 0, s>>>(
+  const int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
+  const int pad_blocks = pad_plan ? Nl * kPadParts : 0;
+  if (tok_blocks + pad_blocks == 0) return;
+  const PlanDev nop{};
+  FM_VPL_DISPATCH(d, (combine_bwd_kernel<V><<<tok_blocks + pad_blocks, warps * 32, 0, s>>>(
                          static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(Y),
-                         pos, w, T, k, static_cast<__nv_bfloat16*>(dYbuf), dl, dl_rows, pp ? *pp : none)));
+                         pos, w, T, k, static_cast<__nv_bfloat16*>(dYbuf), dl, dl_rows, pp ? *pp : none,
+                         tok_blocks, pad_plan ? *pad_plan : nop)));
   FM_LAUNCH_CHECK("combine_bwd_kernel");
 }
 

@@ -31,12 +31,13 @@ void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, 
                  float* topk_w, int32_t* tile_rank, int32_t* tile_counts, cudaStream_t stream);
 void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_t* tile_base,
                         int64_t* hist, int64_t* demand_NG, int G, int me, cudaStream_t s);
-void launch_plan(const int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
-                 const PlanDev& p, cudaStream_t s, const int32_t* counts = nullptr);
+void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
+                 const PlanDev& p, cudaStream_t s, const int32_t* counts, const int64_t* demand = nullptr,
+                 int32_t* status = nullptr);
 void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
                      const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
                      const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
-                     cudaStream_t s, const P2P* pp = nullptr);
+                     cudaStream_t s, const P2P* pp = nullptr, void* pad_buf = nullptr, int Nl = 0);
 void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, int32_t* row_expert, cudaStream_t s);
 void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int max_rows, int d,
                        const float* dl_rows, const int32_t* row_expert, float* dwg, cudaStream_t s);
@@ -47,7 +48,8 @@ void launch_relayout(void* recv, void* perm, int d, int G, int Nl, const PlanDev
 void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T, int d, int k,
                         void* y, cudaStream_t s, const P2P* pp = nullptr);
 void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const float* w, int T,
-                        int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s, const P2P* pp = nullptr);
+                        int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s, const P2P* pp = nullptr,
+                        const PlanDev* pad_plan = nullptr, int Nl = 0);
 void launch_unpermute_bwd(const void* dXbuf, const int32_t* pos, const int32_t* idx, const float* dl,
                           const void* wg, int T, int d, int k, bool gate_grad, void* dx,
                           cudaStream_t s, const P2P* pp = nullptr);
@@ -303,10 +305,10 @@ class Layer {
     gate(x, T, wg, nullptr, s);
     route_device(s);
     timer_.begin(FM_PHASE_DISPATCH, s);
-    launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);
     launch_dispatch(x, T, cfg_.d_model, cfg_.top_k, cfg_.num_experts, 1, 0, true,
                     topk_idx_.as<int32_t>(), tile_rank_.as<int32_t>(), tile_base_.as<int32_t>(),
-                    plan_, pos_.as<int32_t>(), x_perm_.p, nullptr, s);
+                    plan_, pos_.as<int32_t>(), x_perm_.p, nullptr, s, nullptr,
+                    /*pad_buf (zeroed by trailing blocks)*/ x_perm_.p, nl());
     timer_.end(s);
     expert_forward(w1, b1, w2, b2, s);
     combine(y_perm_.p, y, s);
@@ -321,10 +323,7 @@ class Layer {
     if (cfg_.num_gpus != 1)
       throw std::logic_error("fm_layer_backward: fused path is single-GPU; use the phase API");
     if (!fused_state_) throw std::logic_error("fm_layer_backward: no forward state");
-    combine_backward(dy, y_perm_.p, dy_perm_.p, s);
-    timer_.begin(FM_PHASE_COMBINE_BWD, s);
-    launch_zero_pad(dy_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);
-    timer_.end(s);
+    combine_backward(dy, y_perm_.p, dy_perm_.p, s, /*zero_pads=*/true);
     // the dispatched units' share of dWg = per-tile column sums of X_perm
     // weighted by dl per row, reduced with db1 / db2 (dropped units: below)
     const bool dwg_tiles = dwg && cfg_.top_k > 1 && nl() > 0;
@@ -367,10 +366,9 @@ class Layer {
                             dropped_.as<int64_t>(), s);
       routed = kept_.as<int64_t>();
     }
-    route_counts_device(routed, counts_dev_.as<int32_t>(), N, G, flows_.as<int64_t>(),
-                        route_status_.as<int32_t>(), s);
+    // route() over the demand and the dispatch plan in one single-block launch
     launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s,
-                p2p_ ? counts_dev_.as<int32_t>() : nullptr);
+                counts_dev_.as<int32_t>(), routed, route_status_.as<int32_t>());
     timer_.end(s);
   }
 
@@ -502,12 +500,13 @@ class Layer {
     timer_.end(s);
   }
 
-  void combine_backward(const void* dy, const void* back, void* dsend, cudaStream_t s) {
+  // zero_pads (fused path): dsend is dY_perm; trailing blocks zero its padding rows.
+  void combine_backward(const void* dy, const void* back, void* dsend, cudaStream_t s, bool zero_pads = false) {
     const bool gate_grad = cfg_.top_k > 1;
     timer_.begin(FM_PHASE_COMBINE_BWD, s);
     launch_combine_bwd(dy, back, pos_.as<int32_t>(), topk_w_.as<float>(), cur_T_, cfg_.d_model,
                        cfg_.top_k, dsend, dl_.as<float>(), gate_grad ? dl_rows_.as<float>() : nullptr,
-                       s);
+                       s, nullptr, zero_pads ? &plan_ : nullptr, nl());
     timer_.end(s);
   }
 
