@@ -484,7 +484,7 @@ class Layer {
     float* part_dwg = part_db2 + static_cast<size_t>(max_tiles) * d;
     launch_segment_tile_colsum(dwg_tiles ? x_perm_.p : nullptr, dl_rows_.as<float>(), part_dwg,
                                db2 ? dy_perm_.p : nullptr, nullptr, part_db2, d, plan_, Nl, max_tiles, s);
-    if (dwg_tiles)  // experts hosted nowhere keep a zero row
+    if (dwg_tiles && Nl < cfg_.num_experts)  // experts hosted elsewhere keep a zero row here
       FM_CUDA(cudaMemsetAsync(dwg_tiles, 0, sizeof(float) * cfg_.num_experts * d, s));
     launch_segment_tile_reduce(tile_colsum_.as<float>(), f, nullptr, db1, part_db2, d, nullptr, db2, part_dwg, d,
                                local_expert_dev_, dwg_tiles, plan_, Nl, s);
