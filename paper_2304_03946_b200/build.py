@@ -23,6 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 CU_FLAGS = ARCH + COMMON + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+# extra nvcc flags for A/B builds (e.g. NVCC_EXTRA=-DFM_GEMM_DIRECT_STORE)
+CU_FLAGS += os.environ.get("NVCC_EXTRA", "").split()
 
 
 def _deps_newer(src: Path, obj: Path) -> bool:
