@@ -209,22 +209,43 @@ __device__ __forceinline__ void zero_pad_segment(__nv_bfloat16* __restrict__ buf
     b[i] = make_uint4(0, 0, 0, 0);
 }
 
+inline P2P no_p2p() {
+  P2P p{};
+  p.signal_slot = -1;
+  return p;
+}
+
+// Last-block release of rows pushed into peers' arenas (P2P): every thread
+// fences its own stores at system scope, then the block counts itself done;
+// the last block of the grid publishes flags[slot][me] = epoch to every peer.
+__device__ __forceinline__ void p2p_release_when_last(const P2P& pp) {
+  if (pp.signal_slot < 0) return;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int* ctr = pp.done + pp.signal_slot;
+    if (atomicAdd(ctr, 1u) == gridDim.x - 1) {
+      *ctr = 0;  // the next launch of this slot is stream-ordered after this one
+      __threadfence_system();
+      for (int dst = 0; dst < pp.world; ++dst) {
+        unsigned long long* f =
+            reinterpret_cast<unsigned long long*>(pp.base[dst] + pp.flag_off) + pp.signal_slot * kMaxPeers + pp.me;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(pp.epoch) : "memory");
+      }
+    }
+  }
+}
+
 // ----------------------------------------------------------------- dispatch
 // Warp per token: resolve each unit's row in the dispatch buffer and copy the
 // token's activations there (k copies). When `direct` (G == 1), the dispatch
 // buffer is X_perm itself and send_off is replaced by the expert's segment.
-__global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int k, int N,
-                                int G, int me, int direct, const int32_t* __restrict__ idx,
-                                const int32_t* __restrict__ tile_rank,
-                                const int32_t* __restrict__ tile_base, PlanDev p,
-                                int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf,
-                                int32_t* __restrict__ row_expert, const P2P pp, int tok_blocks,
-                                __nv_bfloat16* __restrict__ pad_buf, int Nl) {
-  if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero pad_buf's padding rows
-    const int b = blockIdx.x - tok_blocks;
-    zero_pad_segment(pad_buf, d, p, b / kPadParts, b % kPadParts, kPadParts, row_expert);
-    return;
-  }
+__device__ __forceinline__ void dispatch_tokens(const __nv_bfloat16* __restrict__ x, int T, int d, int k, int N,
+                                                int G, int me, int direct, const int32_t* __restrict__ idx,
+                                                const int32_t* __restrict__ tile_rank,
+                                                const int32_t* __restrict__ tile_base, const PlanDev& p,
+                                                int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf,
+                                                int32_t* __restrict__ row_expert, const P2P& pp) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -268,6 +289,23 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
       if (lane + 32 * i < nvec) dst[lane + 32 * i] = v[i];
   }
 }
+
+__global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int k, int N,
+                                int G, int me, int direct, const int32_t* __restrict__ idx,
+                                const int32_t* __restrict__ tile_rank,
+                                const int32_t* __restrict__ tile_base, PlanDev p,
+                                int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf,
+                                int32_t* __restrict__ row_expert, const P2P pp, int tok_blocks,
+                                __nv_bfloat16* __restrict__ pad_buf, int Nl) {
+  if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero pad_buf's padding rows
+    const int b = blockIdx.x - tok_blocks;
+    zero_pad_segment(pad_buf, d, p, b / kPadParts, b % kPadParts, kPadParts, row_expert);
+  } else {
+    dispatch_tokens(x, T, d, k, N, G, me, direct, idx, tile_rank, tile_base, p, pos_out, buf, row_expert, pp);
+  }
+  p2p_release_when_last(pp);
+}
+
 
 __global__ void zero_pad_kernel(__nv_bfloat16* __restrict__ buf, int d, PlanDev p, int Nl,
                                 int32_t* __restrict__ row_expert) {
@@ -417,16 +455,10 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(const __nv_bfloat16* _
 // P2P: Y rows are read from the expert's GPU, the dY row (and dl for the
 // host's gate-weight gradient) is written straight into its dY_perm / dl rows.
 template <int VPL>
-__global__ void __launch_bounds__(256) combine_bwd_kernel(
+__device__ __forceinline__ void combine_bwd_token(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Yl,
     const int32_t* __restrict__ pos, const float* __restrict__ w, int T, int k,
-    __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P pp,
-    int tok_blocks, PlanDev pad_plan) {
-  if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero dYl's padding rows
-    const int b = blockIdx.x - tok_blocks;
-    zero_pad_segment(dYl, VPL * 256, pad_plan, b / kPadParts, b % kPadParts, kPadParts, nullptr);
-    return;
-  }
+    __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P& pp) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -475,6 +507,21 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
     float* dl_rows = peer_rows(pp, pp.dl_off, my_to, dl_rows_l);
     if (dl_rows && my_pos >= 0) dl_rows[my_pos] = g_l;
   }
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256) combine_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Yl,
+    const int32_t* __restrict__ pos, const float* __restrict__ w, int T, int k,
+    __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P pp,
+    int tok_blocks, PlanDev pad_plan) {
+  if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero dYl's padding rows
+    const int b = blockIdx.x - tok_blocks;
+    zero_pad_segment(dYl, VPL * 256, pad_plan, b / kPadParts, b % kPadParts, kPadParts, nullptr);
+  } else {
+    combine_bwd_token<VPL>(dy, Yl, pos, w, T, k, dYl, dl, dl_rows_l, pp);
+  }
+  p2p_release_when_last(pp);  // P2P: dY rows and dl are in the expert GPUs' arenas
 }
 
 // dx[t] = sum_j dXbuf[pos[t,j]] + sum_j dl[t,j] * Wg[idx[t,j], :]
@@ -830,7 +877,7 @@ void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, b
                      const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
                      const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
                      cudaStream_t s, const P2P* pp, void* pad_buf, int Nl) {
-  const P2P none{};
+  const P2P none = no_p2p();
   if (d % 8 != 0 || d > 2048) throw std::invalid_argument("dispatch: d_model must be a multiple of 8, <= 2048");
   const int warps = 8;
   const int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
@@ -872,7 +919,7 @@ void launch_relayout(void* recv, void* perm, int d, int G, int Nl, const PlanDev
 
 void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T, int d, int k,
                         void* y, cudaStream_t s, const P2P* pp) {
-  const P2P none{};
+  const P2P none = no_p2p();
   if (T <= 0) return;
   if (d % 256 != 0) throw std::invalid_argument("combine: d_model must be a multiple of 256");
   const int warps = 8;
@@ -886,7 +933,7 @@ void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T
 void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const float* w, int T,
                         int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s, const P2P* pp,
                         const PlanDev* pad_plan, int Nl) {
-  const P2P none{};
+  const P2P none = no_p2p();
   if (k > 32) throw std::invalid_argument("combine_bwd: top_k <= 32");
   const int warps = 8;
   const int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
@@ -903,7 +950,7 @@ void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const
 void launch_unpermute_bwd(const void* dXbuf, const int32_t* pos, const int32_t* idx, const float* dl,
                           const void* wg, int T, int d, int k, bool gate_grad, void* dx,
                           cudaStream_t s, const P2P* pp) {
-  const P2P none{};
+  const P2P none = no_p2p();
   if (T <= 0) return;
   const int warps = 8;
   const int grid = (T + warps - 1) / warps;

@@ -555,6 +555,7 @@ class Layer {
     auto al = [](size_t b) { return round_up(b, 256); };
     const size_t rb = al(2 * rows * d);
     pp_ = P2P{};
+    pp_.signal_slot = -1;
     pp_.x_off = 0;
     pp_.y_off = rb;
     pp_.dy_off = 2 * rb;
@@ -574,6 +575,8 @@ class Layer {
     row_cap_ = 0;
     ensure_rows(rows);  // the local per-row buffers at the same capacity
     unit_dst_.reset(sizeof(int32_t) * T * k);
+    p2p_done_.reset(sizeof(unsigned int) * kP2PSlots);
+    FM_CUDA(cudaMemset(p2p_done_.p, 0, sizeof(unsigned int) * kP2PSlots));
     p2p_err_.reset(sizeof(int));
     FM_CUDA(cudaMemset(p2p_err_.p, 0, sizeof(int)));
     pp_.unit_dst = unit_dst_.as<int32_t>();
@@ -617,13 +620,24 @@ class Layer {
     launch_demand_transpose(gathered_GN, cfg_.num_experts, cfg_.num_gpus, demand_.as<int64_t>(), s);
     route_device(s);  // flows + plan incl. every destination's X_perm rows; no host sync
   }
+  // P2P launch parameters; with slot >= 0 the kernel's last block releases
+  // the rows it pushed (flags[slot][me] = epoch on every peer).
+  P2P p2p_args(int slot) const {
+    P2P p = pp_;
+    p.signal_slot = slot;
+    p.me = cfg_.rank;
+    p.world = cfg_.num_gpus;
+    p.epoch = epoch_;
+    p.done = p2p_done_.as<unsigned int>();
+    return p;
+  }
   void dispatch_p2p(const void* x, cudaStream_t s) {
     timer_.begin(FM_PHASE_DISPATCH, s);
+    const P2P p = p2p_args(0);
     launch_dispatch(x, cur_T_, cfg_.d_model, cfg_.top_k, cfg_.num_experts, cfg_.num_gpus, cfg_.rank, false,
                     topk_idx_.as<int32_t>(), tile_rank_.as<int32_t>(), tile_base_.as<int32_t>(), plan_,
-                    pos_.as<int32_t>(), nullptr, nullptr, s, &pp_);
+                    pos_.as<int32_t>(), nullptr, nullptr, s, &p);
     timer_.end(s);
-    p2p_signal(0, s);
   }
   void expert_forward_p2p(const void* w1, const float* b1, const void* w2, const float* b2, cudaStream_t s) {
     launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);  // own pad rows only
@@ -634,17 +648,18 @@ class Layer {
   void combine_p2p(void* y, cudaStream_t s) {
     p2p_wait(1, s);
     timer_.begin(FM_PHASE_COMBINE_FWD, s);
+    const P2P p = p2p_args(-1);
     launch_combine_fwd(y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), cur_T_, cfg_.d_model, cfg_.top_k, y, s,
-                       &pp_);
+                       &p);
     timer_.end(s);
   }
   void combine_backward_p2p(const void* dy, cudaStream_t s) {
     const bool gate_grad = cfg_.top_k > 1;
     timer_.begin(FM_PHASE_COMBINE_BWD, s);
+    const P2P p = p2p_args(2);
     launch_combine_bwd(dy, y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), cur_T_, cfg_.d_model, cfg_.top_k,
-                       dy_perm_.p, dl_.as<float>(), gate_grad ? dl_rows_.as<float>() : nullptr, s, &pp_);
+                       dy_perm_.p, dl_.as<float>(), gate_grad ? dl_rows_.as<float>() : nullptr, s, &p);
     timer_.end(s);
-    p2p_signal(2, s);
   }
   // dwg (optional) receives this GPU's share of the gate-weight gradient: its
   // hosted units (dl-weighted X_perm tile sums), to be summed over all GPUs.
@@ -662,8 +677,9 @@ class Layer {
     const bool gate_grad = k > 1;
     p2p_wait(3, s);
     timer_.begin(FM_PHASE_UNPERMUTE, s);
+    const P2P p = p2p_args(-1);
     launch_unpermute_bwd(dx_perm_.p, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(), wg, T, d, k,
-                         gate_grad, dx, s, &pp_);
+                         gate_grad, dx, s, &p);
     timer_.end(s);
     if (dwg && gate_grad && drops_enabled()) {  // dropped units are in no X_perm: add them here
       timer_.begin(FM_PHASE_GATE_WGRAD, s);
@@ -782,7 +798,7 @@ class Layer {
  private:
   fm_layer_config cfg_;
   bool p2p_ = false;
-  DevBuf arena_, unit_dst_, p2p_err_;
+  DevBuf arena_, unit_dst_, p2p_err_, p2p_done_;
   P2P pp_{};
   std::vector<bool> peer_ipc_;
   unsigned long long epoch_ = 0;

@@ -36,6 +36,12 @@ struct P2P {
   char* base[kMaxPeers];
   int64_t x_off, y_off, dy_off, dx_off, dl_off, flag_off;  // byte offsets inside an arena
   int32_t* unit_dst;                                       // [T*k] destination GPU (-1: dropped)
+  // In-kernel release of pushed rows: with signal_slot >= 0 the kernel's last
+  // block (after every block fenced its peer stores) sets flags[signal_slot][me]
+  // = epoch in every peer's arena. done: this GPU's per-slot block counters.
+  int signal_slot, me, world;
+  unsigned long long epoch;
+  unsigned int* done;
 };
 
 }  // namespace fm
