@@ -5,13 +5,13 @@
 # Output in gpurun_out/; profiles/summarize.py turns it into profiles/*.md|json.
 set -e
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum --clock-control none -s 54 -c 18 --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -s 45 -c 15 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_launches.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:grouped_gemm -s 18 -c 6 \
     -o gpurun_out/prof_gemm -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_gemm.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"gate_kernel|dispatch_kernel|combine_fwd|combine_bwd|unpermute|segment_tile|expert_scan|plan_kernel|route_kernel|zero_pad" \
-    -s 36 -c 12 -o gpurun_out/prof_hbm -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+    -k regex:"gate_kernel|dispatch_kernel|combine_fwd|combine_bwd|unpermute|segment_tile|expert_scan|plan_kernel" \
+    -s 27 -c 9 -o gpurun_out/prof_hbm -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_hbm.log 2>&1
