@@ -1,4 +1,4 @@
-"""The FlexMoE runtime across real processes: two ranks (processes sharing
+"""The FlexMoE runtime across real processes (both token transports): two ranks (processes sharing
 cuda:0), torch.distributed over gloo for the host control plane (histogram
 all-gather, replica-group and gate all-reduces, handle exchange), CUDA IPC
 for everything on the data plane: the P2P token transport between the
@@ -18,6 +18,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 N, K, D, F, T, G, E, STEPS = 8, 2, 256, 256, 512, 2, 6, 10
+TRANSPORTS = ["p2p", "nccl"]  # "nccl": the all-to-all path (gloo stands in for NCCL here)
 
 
 def _free_port():
@@ -28,7 +29,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, transport):
     import torch.distributed as dist
 
     from paper_2304_03946_b200 import scheduler as S
@@ -47,14 +48,15 @@ def _worker(rank, port, q):
         x, dy = xs[rank].cuda(), dys[rank].cuda()
         x[:, 0] = 0.5
         rt = FlexMoERuntime(N, K, D, F, TorchExchange(), S.ClusterProfile.reference_default(G, E), max_tokens=T,
-                            gate_weight=wg, lr=1e-3, transport="p2p")
+                            gate_weight=wg, lr=1e-3, transport=transport)
         hist = []
         for _ in range(STEPS):
             out = rt.step(x, dy)
             hist.append((round(out.balance_ratio, 12), out.replica_counts.tolist(), out.applied, out.accepted))
         torch.cuda.synchronize()
         states = {e: [t.cpu().numpy().copy() for t in rt.store.state(e)] for e in rt.layer.local_experts}  # by value
-        res = dict(hist=hist, states=states, mig=rt.migration_stats(), timed_out=rt.dl.p2p_timed_out())
+        res = dict(hist=hist, states=states, mig=rt.migration_stats(),
+                   timed_out=rt.dl.p2p_timed_out() if transport == "p2p" else False)
         dist.barrier()  # peers are done reading my arena and pool
         q.put((rank, res))
         del rt
@@ -64,13 +66,14 @@ def _worker(rank, port, q):
 
 
 @pytest.mark.timeout(400)
-def test_runtime_two_processes_p2p_ipc():
+@pytest.mark.parametrize("transport", TRANSPORTS)
+def test_runtime_two_processes(transport):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(G)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, transport)) for r in range(G)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=360) for _ in range(G))
