@@ -190,9 +190,13 @@ class TorchExchange(Exchange):
                 pool.open_peer(peer, h)
 
     def share_layer(self, layer):
-        handles = [None] * self.world
-        self.dist.all_gather_object(handles, layer.p2p_handle())
-        for peer, h in enumerate(handles):
+        # the arenas are laid out from the layer shape: every rank must agree on it
+        shape = (layer.N, layer.k, layer.d, layer.f, layer.G, layer.max_tokens)
+        entries = [None] * self.world
+        self.dist.all_gather_object(entries, (shape, layer.p2p_handle()))
+        if any(sh != shape for sh, _ in entries):
+            raise L.InvalidArgument(f"P2P transport: layer shapes differ across ranks: {[sh for sh, _ in entries]}")
+        for peer, (_, h) in enumerate(entries):
             if peer != self.rank:
                 layer.p2p_open_peer(peer, h)
 
