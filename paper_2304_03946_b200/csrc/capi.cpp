@@ -67,10 +67,7 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
   return map;
 }
 
-void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
-                  const void* aux, const int* seg_start, const int* seg_rows,
-                  const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
-                  cudaStream_t stream);
+
 void set_gemm_cta_group(int cg);
 
 }  // namespace fm

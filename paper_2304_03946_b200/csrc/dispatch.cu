@@ -166,6 +166,21 @@ __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
     }
     p.recv_chunk_off[G * Nl] = roff;
     p.totals[2] = roff;  // units received
+    // P2P: which sources' rows each 128-row tile of this GPU's X_perm / dY_perm
+    // holds (the expert GEMMs wait per tile for exactly those arrivals)
+    if (p.tile_src_mask) {
+      for (int li = 0; li < Nl; ++li) {
+        const int e = local_expert[li];
+        for (int t = p.mtile_prefix[li]; t < p.mtile_prefix[li + 1]; ++t) p.tile_src_mask[t] = 0ull;
+        int row = p.seg_start[li];
+        for (int s = 0; s < G; ++s) {
+          const int c = FL(e, s, me);
+          if (c > 0)
+            for (int t = row / kRowAlign; t <= (row + c - 1) / kRowAlign; ++t) p.tile_src_mask[t] |= 1ull << s;
+          row += c;
+        }
+      }
+    }
   }
   // P2P: where (e, me)'s units start in every destination's X_perm. Every GPU
   // lays out its segments the same way (hosted experts ascending, 128-row

@@ -66,4 +66,17 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
 
 int num_sms();
 
+// P2P arrival gating of a token-row grouped GEMM (see grouped_gemm.cu Args).
+struct ArrivalGate {
+  const unsigned long long* flags = nullptr;          // this GPU's flags of one exchange slot [src]
+  const unsigned long long* tile_src_mask = nullptr;  // [128-row tiles] sources present in the tile
+  unsigned long long epoch = 0;
+  int* err = nullptr;
+};
+
+void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
+                  const void* aux, const int* seg_start, const int* seg_rows,
+                  const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
+                  cudaStream_t stream, const ArrivalGate* gate = nullptr);
+
 }  // namespace fm

@@ -82,7 +82,41 @@ struct Args {
   const float* bias;  // [groups][N]
   uint32_t* mask;     // ReLU bits [rows][N/32]: written by kEpiBiasRelu, read by kEpiReluMask
   float* colsum;      // kEpiReluMask (optional): per-128-row-tile column sums [mtiles][N]
+  // P2P arrival gating (kRows, optional): before loading the A rows of global
+  // 128-row tile m, the producer waits until every source s in
+  // tile_src_mask[m] has published arrive_flags[s] >= epoch (rows pushed by
+  // peers over NVLink) — compute on early tiles overlaps later arrivals.
+  const unsigned long long* arrive_flags;
+  const unsigned long long* tile_src_mask;
+  unsigned long long epoch;
+  int* arrive_err;
 };
+
+// Producer-side wait for the sources of one A tile (acquire at system scope,
+// then a proxy fence so the TMA (async proxy) reads see the peers' stores).
+__device__ __forceinline__ void wait_tile_sources(const Args& a, int mtile) {
+  unsigned long long mask = a.tile_src_mask[mtile];
+  if (!mask) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (mask) {
+    const int src = __ffsll(static_cast<long long>(mask)) - 1;
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.arrive_flags + src) : "memory");
+    if (v >= a.epoch) {
+      mask &= mask - 1;
+      continue;
+    }
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - t0 > 20000000000ull) {  // bounded: report instead of hanging
+      atomicExch(a.arrive_err, 1);
+      break;
+    }
+    __nanosleep(128);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 struct Tile {
   int group;
@@ -242,10 +276,15 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int g = 0;
+      int gated_mtile = -1;
       for (int t = cluster; t < ntiles; t += num_clusters) {
         const Tile tl = decode_tile<SCHED, CG>(args, t, g, tb, rank);
         const int b_row_base = tl.group * args.b_rows_per_group;
         const int n_cta = tl.n0 + rank * C::kBNc;  // this CTA's slice of B
+        if (SCHED == kRows && args.arrive_flags && tl.valid && tl.mtile != gated_mtile) {
+          wait_tile_sources(args, tl.mtile);
+          gated_mtile = tl.mtile;
+        }
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes * CG);
@@ -571,7 +610,7 @@ void set_gemm_cta_group(int cg) {
 void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, const ArrivalGate* gate) {
   using namespace gemm;
   if (N % kBN != 0) throw std::invalid_argument("grouped_gemm: N must be a multiple of 256");
   if (num_groups < 1 || num_groups > kMaxGroups)
@@ -590,6 +629,13 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
   a.ldc = N;
   a.bias = bias;
   a.mask = static_cast<uint32_t*>(const_cast<void*>(aux));
+  if (gate && gate->flags) {
+    if (variant == FM_GEMM_WGRAD) throw std::invalid_argument("grouped_gemm: arrival gating is for token-row GEMMs");
+    a.arrive_flags = gate->flags;
+    a.tile_src_mask = gate->tile_src_mask;
+    a.epoch = gate->epoch;
+    a.arrive_err = gate->err;
+  }
   // CTA pairs for the token-row GEMMs when groups are large enough that the
   // odd 128-row tail of each group (computed, not stored) is cheap; always for
   // wgrad (M_w is a multiple of 256).

@@ -65,10 +65,7 @@ void launch_p2p_wait(const void* local_flags, int G, int slot, unsigned long lon
                      cudaStream_t s);
 void launch_dropped_gate_wgrad(const void* x, const int32_t* pos, const int32_t* idx, const float* dl,
                                int T, int d, int k, float* dwg, cudaStream_t s);
-void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
-                  const void* aux, const int* seg_start, const int* seg_rows,
-                  const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
-                  cudaStream_t stream);
+
 
 namespace {
 
@@ -262,6 +259,7 @@ class Layer {
     local_expert_dev_ = take(Nl);
     peer_row_mem_ = take(N * G);
     plan_.peer_row = p2p_ ? peer_row_mem_ : nullptr;
+    plan_.tile_src_mask = p2p_ ? tile_src_mask_.as<unsigned long long>() : nullptr;
     std::vector<int32_t> li(N, -1);
     for (int i = 0; i < Nl; ++i) li[local_[i]] = i;
     FM_CUDA(cudaMemcpy(plan_.local_index, li.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
@@ -423,14 +421,15 @@ class Layer {
     timer_.end(s);
   }
 
+  // gate (P2P): FFN1 waits per 128-row tile for the sources whose rows it holds
   void expert_forward(const void* w1, const float* b1, const void* w2, const float* b2,
-                      cudaStream_t s) {
+                      cudaStream_t s, const ArrivalGate* gate = nullptr) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0) return;
     const int rows = static_cast<int>(row_cap_);
     timer_.begin(FM_PHASE_FFN1_FWD, s);
     grouped_gemm(FM_GEMM_FWD_BIAS_RELU, x_perm_.p, w1, act_.p, b1, relu_mask_.p, plan_.seg_start,
-                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s);
+                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s, gate);
     timer_.end(s);
     timer_.begin(FM_PHASE_FFN2_FWD, s);
     grouped_gemm(FM_GEMM_FWD_BIAS, act_.p, w2, y_perm_.p, b2, nullptr, plan_.seg_start,
@@ -443,7 +442,8 @@ class Layer {
   // signal_dx (P2P): tell the sources dX_perm is complete right after the
   // FFN1 dgrad, so their un-permute overlaps this GPU's weight gradients.
   void expert_backward(const void* w1, const void* w2, float* dw1, float* db1, float* dw2,
-                       float* db2, cudaStream_t s, float* dwg_tiles = nullptr, bool signal_dx = false) {
+                       float* db2, cudaStream_t s, float* dwg_tiles = nullptr, bool signal_dx = false,
+                       const ArrivalGate* gate = nullptr) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0) {
       if (signal_dx) p2p_signal(3, s);
@@ -454,7 +454,7 @@ class Layer {
     timer_.begin(FM_PHASE_FFN2_DGRAD, s);
     grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p,
                  db1 ? tile_colsum_.as<float>() : nullptr, relu_mask_.p, plan_.seg_start,
-                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s);
+                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s, gate);
     timer_.end(s);
     // dX = dH . W1 -> [rows, d]
     timer_.begin(FM_PHASE_FFN1_DGRAD, s);
@@ -583,6 +583,8 @@ class Layer {
     peer_ipc_.assign(G, false);
     pp_.base[cfg_.rank] = a;
     plan_.peer_row = peer_row_mem_;
+    tile_src_mask_.reset(sizeof(unsigned long long) * (rows / 128));
+    plan_.tile_src_mask = tile_src_mask_.as<unsigned long long>();
   }
   void p2p_handle(void* out64) {
     require_p2p();
@@ -639,10 +641,21 @@ class Layer {
                     pos_.as<int32_t>(), nullptr, nullptr, s, &p);
     timer_.end(s);
   }
+  ArrivalGate p2p_gate(int slot) {
+    ArrivalGate g;
+    g.flags = reinterpret_cast<const unsigned long long*>(arena_.as<char>() + pp_.flag_off) + slot * kMaxPeers;
+    g.tile_src_mask = tile_src_mask_.as<unsigned long long>();
+    g.epoch = epoch_;
+    g.err = p2p_err_.as<int>();
+    return g;
+  }
+  // No step-wide wait: FFN1's producer waits per 128-row tile for the sources
+  // whose rows the tile holds, so local rows (route() keeps them local first)
+  // compute while remote ones are still arriving over NVLink.
   void expert_forward_p2p(const void* w1, const float* b1, const void* w2, const float* b2, cudaStream_t s) {
     launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);  // own pad rows only
-    p2p_wait(0, s);
-    expert_forward(w1, b1, w2, b2, s);
+    const ArrivalGate gate = p2p_gate(0);
+    expert_forward(w1, b1, w2, b2, s, &gate);
     p2p_signal(1, s);
   }
   void combine_p2p(void* y, cudaStream_t s) {
@@ -666,11 +679,13 @@ class Layer {
   void expert_backward_p2p(const void* w1, const void* w2, float* dw1, float* db1, float* dw2, float* db2,
                            float* dwg, cudaStream_t s) {
     launch_zero_pad(dy_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);
-    p2p_wait(2, s);
     const bool dwg_tiles = dwg && cfg_.top_k > 1 && nl() > 0;
     if (dwg && !dwg_tiles)
       FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * cfg_.num_experts * cfg_.d_model, s));
-    expert_backward(w1, w2, dw1, db1, dw2, db2, s, dwg_tiles ? dwg : nullptr, /*signal_dx=*/true);
+    // the FFN2 dgrad (first reader of the pushed dY rows) waits per tile; the
+    // later readers (weight gradients, tile sums) run after it
+    const ArrivalGate gate = p2p_gate(2);
+    expert_backward(w1, w2, dw1, db1, dw2, db2, s, dwg_tiles ? dwg : nullptr, /*signal_dx=*/true, &gate);
   }
   void unpermute_backward_p2p(const void* wg, void* dx, float* dwg, cudaStream_t s) {
     const int T = cur_T_, d = cfg_.d_model, k = cfg_.top_k;
@@ -798,7 +813,7 @@ class Layer {
  private:
   fm_layer_config cfg_;
   bool p2p_ = false;
-  DevBuf arena_, unit_dst_, p2p_err_, p2p_done_;
+  DevBuf arena_, unit_dst_, p2p_err_, p2p_done_, tile_src_mask_;
   P2P pp_{};
   std::vector<bool> peer_ipc_;
   unsigned long long epoch_ = 0;

@@ -22,6 +22,7 @@ struct PlanDev {
   int32_t* recv_chunk_dst;  // [G*Nl]  X_perm row of that chunk's first row
   int32_t* totals;          // [4]     padded rows, units sent, units received
   int32_t* peer_row;        // [N][G]  P2P: X_perm row on dst of (e, me)'s first unit (null otherwise)
+  unsigned long long* tile_src_mask;  // [rows/128] P2P: sources with rows in each 128-row tile
 };
 
 // Peer-to-peer transport: every GPU's exchange arena holds its
