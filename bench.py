@@ -307,8 +307,8 @@ class DistArm:
         self.layer, self.dl = self.rt.layer, self.rt.dl
         self.drift = np.random.default_rng(42)  # same walk on every rank
         self.N, self.G = N, G
-        if self.transport == "p2p":  # fwd 11 (1 signal, 1 wait), bwd 11 (1 signal, 1 wait)
-            self.kernels_per_step = 22
+        if self.transport == "p2p":  # fwd 10 (incl. 1 signal), bwd 10 (incl. 1 signal); waits are in-kernel
+            self.kernels_per_step = 20
         else:  # + demand transpose, staging relayouts / pad zeroing, run-based gate wgrad
             self.kernels_per_step = 8 + 13 + (1 if k > 1 else 0)
         self.reset_stats()

@@ -257,6 +257,9 @@ int main(int argc, char** argv) {
   try {
     const Args a = parse(argc, argv);
     if (a.gpus < 1) throw std::invalid_argument("--gpus must be >= 1");
+    // one node: NCCL's bootstrap over loopback (avoids picking a slow or
+    // unreachable interface on the box)
+    setenv("NCCL_SOCKET_IFNAME", "lo", 0);
     ncclUniqueId id;
     nc(ncclGetUniqueId(&id), "ncclGetUniqueId");  // bootstrap root stays in this (parent) process
     std::vector<pid_t> kids;

@@ -379,8 +379,10 @@ int fm_layer_unpermute_backward(fm_layer* layer, const void* dback_buf, const vo
  *   fm_layer_expert_backward_p2p   wait, dgrad, flag "dX ready", weight grads; dwg gets this
  *                            GPU's share of the gate-weight gradient (sum it over all GPUs)
  *   fm_layer_unpermute_backward_p2p  wait, dx from dX rows read from the expert GPUs
- * Waits are device-side (flags in the arena, monotonic epochs) and bounded:
- * after ~20 s a wait gives up and fm_layer_p2p_status reports it. Slots are
+ * Waits are device-side, inside the consuming kernels (flags in the arena,
+ * monotonic epochs; the expert GEMMs wait per 128-row tile for exactly the
+ * sources in it) and bounded: after ~20 s a wait gives up and
+ * fm_layer_p2p_status reports it. Slots are
  * reused across steps only after the next step's demand all-gather, which
  * every GPU joins after finishing the previous step. */
 int fm_layer_enable_p2p(fm_layer* layer);
@@ -441,7 +443,7 @@ int fm_layer_copy_out(fm_layer* layer, int field, void* host, size_t max_bytes, 
 #define FM_PHASE_BIAS_GRAD 12   /* db1, db2 */
 #define FM_PHASE_UNPERMUTE 13   /* dx gather + gate input grad */
 #define FM_PHASE_GATE_WGRAD 14  /* dWg */
-#define FM_PHASE_RELAYOUT 15    /* multi-GPU: a2a order <-> expert segments, or P2P arrival waits */
+#define FM_PHASE_RELAYOUT 15    /* multi-GPU (all-to-all transport): a2a order <-> expert segments */
 #define FM_NUM_PHASES 16
 int fm_layer_set_timing(fm_layer* layer, int enable);
 int fm_layer_read_timing(fm_layer* layer, double* ms_by_phase, int* launches_by_phase);

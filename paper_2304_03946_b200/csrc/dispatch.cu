@@ -94,8 +94,14 @@ __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
                             const int32_t* __restrict__ local_expert, int Nl, PlanDev p,
                             const int32_t* __restrict__ counts, const int64_t* __restrict__ demand,
                             int32_t* __restrict__ status) {
-  extern __shared__ int32_t sf[];  // flows as int32 [N][G][G]
+  extern __shared__ int32_t sf[];  // flows as int32 [N][G][G], then local experts [Nl], segment starts [Nl]
   const int nflow = N * G * G;
+  int32_t* sle = sf + nflow;
+  int32_t* sss = sle + Nl;
+  for (int i = threadIdx.x; i < Nl; i += blockDim.x) sle[i] = local_expert[i];
+  int32_t* scnt = sss + Nl;  // replica counts [N][G] (P2P peer layouts)
+  if (counts)
+    for (int i = threadIdx.x; i < N * G; i += blockDim.x) scnt[i] = counts[i];
   if (demand) {
     if (threadIdx.x == 0 && status) *status = 0;
     __syncthreads();
@@ -122,17 +128,35 @@ __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
     }
   }
   // --- destination side: local segments (rows padded to 128)
+  // (thread 0 works from shared memory only: a chain of dependent global loads
+  // would cost ~0.5 us per step of these loops)
   if (threadIdx.x == 0) {
     int start = 0, mt = 0;
     for (int li = 0; li < Nl; ++li) {
-      const int e = local_expert[li];
+      const int e = sle[li];
       int real = 0;
       for (int s = 0; s < G; ++s) real += FL(e, s, me);
       const int rows = (real + kRowAlign - 1) / kRowAlign * kRowAlign;
       p.seg_start[li] = start;
+      sss[li] = start;
       p.seg_real[li] = real;
       p.seg_rows[li] = rows;
       p.mtile_prefix[li] = mt;
+      if (p.tile_src_mask) {
+        // P2P: sources with rows in each 128-row tile of the segment (the
+        // expert GEMMs wait per tile for exactly those arrivals)
+        for (int t = 0; t < rows / kRowAlign; ++t) {
+          const int t0 = start + t * kRowAlign, t1 = t0 + kRowAlign;
+          unsigned long long m = 0ull;
+          int lo = start;
+          for (int s = 0; s < G; ++s) {
+            const int hi = lo + FL(e, s, me);
+            if (hi > lo && lo < t1 && hi > t0) m |= 1ull << s;
+            lo = hi;
+          }
+          p.tile_src_mask[mt + t] = m;
+        }
+      }
       start += rows;
       mt += rows / kRowAlign;
     }
@@ -155,32 +179,17 @@ __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
     for (int s = 0; s < G; ++s) {
       const int base = roff;
       for (int li = 0; li < Nl; ++li) {
-        const int e = local_expert[li];
+        const int e = sle[li];
         int before = 0;
         for (int s2 = 0; s2 < s; ++s2) before += FL(e, s2, me);
         p.recv_chunk_off[s * Nl + li] = roff;
-        p.recv_chunk_dst[s * Nl + li] = p.seg_start[li] + before;
+        p.recv_chunk_dst[s * Nl + li] = sss[li] + before;
         roff += FL(e, s, me);
       }
       p.recv_rows[s] = roff - base;
     }
     p.recv_chunk_off[G * Nl] = roff;
     p.totals[2] = roff;  // units received
-    // P2P: which sources' rows each 128-row tile of this GPU's X_perm / dY_perm
-    // holds (the expert GEMMs wait per tile for exactly those arrivals)
-    if (p.tile_src_mask) {
-      for (int li = 0; li < Nl; ++li) {
-        const int e = local_expert[li];
-        for (int t = p.mtile_prefix[li]; t < p.mtile_prefix[li + 1]; ++t) p.tile_src_mask[t] = 0ull;
-        int row = p.seg_start[li];
-        for (int s = 0; s < G; ++s) {
-          const int c = FL(e, s, me);
-          if (c > 0)
-            for (int t = row / kRowAlign; t <= (row + c - 1) / kRowAlign; ++t) p.tile_src_mask[t] |= 1ull << s;
-          row += c;
-        }
-      }
-    }
   }
   // P2P: where (e, me)'s units start in every destination's X_perm. Every GPU
   // lays out its segments the same way (hosted experts ascending, 128-row
@@ -190,7 +199,7 @@ __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
     for (int dst = threadIdx.x; dst < G; dst += blockDim.x) {
       int start = 0;
       for (int e = 0; e < N; ++e) {
-        if (counts[e * G + dst] <= 0) {
+        if (scnt[e * G + dst] <= 0) {
           p.peer_row[e * G + dst] = -1;
           continue;
         }
@@ -227,17 +236,44 @@ __device__ __forceinline__ void zero_pad_segment(__nv_bfloat16* __restrict__ buf
 inline P2P no_p2p() {
   P2P p{};
   p.signal_slot = -1;
+  p.wait_slot = -1;
   return p;
 }
 
-// Last-block release of rows pushed into peers' arenas (P2P): every thread
-// fences its own stores at system scope, then the block counts itself done;
-// the last block of the grid publishes flags[slot][me] = epoch to every peer.
+// Block-level arrival wait of a consuming kernel (P2P pulls): one thread per
+// source polls this GPU's own flags (acquire), then the block proceeds.
+__device__ __forceinline__ void p2p_block_wait(const P2P& pp) {
+  if (pp.wait_slot < 0) return;
+  if (static_cast<int>(threadIdx.x) < pp.world) {
+    const unsigned long long* f = reinterpret_cast<const unsigned long long*>(pp.base[pp.me] + pp.flag_off) +
+                                  pp.wait_slot * kMaxPeers + threadIdx.x;
+    unsigned long long t0, now, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v >= pp.epoch) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 20000000000ull) {
+        atomicExch(pp.err, 1);
+        break;
+      }
+      __nanosleep(128);
+    }
+  }
+  __syncthreads();
+}
+
+// Last-block release of rows pushed into peers' arenas (P2P): after a block
+// barrier one thread fences the block's stores at system scope and counts the
+// block done; the last block of the grid publishes flags[slot][me] = epoch to
+// every peer.
 __device__ __forceinline__ void p2p_release_when_last(const P2P& pp) {
   if (pp.signal_slot < 0) return;
-  __threadfence_system();
+  // bar.sync orders the block's stores before thread 0's system-scope fence
+  // (happens-before is transitive), so one fence per block covers them all
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence_system();
     unsigned int* ctr = pp.done + pp.signal_slot;
     if (atomicAdd(ctr, 1u) == gridDim.x - 1) {
       *ctr = 0;  // the next launch of this slot is stream-ordered after this one
@@ -431,6 +467,7 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(const __nv_bfloat16* _
                                                           const int32_t* __restrict__ pos,
                                                           const float* __restrict__ w, int T, int k,
                                                           __nv_bfloat16* __restrict__ y, const P2P pp) {
+  p2p_block_wait(pp);  // P2P: the expert GPUs' Y rows are complete
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -547,6 +584,7 @@ __global__ void __launch_bounds__(256) unpermute_bwd_kernel(
     const int32_t* __restrict__ idx, const float* __restrict__ dl,
     const __nv_bfloat16* __restrict__ wg, int T, int k, int gate_grad,
     __nv_bfloat16* __restrict__ dx, const P2P pp) {
+  p2p_block_wait(pp);  // P2P: the expert GPUs' dX rows are complete
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -785,26 +823,6 @@ __global__ void p2p_signal_kernel(const P2P pp, int G, int me, int slot, unsigne
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
 }
 
-// Waits until every source has signalled `epoch` in `slot` (bounded: after
-// ~20 s it records a timeout in *err and gives up instead of hanging).
-__global__ void p2p_wait_kernel(const unsigned long long* flags, int G, int slot, unsigned long long epoch,
-                                int* err) {
-  const int src = threadIdx.x;
-  if (src >= G) return;
-  const unsigned long long* f = flags + slot * kMaxPeers + src;
-  unsigned long long t0, now, v;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (true) {
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-    if (v >= epoch) break;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    if (now - t0 > 20000000000ull) {
-      atomicExch(err, 1);
-      break;
-    }
-    __nanosleep(256);
-  }
-}
 
 // ------------------------------------------------------------------ launchers
 void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int max_rows, int d,
@@ -877,7 +895,7 @@ void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expe
                  const PlanDev& p, cudaStream_t s, const int32_t* counts, const int64_t* demand,
                  int32_t* status) {
   if (demand && (N > 256 || G > kMaxGpus)) throw std::invalid_argument("route: bad dimensions");
-  const int smem = N * G * G * 4;
+  const int smem = (N * G * G + 2 * Nl + N * G) * 4;
   if (smem > 200 * 1024) throw std::invalid_argument("plan: N*G*G too large");
   static int configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
@@ -982,10 +1000,5 @@ void launch_p2p_signal(const P2P& pp, int G, int me, int slot, unsigned long lon
   FM_LAUNCH_CHECK("p2p_signal_kernel");
 }
 
-void launch_p2p_wait(const void* local_flags, int G, int slot, unsigned long long epoch, int* err,
-                     cudaStream_t s) {
-  p2p_wait_kernel<<<1, 64, 0, s>>>(static_cast<const unsigned long long*>(local_flags), G, slot, epoch, err);
-  FM_LAUNCH_CHECK("p2p_wait_kernel");
-}
 
 }  // namespace fm

@@ -61,8 +61,6 @@ void launch_segment_tile_reduce(const float* partial0, int cols0, const int32_t*
                                 const float* partial2, int cols2, const int32_t* idx2, float* out2,
                                 const PlanDev& p, int Nl, cudaStream_t s);
 void launch_p2p_signal(const P2P& pp, int G, int me, int slot, unsigned long long epoch, cudaStream_t s);
-void launch_p2p_wait(const void* local_flags, int G, int slot, unsigned long long epoch, int* err,
-                     cudaStream_t s);
 void launch_dropped_gate_wgrad(const void* x, const int32_t* pos, const int32_t* idx, const float* dl,
                                int T, int d, int k, float* dwg, cudaStream_t s);
 
@@ -556,6 +554,7 @@ class Layer {
     const size_t rb = al(2 * rows * d);
     pp_ = P2P{};
     pp_.signal_slot = -1;
+    pp_.wait_slot = -1;
     pp_.x_off = 0;
     pp_.y_off = rb;
     pp_.dy_off = 2 * rb;
@@ -624,9 +623,11 @@ class Layer {
   }
   // P2P launch parameters; with slot >= 0 the kernel's last block releases
   // the rows it pushed (flags[slot][me] = epoch on every peer).
-  P2P p2p_args(int slot) const {
+  P2P p2p_args(int slot, int wait_slot = -1) const {
     P2P p = pp_;
     p.signal_slot = slot;
+    p.wait_slot = wait_slot;
+    p.err = p2p_err_.as<int>();
     p.me = cfg_.rank;
     p.world = cfg_.num_gpus;
     p.epoch = epoch_;
@@ -659,9 +660,8 @@ class Layer {
     p2p_signal(1, s);
   }
   void combine_p2p(void* y, cudaStream_t s) {
-    p2p_wait(1, s);
     timer_.begin(FM_PHASE_COMBINE_FWD, s);
-    const P2P p = p2p_args(-1);
+    const P2P p = p2p_args(-1, /*wait for "Y ready"*/ 1);
     launch_combine_fwd(y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), cur_T_, cfg_.d_model, cfg_.top_k, y, s,
                        &p);
     timer_.end(s);
@@ -690,9 +690,8 @@ class Layer {
   void unpermute_backward_p2p(const void* wg, void* dx, float* dwg, cudaStream_t s) {
     const int T = cur_T_, d = cfg_.d_model, k = cfg_.top_k;
     const bool gate_grad = k > 1;
-    p2p_wait(3, s);
     timer_.begin(FM_PHASE_UNPERMUTE, s);
-    const P2P p = p2p_args(-1);
+    const P2P p = p2p_args(-1, /*wait for "dX ready"*/ 3);
     launch_unpermute_bwd(dx_perm_.p, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(), wg, T, d, k,
                          gate_grad, dx, s, &p);
     timer_.end(s);
@@ -796,11 +795,6 @@ class Layer {
   }
   void p2p_signal(int slot, cudaStream_t s) {
     launch_p2p_signal(pp_, cfg_.num_gpus, cfg_.rank, slot, epoch_, s);
-  }
-  void p2p_wait(int slot, cudaStream_t s) {
-    timer_.begin(FM_PHASE_RELAYOUT, s);
-    launch_p2p_wait(arena_.as<char>() + pp_.flag_off, cfg_.num_gpus, slot, epoch_, p2p_err_.as<int>(), s);
-    timer_.end(s);
   }
 
  public:

@@ -43,6 +43,10 @@ struct P2P {
   int signal_slot, me, world;
   unsigned long long epoch;
   unsigned int* done;
+  // With wait_slot >= 0 a consuming kernel's blocks first wait (bounded) until
+  // every peer has published flags[wait_slot][src] >= epoch in this GPU's arena.
+  int wait_slot;
+  int* err;
 };
 
 }  // namespace fm
