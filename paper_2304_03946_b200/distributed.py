@@ -300,12 +300,17 @@ class StepBuffers:
 class DistributedMoELayer:
     """FlexMoE layer on one GPU of G, driving fm_layer_* phases around `exchange`."""
 
-    def __init__(self, layer, exchange: Exchange, transport: str = "nccl"):
+    def __init__(self, layer, exchange: Exchange, transport: str = "nccl", reuse_grads: bool = False):
         """transport "nccl": dispatch / combine and their backward mirrors are
         all-to-alls of staging buffers (plus relayouts). "p2p": token rows
         cross NVLink inside the dispatch / combine / un-permute kernels,
         straight between the token's GPU and its expert GPU's permuted
-        buffers (CUDA IPC-mapped arenas, device-side arrival flags)."""
+        buffers (CUDA IPC-mapped arenas, device-side arrival flags).
+
+        reuse_grads: backward() writes into the same gradient tensors every
+        step (stream-ordered, like MoELayer.backward's `grads` argument) — the
+        runtime consumes them within the step; a caller that keeps a step's
+        gradients past the next backward must leave it off."""
         from .layer import MoELayer
 
         assert isinstance(layer, MoELayer)
@@ -320,6 +325,8 @@ class DistributedMoELayer:
             exchange.share_layer(layer)
         self._st: StepBuffers | None = None
         self._saved = None
+        self.reuse_grads = reuse_grads
+        self._bufs: dict[str, torch.Tensor] = {}
         self._timing = False
         self._marks: list[tuple[str, torch.cuda.Event, torch.cuda.Event]] = []
 
@@ -336,6 +343,24 @@ class DistributedMoELayer:
             v[0] += a.elapsed_time(b)
             v[1] += 1
         return {k: (v[0], v[1]) for k, v in out.items()}
+
+    def _buf(self, name, shape, dtype, device):
+        """A per-layer device buffer, reallocated only when its shape changes."""
+        t = self._bufs.get(name)
+        if t is None or t.shape != torch.Size(shape) or t.dtype != dtype or t.device != device:
+            t = self._bufs[name] = torch.empty(shape, dtype=dtype, device=device)
+        return t
+
+    def _grads(self, T, nl, dev):
+        from .layer import LayerGrads
+
+        lay, f32 = self.layer, torch.float32
+        d, f, N, m = lay.d, lay.f, lay.N, max(nl, 1)
+        shapes = dict(dx=((T, d), torch.bfloat16), dwg=((N, d), f32), dw1=((m, f, d), f32), db1=((m, f), f32),
+                      dw2=((m, d, f), f32), db2=((m, d), f32))
+        if self.reuse_grads:
+            return LayerGrads(**{n: self._buf("g_" + n, s, dt, dev) for n, (s, dt) in shapes.items()})
+        return LayerGrads(**{n: torch.empty(s, dtype=dt, device=dev) for n, (s, dt) in shapes.items()})
 
     def _x(self, name, fn, *args):
         if not self._timing:
@@ -380,7 +405,7 @@ class DistributedMoELayer:
         T = x.shape[0]
         dev = x.device
         stream = L.stream_ptr()
-        hist = torch.empty(N, dtype=torch.int64, device=dev)
+        hist = self._buf("hist", (N,), torch.int64, dev)  # the all-gather copies it out
         self._call("fm_layer_gate", x.data_ptr(), T, wg.data_ptr(), hist.data_ptr(), stream)
         gathered = self._x("all_gather", self.ex.all_gather, hist)  # [G, N]
         if after_gather is not None:
@@ -450,16 +475,10 @@ class DistributedMoELayer:
         return y
 
     def _backward_p2p(self, dy, sync):
-        from .layer import LayerGrads
-
         T, wg, w1, w2, _x = self._saved
         lay, dev, stream = self.layer, dy.device, L.stream_ptr()
         nl = len(lay.local_experts)
-        k, d, f, N = lay.k, lay.d, lay.f, lay.N
-        z = lambda *s: torch.empty(*s, device=dev, dtype=torch.float32)
-        g = LayerGrads(dx=torch.empty(T, d, device=dev, dtype=torch.bfloat16), dwg=z(N, d),
-                       dw1=z(max(nl, 1), f, d), db1=z(max(nl, 1), f), dw2=z(max(nl, 1), d, f),
-                       db2=z(max(nl, 1), d))
+        g = self._grads(T, nl, dev)
         self._call("fm_layer_combine_backward_p2p", dy.data_ptr(), stream)
         self.ex.fence()
         self._call("fm_layer_expert_backward_p2p", w1.data_ptr(), w2.data_ptr(), g.dw1.data_ptr(),
@@ -477,8 +496,6 @@ class DistributedMoELayer:
         return self.layer.p2p_status() != 0
 
     def backward(self, dy, sync=True):
-        from .layer import LayerGrads
-
         if self.transport == "p2p":
             return self._backward_p2p(dy, sync)
         T, wg, w1, w2, _x = self._saved
@@ -487,15 +504,12 @@ class DistributedMoELayer:
         dev = dy.device
         stream = L.stream_ptr()
         nl = len(lay.local_experts)
-        k, d, f, N = lay.k, lay.d, lay.f, lay.N
+        k = lay.k
         dsend = torch.empty_like(st.send)
         drecv = torch.empty_like(st.recv)
         dret = torch.empty_like(st.recv)
         dback = torch.empty_like(st.send)
-        z = lambda *s: torch.empty(*s, device=dev, dtype=torch.float32)
-        g = LayerGrads(dx=torch.empty(T, d, device=dev, dtype=torch.bfloat16), dwg=z(N, d),
-                       dw1=z(max(nl, 1), f, d), db1=z(max(nl, 1), f), dw2=z(max(nl, 1), d, f),
-                       db2=z(max(nl, 1), d))
+        g = self._grads(T, nl, dev)
         R = sum(st.recv_rows)
         self._call("fm_layer_combine_backward", dy.data_ptr(), st.back.data_ptr(), dsend.data_ptr(),
                    stream)

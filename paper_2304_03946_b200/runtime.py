@@ -25,7 +25,7 @@ and the dispatch all-to-all.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 import torch
@@ -37,7 +37,7 @@ from .pool import ExpertStore, SlotAllocator, apply_placement_change
 
 @dataclass
 class RuntimeStep:
-    y: torch.Tensor
+    y: torch.Tensor | None  # None in `history` (entries keep no device tensors)
     balance_ratio: float
     applied: list
     accepted: list
@@ -62,7 +62,7 @@ class FlexMoERuntime:
         self.device = dev
         self.layer = MoELayer(num_experts, top_k, d_model, d_ff, replica_counts=counts, num_gpus=self.G,
                               rank=self.rank, max_tokens=max_tokens, slots_per_gpu=profile.slots_per_gpu)
-        self.dl = DistributedMoELayer(self.layer, exchange, transport=transport)
+        self.dl = DistributedMoELayer(self.layer, exchange, transport=transport, reuse_grads=True)
         # every rank tracks every rank's slot table (same ops, same order): a
         # receiver knows the source's slot without a round trip. A GPU hosts at
         # most E experts; vacated slots stay readable for one step -> 2E slots.
@@ -136,7 +136,7 @@ class FlexMoERuntime:
                           accepted=res.accepted, migration_bytes=mig_bytes,
                           replica_counts=S.counts_from_slots(self.slots, self.N).sum(axis=1),
                           makespan_s=res.report.makespan_s, adjust_bytes=res.report.adjust_bytes)
-        self.history.append(out)
+        self.history.append(replace(out, y=None))  # no device tensors kept past the step
         return out
 
 
@@ -177,7 +177,7 @@ class BaselineRuntime:
                               rank=self.rank, max_tokens=max_tokens, slots_per_gpu=slots)
         if cfg.kind == S.STATIC_EP:
             self.layer.set_capacity_factor(cfg.capacity_factor)
-        self.dl = DistributedMoELayer(self.layer, exchange, transport=transport)
+        self.dl = DistributedMoELayer(self.layer, exchange, transport=transport, reuse_grads=True)
         self.owned = [e for e in range(num_experts) if self.home[e] == self.rank]
         self.store = ExpertStore(d_model, d_ff, dev, capacity=max(1, len(self.owned)), lr=lr)
         for e in self.owned:
@@ -243,5 +243,5 @@ class BaselineRuntime:
             self.store.adam_step(self.owned, sub)
         out = dict(y=y, grads=grads, host=info["host"], demand=info["D"],
                    shadow_bytes=info.get("shadow_bytes", 0), local=list(local))
-        self.history.append(out)
+        self.history.append({kk: v for kk, v in out.items() if kk not in ("y", "grads")})
         return out
