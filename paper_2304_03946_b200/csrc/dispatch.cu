@@ -85,21 +85,55 @@ __global__ void expert_scan_kernel(const int32_t* __restrict__ tile_counts, int 
 }
 
 // ----------------------------------------------------------------- plan
+// Exclusive prefix sum of v[0, n) in shared memory, in place; returns the
+// total. Every thread of the block calls it (scratch: blockDim.x ints).
+__device__ int block_exclusive_scan(int32_t* v, int n, int32_t* scratch) {
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, static_cast<int>(threadIdx.x) * per), hi = min(n, lo + per);
+  int sum = 0;
+  for (int i = lo; i < hi; ++i) sum += v[i];
+  scratch[threadIdx.x] = sum;
+  __syncthreads();
+  for (int off = 1; off < static_cast<int>(blockDim.x); off <<= 1) {
+    const int t = threadIdx.x >= static_cast<unsigned>(off) ? scratch[threadIdx.x - off] : 0;
+    __syncthreads();
+    scratch[threadIdx.x] += t;
+    __syncthreads();
+  }
+  int run = scratch[threadIdx.x] - sum;
+  for (int i = lo; i < hi; ++i) {
+    const int x = v[i];
+    v[i] = run;
+    run += x;
+  }
+  const int total = scratch[blockDim.x - 1];
+  __syncthreads();
+  return total;
+}
+
 // One block. Turns flows[e][src][dst] into the offsets every later kernel
 // uses (see PlanDev in layer_plan.h).
 // With `demand` set, the block first runs route() itself (Alg. 3, one thread
 // per expert: split_expert_demand, the same routine as fm_route_counts) and
 // writes the flows — route + plan in one launch, no kernel boundary between.
+// Every offset table is a block-wide scan over shared memory: a serial walk
+// by one thread is a dependent chain of ~7 cycles per instruction, which at
+// 64 experts cost ~100 us per step.
 __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
                             const int32_t* __restrict__ local_expert, int Nl, PlanDev p,
                             const int32_t* __restrict__ counts, const int64_t* __restrict__ demand,
                             int32_t* __restrict__ status) {
-  extern __shared__ int32_t sf[];  // flows as int32 [N][G][G], then local experts [Nl], segment starts [Nl]
+  // shared: flows as int32 [N][G][G] | local experts [Nl] | segment starts [Nl]
+  //       | replica counts [N][G] | mtile prefix [Nl] | scan buffer [N*G] | scratch [blockDim]
+  extern __shared__ int32_t sf[];
   const int nflow = N * G * G;
   int32_t* sle = sf + nflow;
   int32_t* sss = sle + Nl;
+  int32_t* scnt = sss + Nl;
+  int32_t* smt = scnt + N * G;
+  int32_t* sbuf = smt + Nl;
+  int32_t* scratch = sbuf + N * G;
   for (int i = threadIdx.x; i < Nl; i += blockDim.x) sle[i] = local_expert[i];
-  int32_t* scnt = sss + Nl;  // replica counts [N][G] (P2P peer layouts)
   if (counts)
     for (int i = threadIdx.x; i < N * G; i += blockDim.x) scnt[i] = counts[i];
   if (demand) {
@@ -128,89 +162,104 @@ __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
     }
   }
   // --- destination side: local segments (rows padded to 128)
-  // (thread 0 works from shared memory only: a chain of dependent global loads
-  // would cost ~0.5 us per step of these loops)
+  for (int li = threadIdx.x; li < Nl; li += blockDim.x) {
+    const int e = sle[li];
+    int real = 0;
+    for (int s = 0; s < G; ++s) real += FL(e, s, me);
+    const int rows = (real + kRowAlign - 1) / kRowAlign * kRowAlign;
+    p.seg_real[li] = real;
+    p.seg_rows[li] = rows;
+    sss[li] = rows;
+    smt[li] = rows / kRowAlign;
+  }
+  __syncthreads();
+  const int total_rows = block_exclusive_scan(sss, Nl, scratch);
+  const int total_mt = block_exclusive_scan(smt, Nl, scratch);
+  for (int li = threadIdx.x; li < Nl; li += blockDim.x) {
+    p.seg_start[li] = sss[li];
+    p.mtile_prefix[li] = smt[li];
+  }
   if (threadIdx.x == 0) {
-    int start = 0, mt = 0;
-    for (int li = 0; li < Nl; ++li) {
-      const int e = sle[li];
-      int real = 0;
-      for (int s = 0; s < G; ++s) real += FL(e, s, me);
-      const int rows = (real + kRowAlign - 1) / kRowAlign * kRowAlign;
-      p.seg_start[li] = start;
-      sss[li] = start;
-      p.seg_real[li] = real;
-      p.seg_rows[li] = rows;
-      p.mtile_prefix[li] = mt;
-      if (p.tile_src_mask) {
-        // P2P: sources with rows in each 128-row tile of the segment (the
-        // expert GEMMs wait per tile for exactly those arrivals)
-        for (int t = 0; t < rows / kRowAlign; ++t) {
-          const int t0 = start + t * kRowAlign, t1 = t0 + kRowAlign;
-          unsigned long long m = 0ull;
-          int lo = start;
-          for (int s = 0; s < G; ++s) {
-            const int hi = lo + FL(e, s, me);
-            if (hi > lo && lo < t1 && hi > t0) m |= 1ull << s;
-            lo = hi;
-          }
-          p.tile_src_mask[mt + t] = m;
-        }
+    p.mtile_prefix[Nl] = total_mt;
+    p.totals[0] = total_rows;  // padded rows on this GPU
+  }
+  if (p.tile_src_mask) {
+    // P2P: sources with rows in each 128-row tile (the expert GEMMs wait per
+    // tile for exactly those arrivals); a tile's segment is the last one whose
+    // first tile is <= it (empty segments share their successor's prefix)
+    for (int t = threadIdx.x; t < total_mt; t += blockDim.x) {
+      int lo = 0, hi = Nl - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (smt[mid] <= t) lo = mid;
+        else hi = mid - 1;
       }
-      start += rows;
-      mt += rows / kRowAlign;
-    }
-    p.mtile_prefix[Nl] = mt;
-    p.totals[0] = start;  // padded rows on this GPU
-    // send side totals per destination, and send offsets (dst-major, expert-minor)
-    int off = 0;
-    for (int dst = 0; dst < G; ++dst) {
-      const int begin = off;
-      for (int e = 0; e < N; ++e) {
-        p.send_off[e * G + dst] = off;
-        off += FL(e, me, dst);
+      const int e = sle[lo];
+      const int t0 = sss[lo] + (t - smt[lo]) * kRowAlign, t1 = t0 + kRowAlign;
+      unsigned long long m = 0ull;
+      int r = sss[lo];
+      for (int s = 0; s < G; ++s) {
+        const int r1 = r + FL(e, s, me);
+        if (r1 > r && r < t1 && r1 > t0) m |= 1ull << s;
+        r = r1;
       }
-      p.send_rows[dst] = off - begin;
+      p.tile_src_mask[t] = m;
     }
-    p.totals[1] = off;  // units sent (== T * k)
-    // receive side: chunk offsets in the a2a receive buffer (src-major,
-    // local-expert-minor) and their X_perm destinations
-    int roff = 0;
-    for (int s = 0; s < G; ++s) {
-      const int base = roff;
-      for (int li = 0; li < Nl; ++li) {
-        const int e = sle[li];
-        int before = 0;
-        for (int s2 = 0; s2 < s; ++s2) before += FL(e, s2, me);
-        p.recv_chunk_off[s * Nl + li] = roff;
-        p.recv_chunk_dst[s * Nl + li] = sss[li] + before;
-        roff += FL(e, s, me);
-      }
-      p.recv_rows[s] = roff - base;
-    }
-    p.recv_chunk_off[G * Nl] = roff;
-    p.totals[2] = roff;  // units received
+  }
+  // --- send side: offsets in the dispatch buffer (dst-major, expert-minor)
+  for (int j = threadIdx.x; j < N * G; j += blockDim.x) sbuf[j] = FL(j % N, me, j / N);
+  __syncthreads();
+  const int sent = block_exclusive_scan(sbuf, N * G, scratch);
+  for (int j = threadIdx.x; j < N * G; j += blockDim.x) p.send_off[(j % N) * G + j / N] = sbuf[j];
+  for (int dst = threadIdx.x; dst < G; dst += blockDim.x)
+    p.send_rows[dst] = (dst + 1 < G ? sbuf[(dst + 1) * N] : sent) - sbuf[dst * N];
+  if (threadIdx.x == 0) p.totals[1] = sent;  // units sent (== T * k)
+  __syncthreads();
+  // --- receive side: chunk offsets in the a2a receive buffer (src-major,
+  // local-expert-minor) and their X_perm destinations
+  const int nrc = G * Nl;
+  for (int j = threadIdx.x; j < nrc; j += blockDim.x) sbuf[j] = FL(sle[j % Nl], j / Nl, me);
+  __syncthreads();
+  const int recvd = block_exclusive_scan(sbuf, nrc, scratch);
+  for (int j = threadIdx.x; j < nrc; j += blockDim.x) {
+    const int src = j / Nl, li = j % Nl, e = sle[li];
+    int before = 0;
+    for (int s2 = 0; s2 < src; ++s2) before += FL(e, s2, me);
+    p.recv_chunk_off[j] = sbuf[j];
+    p.recv_chunk_dst[j] = sss[li] + before;
+  }
+  for (int src = threadIdx.x; src < G; src += blockDim.x) {
+    const int a = src * Nl < nrc ? sbuf[src * Nl] : recvd;
+    const int b = (src + 1) * Nl < nrc ? sbuf[(src + 1) * Nl] : recvd;
+    p.recv_rows[src] = b - a;
+  }
+  if (threadIdx.x == 0) {
+    p.recv_chunk_off[nrc] = recvd;
+    p.totals[2] = recvd;  // units received
   }
   // P2P: where (e, me)'s units start in every destination's X_perm. Every GPU
   // lays out its segments the same way (hosted experts ascending, 128-row
   // padded, sources ascending inside a segment), so each source computes its
   // destinations' layouts from the shared flows and replica counts.
   if (p.peer_row) {
-    for (int dst = threadIdx.x; dst < G; dst += blockDim.x) {
-      int start = 0;
-      for (int e = 0; e < N; ++e) {
-        if (scnt[e * G + dst] <= 0) {
-          p.peer_row[e * G + dst] = -1;
-          continue;
-        }
-        int real = 0, before = 0;
-        for (int s = 0; s < G; ++s) {
-          real += FL(e, s, dst);
-          if (s < me) before += FL(e, s, dst);
-        }
-        p.peer_row[e * G + dst] = start + before;
-        start += (real + kRowAlign - 1) / kRowAlign * kRowAlign;
+    __syncthreads();  // sbuf reuse
+    for (int j = threadIdx.x; j < N * G; j += blockDim.x) {
+      const int dst = j / N, e = j % N;
+      int real = 0;
+      for (int s = 0; s < G; ++s) real += FL(e, s, dst);
+      sbuf[j] = scnt[e * G + dst] > 0 ? (real + kRowAlign - 1) / kRowAlign * kRowAlign : 0;
+    }
+    __syncthreads();
+    block_exclusive_scan(sbuf, N * G, scratch);
+    for (int j = threadIdx.x; j < N * G; j += blockDim.x) {
+      const int dst = j / N, e = j % N;
+      if (scnt[e * G + dst] <= 0) {
+        p.peer_row[e * G + dst] = -1;
+        continue;
       }
+      int before = 0;
+      for (int s = 0; s < me; ++s) before += FL(e, s, dst);
+      p.peer_row[e * G + dst] = sbuf[j] - sbuf[dst * N] + before;
     }
   }
 #undef FL
@@ -895,14 +944,15 @@ void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expe
                  const PlanDev& p, cudaStream_t s, const int32_t* counts, const int64_t* demand,
                  int32_t* status) {
   if (demand && (N > 256 || G > kMaxGpus)) throw std::invalid_argument("route: bad dimensions");
-  const int smem = (N * G * G + 2 * Nl + N * G) * 4;
+  constexpr int kPlanThreads = 256;
+  const int smem = (N * G * G + 3 * Nl + 2 * N * G + kPlanThreads) * 4;
   if (smem > 200 * 1024) throw std::invalid_argument("plan: N*G*G too large");
   static int configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     FM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = smem;
   }
-  plan_kernel<<<1, 256, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status);
+  plan_kernel<<<1, kPlanThreads, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status);
   FM_LAUNCH_CHECK("plan_kernel");
 }
 
