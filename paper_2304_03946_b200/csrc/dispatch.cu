@@ -13,6 +13,8 @@
 //     inside a segment rows are ordered by source GPU, then rank.
 // Everything here is integer-exact and deterministic; the only atomics are
 // fp32 additions into bias / gate-weight gradients.
+#include <mutex>
+#include <unordered_map>
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -315,14 +317,16 @@ __device__ __forceinline__ void p2p_block_wait(const P2P& pp) {
 // Last-block release of rows pushed into peers' arenas (P2P): after a block
 // barrier one thread fences the block's stores at system scope and counts the
 // block done; the last block of the grid publishes flags[slot][me] = epoch to
-// every peer.
-__device__ __forceinline__ void p2p_release_when_last(const P2P& pp) {
+// every peer. A block that wrote only its own GPU's memory skips the fence
+// (the last block fences before publishing; same-GPU consumers are
+// stream-ordered after this kernel anyway).
+__device__ __forceinline__ void p2p_release_when_last(const P2P& pp, bool wrote_peer) {
   if (pp.signal_slot < 0) return;
   // bar.sync orders the block's stores before thread 0's system-scope fence
   // (happens-before is transitive), so one fence per block covers them all
-  __syncthreads();
+  const int any_peer = __syncthreads_or(wrote_peer);
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    if (any_peer) __threadfence_system();
     unsigned int* ctr = pp.done + pp.signal_slot;
     if (atomicAdd(ctr, 1u) == gridDim.x - 1) {
       *ctr = 0;  // the next launch of this slot is stream-ordered after this one
@@ -340,15 +344,14 @@ __device__ __forceinline__ void p2p_release_when_last(const P2P& pp) {
 // Warp per token: resolve each unit's row in the dispatch buffer and copy the
 // token's activations there (k copies). When `direct` (G == 1), the dispatch
 // buffer is X_perm itself and send_off is replaced by the expert's segment.
-__device__ __forceinline__ void dispatch_tokens(const __nv_bfloat16* __restrict__ x, int T, int d, int k, int N,
+__device__ __forceinline__ void dispatch_token(int t, bool& wrote_peer, const __nv_bfloat16* __restrict__ x, int d,
+                                               int k, int N,
                                                 int G, int me, int direct, const int32_t* __restrict__ idx,
                                                 const int32_t* __restrict__ tile_rank,
                                                 const int32_t* __restrict__ tile_base, const PlanDev& p,
                                                 int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf,
                                                 int32_t* __restrict__ row_expert, const P2P& pp) {
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (t >= T) return;
   const int nvec = d / 8;  // uint4 per row
   const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * d);
   uint4 v[8];
@@ -382,6 +385,7 @@ __device__ __forceinline__ void dispatch_tokens(const __nv_bfloat16* __restrict_
       if (row_expert && row >= 0) row_expert[row] = e;
     }
     if (row < 0) continue;
+    wrote_peer |= pp.unit_dst && to != pp.me;
     __nv_bfloat16* out = pp.unit_dst ? reinterpret_cast<__nv_bfloat16*>(pp.base[to] + pp.x_off) : buf;
     uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d);
 #pragma unroll
@@ -397,13 +401,17 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
                                 int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf,
                                 int32_t* __restrict__ row_expert, const P2P pp, int tok_blocks,
                                 __nv_bfloat16* __restrict__ pad_buf, int Nl) {
+  bool wrote_peer = false;
   if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero pad_buf's padding rows
     const int b = blockIdx.x - tok_blocks;
     zero_pad_segment(pad_buf, d, p, b / kPadParts, b % kPadParts, kPadParts, row_expert);
-  } else {
-    dispatch_tokens(x, T, d, k, N, G, me, direct, idx, tile_rank, tile_base, p, pos_out, buf, row_expert, pp);
+  } else {  // token blocks stride over the tokens (one release per block, not per 8 tokens)
+    const int warps = tok_blocks * (blockDim.x >> 5);
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += warps)
+      dispatch_token(t, wrote_peer, x, d, k, N, G, me, direct, idx, tile_rank, tile_base, p, pos_out, buf,
+                     row_expert, pp);
   }
-  p2p_release_when_last(pp);
+  p2p_release_when_last(pp, wrote_peer);
 }
 
 
@@ -557,12 +565,10 @@ __global__ void __launch_bounds__(256) combine_fwd_kernel(const __nv_bfloat16* _
 // host's gate-weight gradient) is written straight into its dY_perm / dl rows.
 template <int VPL>
 __device__ __forceinline__ void combine_bwd_token(
-    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Yl,
-    const int32_t* __restrict__ pos, const float* __restrict__ w, int T, int k,
+    int t, bool& wrote_peer, const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Yl,
+    const int32_t* __restrict__ pos, const float* __restrict__ w, int k,
     __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P& pp) {
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (t >= T) return;
   const int d = VPL * 256;
   int my_pos;
   float my_w;
@@ -579,6 +585,7 @@ __device__ __forceinline__ void combine_bwd_token(
       continue;
     }
     const int to = __shfl_sync(0xffffffffu, my_to, j);
+    wrote_peer |= to >= 0 && to != pp.me;
     uint4 q[VPL];
     load_unit_row<VPL>(pp, pp.y_off, to, Yl, row, d, lane, q);
     uint4* dst = reinterpret_cast<uint4*>(peer_rows(pp, pp.dy_off, to, dYl) + static_cast<size_t>(row) * d);
@@ -616,13 +623,16 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
     const int32_t* __restrict__ pos, const float* __restrict__ w, int T, int k,
     __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P pp,
     int tok_blocks, PlanDev pad_plan) {
+  bool wrote_peer = false;
   if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero dYl's padding rows
     const int b = blockIdx.x - tok_blocks;
     zero_pad_segment(dYl, VPL * 256, pad_plan, b / kPadParts, b % kPadParts, kPadParts, nullptr);
-  } else {
-    combine_bwd_token<VPL>(dy, Yl, pos, w, T, k, dYl, dl, dl_rows_l, pp);
+  } else {  // token blocks stride over the tokens (one release per block)
+    const int warps = tok_blocks * (blockDim.x >> 5);
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += warps)
+      combine_bwd_token<VPL>(t, wrote_peer, dy, Yl, pos, w, k, dYl, dl, dl_rows_l, pp);
   }
-  p2p_release_when_last(pp);  // P2P: dY rows and dl are in the expert GPUs' arenas
+  p2p_release_when_last(pp, wrote_peer);  // P2P: dY rows and dl are in the expert GPUs' arenas
 }
 
 // dx[t] = sum_j dXbuf[pos[t,j]] + sum_j dl[t,j] * Wg[idx[t,j], :]
@@ -956,6 +966,21 @@ void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expe
   FM_LAUNCH_CHECK("plan_kernel");
 }
 
+// Blocks of `kern` resident on the whole GPU at `threads` per block (cached
+// per kernel): the grid of the token-striding kernels.
+int resident_grid(const void* kern, int threads) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(kern);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  FM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+  const int grid = std::max(1, per_sm) * num_sms();
+  cache.emplace(kern, grid);
+  return grid;
+}
+
 void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
                      const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
                      const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
@@ -963,7 +988,11 @@ void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, b
   const P2P none = no_p2p();
   if (d % 8 != 0 || d > 2048) throw std::invalid_argument("dispatch: d_model must be a multiple of 8, <= 2048");
   const int warps = 8;
-  const int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
+  // P2P pushes: one resident wave striding over the tokens, so each block's
+  // system-scope release is paid once per block rather than per 8 tokens
+  int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
+  if (pp && pp->signal_slot >= 0)
+    tok_blocks = std::min(tok_blocks, resident_grid(reinterpret_cast<const void*>(dispatch_kernel), warps * 32));
   const int pad_blocks = pad_buf ? Nl * kPadParts : 0;
   if (tok_blocks + pad_blocks == 0) return;
   dispatch_kernel<<<tok_blocks + pad_blocks, warps * 32, 0, s>>>(
@@ -1019,10 +1048,13 @@ void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const
   const P2P none = no_p2p();
   if (k > 32) throw std::invalid_argument("combine_bwd: top_k <= 32");
   const int warps = 8;
-  const int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
   const int pad_blocks = pad_plan ? Nl * kPadParts : 0;
-  if (tok_blocks + pad_blocks == 0) return;
   const PlanDev nop{};
+  int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
+  if (pp && pp->signal_slot >= 0)  // P2P pushes: one resident wave (see launch_dispatch)
+    FM_VPL_DISPATCH(d, (tok_blocks = std::min(tok_blocks, resident_grid(
+                                                  reinterpret_cast<const void*>(combine_bwd_kernel<V>), warps * 32))));
+  if (tok_blocks + pad_blocks == 0) return;
   FM_VPL_DISPATCH(d, (combine_bwd_kernel<V><<<tok_blocks + pad_blocks, warps * 32, 0, s>>>(
                          static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(Y),
                          pos, w, T, k, static_cast<__nv_bfloat16*>(dYbuf), dl, dl_rows, pp ? *pp : none,
