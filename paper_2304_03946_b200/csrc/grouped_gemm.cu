@@ -637,12 +637,13 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
     a.arrive_err = gate->err;
   }
   // CTA pairs for the token-row GEMMs when groups are large enough that the
-  // odd 128-row tail of each group (computed, not stored) is cheap; always for
-  // wgrad (M_w is a multiple of 256).
+  // odd 128-row tail of each group (computed, not stored) is cheap — measured
+  // break-even near 900 rows per group (configs[2]: 64 groups of ~1024 rows run
+  // 3-6% faster in pairs); always for wgrad (M_w is a multiple of 256).
   int cg = g_cta_group;
   if (cg == 0) {
     if (variant == FM_GEMM_WGRAD) cg = (M_w % 256 == 0) ? 2 : 1;
-    else cg = (total_rows / num_groups >= 2048) ? 2 : 1;
+    else cg = (total_rows / num_groups >= 1024) ? 2 : 1;
   }
   if (variant == FM_GEMM_WGRAD && M_w % (kBM * cg) != 0) cg = 1;
   CUtensorMap m1[3], m2[3];
