@@ -405,7 +405,7 @@ __global__ void dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int 
   if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero pad_buf's padding rows
     const int b = blockIdx.x - tok_blocks;
     zero_pad_segment(pad_buf, d, p, b / kPadParts, b % kPadParts, kPadParts, row_expert);
-  } else {  // token blocks stride over the tokens (one release per block, not per 8 tokens)
+  } else {  // token blocks stride over the tokens (P2P: one release per block, not per 8 tokens)
     const int warps = tok_blocks * (blockDim.x >> 5);
     for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += warps)
       dispatch_token(t, wrote_peer, x, d, k, N, G, me, direct, idx, tile_rank, tile_base, p, pos_out, buf,
@@ -617,8 +617,10 @@ __device__ __forceinline__ void combine_bwd_token(
   }
 }
 
+// 3 blocks per SM up to d = 1024: 80 registers (allocated 8 per thread, so 81-88
+// would leave 2 blocks and cost ~25 % at VPL 4)
 template <int VPL>
-__global__ void __launch_bounds__(256) combine_bwd_kernel(
+__global__ void __launch_bounds__(256, VPL <= 4 ? 3 : 1) combine_bwd_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Yl,
     const int32_t* __restrict__ pos, const float* __restrict__ w, int T, int k,
     __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P pp,
@@ -627,7 +629,7 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
   if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero dYl's padding rows
     const int b = blockIdx.x - tok_blocks;
     zero_pad_segment(dYl, VPL * 256, pad_plan, b / kPadParts, b % kPadParts, kPadParts, nullptr);
-  } else {  // token blocks stride over the tokens (one release per block)
+  } else {  // token blocks stride over the tokens (P2P: one release per block)
     const int warps = tok_blocks * (blockDim.x >> 5);
     for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += warps)
       combine_bwd_token<VPL>(t, wrote_peer, dy, Yl, pos, w, k, dYl, dl, dl_rows_l, pp);
