@@ -57,6 +57,9 @@ PLACEMENTS = {
     # hot expert replicated everywhere, two slots of expert 3 on GPU 0
     "replicated": (8, 4, [(e, e % 4) for e in range(8)] + [(5, 0), (5, 2), (5, 3), (3, 0)]),
     "two_gpus": (16, 2, [(e, e % 2) for e in range(16)] + [(1, 0), (2, 1)]),
+    # configs[2]-like width: N*G = 512 > the plan kernel's 256 threads (multi-
+    # element scans), a hot expert on four GPUs
+    "wide_8gpus": (64, 8, [(e, e % 8) for e in range(64)] + [(0, 1), (0, 2), (0, 3), (5, 0), (9, 7)]),
 }
 
 
