@@ -261,6 +261,9 @@ class FusedArm:
     def hist(self):
         return self.layer.read("hist", self.N)
 
+    def hist_async(self, host):
+        return self.layer.copy_out_async("hist", host)
+
 
 def measured_tps(N, k, d, f):
     """(TPS, source): the committed B200 measurement for this model shape, if any."""
@@ -358,6 +361,9 @@ class DistArm:
     def hist(self):
         return self.layer.read("hist", self.N)
 
+    def hist_async(self, host):
+        return self.layer.copy_out_async("hist", host)
+
     def summary(self, steps):
         return {"placement": "dynamic (host scheduler: expand/shrink/migrate, B200 profile)",
                 "token_transport": ("P2P: rows written/read in the expert GPU's permuted buffers inside "
@@ -441,6 +447,9 @@ def run_ours(args, world, rank, local_rank):
     dyb = [torch.empty_like(dy), torch.empty_like(dy)]
     copy_stream = torch.cuda.Stream(device=dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
+    hist_h = [torch.empty(N, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+    hist_read = [torch.cuda.Event(), torch.cuda.Event()]
+    seen_units = []
 
     def e2e_run(n):
         with torch.cuda.stream(copy_stream):
@@ -457,7 +466,16 @@ def run_ours(args, world, rank, local_rank):
                     copied[nxt].record(copy_stream)
             stream.wait_event(copied[cur])
             arm.step(xb[cur], dyb[cur])
-            arm.hist()  # expert histogram to the host every step (placement-policy input)
+            # the step's expert histogram to the host (placement-policy input):
+            # enqueued behind the step, read one step later, so the host never
+            # drains the device between steps
+            arm.hist_async(hist_h[cur])
+            hist_read[cur].record(stream)
+            if i > 0:
+                hist_read[nxt].synchronize()
+                seen_units.append(int(hist_h[nxt].sum()))
+        hist_read[(n - 1) % 2].synchronize()
+        seen_units.append(int(hist_h[(n - 1) % 2].sum()))
 
     e2e_run(2)
     torch.cuda.synchronize()
@@ -469,6 +487,8 @@ def run_ours(args, world, rank, local_rank):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
+    if any(u != units for u in seen_units):  # every step's histogram read back holds T*k units
+        raise RuntimeError(f"e2e: histogram read-back {seen_units[:4]}... != {units} units per step")
     if dist:
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

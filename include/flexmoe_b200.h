@@ -424,6 +424,11 @@ int fm_layer_unpermute_backward_p2p(fm_layer* layer, const void* wg, void* dx, f
 #define FM_FIELD_KEPT 20        /* int64 [N,G] StaticEP kept demand (capacity mode) */
 #define FM_FIELD_DROPPED 21     /* int64 [1]   units dropped this step (capacity mode) */
 int fm_layer_copy_out(fm_layer* layer, int field, void* host, size_t max_bytes, size_t* written);
+/* The same copy enqueued on `stream` after the work already queued there (no
+ * device synchronisation; asynchronous into page-locked `host` memory): a
+ * step's histogram can be read back while the next step runs. */
+int fm_layer_copy_out_async(fm_layer* layer, int field, void* host, size_t max_bytes, size_t* written,
+                            void* stream);
 
 /* Per-phase CUDA-event timing on the launching stream (off by default).
  * fm_layer_read_timing synchronises the device and returns accumulated

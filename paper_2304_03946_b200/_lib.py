@@ -93,6 +93,7 @@ _SIGNATURES = {
     "fm_layer_forward": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P],
     "fm_layer_backward": [_P] * 9,
     "fm_layer_copy_out": [_P, _I, _P, C.c_size_t, C.POINTER(C.c_size_t)],
+    "fm_layer_copy_out_async": [_P, _I, _P, C.c_size_t, C.POINTER(C.c_size_t), _P],
     "fm_layer_set_timing": [_P, _I],
     "fm_profile_reference_default": [_I, _I, _P],
     "fm_step_cost": [_P, _P, _I, _P, _P, _P],

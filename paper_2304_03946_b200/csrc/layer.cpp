@@ -727,7 +727,10 @@ class Layer {
   const std::vector<int32_t>& local() const { return local_; }
   const fm_layer_config& cfg() const { return cfg_; }
 
-  void copy_out(int field, void* host, size_t max_bytes, size_t* written) {
+  // stream == nullptr: synchronise the device, then copy; else enqueue the copy
+  // on `stream` (asynchronous when `host` is pinned)
+  void copy_out(int field, void* host, size_t max_bytes, size_t* written, cudaStream_t stream = nullptr,
+                bool async = false) {
     const int T = std::max(cur_T_, 0), k = cfg_.top_k, N = cfg_.num_experts, G = cfg_.num_gpus;
     const void* src = nullptr;
     size_t bytes = 0;
@@ -757,8 +760,12 @@ class Layer {
       default: throw std::invalid_argument("fm_layer_copy_out: unknown field");
     }
     bytes = std::min(bytes, max_bytes);
-    FM_CUDA(cudaDeviceSynchronize());
-    if (bytes) FM_CUDA(cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost));
+    if (async) {
+      if (bytes) FM_CUDA(cudaMemcpyAsync(host, src, bytes, cudaMemcpyDeviceToHost, stream));
+    } else {
+      FM_CUDA(cudaDeviceSynchronize());
+      if (bytes) FM_CUDA(cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost));
+    }
     if (written) *written = bytes;
   }
 
@@ -1008,6 +1015,13 @@ int fm_layer_read_timing(fm_layer* h, double* ms_by_phase, int* launches_by_phas
 
 int fm_layer_copy_out(fm_layer* h, int field, void* host, size_t max_bytes, size_t* written) {
   return fm::guarded([&] { h->impl->copy_out(field, host, max_bytes, written); });
+}
+
+int fm_layer_copy_out_async(fm_layer* h, int field, void* host, size_t max_bytes, size_t* written,
+                            void* stream) {
+  return fm::guarded([&] {
+    h->impl->copy_out(field, host, max_bytes, written, static_cast<cudaStream_t>(stream), true);
+  });
 }
 
 }  // extern "C"

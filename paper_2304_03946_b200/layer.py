@@ -174,6 +174,15 @@ class MoELayer:
         return {name: (float(ms[i]), int(n[i])) for i, name in enumerate(PHASES)}
 
     # ---------------------------------------------------------------- introspection
+    def copy_out_async(self, field: str, host: torch.Tensor, stream=None) -> int:
+        """Enqueue a copy of `field` into the page-locked tensor `host` on the
+        stream (no device synchronisation); returns the bytes it will write."""
+        code, _ = FIELDS[field]
+        written = C.c_size_t(0)
+        L.check(L.lib().fm_layer_copy_out_async(self._h, code, host.data_ptr(), host.numel() * host.element_size(),
+                                                C.byref(written), L.stream_ptr(stream)))
+        return written.value
+
     def read(self, field: str, count: int | None = None) -> np.ndarray:
         code, dt = FIELDS[field]
         itemsize = np.dtype(dt).itemsize
