@@ -139,6 +139,14 @@ def test_layer_repeatable_and_deterministic_permutation():
     p2 = layer.read("unit_pos", T * k)
     assert (p1 == p2).all()
     assert torch.equal(y1, y2)
+    # stream-ordered read-back (fm_layer_copy_out_async) == the synchronous one
+    hist = torch.zeros(N, dtype=torch.int64, pin_memory=True)
+    pos = torch.zeros(T * k, dtype=torch.int32, pin_memory=True)
+    assert layer.copy_out_async("hist", hist) == 8 * N
+    assert layer.copy_out_async("unit_pos", pos) == 4 * T * k
+    torch.cuda.current_stream().synchronize()
+    assert (hist.numpy() == layer.read("hist", N)).all() and int(hist.sum()) == T * k
+    assert (pos.numpy() == p2).all()
 
 
 @pytest.mark.parametrize("cf", [1.0, 1.25])
