@@ -15,3 +15,7 @@ ncu --set full --clock-control none --import-source on \
     -k regex:"gate_kernel|dispatch_kernel|combine_fwd|combine_bwd|unpermute|segment_tile|expert_scan|plan_kernel" \
     -s 27 -c 9 -o gpurun_out/prof_hbm -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_hbm.log 2>&1
+ncu --target-processes all --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+    --log-file gpurun_out/dist_launches.csv python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 \
+    --master-addr 127.0.0.1 --master-port 29613 bench.py --gpus 1 --workload cfg3 --steps 3 --warmup 3 \
+    --no-cpu-baseline > gpurun_out/ncu_dist.log 2>&1

@@ -57,8 +57,8 @@ def raw(rep: Path):
     return out
 
 
-def launches():
-    p = OUT / "launches.csv"
+def launches(name="launches.csv"):
+    p = OUT / name
     rows = list(csv.reader(open(p)))
     hdr = None
     out = []
@@ -88,6 +88,20 @@ def main(tag="r01"):
             lines.append(f"| {name} | {t:.1f} | {100 * t / tot:.1f}% |")
         lines += ["", f"Total {tot:.0f} µs over {len(L)} launches.", ""]
         summary["launches"] = [{"kernel": n, "us": t} for n, t in L]
+    if (OUT / "dist_launches.csv").exists():
+        # configs[2] through the multi-GPU P2P phases (torchrun, N = 1): the
+        # second-to-last complete step, steps delimited by the gate launch
+        L = launches("dist_launches.csv")
+        starts = [i for i, (n, _) in enumerate(L) if "gate_kernel" in n]
+        if len(starts) >= 3:
+            step = L[starts[-3]:starts[-2]]
+            tot = sum(t for _, t in step)
+            lines += ["## configs[2] P2P step (multi-GPU phases at N = 1, torchrun; cold-cache, serialised)", "",
+                      "| kernel | µs | share |", "|---|---:|---:|"]
+            for name, t in step:
+                lines.append(f"| {name} | {t:.1f} | {100 * t / tot:.1f}% |")
+            lines += ["", f"Total {tot:.0f} µs over {len(step)} launches.", ""]
+            summary["dist_launches"] = [{"kernel": n, "us": t} for n, t in step]
     for rep, title in [("prof_gemm", "Grouped GEMM (tcgen05) — six launches of one step"),
                        ("prof_hbm", "Gate / dispatch / combine / reductions")]:
         f = OUT / f"{rep}.ncu-rep"
