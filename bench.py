@@ -322,8 +322,8 @@ class DistArm:
         self.layer, self.dl = self.rt.layer, self.rt.dl
         self.drift = np.random.default_rng(42)  # same walk on every rank
         self.N, self.G = N, G
-        if self.transport == "p2p":  # fwd 10 (incl. 1 signal), bwd 10 (incl. 1 signal); waits are in-kernel
-            self.kernels_per_step = 20
+        if self.transport == "p2p":  # fwd 9 (incl. 1 signal), bwd 9 (incl. 1 signal); waits in-kernel,
+            self.kernels_per_step = 18  # pad rows zeroed by dispatch / combine-bwd
         else:  # + demand transpose, staging relayouts / pad zeroing, run-based gate wgrad
             self.kernels_per_step = 8 + 13 + (1 if k > 1 else 0)
         self.reset_stats()

@@ -639,7 +639,7 @@ class Layer {
     const P2P p = p2p_args(0);
     launch_dispatch(x, cur_T_, cfg_.d_model, cfg_.top_k, cfg_.num_experts, cfg_.num_gpus, cfg_.rank, false,
                     topk_idx_.as<int32_t>(), tile_rank_.as<int32_t>(), tile_base_.as<int32_t>(), plan_,
-                    pos_.as<int32_t>(), nullptr, nullptr, s, &p);
+                    pos_.as<int32_t>(), nullptr, nullptr, s, &p, x_perm_.p, nl());  // + own pad rows
     timer_.end(s);
   }
   ArrivalGate p2p_gate(int slot) {
@@ -654,7 +654,6 @@ class Layer {
   // whose rows the tile holds, so local rows (route() keeps them local first)
   // compute while remote ones are still arriving over NVLink.
   void expert_forward_p2p(const void* w1, const float* b1, const void* w2, const float* b2, cudaStream_t s) {
-    launch_zero_pad(x_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);  // own pad rows only
     const ArrivalGate gate = p2p_gate(0);
     expert_forward(w1, b1, w2, b2, s, &gate);
     p2p_signal(1, s);
@@ -671,14 +670,14 @@ class Layer {
     timer_.begin(FM_PHASE_COMBINE_BWD, s);
     const P2P p = p2p_args(2);
     launch_combine_bwd(dy, y_perm_.p, pos_.as<int32_t>(), topk_w_.as<float>(), cur_T_, cfg_.d_model, cfg_.top_k,
-                       dy_perm_.p, dl_.as<float>(), gate_grad ? dl_rows_.as<float>() : nullptr, s, &p);
+                       dy_perm_.p, dl_.as<float>(), gate_grad ? dl_rows_.as<float>() : nullptr, s, &p, &plan_,
+                       nl());  // trailing blocks zero this GPU's dY_perm pad rows
     timer_.end(s);
   }
   // dwg (optional) receives this GPU's share of the gate-weight gradient: its
   // hosted units (dl-weighted X_perm tile sums), to be summed over all GPUs.
   void expert_backward_p2p(const void* w1, const void* w2, float* dw1, float* db1, float* dw2, float* db2,
                            float* dwg, cudaStream_t s) {
-    launch_zero_pad(dy_perm_.p, cfg_.d_model, plan_, nl(), nullptr, s);
     const bool dwg_tiles = dwg && cfg_.top_k > 1 && nl() > 0;
     if (dwg && !dwg_tiles)
       FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * cfg_.num_experts * cfg_.d_model, s));
