@@ -17,9 +17,12 @@ def test_cpp_host_driver_runs_the_p2p_step():
     exe = ROOT / "host" / "bin" / "flexmoe_step"
     if not exe.exists():  # built by __graft_entry__.build() / make -C host driver
         subprocess.run(["make", "-C", str(ROOT / "host"), "driver"], check=True, capture_output=True)
-    res = subprocess.run([str(exe), "--gpus", "1", "--steps", "5", "--warmup", "2", "--experts", "16",
-                          "--topk", "2", "--tokens", "8192", "--replicate", "2"],
-                         capture_output=True, text=True, timeout=240)
+    cmd = [str(exe), "--gpus", "1", "--steps", "5", "--warmup", "2", "--experts", "16", "--topk", "2",
+           "--tokens", "8192", "--replicate", "2"]
+    try:  # a run takes seconds; one retry covers a stalled NCCL socket bootstrap on the host
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=120)
+    except subprocess.TimeoutExpired:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=120)
     assert res.returncode == 0, res.stderr
     line = json.loads(res.stdout.strip().splitlines()[-1])
     assert line["p2p_timeouts"] == 0
