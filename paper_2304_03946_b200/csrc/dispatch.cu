@@ -786,7 +786,7 @@ __global__ void demand_transpose_kernel(const int64_t* __restrict__ gathered_GN,
 // 128-row aligned, so a tile belongs to one expert): partial[tile][c] =
 // sum over the tile's real rows r of w[r] * buf[r][c] (w = 1 when row_w is
 // null). Job 0 / 1 in blockIdx.y (e.g. dWg from X_perm with dl per row, db2
-// from dY_perm). Thread = 8 columns (16-byte loads), 8 rows in flight.
+// from dY_perm). Thread = 8 columns (16-byte loads), 32 rows in flight.
 // Plain stores, then segment_tile_reduce: deterministic, no atomics.
 struct TileSumJob {
   const __nv_bfloat16* buf;
@@ -810,7 +810,9 @@ __global__ void __launch_bounds__(256) segment_tile_colsum_kernel(TileSumJob j0,
   const int c8 = threadIdx.x * 8;
   if (c8 >= cols) return;
   float acc[8] = {};
-  constexpr int kB = 8;
+  // 32 rows in flight: a block's 128 rows are 4 dependent DRAM round trips
+  // (8 in flight: 16), which matters when few tiles fill the GPU (top-1)
+  constexpr int kB = 32;
   for (int rb = r0; rb < r1; rb += kB) {
     uint4 v[kB];
     float w[kB];
