@@ -568,7 +568,11 @@ def run_ours(args, world, rank, local_rank):
                    "zipf": cfg["zipf"], "units_per_step_rank0": units,
                    "expert_load_max_over_mean": float(hist.max() / max(hist.mean(), 1e-9)),
                    "placement": "dynamic" if multi else "static",
-                   "l2": "per-step working set > L2 (no flush)"},
+                   "l2": "per-step working set > L2 (no flush)",
+                   "step": ("gate top-k + histogram, route + plan, dispatch, expert FFN, combine; backward "
+                            "of all of it incl. dx and every weight / bias / gate-weight gradient"
+                            + (", replica-group gradient all-reduce" if multi else "")
+                            + " (the BASELINE metric is the layer's fwd+bwd; the optimizer is outside it)")},
         "e2e": {"value": T * world / (e2e_ms * 1e-3 / args.steps), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(2 * T * d * 2), "d2h_bytes_per_step": int(N * 8)},
         "gpu_launches": arm.kernels_per_step * args.steps,
