@@ -184,11 +184,17 @@ def run_reference_arm(args, world, rank):
     # the same workload our arm runs at this N (configs[1] at 1 GPU, configs[2..4] otherwise)
     multi = world > 1 or args.workload in WORKLOADS
     cfg = dict(WORKLOADS[args.workload or "cfg3"] if multi else CFG2)
-    # whole run bounded to ~2 minutes of host work: per-step sample sized to it
-    budget = max(0.25, 120.0 / max(1, args.steps + args.warmup))
-    t_small, hist = cpu_layer_sample(cfg, 256)
-    tokens = max(128, int(256 * budget / max(t_small, 1e-3)) // 128 * 128)
-    tokens = min(tokens, 16384)
+    # whole run bounded to ~3 minutes of host work: the per-step sample is the
+    # largest that fits, from a two-point fit t(n) = a + b*n (the port has a
+    # per-step cost that does not shrink with n: every expert's weights are read)
+    budget = max(0.5, 180.0 / max(1, args.steps + args.warmup))
+    cpu_layer_sample(cfg, 256)  # warm the weights cache
+    t1, _ = cpu_layer_sample(cfg, 256)
+    t2, _ = cpu_layer_sample(cfg, 1024)
+    b = max((t2 - t1) / 768.0, 1e-7)
+    a_fixed = max(t1 - 256 * b, 0.0)
+    tokens = int((budget - a_fixed) / b) // 128 * 128
+    tokens = min(max(tokens, 256), 16384)
     ref = oracle.Reference() if oracle.Reference.available() else None
     times = []
     for i in range(args.warmup + args.steps):
