@@ -60,6 +60,8 @@ PLACEMENTS = {
     # configs[2]-like width: N*G = 512 > the plan kernel's 256 threads (multi-
     # element scans), a hot expert on four GPUs
     "wide_8gpus": (64, 8, [(e, e % 8) for e in range(64)] + [(0, 1), (0, 2), (0, 3), (5, 0), (9, 7)]),
+    # a GPU that hosts no expert: it only sends its tokens and receives outputs
+    "idle_gpu": (8, 4, [(e, e % 3) for e in range(8)] + [(0, 1)]),
 }
 
 
@@ -185,3 +187,46 @@ def test_phase_api_single_gpu_matches_fused():
     assert torch.equal(g1.dx, g2.dx)
     for a, b in [(g1.dw1, g2.dw1), (g1.dw2, g2.dw2), (g1.db1, g2.db1)]:
         assert torch.allclose(a, b, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_multigpu_rank_without_tokens(transport):
+    """Ragged ranks: GPU 1 contributes no tokens this step but hosts experts —
+    it still receives GPU 0's units, computes them and returns the outputs;
+    GPU 0's y / dx equal the single-GPU step on its tokens (bit-identical),
+    GPU 1's are empty."""
+    N, k, d, f, G = 8, 2, 256, 512, 2
+    Ts = [700, 0]
+    cnt = np.zeros((N, G), np.int32)
+    for e in range(N):
+        cnt[e, e % G] = 1
+    cnt[0, 1] = 1
+    rng = np.random.default_rng(21)
+    x, wg, w1, b1, w2, b2 = OL.exact_inputs(rng, Ts[0], d, N, f)
+    dY = OL.bf16(rng.standard_normal((Ts[0], d)) * 0.5)
+    bf = torch.bfloat16
+    dev = lambda a, dt=bf: torch.tensor(np.asarray(a), dtype=dt, device="cuda")
+    single = MoELayer(N, k, d, f, max_tokens=Ts[0])
+    y1 = single.forward(dev(x), dev(wg), dev(w1), dev(b1, torch.float32), dev(w2), dev(b2, torch.float32))
+    g1 = single.backward(dev(dY))
+    torch.cuda.synchronize()
+    hub = LoopbackHub(G)
+
+    def rank_fn(r):
+        torch.cuda.set_device(0)
+        lay = MoELayer(N, k, d, f, replica_counts=cnt, num_gpus=G, rank=r, max_tokens=max(Ts))
+        loc = lay.local_experts
+        dl = DistributedMoELayer(lay, hub.endpoint(r), transport=transport)
+        xr = dev(x) if r == 0 else torch.empty(0, d, dtype=bf, device="cuda")
+        dyr = dev(dY) if r == 0 else torch.empty(0, d, dtype=bf, device="cuda")
+        y = dl.forward(xr, dev(wg), dev(w1[loc]), dev(b1[loc], torch.float32), dev(w2[loc]),
+                       dev(b2[loc], torch.float32))
+        g = dl.backward(dyr)
+        torch.cuda.synchronize()
+        if transport == "p2p":
+            assert not dl.p2p_timed_out()
+        return y.clone(), g.dx.clone()
+
+    outs = run_ranks(G, rank_fn)
+    assert torch.equal(outs[0][0], y1) and torch.equal(outs[0][1], g1.dx)
+    assert outs[1][0].shape == (0, d) and outs[1][1].shape == (0, d)
