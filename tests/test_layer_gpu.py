@@ -61,6 +61,9 @@ CASES = [
     (16, 2, 768, 3072, 2048, "zipf"),
     (8, 2, 256, 256, 1, None),
     (8, 1, 256, 256, 31, None),
+    # the widest d_model the row kernels take (16-byte vectors, VPL 8) and VPL 6
+    (8, 2, 2048, 512, 300, None),
+    (8, 2, 1536, 256, 200, "zipf"),
 ]
 
 
