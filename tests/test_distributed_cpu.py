@@ -218,3 +218,36 @@ def test_p2p_migration_transport_gloo():
     (ra0, rb0), (ra1, rb1) = _spawn(_p2p_body)
     assert torch.equal(ra0, torch.full((4, 3), 2.0)) and torch.equal(ra1, torch.full((4, 3), 1.0))
     assert torch.equal(rb0, torch.arange(5.0) + 10) and torch.equal(rb1, torch.arange(5.0))
+
+
+# three GPUs, four distinct replica groups ({0,1}, {1,2}, {0,2}, {0,1,2}): with a
+# two-entry communicator cache every step evicts groups that some ranks are not
+# members of (torch hands non-members a placeholder, not a process group)
+CNT3 = np.array([[1, 1, 0], [0, 1, 1], [1, 0, 1], [1, 1, 1], [1, 0, 0]], np.int32)
+
+
+def _evict_body(rank, world):
+    ex = TorchExchange(max_live_groups=2)
+    local = [e for e in range(CNT3.shape[0]) if CNT3[e, rank] > 0]
+    outs = []
+    for step in range(2):
+        g = _Grads(len(local), CNT3.shape[0], 4, 8, seed=10 * step + rank)
+        before = {k: getattr(g, k).numpy().copy() for k in ("dw1", "db1", "dw2", "db2")}
+        sync_replica_grads(ex, CNT3, local, g)
+        outs.append((before, {k: getattr(g, k).numpy().copy() for k in before}))
+    return local, outs, ex.groups.misses  # numpy: tensors in the queue outlive the worker
+
+
+@pytest.mark.timeout(300)
+def test_replica_grad_sync_group_eviction_gloo():
+    res = _spawn(_evict_body, world=3)
+    for step in range(2):
+        for e in range(CNT3.shape[0]):
+            members = [r for r in range(3) if CNT3[e, r] > 0]
+            if len(members) < 2:
+                continue
+            for k in ("dw1", "db1", "dw2", "db2"):
+                s = sum(res[r][1][step][0][k][res[r][0].index(e)] for r in members)
+                for r in members:
+                    assert np.allclose(res[r][1][step][1][k][res[r][0].index(e)], s, atol=1e-5)
+    assert all(m == 8 for _, _, m in res)  # 4 groups x 2 steps, cache of 2: every touch misses
