@@ -125,6 +125,12 @@ class Exchange:
         group in the same order; ranks outside the group pass t=None."""
         raise NotImplementedError
 
+    def all_reduce_many(self, ts, group: tuple[int, ...]) -> None:
+        """SUM of several tensors over one replica group (ts = None on ranks
+        outside it); the same call order rules as all_reduce."""
+        for t in (ts if ts is not None else [None] * 4):
+            self.all_reduce(t, group)
+
     def sync_group(self, group: tuple[int, ...]) -> None:
         """Called on EVERY rank, in ascending expert id, for every replica group
         (group creation is collective over the world in torch.distributed)."""
@@ -205,6 +211,21 @@ class TorchExchange(Exchange):
             self.dist.all_reduce(t)
         elif t is not None and self.rank in group:
             self.dist.all_reduce(t, group=self.groups.get(group))
+
+    def all_reduce_many(self, ts, group):
+        """One NCCL group launch for an expert's four gradient slices (NCCL:
+        coalesced; other backends: one call each)."""
+        if ts is None or self.rank not in group:
+            return
+        pg = self.groups.get(group)
+        if (ts[0].is_cuda and hasattr(self.dist, "_coalescing_manager")
+                and self.dist.get_backend(pg) == "nccl"):
+            with self.dist._coalescing_manager(group=pg, device=ts[0].device):
+                for t in ts:
+                    self.dist.all_reduce(t, group=pg)
+        else:
+            for t in ts:
+                self.dist.all_reduce(t, group=pg)
 
 
 class LoopbackHub:
@@ -545,10 +566,8 @@ def sync_replica_grads(ex: Exchange, replica_counts, local_experts, g):
         ex.sync_group(grp)
         if ex.rank in grp:
             i = li[e]
-            for t in (g.dw1[i], g.db1[i], g.dw2[i], g.db2[i]):
-                ex.all_reduce(t, grp)
+            ex.all_reduce_many([g.dw1[i], g.db1[i], g.dw2[i], g.db2[i]], grp)
         else:  # non-members take part in the same calls (loopback rendezvous)
-            for _ in range(4):
-                ex.all_reduce(None, grp)
+            ex.all_reduce_many(None, grp)
     ex.all_reduce(g.dwg, None)
     return g
