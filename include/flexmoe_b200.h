@@ -372,8 +372,8 @@ int fm_layer_unpermute_backward(fm_layer* layer, const void* dback_buf, const vo
  *   fm_layer_gate            (as above; advances the exchange epoch)
  *   host: all-gather hist_out -> gathered [G][N]
  *   fm_layer_route_p2p       route() + plan incl. every peer's X_perm layout (no host sync)
- *   fm_layer_dispatch_p2p    x rows -> the expert GPUs' X_perm; flags
- *   fm_layer_expert_forward_p2p   wait for all sources, FFN, flag "Y ready"
+ *   fm_layer_dispatch_p2p    x rows -> the expert GPUs' X_perm (+ own pad rows); flags
+ *   fm_layer_expert_forward_p2p   FFN (each tile waits for its sources), flag "Y ready"
  *   fm_layer_combine_p2p     wait, y = sum_j w_j Y rows read from the expert GPUs
  *   fm_layer_combine_backward_p2p  dY rows (+ gate dl) -> the expert GPUs' dY_perm; flags
  *   fm_layer_expert_backward_p2p   wait, dgrad, flag "dX ready", weight grads; dwg gets this
