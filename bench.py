@@ -529,6 +529,8 @@ def run_ours(args, world, rank, local_rank):
         traffic = json.loads(tp.read_text()).get("bytes_per_launch")
     hbm_bytes = {  # algorithmic bytes per step
         "gate": T * d * 2 + N * d * 2 + units * 12,
+        # expert scan: per-128-token-tile expert counts in, tile bases out (+ histogram)
+        "scan": 2 * (-(-T // 128)) * N * 4 + N * 8,
         "dispatch": T * d * 2 + units * d * 2 + units * 4,
         "combine_fwd": units * (d * 2 + 8) + T * d * 2,
         "combine_bwd": T * d * 2 + units * (d * 2 * 2 + 12),
