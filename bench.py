@@ -282,6 +282,11 @@ class FusedArm:
     def hist_async(self, host):
         return self.layer.copy_out_async("hist", host)
 
+    def check(self):
+        """Raise if a device-side P2P arrival wait gave up during the run."""
+        if getattr(self, "transport", None) == "p2p" and self.dl.p2p_timed_out():
+            raise RuntimeError("P2P arrival wait timed out: the measured steps are invalid")
+
 
 def measured_tps(N, k, d, f):
     """(TPS, source): the committed B200 measurement for this model shape, if any."""
@@ -381,6 +386,11 @@ class DistArm:
 
     def hist_async(self, host):
         return self.layer.copy_out_async("hist", host)
+
+    def check(self):
+        """Raise if a device-side P2P arrival wait gave up during the run."""
+        if getattr(self, "transport", None) == "p2p" and self.dl.p2p_timed_out():
+            raise RuntimeError("P2P arrival wait timed out: the measured steps are invalid")
 
     def summary(self, steps):
         return {"placement": "dynamic (host scheduler: expand/shrink/migrate, B200 profile)",
@@ -505,6 +515,7 @@ def run_ours(args, world, rank, local_rank):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
+    arm.check()
     if any(u != units for u in seen_units):  # every step's histogram read back holds T*k units
         raise RuntimeError(f"e2e: histogram read-back {seen_units[:4]}... != {units} units per step")
     if dist:
