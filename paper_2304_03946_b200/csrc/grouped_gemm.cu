@@ -401,7 +401,11 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       ptx::mbar_wait(&tfull_bar[ab], (iter >> 1) & 1);
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + ab * kBN + col0;
+#ifdef FM_DEBUG_NO_TMEM_LD
+      const bool empty_k = true;  // diagnostic build: the epilogue skips its TMEM reads
+#else
       const bool empty_k = tl.num_kb == 0;
+#endif
       uint32_t ra[32], rb[32];
       uint32_t relu_bits[kChunks];
       // Output staging: this warp's 32 rows x 64 B go to a swizzled smem box
