@@ -210,6 +210,13 @@ __device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g, const 
   return tl;
 }
 
+// relu + round to a bf16 pair in one instruction (lo in the low half)
+__device__ __forceinline__ uint32_t pack_relu_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -466,13 +473,25 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
           for (int i = 0; i < 32; ++i) v[i] += bs[col0 + c * 32 + i];
         }
         if (EPI == kEpiBiasRelu) {
+          // ReLU, bf16 rounding and the mask bits from the rounded pairs: bit =
+          // (bf16(relu(h)) != 0), i.e. h > 0 unless h rounds to zero in bf16
+          // (|h| below the smallest bf16 subnormal) — the bit the backward needs
+          // for the stored activation
+          uint32_t w[16];
           uint32_t bits = 0;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            bits |= (v[i] > 0.0f ? 1u : 0u) << i;
-            v[i] = fmaxf(v[i], 0.0f);
+          for (int j = 0; j < 16; ++j) {
+            w[j] = pack_relu_bf16(v[2 * j], v[2 * j + 1]);
+            const uint32_t nz = __vcmpne2(w[j], 0u) & 0x00010001u;  // bit 0: low half, bit 16: high
+            bits |= ((nz | (nz >> 15)) & 3u) << (2 * j);
           }
           relu_bits[c] = bits;
+          uint8_t* buf = stage_begin();
+          const uint4 p[4] = {make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]),
+                              make_uint4(w[8], w[9], w[10], w[11]), make_uint4(w[12], w[13], w[14], w[15])};
+          stage_row(buf, p);
+          stage_commit(buf, col, tl.m0 + q * 32);
+          return;
         }
         if (EPI == kEpiReluMask) {
 #pragma unroll
