@@ -324,14 +324,21 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
-    if (lane == 0 && leader) {
+    // The whole warp runs the loop (its state is warp-uniform, so descriptors
+    // live in uniform registers) and one elected lane issues: a lane-0-only
+    // loop costs ~20 instructions of register->uniform shuffling per MMA, issue
+    // slots the epilogue warps on this SM sub-partition compete for.
+    if (leader) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::kTileM, kBN, A_MN, B_MN);
       constexpr uint32_t a_lbo = A_MN ? kMnChunkBytes : 16;
       constexpr uint32_t b_lbo = B_MN ? kMnChunkBytes : 16;
       // Advance per UMMA_K=16 step: 32 B inside a K-major swizzle row,
-      // 16 K-rows (2 KB) for MN-major.
+      // 16 K-rows (2 KB) for MN-major. Descriptor start addresses are in
+      // 16-byte units (bits 0-13): stage / k-step offsets are plain adds.
       constexpr uint32_t a_kstep = A_MN ? 16 * 128 : 32;
       constexpr uint32_t b_kstep = B_MN ? 16 * 128 : 32;
+      const uint64_t da0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_a), a_lbo, 1024);
+      const uint64_t db0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_b), b_lbo, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int iter = 0;
@@ -347,24 +354,29 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
-          const uint32_t sb = ptx::smem_u32(smem_b + stage * C::kBBytes);
+          const uint64_t da = da0 + static_cast<uint32_t>((stage * kABytes) >> 4);
+          const uint64_t db = db0 + static_cast<uint32_t>((stage * C::kBBytes) >> 4);
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t da = ptx::umma_desc_sw128(sa + k * a_kstep, a_lbo, 1024);
-            const uint64_t db = ptx::umma_desc_sw128(sb + k * b_kstep, b_lbo, 1024);
-            if (CG == 1) ptx::mma_bf16_ss(d_tmem, da, db, idesc, (kb | k) != 0);
-            else ptx::mma_bf16_ss_pair(d_tmem, da, db, idesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t dak = da + ((k * a_kstep) >> 4), dbk = db + ((k * b_kstep) >> 4);
+              if (CG == 1) ptx::mma_bf16_ss(d_tmem, dak, dbk, idesc, (kb | k) != 0);
+              else ptx::mma_bf16_ss_pair(d_tmem, dak, dbk, idesc, (kb | k) != 0);
+            }
+            if (CG == 1) ptx::mma_commit(&empty_bar[stage]);
+            else ptx::mma_commit_pair(&empty_bar[stage], 0x3);
           }
-          if (CG == 1) ptx::mma_commit(&empty_bar[stage]);
-          else ptx::mma_commit_pair(&empty_bar[stage], 0x3);
+          __syncwarp();
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (CG == 1) ptx::mma_commit(&tfull_bar[ab]);
-        else ptx::mma_commit_pair(&tfull_bar[ab], 0x3);
+        if (ptx::elect_one()) {
+          if (CG == 1) ptx::mma_commit(&tfull_bar[ab]);
+          else ptx::mma_commit_pair(&tfull_bar[ab], 0x3);
+        }
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {
