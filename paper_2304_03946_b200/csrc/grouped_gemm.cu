@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer (every CTA)
-    if (lane == 0) {
+    // Whole warp, one elected lane issues (as for the MMA issuer below).
+    {
       // CG == 2: both CTAs' loads complete on the leader's full barrier
       const uint32_t lead_full = CG == 2 ? ptx::mapa(ptx::smem_u32(full_bar), 0) : 0;
       int stage = 0;
@@ -294,27 +295,31 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
         }
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes * CG);
-          uint8_t* sa = smem_a + stage * kABytes;
-          uint8_t* sb = smem_b + stage * C::kBBytes;
-          const int k0 = kb * kBK;
-          auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
-            if (CG == 1) ptx::tma_load_2d(dst, m, &full_bar[stage], c0, c1);
-            else ptx::tma_load_2d_2sm(dst, m, lead_full + stage * 8, c0, c1);
-          };
-          if (!A_MN) {
-            load(sa, &map_a, k0, tl.m0);
-          } else {
+          if (ptx::elect_one()) {
+            if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes * CG);
+            uint8_t* sa = smem_a + stage * kABytes;
+            uint8_t* sb = smem_b + stage * C::kBBytes;
+            const int k0 = kb * kBK;
+            auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+              if (CG == 1) ptx::tma_load_2d(dst, m, &full_bar[stage], c0, c1);
+              else ptx::tma_load_2d_2sm(dst, m, lead_full + stage * 8, c0, c1);
+            };
+            if (!A_MN) {
+              load(sa, &map_a, k0, tl.m0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < kBM / 64; ++j) load(sa + j * kMnChunkBytes, &map_a, tl.m0 + j * 64, tl.k_row0 + k0);
-          }
-          if (!B_MN) {
-            load(sb, &map_b, k0, b_row_base + n_cta);
-          } else {
-            const int krow = (SCHED == kRows) ? b_row_base + k0 : tl.k_row0 + k0;
+              for (int j = 0; j < kBM / 64; ++j)
+                load(sa + j * kMnChunkBytes, &map_a, tl.m0 + j * 64, tl.k_row0 + k0);
+            }
+            if (!B_MN) {
+              load(sb, &map_b, k0, b_row_base + n_cta);
+            } else {
+              const int krow = (SCHED == kRows) ? b_row_base + k0 : tl.k_row0 + k0;
 #pragma unroll
-            for (int j = 0; j < C::kBNc / 64; ++j) load(sb + j * kMnChunkBytes, &map_b, n_cta + j * 64, krow);
+              for (int j = 0; j < C::kBNc / 64; ++j) load(sb + j * kMnChunkBytes, &map_b, n_cta + j * 64, krow);
+            }
           }
+          __syncwarp();
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
