@@ -93,52 +93,57 @@ __global__ void __launch_bounds__(kThreads, 2)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
+  // producer and MMA issuer: the whole warp runs the (warp-uniform) loop, one
+  // elected lane issues — no per-instruction register->uniform shuffles
   if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (ptx::elect_one()) {
           ptx::mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
           ptx::tma_load_2d(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM);
           ptx::tma_load_2d(smem_b + stage * b_bytes, &map_w, &full_bar[stage], kb * kBK, 0);
-          if (++stage == a.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == a.stages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = ptx::idesc_bf16_f32(kTM, a.Npad, false, false);
-      int stage = 0;
-      uint32_t phase = 0;
-      int iter = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
-        const int ab = iter & 1;
-        ptx::mbar_wait(&tempty_bar[ab], ((iter >> 1) & 1) ^ 1);
+    const uint32_t idesc = ptx::idesc_bf16_f32(kTM, a.Npad, false, false);
+    const uint64_t da0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_a), 16, 1024);
+    const uint64_t db0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_b), 16, 1024);
+    int stage = 0;
+    uint32_t phase = 0;
+    int iter = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+      const int ab = iter & 1;
+      ptx::mbar_wait(&tempty_bar[ab], ((iter >> 1) & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + ab * a.Npad;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        ptx::mbar_wait(&full_bar[stage], phase);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + ab * a.Npad;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&full_bar[stage], phase);
-          ptx::tc_fence_after();
-          const uint32_t sa = ptx::smem_u32(smem_a + stage * kABytes);
-          const uint32_t sb = ptx::smem_u32(smem_b + stage * b_bytes);
+        // descriptor start addresses are in 16-byte units: offsets are adds
+        const uint64_t da = da0 + static_cast<uint32_t>((stage * kABytes) >> 4);
+        const uint64_t db = db0 + static_cast<uint32_t>((stage * b_bytes) >> 4);
+        if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            ptx::mma_bf16_ss(d_tmem, ptx::umma_desc_sw128(sa + k * 32, 16, 1024),
-                             ptx::umma_desc_sw128(sb + k * 32, 16, 1024), idesc, (kb | k) != 0);
-          }
+          for (int k = 0; k < kBK / 16; ++k) ptx::mma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
           ptx::mma_commit(&empty_bar[stage]);
-          if (++stage == a.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        ptx::mma_commit(&tfull_bar[ab]);
+        __syncwarp();
+        if (++stage == a.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      if (ptx::elect_one()) ptx::mma_commit(&tfull_bar[ab]);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
