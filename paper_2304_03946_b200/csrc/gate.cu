@@ -32,6 +32,10 @@ constexpr int kMaxExperts = 256;
 constexpr int kMaxTopK = 8;
 constexpr int kABytes = kTM * kBK * 2;
 constexpr int kThreads = 256;
+#ifndef FM_GATE_CTAS
+#define FM_GATE_CTAS 2
+#endif
+constexpr int kCtas = FM_GATE_CTAS;  // resident CTAs per SM (A/B knob)
 
 struct Args {
   int T, N, Npad, K, top_k, stages;
@@ -49,7 +53,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 // Two CTAs per SM: the per-tile chain (TMA -> MMA -> top-k epilogue) is
 // latency-bound, a second resident CTA overlaps it (measured: 1.3x over one).
 template <int KT>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, kCtas)
     gate_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                 const Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -258,7 +262,7 @@ void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, 
   const int Npad = ((N + 31) / 32) * 32;
   const int stage_bytes0 = kABytes + Npad * kBK * 2;
   // two CTAs per SM when both TMEM double-buffers fit (2 x 2 x Npad <= 512 columns)
-  const int kCtasPerSm = Npad <= 128 ? 2 : 1;
+  const int kCtasPerSm = Npad * kCtas <= 256 ? kCtas : (Npad <= 128 ? 2 : 1);
   const int stages = std::max(2, std::min(kMaxStages, (200 * 1024 / kCtasPerSm) / stage_bytes0));
   Args a{T, N, Npad, d, top_k, stages, topk_idx, topk_w, tile_rank, tile_counts};
   CUtensorMap mx = make_tmap_bf16(x, d, T, d, 64, kTM);
