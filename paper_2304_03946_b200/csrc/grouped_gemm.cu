@@ -118,6 +118,10 @@ __device__ __forceinline__ void wait_tile_sources(const Args& a, int mtile) {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+#ifndef FM_WGRAD_HINT
+#define FM_WGRAD_HINT 0
+#endif
+
 struct Tile {
   int group;
   int m0;      // this CTA's first row (kRows: token row; kWgrad: output row)
@@ -281,6 +285,11 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     {
       // CG == 2: both CTAs' loads complete on the leader's full barrier
       const uint32_t lead_full = CG == 2 ? ptx::mapa(ptx::smem_u32(full_bar), 0) : 0;
+      // A/B knob FM_WGRAD_HINT (wgrad only): 1 = A operand evict_last, B evict_first;
+      // 2 = the reverse; 0 (default) = no hint
+      constexpr bool kHint = FM_WGRAD_HINT != 0;
+      const uint64_t pol_a = FM_WGRAD_HINT == 1 ? ptx::l2_policy_evict_last() : ptx::l2_policy_evict_first();
+      const uint64_t pol_b = FM_WGRAD_HINT == 1 ? ptx::l2_policy_evict_first() : ptx::l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       int g = 0;
@@ -301,8 +310,15 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
             uint8_t* sb = smem_b + stage * C::kBBytes;
             const int k0 = kb * kBK;
             auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
-              if (CG == 1) ptx::tma_load_2d(dst, m, &full_bar[stage], c0, c1);
-              else ptx::tma_load_2d_2sm(dst, m, lead_full + stage * 8, c0, c1);
+              if (kHint && SCHED == kWgrad) {
+                const uint64_t pol = m == &map_a ? pol_a : pol_b;
+                if (CG == 1) ptx::tma_load_2d_hint(dst, m, &full_bar[stage], c0, c1, pol);
+                else ptx::tma_load_2d_2sm_hint(dst, m, lead_full + stage * 8, c0, c1, pol);
+              } else if (CG == 1) {
+                ptx::tma_load_2d(dst, m, &full_bar[stage], c0, c1);
+              } else {
+                ptx::tma_load_2d_2sm(dst, m, lead_full + stage * 8, c0, c1);
+              }
             };
             if (!A_MN) {
               load(sa, &map_a, k0, tl.m0);
