@@ -262,7 +262,12 @@ void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, 
   const int Npad = ((N + 31) / 32) * 32;
   const int stage_bytes0 = kABytes + Npad * kBK * 2;
   // two CTAs per SM when both TMEM double-buffers fit (2 x 2 x Npad <= 512 columns)
-  const int kCtasPerSm = Npad * kCtas <= 256 ? kCtas : (Npad <= 128 ? 2 : 1);
+#ifndef FM_GATE_WIDE_CTAS
+#define FM_GATE_WIDE_CTAS 2
+#endif
+  // Npad >= 128: FM_GATE_WIDE_CTAS per SM (A/B knob: 1 CTA gets twice the stages)
+  const int kCtasPerSm = Npad >= 128 ? (Npad == 128 ? FM_GATE_WIDE_CTAS : 1)
+                                     : (Npad * kCtas <= 256 ? kCtas : 2);
   const int stages = std::max(2, std::min(kMaxStages, (200 * 1024 / kCtasPerSm) / stage_bytes0));
   Args a{T, N, Npad, d, top_k, stages, topk_idx, topk_w, tile_rank, tile_counts};
   CUtensorMap mx = make_tmap_bf16(x, d, T, d, 64, kTM);
