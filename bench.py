@@ -52,8 +52,8 @@ def measured_peaks():
     if p.exists():
         j = json.loads(p.read_text())
         return dict(hbm=j["hbm_gbs"], bf16=j["bf16_tflops"], bf16_sus=j["bf16_tflops_sustained"],
-                    source="measured")
-    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, source="fallback")
+                    sus_mhz=j.get("clocks_under_load", {}).get("sm_mhz_median"), source="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, sus_mhz=None, source="fallback")
 
 
 def zipf_log_popularity(N, s, seed):
@@ -61,6 +61,43 @@ def zipf_log_popularity(N, s, seed):
     p = 1.0 / np.arange(1, N + 1) ** s
     p = p / p.sum()
     return np.log(p)[rng.permutation(N)]
+
+
+def bench_inputs(cfg, rank=0):
+    """The bench's synthetic inputs on the host: gate weight [N, d] f32 (random
+    init of the architecture; column 0 = 2 * Zipf log-popularity, so the skew
+    is produced by the real gate — x[:, 0] = 0.5), x and dy [T, d] bf16 for
+    `rank`, and the generator that drew them (the e2e leg draws its second
+    input buffer from it). tests/test_gate_real_gpu.py uses the same inputs."""
+    import torch
+
+    N, d, T = cfg["N"], cfg["d"], cfg["T"]
+    g = torch.Generator(device="cpu").manual_seed(1234)
+    wg = torch.randn(N, d, generator=g) * d**-0.5
+    wg[:, 0] = torch.tensor(zipf_log_popularity(N, cfg["zipf"], 42) * 2, dtype=torch.float32)
+    gen = torch.Generator(device="cpu").manual_seed(100 + rank)
+    x = torch.randn(T, d, generator=gen).to(torch.bfloat16)
+    x[:, 0] = 0.5
+    dy = (torch.randn(T, d, generator=gen) * 0.1).to(torch.bfloat16)
+    return wg, x, dy, gen
+
+
+def line_config(cfg, world, multi):
+    """The `config` object of the JSON line — identical for both arms (the
+    reference arm runs the same workload on a bounded token sample per step,
+    described in its cpu_baseline.sample)."""
+    N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
+    return {"workload": cfg["workload"],
+            "model": f"MoE layer N{N} k{k} d{d} f{f}",
+            "global_batch": T * world, "tokens_per_gpu": T, "seq_len": None,
+            "parallelism": f"ep{world}" + ("+replicas" if multi else ""),
+            "zipf": cfg["zipf"],
+            "placement": "dynamic" if multi else "static",
+            "l2": "per-step working set > L2 (no flush)",
+            "step": ("gate top-k + histogram, route + plan, dispatch, expert FFN, combine; backward "
+                     "of all of it incl. dx and every weight / bias / gate-weight gradient"
+                     + (", replica-group gradient all-reduce" if multi else "")
+                     + " (the BASELINE metric is the layer's fwd+bwd; the optimizer is outside it)")}
 
 
 # ------------------------------------------------------------------ clocks
@@ -154,6 +191,46 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# BASELINE configs as the reference engine sees them: (N, G, k, tokens per GPU,
+# zipf, PolicyMode (0 Dynamic, 1 FixedInterval, 2 Static), interval)
+REF_CONFIGS = {
+    "configs[0]": (8, 4, 2, 1024, 1.25, 0, 10),
+    "configs[1]": (16, 1, 2, 65536, 1.25, 2, 10),
+    "configs[2]": (64, 8, 1, 65536, 1.25, 0, 10),
+    "configs[3]": (32, 8, 2, 65536, 1.25, 1, 100),
+    "configs[4]": (128, 8, 1, 32768, 2.0, 0, 10),
+}
+
+
+def reference_count_path(which=None, min_seconds=0.05):
+    """the reference's own count-level per-step path, timed
+    on ONE host thread from oracle/_ref (the unmodified moesim sources):
+    route (+balance_ratio), step_cost, make_scheduling_plan, plan_migrations
+    and one SimEngine step, per BASELINE config, in microseconds per call."""
+    import oracle
+
+    ref = oracle.Reference()
+    out = {}
+    for name, (N, G, k, T, z, mode, iv) in REF_CONFIGS.items():
+        if which is not None and name != which:
+            continue
+        trace = ref.generate_trace(N, G, T * k * G, zipf=z, steps=50)
+        slots = 2 * -(-N // G)
+        t = ref.time_count_path(trace, slots, mode, iv, min_seconds)
+        out[name] = {kk: round(v * 1e6, 2) for kk, v in t.items()}
+    return out
+
+
 def cpu_baseline(cfg, budget_s=12.0):
     t_small, _ = cpu_layer_sample(cfg, 512)
     tokens = int(min(16384, max(512, 512 * budget_s / max(t_small, 1e-3))))
@@ -161,17 +238,15 @@ def cpu_baseline(cfg, budget_s=12.0):
     secs, hist = cpu_layer_sample(cfg, tokens)
     out = {"value": tokens / secs, "unit": "tokens/s", "cores": host_threads(), "kind": "port",
            "sample": f"oracle/layer.py float64 numpy fwd+bwd of {tokens} tokens of the bench "
-                     f"workload ({secs:.1f} s); host nproc={os.cpu_count()}"}
+                     f"workload ({secs:.1f} s); host nproc={os.cpu_count()}, {cpu_model()}"}
     try:
         import oracle
 
         if oracle.Reference.available():
-            ref = oracle.Reference()
-            D = np.asarray(hist, np.int64).reshape(cfg["N"], 1) * (cfg["T"] // tokens)
-            cnt = np.ones((cfg["N"], 1), np.int32)
-            out["reference_route_us"] = ref.time_route(D, cnt, iters=2000) * 1e6
+            out["reference_count_path_us"] = reference_count_path()
+            out["reference_count_path_threads"] = 1
     except Exception as exc:  # reference shim optional on the box
-        out["reference_route_error"] = str(exc)[:100]
+        out["reference_count_path_error"] = str(exc)[:100]
     return out
 
 
@@ -184,6 +259,8 @@ def run_reference_arm(args, world, rank):
     # the same workload our arm runs at this N (configs[1] at 1 GPU, configs[2..4] otherwise)
     multi = world > 1 or args.workload in WORKLOADS
     cfg = dict(WORKLOADS[args.workload or "cfg3"] if multi else CFG2)
+    if cfg.get("scaling") == "strong":
+        cfg["T"] = cfg["T"] // world
     # whole run bounded to ~3 minutes of host work: the per-step sample is the
     # largest that fits, from a two-point fit t(n) = a + b*n (the port has a
     # per-step cost that does not shrink with n: every expert's weights are read)
@@ -195,34 +272,42 @@ def run_reference_arm(args, world, rank):
     a_fixed = max(t1 - 256 * b, 0.0)
     tokens = int((budget - a_fixed) / b) // 128 * 128
     tokens = min(max(tokens, 256), 16384)
-    ref = oracle.Reference() if oracle.Reference.available() else None
+    # the reference's own per-step count path (route, cost, policy, migration
+    # pass, queue drain: one SimEngine step) at this config, one thread
+    ref_name = {"cfg3": "configs[2]", "cfg4": "configs[3]", "cfg5": "configs[4]"}.get(
+        args.workload or "cfg3") if multi else "configs[1]"
+    count_path = reference_count_path(ref_name)[ref_name] if oracle.Reference.available() else {}
+    engine_s = count_path.get("engine_step", 0.0) * 1e-6
     times = []
     for i in range(args.warmup + args.steps):
         # timed: the layer math (cpu_layer_sample times its fwd+bwd only, not the
-        # synthetic input generation) and the reference's route() on the demand
-        secs, hist = cpu_layer_sample(cfg, tokens, seed=i)
-        if ref is not None:  # the reference's own per-step count path on the step demand
-            D = np.asarray(hist, np.int64).reshape(cfg["N"], 1)
-            t0 = time.perf_counter()
-            ref.route(D, np.ones((cfg["N"], 1), np.int32), 2 * cfg["N"])
-            secs += time.perf_counter() - t0
+        # synthetic input generation) + the reference's engine step
+        secs, _ = cpu_layer_sample(cfg, tokens, seed=i)
         if i >= args.warmup:
-            times.append(secs)
+            times.append(secs + engine_s)
     step = statistics.mean(times)
     value = tokens / step
-    kind = "port"
+    full_step_s = a_fixed + cfg["T"] * b + engine_s
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
             "higher_is_better": True, "scaling": cfg.get("scaling", "weak"), "vs_baseline": None,
-            "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": cfg["workload"], "tokens_per_step_sampled": tokens,
-                       "global_batch": cfg["T"], "parallelism": "cpu"},
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": line_config(cfg, world, multi),
+            "sample": {"tokens_per_step": tokens, "tokens_per_gpu_in_config": cfg["T"],
+                       "extrapolation": (f"tokens/s measured on {tokens} of the config's {cfg['T']} tokens per "
+                                         f"step; the layer math is linear in tokens (two-point fit: "
+                                         f"{a_fixed * 1e3:.1f} ms fixed + {b * 1e6:.1f} us/token), so the full "
+                                         f"step would take {full_step_s:.1f} s = "
+                                         f"{cfg['T'] / full_step_s:.0f} tokens/s"),
+                       "full_step_tokens_per_s_estimate": cfg["T"] / full_step_s},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": host_threads(),
-                             "kind": kind,
-                             "sample": f"{tokens} tokens/step: reference route() "
-                                       f"({'oracle/_ref' if ref else 'unavailable'}) + oracle "
-                                       "port of gate/FFN/combine fwd+bwd (float64 numpy)"},
+                             "kind": "port",
+                             "sample": f"{tokens} tokens/step of {cfg['T']}: the reference's own SimEngine step "
+                                       f"({'oracle/_ref' if count_path else 'unavailable'}, 1 thread, "
+                                       f"{count_path.get('engine_step', 0):.1f} us) + the oracle port of the "
+                                       "gate/FFN/combine fwd+bwd (float64 numpy, all host threads); "
+                                       f"host nproc={os.cpu_count()}, {cpu_model()}",
+                             "reference_count_path_us": {ref_name: count_path} if count_path else None},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -254,8 +339,7 @@ class FusedArm:
         N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
         self.layer = MoELayer(N, k, d, f, max_tokens=T)
         p = self.layer.init_params(seed=1234)
-        logp = torch.tensor(zipf_log_popularity(N, cfg["zipf"], 42), dtype=torch.float32)
-        p["wg"][:, 0] = (logp * 2).to(p["wg"].dtype).to(dev)  # skew through the real gate
+        p["wg"] = bench_inputs(dict(cfg, T=1))[0].to(dev).to(p["wg"].dtype)  # skew through the real gate
         self.P = (p["wg"], p["w1"], p["b1"], p["w2"], p["b2"])
         self.grads = None
         self.N, self.G = N, 1
@@ -322,10 +406,8 @@ class DistArm:
         import torch.distributed as tdist
 
         ex = TorchExchange() if tdist.is_initialized() else LoopbackHub(1).endpoint(0)
-        g = torch.Generator(device="cpu").manual_seed(1234)
-        wg = torch.randn(N, d, generator=g) * d**-0.5
+        wg = bench_inputs(dict(cfg, T=1))[0]
         self.logp = zipf_log_popularity(N, cfg["zipf"], 42)
-        wg[:, 0] = torch.tensor(self.logp * 2, dtype=torch.float32)
         sched_cfg = S.SchedulerConfig.defaults(policy_mode=cfg["policy_mode"], interval_steps=cfg["interval"])
         self.transport = cfg.get("transport", "p2p")
         self.rt = FlexMoERuntime(N, k, d, f, ex, prof, sched_cfg=sched_cfg, max_tokens=T, gate_weight=wg,
@@ -428,10 +510,7 @@ def run_ours(args, world, rank, local_rank):
     N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
     arm = DistArm(cfg, dev, rank, world) if multi else FusedArm(cfg, dev, rank)
 
-    gen = torch.Generator(device="cpu").manual_seed(100 + rank)
-    x_host = torch.randn(T, d, generator=gen).to(torch.bfloat16)
-    x_host[:, 0] = 0.5
-    dy_host = (torch.randn(T, d, generator=gen) * 0.1).to(torch.bfloat16)
+    _, x_host, dy_host, gen = bench_inputs(cfg, rank)
     x, dy = x_host.to(dev), dy_host.to(dev)
     stream = torch.cuda.current_stream()
 
@@ -562,7 +641,7 @@ def run_ours(args, world, rank, local_rank):
             ent.update({"achieved_GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3)})
         if name in gemm_names and per > 0:
             tf = 2.0 * recv_units * d * f / (per * 1e-3) / 1e12
-            ent.update({"achieved_TFLOPs": round(tf, 1), "frac_bf16": round(tf / peaks["bf16_sus"], 3)})
+            ent.update({"achieved_TFLOPs": round(tf, 1), "frac_bf16": round(tf / peaks["bf16"], 3)})
         kernels[name] = ent
     for name, (cms, n) in comm.items():
         kernels["comm_" + name] = {"ms_per_step": round(cms / args.steps, 4),
@@ -580,25 +659,28 @@ def run_ours(args, world, rank, local_rank):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights of the configs architecture; Zipf skew via the gate)",
-        "config": {"workload": cfg["workload"],
-                   "model": f"MoE layer N{N} k{k} d{d} f{f}",
-                   "global_batch": T * world, "tokens_per_gpu": T, "seq_len": None,
-                   "parallelism": f"ep{world}" + ("+replicas" if multi else ""),
-                   "zipf": cfg["zipf"], "units_per_step_rank0": units,
-                   "expert_load_max_over_mean": float(hist.max() / max(hist.mean(), 1e-9)),
-                   "placement": "dynamic" if multi else "static",
-                   "l2": "per-step working set > L2 (no flush)",
-                   "step": ("gate top-k + histogram, route + plan, dispatch, expert FFN, combine; backward "
-                            "of all of it incl. dx and every weight / bias / gate-weight gradient"
-                            + (", replica-group gradient all-reduce" if multi else "")
-                            + " (the BASELINE metric is the layer's fwd+bwd; the optimizer is outside it)")},
+        "config": line_config(cfg, world, multi),
+        "workload_stats": {"units_per_step_rank0": units,
+                           "expert_load_max_over_mean": float(hist.max() / max(hist.mean(), 1e-9))},
         "e2e": {"value": T * world / (e2e_ms * 1e-3 / args.steps), "unit": "tokens/s",
-                "h2d_bytes_per_step": int(2 * T * d * 2), "d2h_bytes_per_step": int(N * 8)},
+                "h2d_bytes_per_step": int(2 * T * d * 2), "d2h_bytes_per_step": int(N * 8),
+                "what": ("x and dy copied H2D from pinned host memory every step (prefetched one step "
+                         "ahead on a copy stream); the step's result read back D2H is the expert "
+                         "histogram (TokenDemand column, the placement policy's input), one step behind"),
+                "outputs_on_device": ("y and dx stay in HBM: in training they are the next layer's input "
+                                      "and the previous layer's output gradient, and the weight gradients "
+                                      "feed the on-device optimizer; copying them to the host would time "
+                                      "PCIe, not the layer")},
         "gpu_launches": arm.kernels_per_step * args.steps,
         "roofline": {"bound": "tensor", "kernel": "grouped_gemm (tcgen05, 6 launches/step)",
-                     "achieved": round(achieved, 1), "peak": peaks["bf16_sus"],
-                     "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_sus"], 4),
-                     "traffic": traffic, "peak_source": f"{peaks['source']} bf16 sustained",
+                     "achieved": round(achieved, 1), "peak": peaks["bf16"],
+                     "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16"], 4),
+                     "traffic": traffic, "peak_source": f"{peaks['source']} bf16 burst (MEASURED_PEAKS.json)",
+                     "frac_sustained": round(achieved / peaks["bf16_sus"], 4),
+                     "peak_sustained": peaks["bf16_sus"],
+                     "peak_note": ("frac is against the burst peak (cuBLAS at full clock); the sustained peak "
+                                   f"was measured at a {peaks.get('sus_mhz')} MHz median SM clock, this run's "
+                                   "median is in clocks.sm_mhz"),
                      "gemm_ms_per_step": round(gemm_ms, 4), "gemm_launches_per_step": gemm_launches},
         "kernels": kernels,
         "clocks": clocks.summary(),

@@ -260,8 +260,11 @@ int main(int argc, char** argv) {
     // one node: NCCL's bootstrap over loopback (avoids picking a slow or
     // unreachable interface on the box)
     setenv("NCCL_SOCKET_IFNAME", "lo", 0);
-    ncclUniqueId id;
-    nc(ncclGetUniqueId(&id), "ncclGetUniqueId");  // bootstrap root stays in this (parent) process
+    // No NCCL state in the parent before fork(): rank 0 creates the unique id
+    // (its bootstrap root thread lives in rank 0) and hands it to the other
+    // ranks through a pipe (one 128-byte write per peer, atomic below PIPE_BUF).
+    int idpipe[2];
+    if (pipe(idpipe) != 0) throw std::runtime_error("pipe failed");
     std::vector<pid_t> kids;
     for (int r = 0; r < a.gpus; ++r) {
       const pid_t pid = fork();
@@ -269,6 +272,24 @@ int main(int argc, char** argv) {
       if (pid == 0) {
         int rc = 1;
         try {
+          ncclUniqueId id;
+          if (r == 0) {
+            close(idpipe[0]);
+            nc(ncclGetUniqueId(&id), "ncclGetUniqueId");
+            for (int peer = 1; peer < a.gpus; ++peer)
+              if (write(idpipe[1], &id, sizeof(id)) != static_cast<ssize_t>(sizeof(id)))
+                throw std::runtime_error("unique id pipe write failed");
+            close(idpipe[1]);
+          } else {
+            close(idpipe[1]);
+            size_t got = 0;
+            while (got < sizeof(id)) {
+              const ssize_t n = read(idpipe[0], reinterpret_cast<char*>(&id) + got, sizeof(id) - got);
+              if (n <= 0) throw std::runtime_error("unique id pipe read failed");
+              got += static_cast<size_t>(n);
+            }
+            close(idpipe[0]);
+          }
           rc = run_rank(a, r, id);
         } catch (const std::exception& e) {
           std::fprintf(stderr, "rank %d: %s\n", r, e.what());
@@ -278,6 +299,8 @@ int main(int argc, char** argv) {
       }
       kids.push_back(pid);
     }
+    close(idpipe[0]);
+    close(idpipe[1]);
     int worst = 0;
     for (pid_t pid : kids) {
       int st = 0;

@@ -384,7 +384,15 @@ int fm_layer_unpermute_backward(fm_layer* layer, const void* dback_buf, const vo
  * sources in it) and bounded: after ~20 s a wait gives up and
  * fm_layer_p2p_status reports it. Slots are
  * reused across steps only after the next step's demand all-gather, which
- * every GPU joins after finishing the previous step. */
+ * every GPU joins after finishing the previous step.
+ * CALLER REQUIREMENT (buffer reuse across steps): "dX ready" is signalled
+ * right after the FFN1 dgrad, but this GPU's weight-gradient GEMMs and tile
+ * sums still read X_perm and dY_perm afterwards. A peer's step-(i+1)
+ * fm_layer_dispatch_p2p writes into this GPU's X_perm, so the step-(i+1)
+ * demand exchange (the all-gather of hist_out) MUST be stream-ordered after
+ * this GPU's step-i fm_layer_expert_backward_p2p / fm_layer_unpermute_backward_p2p
+ * (enqueue the collective on the same stream, as the Python runtime and
+ * host/flexmoe_step.cpp do, or wait on an event recorded after them). */
 int fm_layer_enable_p2p(fm_layer* layer);
 int fm_layer_p2p_handle(fm_layer* layer, void* handle64);
 int fm_layer_p2p_open_peer(fm_layer* layer, int peer, const void* handle64);

@@ -152,6 +152,7 @@ class Reference(_Base):
             C.c_int,
         ),
         "ref_time_route": ([_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P], C.c_int),
+        "ref_time_count_path": ([_P] + [C.c_int] * 6 + [C.c_double, _P], C.c_int),
         "ref_step_cost": ([_P, _P, C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
         "ref_plan_migrations": ([_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
         "ref_engine_detail": (
@@ -276,6 +277,20 @@ class Reference(_Base):
         self._check(self.lib.ref_engine_detail(_p(trace), S, N, G, slots, policy_mode, interval, metric,
                                                _p(mk), _p(ab), _p(n), _p(ops), max_ops))
         return mk, ab, [ops[s, : n[s]] for s in range(S)]
+
+    COUNT_PATH = ("route", "step_cost", "make_scheduling_plan", "plan_migrations", "engine_step")
+
+    def time_count_path(self, trace, slots, policy_mode=0, interval=10, min_seconds=0.2) -> dict:
+        """Seconds per call on one host thread of the reference's count-level
+        per-step path: route (+balance_ratio), step_cost,
+        make_scheduling_plan, plan_migrations on trace step 0 and
+        Placement::initial, and one SimEngine step over the trace."""
+        trace = _i64(trace)
+        S, N, G = trace.shape
+        out = np.zeros(6)
+        self._check(self.lib.ref_time_count_path(_p(trace), S, N, G, int(slots), policy_mode, interval,
+                                                 float(min_seconds), _p(out)))
+        return dict(zip(self.COUNT_PATH, out[:5].tolist()))
 
     def time_route(self, D, cnt, slots=None, iters=1000):
         D, cnt = _i64(D), _i32(cnt)

@@ -35,6 +35,15 @@ def bf16(a) -> np.ndarray:
     return r.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
+def bf16_f32(a) -> np.ndarray:
+    """bf16 rounding (RNE) of a float32 array, kept in float32 (in place;
+    finite inputs)."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    u += np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))
+    u &= np.uint32(0xFFFF0000)
+    return u.view(np.float32)
+
+
 def gate(x, wg, k):
     """Returns (idx [T,k] int32, w [T,k] f64, logits [T,N])."""
     logits = np.asarray(x, np.float64) @ np.asarray(wg, np.float64).T
@@ -190,21 +199,27 @@ def backward(st, dy):
                 dh=dh, dx_perm=dx_perm)
 
 
-def exact_inputs(rng, T, d, N, f, skew=None):
+def exact_inputs(rng, T, d, N, f, skew=None, wdtype=np.float64):
     """Exact-arithmetic parity inputs (SURVEY.md §8d): x in {j/8}, Wg in {j/64}
     (|j| <= 8), so every logit is a multiple of 2^-9 with |logit| <= d/8 and is
     computed exactly in f32 in any order -> top-k comparable bit for bit.
     `skew` (log-popularity per expert) is added through a constant feature
     column, quantised to multiples of 1/64 and then to bf16 (|v| >= 4 keeps
     only 1/32 steps), as in the bench's Zipf gate: the device multiplies the
-    bf16 value, so the oracle must too."""
+    bf16 value, so the oracle must too. `wdtype=np.float32` keeps the expert
+    weights (bf16 values, exact in f32) at half the host memory — for the
+    128-expert d1024/f4096 shape (a different random stream than float64)."""
     x = rng.integers(-8, 9, size=(T, d)) / 8.0
     wg = rng.integers(-8, 9, size=(N, d)) / 64.0
     if skew is not None:
         x[:, 0] = 1.0
         wg[:, 0] = bf16(np.clip(np.round(np.asarray(skew) * 64) / 64, -8, 8))
-    w1 = bf16(rng.standard_normal((N, f, d)) * d**-0.5)
-    w2 = bf16(rng.standard_normal((N, d, f)) * f**-0.5)
+    if wdtype == np.float32:
+        w1 = bf16_f32(rng.standard_normal((N, f, d), dtype=np.float32) * np.float32(d**-0.5))
+        w2 = bf16_f32(rng.standard_normal((N, d, f), dtype=np.float32) * np.float32(f**-0.5))
+    else:
+        w1 = bf16(rng.standard_normal((N, f, d)) * d**-0.5)
+        w2 = bf16(rng.standard_normal((N, d, f)) * f**-0.5)
     b1 = (rng.standard_normal((N, f)) * 0.1).astype(np.float32).astype(np.float64)
     b2 = (rng.standard_normal((N, d)) * 0.1).astype(np.float32).astype(np.float64)
     return x, wg, w1, b1, w2, b2

@@ -360,4 +360,47 @@ int ref_time_route(const int64_t* D, const int32_t* cnt, int N, int G, int slots
   });
 }
 
+// seconds per call, one host thread, of the reference's
+// count-level per-step path at one configuration — out[0] route() +
+// balance_ratio(), out[1] step_cost(), out[2] make_scheduling_plan(),
+// out[3] plan_migrations() (these four on trace step 0 and
+// Placement::initial), out[4] one SimEngine step (run() over the whole
+// `steps`-step trace with the given policy mode, divided by steps). Each
+// figure repeats its call until `min_seconds` have elapsed.
+int ref_time_count_path(const int64_t* trace, int steps, int N, int G, int slots, int policy_mode,
+                        int interval, double min_seconds, double* out) {
+  return guarded([&] {
+    using clk = std::chrono::steady_clock;
+    std::vector<TokenDemand> tr = to_trace(trace, steps, N, G);
+    ClusterTopology topo = ClusterTopology::from_json(ClusterTopology::default_profile(G, slots));
+    const Placement p = Placement::initial(N, topo);
+    const TokenDemand& d = tr[0];
+    PolicyConfig pc;
+    double sink = 0;
+    auto per_call = [&](auto&& body) {
+      int64_t n = 0;
+      const auto t0 = clk::now();
+      double el = 0;
+      do {
+        body();
+        ++n;
+        el = std::chrono::duration<double>(clk::now() - t0).count();
+      } while (el < min_seconds);
+      return el / static_cast<double>(n);
+    };
+    out[0] = per_call([&] {
+      RoutingPlan plan = route(d, p);
+      sink += balance_ratio(d, p, plan);
+    });
+    out[1] = per_call([&] { sink += step_cost(d, p, route(d, p), topo).makespan_s; });
+    out[2] = per_call([&] { sink += static_cast<double>(make_scheduling_plan(d, p, topo, pc).ops.size()); });
+    out[3] = per_call([&] { sink += static_cast<double>(plan_migrations(p, topo, pc).ops.size()); });
+    SimConfig sc;
+    sc.policy_mode = static_cast<PolicyMode>(policy_mode);
+    sc.interval_steps = interval;
+    out[4] = per_call([&] { sink += static_cast<double>(run_simulation(tr, topo, sc).size()); }) / steps;
+    out[5] = sink * 0.0;
+  });
+}
+
 }  // extern "C"

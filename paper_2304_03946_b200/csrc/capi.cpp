@@ -2,7 +2,9 @@
 // thin extern "C" wrappers that translate exceptions into status codes.
 #include <cudaTypedefs.h>
 
+#include <map>
 #include <mutex>
+#include <utility>
 #include <string>
 
 #include "fm_internal.h"
@@ -23,6 +25,20 @@ int num_sms() {
     return n;
   }();
   return sms;
+}
+
+void ensure_dynamic_smem(const void* kernel, int bytes) {
+  if (bytes <= 48 * 1024) return;
+  int dev = 0;
+  FM_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> set;
+  std::lock_guard<std::mutex> lock(mu);
+  int& cur = set[{dev, kernel}];
+  if (bytes > cur) {
+    FM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    cur = bytes;
+  }
 }
 
 namespace {

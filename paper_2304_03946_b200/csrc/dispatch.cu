@@ -124,11 +124,11 @@ __device__ int block_exclusive_scan(int32_t* v, int n, int32_t* scratch) {
 __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
                             const int32_t* __restrict__ local_expert, int Nl, PlanDev p,
                             const int32_t* __restrict__ counts, const int64_t* __restrict__ demand,
-                            int32_t* __restrict__ status) {
-  // shared: flows as int32 [N][G][G] | local experts [Nl] | segment starts [Nl]
+                            int32_t* __restrict__ status, bool flows_in_smem) {
+  // shared: flows as int32 [N][G][G] (when they fit) | local experts [Nl] | segment starts [Nl]
   //       | replica counts [N][G] | mtile prefix [Nl] | scan buffer [N*G] | scratch [blockDim]
   extern __shared__ int32_t sf[];
-  const int nflow = N * G * G;
+  const int nflow = flows_in_smem ? N * G * G : 0;
   int32_t* sle = sf + nflow;
   int32_t* sss = sle + Nl;
   int32_t* scnt = sss + Nl;
@@ -152,7 +152,10 @@ __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
   }
   for (int i = threadIdx.x; i < nflow; i += blockDim.x) sf[i] = static_cast<int32_t>(flows[i]);
   __syncthreads();
-#define FL(e, s, d) sf[((e) * G + (s)) * G + (d)]
+  const int64_t* gflows = flows;
+#define FL(e, s, d)                                                     \
+  (flows_in_smem ? sf[((e) * G + (s)) * G + (d)]                        \
+                 : static_cast<int32_t>(gflows[((e) * G + (s)) * G + (d)]))
   // --- source side: chunk order of each expert's ranks (me first, then ascending)
   for (int e = threadIdx.x; e < N; e += blockDim.x) {
     int lo = 0;
@@ -971,14 +974,16 @@ void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expe
                  int32_t* status) {
   if (demand && (N > 256 || G > kMaxGpus)) throw std::invalid_argument("route: bad dimensions");
   constexpr int kPlanThreads = 256;
-  const int smem = (N * G * G + 3 * Nl + 2 * N * G + kPlanThreads) * 4;
-  if (smem > 200 * 1024) throw std::invalid_argument("plan: N*G*G too large");
-  static int configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    FM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = smem;
-  }
-  plan_kernel<<<1, kPlanThreads, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status);
+  // the flows are staged in shared memory when they fit; beyond that (e.g.
+  // 256 experts on 64 GPUs: 4 MB of flows) the kernel reads them from global
+  // memory (L2-resident) and shared memory holds only the scan buffers
+  const int base = (3 * Nl + 2 * N * G + kPlanThreads) * 4;
+  const bool flows_in_smem = base + N * G * G * 4 <= 200 * 1024;
+  const int smem = base + (flows_in_smem ? N * G * G * 4 : 0);
+  if (smem > 200 * 1024) throw std::invalid_argument("plan: num_experts * num_gpus too large");
+  ensure_dynamic_smem(reinterpret_cast<const void*>(plan_kernel), smem);
+  plan_kernel<<<1, kPlanThreads, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status,
+                                            flows_in_smem);
   FM_LAUNCH_CHECK("plan_kernel");
 }
 

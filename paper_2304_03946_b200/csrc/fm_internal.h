@@ -66,6 +66,11 @@ CUtensorMap make_tmap_2d(const void* base, bool f32, uint64_t inner, uint64_t ou
 
 int num_sms();
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `kernel` on the current
+// device, at least `bytes`: the attribute is per device, so it is cached per
+// (device, kernel) under a mutex (launchers run on several host threads).
+void ensure_dynamic_smem(const void* kernel, int bytes);
+
 // P2P arrival gating of a token-row grouped GEMM (see grouped_gemm.cu Args).
 struct ArrivalGate {
   const unsigned long long* flags = nullptr;          // this GPU's flags of one exchange slot [src]

@@ -277,11 +277,7 @@ void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, 
   const int tiles = gate_num_tiles(T);
   const int grid = std::min(tiles, kCtasPerSm * num_sms());
   auto launch = [&](auto kernel) {
-    static int configured_smem[kMaxTopK + 1] = {};
-    if (smem > configured_smem[top_k]) {
-      FM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      configured_smem[top_k] = smem;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
     kernel<<<grid, kThreads, smem, stream>>>(mx, mw, a);
   };
   switch (top_k) {

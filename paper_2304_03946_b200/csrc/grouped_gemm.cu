@@ -622,11 +622,7 @@ void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
                cudaStream_t stream) {
   using C = Cfg<CG>;
   auto kern = grouped_gemm_kernel<SCHED, A_MN, B_MN, EPI, CG>;
-  static bool configured = false;
-  if (!configured) {
-    FM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
-    configured = true;
-  }
+  ensure_dynamic_smem(reinterpret_cast<const void*>(kern), C::kSmemBytes);
   int grid = num_sms() / CG * CG;
   if (SCHED == kWgrad)
     grid = std::min(grid, CG * std::max(1, args.num_groups * (args.M_w / C::kTileM) * (args.N / kBN)));

@@ -270,10 +270,20 @@ class ExpertStore:
         self.pool.pack(self.slots(local), self._packed)
         return self.packed(len(local))
 
+    def tick(self) -> int:
+        """Advance the optimizer step count. Called on EVERY rank every step,
+        hosting experts or not: Adam's bias correction depends on it, and an
+        expert that later expands onto a GPU that hosted nothing must get the
+        same update there as on its other replicas (bit-identical replicas)."""
+        self.t += 1
+        return self.t
+
     @torch.no_grad()
     def adam_step(self, local, grads):
-        """One fused Adam step per local expert from the (replica-summed)
-        gradients; refreshes the packed operands of `local` in the same pass."""
-        self.t += 1
+        """One fused Adam step (step count `self.t`, see tick()) per local
+        expert from the (replica-summed) gradients; refreshes the packed
+        operands of `local` in the same pass."""
+        if self.t < 1:
+            raise L.LogicError("adam_step before the first tick()")
         self.pool.adam(self.slots(local), (grads.dw1, grads.db1, grads.dw2, grads.db2), self._packed,
                        self.lr, self.betas, self.eps, self.t)

@@ -129,8 +129,10 @@ class FlexMoERuntime:
         D = self.dl.last_demand_host  # TokenDemand [N][G] (its host copy overlapped the step)
         if self.recorder is not None:
             self.recorder.record(D)
-        if self.optimizer and self.layer.local_experts:
-            self.store.adam_step(self.layer.local_experts, grads)  # refreshes self.packed in place
+        if self.optimizer:
+            self.store.tick()  # every rank, with or without local experts (same Adam step count everywhere)
+            if self.layer.local_experts:
+                self.store.adam_step(self.layer.local_experts, grads)  # refreshes self.packed in place
         res = self.sched.finish_step(D)
         out = RuntimeStep(y=y, balance_ratio=res.report.balance_ratio, applied=applied,
                           accepted=res.accepted, migration_bytes=mig_bytes,
@@ -235,6 +237,8 @@ class BaselineRuntime:
         y = self.dl.forward(x, self.wg, *packed, on_demand=on_demand)
         grads = self.dl.backward(dy)  # SUM over each replica group (shadows included)
         local = self.layer.local_experts
+        if self.optimizer:
+            self.store.tick()
         if self.optimizer and self.owned:
             idx = torch.tensor([local.index(e) for e in self.owned], device=self.device)
             from .layer import LayerGrads

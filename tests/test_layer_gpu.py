@@ -64,7 +64,21 @@ CASES = [
     # the widest d_model the row kernels take (16-byte vectors, VPL 8) and VPL 6
     (8, 2, 2048, 512, 300, None),
     (8, 2, 1536, 256, 200, "zipf"),
+    # configs[4]'s expert shape: 128 experts, top-1, d_model 1024, d_ff 4096
+    (128, 1, 1024, 4096, 640, "zipf"),
 ]
+
+
+def close_f32_per_expert(out_t, ref, name, tol=1e-2):
+    """close_f32 over [N, ...] gradients one expert at a time (the 128-expert
+    d1024/f4096 shape holds 537M parameters per weight)."""
+    num = den = 0.0
+    for e in range(ref.shape[0]):
+        o = out_t[e].double().cpu().numpy()
+        num += float(((o - ref[e]) ** 2).sum())
+        den += float((ref[e] ** 2).sum())
+    rel = np.sqrt(num) / max(np.sqrt(den), 1e-30)
+    assert rel <= tol, f"{name}: rel {rel:.3e}"
 
 
 @pytest.mark.parametrize("N,k,d,f,T,skew", CASES)
@@ -74,7 +88,9 @@ def test_layer_forward_backward_parity(N, k, d, f, T, skew):
     if skew == "zipf":
         p = 1.0 / np.arange(1, N + 1) ** 1.25
         sk = np.log(p / p.sum())[rng.permutation(N)] + 3
-    x, wg, w1, b1, w2, b2 = OL.exact_inputs(rng, T, d, N, f, skew=sk)
+    big = N * f * d > (1 << 28)
+    x, wg, w1, b1, w2, b2 = OL.exact_inputs(rng, T, d, N, f, skew=sk,
+                                            wdtype=np.float32 if big else np.float64)
     st = OL.forward(x, wg, w1, b1, w2, b2, k)
     dy = OL.bf16(rng.standard_normal((T, d)) * 0.5)
     gr = OL.backward(st, dy)
@@ -116,8 +132,12 @@ def test_layer_forward_backward_parity(N, k, d, f, T, skew):
     dh = bf16_from_u16(layer.read("dh", rows * f)).reshape(rows, f)
     close_bf16(dh, gr["dh"], "dh")
     close_bf16(grads.dx.float().cpu().numpy(), gr["dx"], "dx")
-    close_f32(grads.dw1.cpu().numpy(), gr["dw1"], "dw1")
-    close_f32(grads.dw2.cpu().numpy(), gr["dw2"], "dw2")
+    if big:
+        close_f32_per_expert(grads.dw1, gr["dw1"], "dw1")
+        close_f32_per_expert(grads.dw2, gr["dw2"], "dw2")
+    else:
+        close_f32(grads.dw1.cpu().numpy(), gr["dw1"], "dw1")
+        close_f32(grads.dw2.cpu().numpy(), gr["dw2"], "dw2")
     close_f32(grads.db1.cpu().numpy(), gr["db1"], "db1")
     close_f32(grads.db2.cpu().numpy(), gr["db2"], "db2")
     if k > 1:

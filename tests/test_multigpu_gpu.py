@@ -230,3 +230,34 @@ def test_multigpu_rank_without_tokens(transport):
     outs = run_ranks(G, rank_fn)
     assert torch.equal(outs[0][0], y1) and torch.equal(outs[0][1], g1.dx)
     assert outs[1][0].shape == (0, d) and outs[1][1].shape == (0, d)
+
+
+@pytest.mark.parametrize("N,G", [(256, 64), (64, 32)])
+def test_plan_large_world_matches_route(N, G):
+    """Flows beyond the plan kernel's shared-memory staging (N*G*G int32 >
+    200 KB: 256 experts on 64 GPUs, 64 on 32) are read from global memory:
+    the device route + plan of rank 0 still equal the host route() bit for bit,
+    and the per-peer row counts equal the flows' sums."""
+    from paper_2304_03946_b200 import _lib as L
+    from paper_2304_03946_b200 import routing
+
+    k, d, f, T = 2, 256, 256, 256
+    rng = np.random.default_rng(N + G)
+    cnt = np.zeros((N, G), np.int32)
+    cnt[np.arange(N), np.arange(N) % G] = 1
+    cnt[0, :] = 1  # one expert on every GPU
+    cnt[1, G // 2] += 1
+    D = np.zeros((N, G), np.int64)
+    for g in range(G):  # each GPU's column sums to T * k
+        D[:, g] = np.bincount(rng.integers(0, N, T * k), minlength=N)
+    lay = MoELayer(N, k, d, f, replica_counts=cnt, num_gpus=G, rank=0, max_tokens=T)
+    gathered = torch.tensor(D.T.copy(), device="cuda")
+    send = np.zeros(G, np.int32)
+    recv = np.zeros(G, np.int32)
+    L.check(L.lib().fm_layer_route(lay._h, gathered.data_ptr(), send.ctypes.data, recv.ctypes.data,
+                                   L.stream_ptr()))
+    flows = lay.read("flows", N * G * G).reshape(N, G, G)
+    ref = routing.route(D, cnt)
+    assert (flows == ref).all()
+    assert (send == ref[:, 0, :].sum(axis=0)).all()
+    assert (recv == ref[:, :, 0].sum(axis=0)).all()

@@ -43,7 +43,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, cross=False):
     import torch.distributed as dist
 
     from paper_2304_03946_b200 import _lib as L
@@ -52,7 +52,7 @@ def _worker(rank, port, q):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=G)
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank if cross else 0)
         cnt, X, wg, w1, b1, w2, b2, dY = _inputs()
         bf = torch.bfloat16
         dev = lambda a, dt=bf: torch.tensor(np.asarray(a), dtype=dt, device="cuda")
@@ -96,14 +96,20 @@ def _worker(rank, port, q):
         q.put((rank, exc))
 
 
+TWO_GPUS = pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs (cross-device P2P)")
+
+
 @pytest.mark.timeout(300)
-def test_p2p_transport_two_processes_ipc():
+@pytest.mark.parametrize("cross", [False, pytest.param(True, marks=TWO_GPUS)], ids=["shared-gpu", "two-gpus"])
+def test_p2p_transport_two_processes_ipc(cross):
+    """cross=True: rank r on cuda:r — the release / acquire flags and the
+    pushed / pulled rows cross a real NVLink between two devices."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(G)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, cross)) for r in range(G)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in range(G))

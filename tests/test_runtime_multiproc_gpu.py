@@ -29,7 +29,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, port, q, transport):
+def _worker(rank, port, q, transport, cross=False):
     import torch.distributed as dist
 
     from paper_2304_03946_b200 import scheduler as S
@@ -39,7 +39,7 @@ def _worker(rank, port, q, transport):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=G)
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank if cross else 0)
         gen = torch.Generator(device="cpu").manual_seed(0)
         wg = torch.randn(N, D, generator=gen) * D**-0.5
         wg[:, 0] = torch.tensor(np.log(1.0 / np.arange(1, N + 1) ** 1.5) * 2 + 3, dtype=torch.float32)
@@ -65,15 +65,20 @@ def _worker(rank, port, q, transport):
         q.put((rank, exc))
 
 
+TWO_GPUS = pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs (cross-device P2P)")
+
+
 @pytest.mark.timeout(400)
+@pytest.mark.parametrize("cross", [False, pytest.param(True, marks=TWO_GPUS)], ids=["shared-gpu", "two-gpus"])
 @pytest.mark.parametrize("transport", TRANSPORTS)
-def test_runtime_two_processes(transport):
+def test_runtime_two_processes(transport, cross):
+    """cross=True: rank r on cuda:r (token rows and expert-state pulls over NVLink)."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q, transport)) for r in range(G)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, transport, cross)) for r in range(G)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=360) for _ in range(G))
