@@ -39,7 +39,7 @@ def _compile(src: Path, verbose: bool) -> tuple[Path, str]:
     obj = BUILD / (src.name + ".o")
     if not _deps_newer(src, obj):
         return obj, ""
-    flags = CU_FLAGS if src.suffix == ".cu" else ARCH + COMMON
+    flags = CU_FLAGS if src.suffix == ".cu" else ARCH + COMMON + os.environ.get("NVCC_EXTRA", "").split()
     cmd = [NVCC, *flags, "-c", str(src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

@@ -36,6 +36,9 @@ constexpr int kThreads = 256;
 #define FM_GATE_CTAS 2
 #endif
 constexpr int kCtas = FM_GATE_CTAS;  // resident CTAs per SM (A/B knob)
+#ifndef FM_GATE_X_EVICT_FIRST
+#define FM_GATE_X_EVICT_FIRST 1
+#endif
 
 struct Args {
   int T, N, Npad, K, top_k, stages;
@@ -102,12 +105,21 @@ __global__ void __launch_bounds__(kThreads, kCtas)
   if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
+#if FM_GATE_X_EVICT_FIRST
+    // x is streamed once: its lines are the first L2 victims, so the gate does
+    // not evict (and pay the write-back of) the predecessor's dirty lines
+    const uint64_t pol_x = ptx::l2_policy_evict_first();
+#endif
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       for (int kb = 0; kb < num_kb; ++kb) {
         ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
         if (ptx::elect_one()) {
           ptx::mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
+#if FM_GATE_X_EVICT_FIRST
+          ptx::tma_load_2d_hint(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM, pol_x);
+#else
           ptx::tma_load_2d(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM);
+#endif
           ptx::tma_load_2d(smem_b + stage * b_bytes, &map_w, &full_bar[stage], kb * kBK, 0);
         }
         __syncwarp();

@@ -118,6 +118,12 @@ __device__ __forceinline__ void wait_tile_sources(const Args& a, int mtile) {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// A/B knob: wgrad's f32 output stored with an L2 evict-first policy. Measured
+// and rejected (profiles/r02_gate_context.log): the next kernel pays the same
+// dirty-line write-back either way.
+#ifndef FM_WGRAD_STORE_HINT
+#define FM_WGRAD_STORE_HINT 0
+#endif
 #ifndef FM_WGRAD_HINT
 #define FM_WGRAD_HINT 0
 #endif
@@ -414,6 +420,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     uint8_t* warp_out = smem_out + ew * C::kOutBufs * kStageOutBytes;
     // release of the accumulator goes to the leader's barrier
     const uint32_t lead_tempty = CG == 2 ? ptx::mapa(ptx::smem_u32(tempty_bar), 0) : 0;
+    const uint64_t store_policy = ptx::l2_policy_evict_first();
     uint32_t out_seq = 0;
     int g = 0;
     int iter = 0;
@@ -470,7 +477,8 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
         __syncwarp();
         if (lane == 0) {
 #ifndef FM_DEBUG_NO_STORE
-          ptx::tma_store_2d(&map_c, buf, x, y);
+          if (EPI == kEpiF32 && FM_WGRAD_STORE_HINT) ptx::tma_store_2d_hint(&map_c, buf, x, y, store_policy);
+          else ptx::tma_store_2d(&map_c, buf, x, y);
 #endif
           ptx::bulk_commit();
         }

@@ -23,6 +23,13 @@
 #include "layer_plan.h"
 #include "routing.cuh"
 
+// A/B knob: 1 = backward as combine^T, dgrads, un-permute, tile sums, then the
+// two weight-gradient GEMMs last (measured: the next step's gate is not faster,
+// profiles/r02_gate_context.log; default keeps the round-1 order)
+#ifndef FM_BWD_ORDER
+#define FM_BWD_ORDER 0
+#endif
+
 namespace fm {
 
 // launchers (gate.cu, dispatch.cu, grouped_gemm.cu)
@@ -323,9 +330,19 @@ class Layer {
     // the dispatched units' share of dWg = per-tile column sums of X_perm
     // weighted by dl per row, reduced with db1 / db2 (dropped units: below)
     const bool dwg_tiles = dwg && cfg_.top_k > 1 && nl() > 0;
+#if FM_BWD_ORDER == 1
+    // memory-bound work first (dx right after the dgrad that produced dX_perm,
+    // then the bias / gate tile sums), the weight-gradient GEMMs last
+    expert_dgrad(saved_w1_, saved_w2_, db1, s);
+    unpermute(dx_perm_.p, saved_wg_, dx, s);
+    bias_grads(db1, db2, s, dwg_tiles ? dwg : nullptr);
+    gate_wgrad(x_perm_.p, plan_.totals, static_cast<int>(row_cap_), dwg, s, dwg_tiles);
+    expert_wgrad(dw1, dw2, s);
+#else
     expert_backward(saved_w1_, saved_w2_, dw1, db1, dw2, db2, s, dwg_tiles ? dwg : nullptr);
     unpermute_backward(dx_perm_.p, x_perm_.p, plan_.totals, static_cast<int>(row_cap_), saved_wg_, dx,
                        dwg, s, dwg_tiles);
+#endif
   }
 
   // ------------------------------------------------------------ phases
@@ -442,11 +459,20 @@ class Layer {
   void expert_backward(const void* w1, const void* w2, float* dw1, float* db1, float* dw2,
                        float* db2, cudaStream_t s, float* dwg_tiles = nullptr, bool signal_dx = false,
                        const ArrivalGate* gate = nullptr) {
-    const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
-    if (Nl == 0) {
+    if (nl() == 0) {
       if (signal_dx) p2p_signal(3, s);
       return;
     }
+    expert_dgrad(w1, w2, db1, s, gate);
+    if (signal_dx) p2p_signal(3, s);
+    expert_wgrad(dw1, dw2, s);
+    bias_grads(db1, db2, s, dwg_tiles);
+  }
+
+  // dH (masked by relu'), db1 tile partials, dX_perm
+  void expert_dgrad(const void* w1, const void* w2, float* db1, cudaStream_t s, const ArrivalGate* gate = nullptr) {
+    const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
+    if (Nl == 0) return;
     const int rows = static_cast<int>(row_cap_);
     // dA = dY . W2 masked by relu'(H) -> dH [rows, f]; db1 partials per 128-row tile
     timer_.begin(FM_PHASE_FFN2_DGRAD, s);
@@ -459,7 +485,12 @@ class Layer {
     grouped_gemm(FM_GEMM_DGRAD, dh_.p, w1, dx_perm_.p, nullptr, nullptr, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s);
     timer_.end(s);
-    if (signal_dx) p2p_signal(3, s);
+  }
+
+  void expert_wgrad(float* dw1, float* dw2, cudaStream_t s) {
+    const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
+    if (Nl == 0) return;
+    const int rows = static_cast<int>(row_cap_);
     // dW2[li] = dY^T . act  [d, f];  dW1[li] = dH^T . X  [f, d]
     if (dw2) {
       timer_.begin(FM_PHASE_FFN2_WGRAD, s);
@@ -473,9 +504,14 @@ class Layer {
                    plan_.seg_rows, nullptr, Nl, rows, f, d, 0, s);
       timer_.end(s);
     }
-    // bias / gate-weight gradients: per-128-row-tile column sums (db1's come from
-    // the dgrad epilogue; dY_perm's and the dl-weighted X_perm's here), then one
-    // fixed-order reduce per segment (deterministic, no atomics)
+  }
+
+  // bias / gate-weight gradients: per-128-row-tile column sums (db1's come from
+  // the dgrad epilogue; dY_perm's and the dl-weighted X_perm's here), then one
+  // fixed-order reduce per segment (deterministic, no atomics)
+  void bias_grads(float* db1, float* db2, cudaStream_t s, float* dwg_tiles) {
+    const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
+    if (Nl == 0) return;
     timer_.begin(FM_PHASE_BIAS_GRAD, s);
     const int max_tiles = static_cast<int>(row_cap_ / 128);
     float* part_db2 = tile_sum_.as<float>();
@@ -515,12 +551,19 @@ class Layer {
   // path, tile sums); only the units dropped by the capacity rule remain.
   void unpermute_backward(const void* dback, const void* xrows, const int* rows_dev, int rows,
                           const void* wg, void* dx, float* dwg, cudaStream_t s, bool dwg_done = false) {
-    const int T = cur_T_, d = cfg_.d_model, k = cfg_.top_k, N = cfg_.num_experts;
-    const bool gate_grad = k > 1;
+    unpermute(dback, wg, dx, s);
+    gate_wgrad(xrows, rows_dev, rows, dwg, s, dwg_done);
+  }
+  void unpermute(const void* dback, const void* wg, void* dx, cudaStream_t s) {
+    const int T = cur_T_, d = cfg_.d_model, k = cfg_.top_k;
     timer_.begin(FM_PHASE_UNPERMUTE, s);
     launch_unpermute_bwd(dback, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(), wg, T,
-                         d, k, gate_grad, dx, s);
+                         d, k, k > 1, dx, s);
     timer_.end(s);
+  }
+  void gate_wgrad(const void* xrows, const int* rows_dev, int rows, float* dwg, cudaStream_t s, bool dwg_done) {
+    const int T = cur_T_, d = cfg_.d_model, k = cfg_.top_k, N = cfg_.num_experts;
+    const bool gate_grad = k > 1;
     if (dwg) {
       timer_.begin(FM_PHASE_GATE_WGRAD, s);
       if (!dwg_done) FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
