@@ -410,8 +410,12 @@ class DistArm:
         self.logp = zipf_log_popularity(N, cfg["zipf"], 42)
         sched_cfg = S.SchedulerConfig.defaults(policy_mode=cfg["policy_mode"], interval_steps=cfg["interval"])
         self.transport = cfg.get("transport", "p2p")
+        # placement flips on completed state copies, policy on the scheduler's worker thread
+        # (include/flexmoe_b200.h fm_scheduler_config); --flip modelled = the reference's drain
+        self.flip = cfg.get("flip", "copy")
         self.rt = FlexMoERuntime(N, k, d, f, ex, prof, sched_cfg=sched_cfg, max_tokens=T, gate_weight=wg,
-                                 optimizer=False, transport=self.transport)
+                                 optimizer=False, transport=self.transport, flip=self.flip,
+                                 async_policy=self.flip == "copy")
         self.layer, self.dl = self.rt.layer, self.rt.dl
         self.drift = np.random.default_rng(42)  # same walk on every rank
         self.N, self.G = N, G
@@ -485,8 +489,14 @@ class DistArm:
                 "ops_accepted": self.accepted, "ops_applied": self.applied,
                 "migration_bytes_per_step": self.mig_bytes / steps,
                 "migration_copy_ms_per_step": (self.rt.migration_stats()["copy_ms"] - self.mig0["copy_ms"]) / steps,
-                "migration_transport": "P2P cudaMemcpyAsync of pool slots on a side stream (CUDA IPC), "
-                                       "overlapped with gate/routing/dispatch",
+                "migration_transport": "P2P cudaMemcpyAsync of pool slots on a side stream (CUDA IPC)",
+                "placement_flip": ("copy: ops issued at one boundary, state pulled during that step (the "
+                                   "receiver joins the replica group with zero rows and waits for the copy "
+                                   "only before the group all-reduce), effective at the next boundary; "
+                                   "policy on the scheduler's worker thread; table-only placement switch "
+                                   "(no allocation, no host sync)") if self.flip == "copy" else
+                                  ("modelled: ops effective when their modelled bytes drain (reference); "
+                                   "the expert FFN waits for the pull in the same step"),
                 "replica_counts": self.rt.history[-1].replica_counts.tolist() if self.rt.history else None}
 
 
@@ -505,6 +515,7 @@ def run_ours(args, world, rank, local_rank):
     multi = world > 1 or args.workload in WORKLOADS
     cfg = dict(WORKLOADS[args.workload or "cfg3"] if multi else CFG2)
     cfg["transport"] = args.transport
+    cfg["flip"] = args.flip
     if cfg.get("scaling") == "strong":  # fixed total tokens, split over the GPUs
         cfg["T"] = cfg["T"] // world
     N, k, d, f, T = cfg["N"], cfg["k"], cfg["d"], cfg["f"], cfg["T"]
@@ -707,6 +718,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="multi-GPU token transport (configs[2..4] workloads)")
+    ap.add_argument("--flip", default="copy", choices=["copy", "modelled"],
+                    help="dynamic placement: ops become effective when their state copies complete "
+                         "(copy, default) or when their modelled bytes drain (the reference's rule)")
     ap.add_argument("--workload", default=None, choices=[None, "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="default: cfg2 at 1 GPU, cfg3 (multi-GPU runtime) at N > 1; "
                          "cfg3-5 run the multi-GPU runtime at any N")

@@ -148,6 +148,21 @@ typedef struct fm_scheduler_config {
   double adjust_bandwidth_fraction;
   int max_live_groups;
   double group_creation_latency_s;
+  /* B200 runtime extensions (0/0 = the reference's behaviour):
+   * flip_mode 0: ops become effective when their MODELLED bytes drain within
+   *   adjust_bandwidth_fraction x the previous makespan (sim_engine.cpp:331-336);
+   * flip_mode 1: ops become effective when their REAL state copies complete —
+   *   begin_step issues the next queue prefix that fits the same budget (at
+   *   least one op; fm_scheduler_ops which=2); the runtime copies their state
+   *   during that step (the receivers join the replica groups with zero
+   *   tokens and wait for the copy before the group all-reduce), and the
+   *   next begin_step makes them effective. No host sync anywhere.
+   * async_policy 1: the policy half of finish_step runs on a worker thread
+   *   over a snapshot of the target placement; its ops enter the queue at the
+   *   next finish_step (or fm_scheduler_join_policy), one step later than
+   *   the reference. */
+  int flip_mode;
+  int async_policy;
 } fm_scheduler_config;
 
 typedef struct fm_step_report {
@@ -160,6 +175,7 @@ typedef struct fm_step_report {
   int n_accepted; /* ops accepted into the adjustment queue (target placement) */
   int n_applied;  /* ops that became effective at the start of this step */
   int pending_ops;
+  int n_issued; /* flip_mode 1: ops whose state copies start this step */
 } fm_step_report;
 
 typedef struct fm_scheduler fm_scheduler;
@@ -176,11 +192,15 @@ int fm_scheduler_step(fm_scheduler* s, const int64_t* demand_NG, fm_step_report*
  * on the step's demand. begin + finish == step. */
 int fm_scheduler_begin_step(fm_scheduler* s, fm_step_report* out);
 int fm_scheduler_finish_step(fm_scheduler* s, const int64_t* demand_NG, fm_step_report* out);
-/* which: 0 = ops accepted this step, 1 = ops applied (made effective) this step */
+/* which: 0 = ops accepted this step, 1 = ops applied (made effective) this
+ * step, 2 = ops issued this step (flip_mode 1) */
 int fm_scheduler_ops(fm_scheduler* s, int which, fm_placement_op* ops, int max_ops, int* n_ops);
 /* which: 0 = effective placement, 1 = target placement */
 int fm_scheduler_placement(fm_scheduler* s, int which, int32_t* slots_GE, int32_t* counts_NG);
 int fm_scheduler_reset(fm_scheduler* s, const int32_t* slots_GE);
+/* async_policy: wait for the policy worker and enqueue its ops now (they are
+ * appended to the ops reported as accepted). */
+int fm_scheduler_join_policy(fm_scheduler* s, int* n_committed);
 
 /* ------------------------------------------------------------------------
  * Comparison baselines, one step at a time:
@@ -309,8 +329,26 @@ typedef struct fm_layer fm_layer;
 /* replica_counts_NG as Placement::replica_count_on (placement.hpp:80-82). */
 int fm_layer_create(const fm_layer_config* cfg, const int32_t* replica_counts_NG, fm_layer** out);
 int fm_layer_destroy(fm_layer* layer);
-/* Placement change (Expand / Shrink / Migrate applied, placement.hpp:92-104). */
+/* Placement change (Expand / Shrink / Migrate applied, placement.hpp:92-104).
+ * Synchronous: returns once the device tables are updated. */
 int fm_layer_set_placement(fm_layer* layer, const int32_t* replica_counts_NG);
+/* The same switch enqueued on `stream`: no allocation, no host sync (one
+ * cudaMemcpyAsync from a pinned staging ring, ordered after every kernel
+ * already enqueued on the stream). hosted_N (optional, [N], nonzero = yes):
+ * experts whose state this rank keeps with replica count 0 — a replica whose
+ * state copy is in flight (fm_scheduler flip_mode 1). They are local experts
+ * (gradient slices in ascending-id local order, replica-group members) with
+ * no token rows routed to them; their weight gradients are zero. */
+int fm_layer_set_placement_async(fm_layer* layer, const int32_t* replica_counts_NG, const int32_t* hosted_N,
+                                 void* stream);
+/* Expert-operand addressing. slot_N[e] = row of expert e inside the w1 / b1 /
+ * w2 / b2 operands passed to the expert phases (w1 [capacity, f, d] ...), for
+ * every local expert; entries of other experts are ignored. With it the
+ * operands stay where the expert-state pool keeps them (fm_pool_set_operand_
+ * layout) and a placement switch moves no weights. slot_N == NULL restores
+ * the packed layout (local experts ascending, row i = i-th local expert).
+ * Enqueued on `stream` like fm_layer_set_placement_async. */
+int fm_layer_set_operand_slots(fm_layer* layer, const int32_t* slot_N, int capacity, void* stream);
 /* StaticEP mode (proj/src/baselines.cpp:81-131): capacity_factor > 0 and finite
  * drops, each step, the units beyond fm_static_ep_kept's kept[e][g] on every
  * source GPU — the LAST ones in the canonical unit order — before routing;
@@ -520,6 +558,12 @@ int fm_pool_migrate(fm_expert_pool* pool, const int32_t* moves_n3, int num_moves
                     const int32_t* local_slots, int num_local, void* w1, float* b1, void* w2,
                     float* b2, void* stream);
 int fm_pool_wait_ready(fm_expert_pool* pool, void* stream);
+/* Operand layout of fm_pool_pack / fm_pool_adam / fm_pool_migrate: 0 (default)
+ * = row i of the w1/b1/w2/b2 outputs is the i-th slot of the list (packed,
+ * ascending local order); 1 = row `slot` (operands of capacity = pool slots,
+ * addressed by the layer through fm_layer_set_operand_slots, so a placement
+ * switch moves no weights and a migration re-packs only the pulled slots). */
+int fm_pool_set_operand_layout(fm_expert_pool* pool, int by_slot);
 /* Packing alone, on `stream`. */
 int fm_pool_pack(fm_expert_pool* pool, const int32_t* local_slots, int num_local, void* w1, float* b1,
                  void* w2, float* b2, void* stream);

@@ -89,6 +89,8 @@ _SIGNATURES = {
     "fm_layer_create": [_P, _P, C.POINTER(_P)],
     "fm_layer_destroy": [_P],
     "fm_layer_set_placement": [_P, _P],
+    "fm_layer_set_placement_async": [_P, _P, _P, _P],
+    "fm_layer_set_operand_slots": [_P, _P, _I, _P],
     "fm_layer_local_experts": [_P, C.POINTER(_I), _P],
     "fm_layer_forward": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P],
     "fm_layer_backward": [_P] * 9,
@@ -108,6 +110,7 @@ _SIGNATURES = {
     "fm_scheduler_ops": [_P, _I, _P, _I, _P],
     "fm_scheduler_placement": [_P, _I, _P, _P],
     "fm_scheduler_reset": [_P, _P],
+    "fm_scheduler_join_policy": [_P, _P],
     "fm_baseline_create": [_P, _P, _I, _P],
     "fm_baseline_destroy": [_P],
     "fm_baseline_step": [_P, _P, _P, _P, _P, _P],
@@ -141,6 +144,7 @@ _SIGNATURES = {
     "fm_pool_open_peer": [_P, _I, _P],
     "fm_pool_link_peer": [_P, _I, _P],
     "fm_pool_migrate": [_P, _P, _I, _P, _I, _P, _P, _P, _P, _P],
+    "fm_pool_set_operand_layout": [_P, _I],
     "fm_pool_wait_ready": [_P, _P],
     "fm_pool_pack": [_P, _P, _I, _P, _P, _P, _P, _P],
     "fm_pool_adam": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],

@@ -34,6 +34,7 @@ constexpr int kMaxLocal = 256;
 struct SlotList {
   int n;
   int slot[kMaxLocal];
+  int out[kMaxLocal];  // operand row written for entry i: i (packed) or slot[i] (by slot)
 };
 
 // The four tensor segments of one expert's parameter set, in slot order.
@@ -85,7 +86,7 @@ __global__ void pack_kernel(const float* __restrict__ base, int64_t slot_floats,
   const int64_t n4 = sg.len[seg] / 4;
   for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n4;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    store_operand(out, seg, i, sg, j, __ldg(src + j));
+    store_operand(out, seg, sl.out[i], sg, j, __ldg(src + j));
 }
 
 struct Grads {
@@ -121,7 +122,7 @@ __global__ void adam_kernel(float* __restrict__ base, int64_t slot_floats, const
     m4[j] = m;
     v4[j] = v;
     w4[j] = p;
-    store_operand(out, seg, i, sg, j, p);
+    store_operand(out, seg, sl.out[i], sg, j, p);
   }
 }
 
@@ -161,6 +162,7 @@ struct fm_expert_pool {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing;  // per migrate call
   double copy_ms = 0.0;
   int64_t bytes = 0, copies = 0;
+  bool by_slot = false;  // operand row of a slot = the slot (else: position in the list)
 };
 
 namespace {
@@ -175,6 +177,7 @@ void check_local(const fm_expert_pool* p, const int32_t* local_slots, int n, Slo
     if (local_slots[i] < 0 || local_slots[i] >= p->slots)
       throw std::out_of_range("fm_pool: slot " + std::to_string(local_slots[i]) + " out of range");
     sl.slot[i] = local_slots[i];
+    sl.out[i] = p->by_slot ? local_slots[i] : i;
   }
 }
 
@@ -335,6 +338,13 @@ int fm_pool_migrate(fm_expert_pool* p, const int32_t* moves, int n, const int32_
     launch_pack(p, sl, w1, b1, w2, b2, p->side);
     FM_CUDA(cudaEventRecord(p->ready, p->side));
     p->ready_pending = true;
+  });
+}
+
+int fm_pool_set_operand_layout(fm_expert_pool* p, int by_slot) {
+  return fm::guarded([&] {
+    if (!p) throw std::invalid_argument("fm_pool_set_operand_layout: null pool");
+    p->by_slot = by_slot != 0;
   });
 }
 

@@ -82,6 +82,7 @@ struct ArrivalGate {
 void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
-                  cudaStream_t stream, const ArrivalGate* gate = nullptr);
+                  cudaStream_t stream, const ArrivalGate* gate = nullptr, const int* b_slot = nullptr,
+                  int b_groups = 0);
 
 }  // namespace fm

@@ -79,7 +79,11 @@ struct Args {
   int b_rows_per_group;    // kRows: B tensor-map rows between consecutive groups
   void* out;
   int ldc;
-  const float* bias;  // [groups][N]
+  const float* bias;  // [b groups][N]
+  // kRows (optional, device [groups]): row of group g's weights / bias in the
+  // B operand (an expert-state slot); null = g. Placement changes rewrite this
+  // table instead of moving weights.
+  const int* b_slot;
   uint32_t* mask;     // ReLU bits [rows][N/32]: written by kEpiBiasRelu, read by kEpiReluMask
   float* colsum;      // kEpiReluMask (optional): per-128-row-tile column sums [mtiles][N]
   // P2P arrival gating (kRows, optional): before loading the A rows of global
@@ -143,6 +147,7 @@ struct Tile {
 // dependent L2 round trip at every tile boundary shows up as an MMA bubble).
 //   order_s   kWgrad: groups longest-reduction-first (LPT), so long tiles
 //             start in the first waves; kb_s: k-blocks per LPT slot
+//             kRows: B row group (expert slot) of each group (Args::b_slot)
 //   pair_s    kRows CG == 2: prefix of 256-row tile pairs per group
 //   tp_s      kRows: tile_prefix;  ss_s: seg_start
 struct Tables {
@@ -158,8 +163,11 @@ __device__ __forceinline__ void build_tables(const Args& a, const Tables& tb) {
   int* pair_prefix_s = tb.pair_s;
   int* kb_s = tb.tp_s;
   for (int i = threadIdx.x; i < a.num_groups; i += blockDim.x) tb.ss_s[i] = __ldg(a.seg_start + i);
-  if (SCHED == kRows)
+  if (SCHED == kRows) {
     for (int i = threadIdx.x; i <= a.num_groups; i += blockDim.x) tb.tp_s[i] = __ldg(a.tile_prefix + i);
+    for (int i = threadIdx.x; i < a.num_groups; i += blockDim.x)  // B row group (expert slot) of group i
+      tb.order_s[i] = a.b_slot ? __ldg(a.b_slot + i) : i;
+  }
   if (SCHED == kWgrad) {
     for (int i = threadIdx.x; i < a.num_groups; i += blockDim.x) {
       const int ri = __ldg(a.seg_rows + i);
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       int gated_mtile = -1;
       for (int t = cluster; t < ntiles; t += num_clusters) {
         const Tile tl = decode_tile<SCHED, CG>(args, t, g, tb, rank);
-        const int b_row_base = tl.group * args.b_rows_per_group;
+        const int b_row_base = (SCHED == kRows ? tb.order_s[tl.group] : tl.group) * args.b_rows_per_group;
         const int n_cta = tl.n0 + rank * C::kBNc;  // this CTA's slice of B
         if (SCHED == kRows && args.arrive_flags && tl.valid && tl.mtile != gated_mtile) {
           wait_tile_sources(args, tl.mtile);
@@ -431,7 +439,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       // waiting on it: the tile's bias slice (to smem) and the ReLU mask bits.
       float* bs = bias_s + ab * kBN;
       if (kBias) {
-        const float* bp = args.bias + static_cast<size_t>(tl.group) * args.N + tl.n0;
+        const float* bp = args.bias + static_cast<size_t>(tb.order_s[tl.group]) * args.N + tl.n0;
         for (int i = et; i < kBN; i += kEpiThreads) bs[i] = __ldg(bp + i);
         ptx::named_bar_sync(1, kEpiThreads);
       }
@@ -670,7 +678,7 @@ void set_gemm_cta_group(int cg) {
 void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
-                  cudaStream_t stream, const ArrivalGate* gate) {
+                  cudaStream_t stream, const ArrivalGate* gate, const int* b_slot, int b_groups) {
   using namespace gemm;
   if (N % kBN != 0) throw std::invalid_argument("grouped_gemm: N must be a multiple of 256");
   if (num_groups < 1 || num_groups > kMaxGroups)
@@ -689,6 +697,10 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
   a.ldc = N;
   a.bias = bias;
   a.mask = static_cast<uint32_t*>(const_cast<void*>(aux));
+  if (b_slot && variant == FM_GEMM_WGRAD) throw std::invalid_argument("grouped_gemm: b_slot is for token-row GEMMs");
+  a.b_slot = b_slot;
+  const int nb = b_slot ? b_groups : num_groups;  // rows of B (in groups) the tensor map spans
+  if (nb < 1) throw std::invalid_argument("grouped_gemm: b_groups must be >= 1 with b_slot");
   if (gate && gate->flags) {
     if (variant == FM_GEMM_WGRAD) throw std::invalid_argument("grouped_gemm: arrival gating is for token-row GEMMs");
     a.arrive_flags = gate->flags;
@@ -713,8 +725,8 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
       if (K % kBK != 0) throw std::invalid_argument("grouped_gemm: K must be a multiple of 64");
       // A [rows, K] K-major; B = W_g [N, K] K-major, groups stacked.
       m1[0] = m2[0] = make_tmap_bf16(A, K, total_rows, K, 64, kBM);
-      m1[1] = make_tmap_bf16(B, K, static_cast<uint64_t>(num_groups) * N, K, 64, kBN);
-      m2[1] = make_tmap_bf16(B, K, static_cast<uint64_t>(num_groups) * N, K, 64, kBN / 2);
+      m1[1] = make_tmap_bf16(B, K, static_cast<uint64_t>(nb) * N, K, 64, kBN);
+      m2[1] = make_tmap_bf16(B, K, static_cast<uint64_t>(nb) * N, K, 64, kBN / 2);
       m1[2] = m2[2] = make_tmap_2d(C, false, N, total_rows, N, 32, 32, 64);
       a.b_rows_per_group = N;
       if (variant == FM_GEMM_FWD_BIAS_RELU)
@@ -728,7 +740,7 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
       if (K % kBK != 0) throw std::invalid_argument("grouped_gemm: K must be a multiple of 64");
       // A [rows, K] K-major; B = W_g viewed [K, N] (N contiguous) -> MN-major.
       m1[0] = m2[0] = make_tmap_bf16(A, K, total_rows, K, 64, kBM);
-      m1[1] = m2[1] = make_tmap_bf16(B, N, static_cast<uint64_t>(num_groups) * K, N, 64, kBK);
+      m1[1] = m2[1] = make_tmap_bf16(B, N, static_cast<uint64_t>(nb) * K, N, 64, kBK);
       m1[2] = m2[2] = make_tmap_2d(C, false, N, total_rows, N, 32, 32, 64);
       a.b_rows_per_group = K;
       if (variant == FM_GEMM_DGRAD_RELU_MASK) {

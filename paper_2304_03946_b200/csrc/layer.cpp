@@ -200,16 +200,58 @@ class Layer {
     hist_.reset(sizeof(int64_t) * N);
     demand_.reset(sizeof(int64_t) * N * G);
     flows_.reset(sizeof(int64_t) * N * G * G);
-    counts_dev_.reset(sizeof(int32_t) * N * G);
     route_status_.reset(sizeof(int32_t));
     counts_.assign(static_cast<size_t>(N) * G, 0);
     host_counts_.assign(2 * G + 1, 0);
     kept_.reset(sizeof(int64_t) * N * G);
     dropped_.reset(sizeof(int64_t));
     FM_CUDA(cudaMemset(dropped_.p, 0, sizeof(int64_t)));
+    // placement tables (uploaded per switch) and plan arrays, sized for Nl = N
+    ctl_mem_.reset(sizeof(int32_t) * (3 * N + N * G));
+    plan_.local_index = ctl_mem_.as<int32_t>();
+    local_expert_dev_ = plan_.local_index + N;
+    local_slot_dev_ = plan_.local_index + 2 * N;
+    counts_dev_ = plan_.local_index + 3 * N;
+    const int Nm = N;
+    const size_t n_plan = 3 * N * G + 2 * G + 3 * Nm + (Nm + 1) + (G * Nm + 1) + G * Nm + 4 + N * G /*peer_row*/;
+    plan_mem_.reset(sizeof(int32_t) * n_plan);
+    int32_t* q = plan_mem_.as<int32_t>();
+    auto take = [&](size_t n) {
+      int32_t* r = q;
+      q += n;
+      return r;
+    };
+    plan_.chunk_lo = take(N * G);
+    plan_.chunk_cnt = take(N * G);
+    plan_.send_off = take(N * G);
+    plan_.send_rows = take(G);
+    plan_.recv_rows = take(G);
+    plan_.seg_start = take(Nm);
+    plan_.seg_real = take(Nm);
+    plan_.seg_rows = take(Nm);
+    plan_.mtile_prefix = take(Nm + 1);
+    plan_.recv_chunk_off = take(G * Nm + 1);
+    plan_.recv_chunk_dst = take(G * Nm);
+    plan_.totals = take(4);
+    peer_row_mem_ = take(N * G);
+    plan_.peer_row = nullptr;
+    plan_.tile_src_mask = nullptr;
+    for (Staging& st : staging_) {
+      FM_CUDA(cudaMallocHost(&st.host, sizeof(int32_t) * (3 * N + N * G)));
+      FM_CUDA(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
+    }
   }
 
-  void set_placement(const int32_t* counts_NG) {
+  // Placement switch without allocation or host synchronisation: the plan
+  // arrays are sized once for every expert being local (Nl <= N), and the
+  // placement tables reach the device by one cudaMemcpyAsync on `s` from a
+  // pinned staging ring, stream-ordered after every kernel that read the
+  // previous tables. hosted_N (optional, [N]): experts whose state this rank
+  // keeps although its replica count is 0 — a replica whose state copy is in
+  // flight: it is local (gradient slices, replica-group all-reduce) with no
+  // rows routed to it.
+  void set_placement(const int32_t* counts_NG, const int32_t* hosted_N = nullptr, cudaStream_t s = nullptr,
+                     bool sync = true) {
     const int N = cfg_.num_experts, G = cfg_.num_gpus;
     std::vector<int32_t> c(counts_NG, counts_NG + static_cast<size_t>(N) * G);
     std::vector<int32_t> local;
@@ -222,7 +264,7 @@ class Layer {
       }
       if (total < 1)
         throw std::invalid_argument("fm_layer: expert " + std::to_string(e) + " has no replica");
-      if (c[static_cast<size_t>(e) * G + cfg_.rank] > 0) local.push_back(e);
+      if (c[static_cast<size_t>(e) * G + cfg_.rank] > 0 || (hosted_N && hosted_N[e] != 0)) local.push_back(e);
     }
     if (cfg_.slots_per_gpu > 0) {
       for (int g = 0; g < G; ++g) {
@@ -237,48 +279,59 @@ class Layer {
       throw std::logic_error("fm_layer: single GPU must host every expert");
     counts_ = c;
     local_ = local;
-    const int Nl = static_cast<int>(local_.size());
-    // plan arrays: one int32 allocation
-    const size_t n_plan = 3 * N * G + 2 * G + N + 3 * Nl + (Nl + 1) + (G * Nl + 1) + G * Nl + 4 +
-                          Nl /*local_expert*/ + N * G /*peer_row*/;
-    plan_mem_.reset(sizeof(int32_t) * n_plan);
-    int32_t* q = plan_mem_.as<int32_t>();
-    auto take = [&](size_t n) {
-      int32_t* r = q;
-      q += n;
-      return r;
-    };
-    plan_.chunk_lo = take(N * G);
-    plan_.chunk_cnt = take(N * G);
-    plan_.send_off = take(N * G);
-    plan_.send_rows = take(G);
-    plan_.recv_rows = take(G);
-    plan_.local_index = take(N);
-    plan_.seg_start = take(Nl);
-    plan_.seg_real = take(Nl);
-    plan_.seg_rows = take(Nl);
-    plan_.mtile_prefix = take(Nl + 1);
-    plan_.recv_chunk_off = take(G * Nl + 1);
-    plan_.recv_chunk_dst = take(G * Nl);
-    plan_.totals = take(4);
-    local_expert_dev_ = take(Nl);
-    peer_row_mem_ = take(N * G);
-    plan_.peer_row = p2p_ ? peer_row_mem_ : nullptr;
-    plan_.tile_src_mask = p2p_ ? tile_src_mask_.as<unsigned long long>() : nullptr;
-    std::vector<int32_t> li(N, -1);
-    for (int i = 0; i < Nl; ++i) li[local_[i]] = i;
-    FM_CUDA(cudaMemcpy(plan_.local_index, li.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
-    if (Nl)
-      FM_CUDA(cudaMemcpy(local_expert_dev_, local_.data(), sizeof(int32_t) * Nl,
-                         cudaMemcpyHostToDevice));
-    FM_CUDA(cudaMemcpy(counts_dev_.p, counts_.data(), sizeof(int32_t) * N * G,
-                       cudaMemcpyHostToDevice));
-    // Row capacity of the permuted buffers: every unit could land here
-    // (worst case of route()), plus per-segment padding.
-    // (G > 1 starts at twice the local units and grows in route_gathered.)
-    const size_t units = static_cast<size_t>(cfg_.max_tokens) * cfg_.top_k * (G == 1 ? 1 : 2);
-    ensure_rows(round_up(units + static_cast<size_t>(Nl) * 127, 128));
+    upload_placement(s, sync);
   }
+
+  // slot_N[e]: row (group) of expert e in the w1/b1/w2/b2 operands passed to
+  // the expert GEMMs, for every local expert; capacity = rows of those
+  // operands. Null restores the packed layout (local experts ascending).
+  void set_operand_slots(const int32_t* slot_N, int capacity, cudaStream_t s) {
+    const int N = cfg_.num_experts;
+    if (slot_N) {
+      if (capacity < 1 || capacity > 4096) throw std::invalid_argument("fm_layer: operand capacity must be in [1, 4096]");
+      operand_slot_.assign(slot_N, slot_N + N);
+      operand_cap_ = capacity;
+    } else {
+      operand_slot_.clear();
+      operand_cap_ = 0;
+    }
+    upload_placement(s, false);
+  }
+
+  void upload_placement(cudaStream_t s, bool sync) {
+    const int N = cfg_.num_experts, G = cfg_.num_gpus, Nl = nl();
+    Staging& st = staging_[staging_next_];
+    staging_next_ = (staging_next_ + 1) % kStaging;
+    FM_CUDA(cudaEventSynchronize(st.done));  // the upload kStaging switches ago (long complete)
+    int32_t* h = st.host;  // [local_index N | local_expert N | operand slot N | counts N*G]
+    std::fill(h, h + N, -1);
+    for (int i = 0; i < Nl; ++i) {
+      h[local_[i]] = i;
+      h[N + i] = local_[i];
+      h[2 * N + i] = operand_slot_.empty() ? i : operand_slot_[local_[i]];  // validated at GEMM enqueue
+    }
+    std::memcpy(h + 3 * N, counts_.data(), sizeof(int32_t) * N * G);
+    FM_CUDA(cudaMemcpyAsync(ctl_mem_.p, h, sizeof(int32_t) * (3 * N + N * G), cudaMemcpyHostToDevice, s));
+    FM_CUDA(cudaEventRecord(st.done, s));
+    if (sync) FM_CUDA(cudaEventSynchronize(st.done));
+    // Row capacity of the permuted buffers: every unit could land here
+    // (worst case of route()), plus per-segment padding. G > 1 without P2P
+    // starts at twice the local units and grows in route_gathered (that path
+    // synchronises per step anyway); P2P sizes its arena for the worst case.
+    const size_t units = static_cast<size_t>(cfg_.max_tokens) * cfg_.top_k * (G == 1 ? 1 : 2);
+    ensure_rows(round_up(units + static_cast<size_t>(N) * 127, 128));
+  }
+
+  // checked when the expert GEMMs are enqueued: a placement switch and the
+  // operand table that goes with it arrive in two calls
+  const int32_t* operand_slots_dev() const {
+    if (operand_slot_.empty()) return nullptr;
+    for (int e : local_)
+      if (operand_slot_[e] < 0 || operand_slot_[e] >= operand_cap_)
+        throw std::out_of_range("fm_layer: local expert " + std::to_string(e) + " has no operand slot");
+    return local_slot_dev_;
+  }
+  int operand_groups() const { return operand_slot_.empty() ? nl() : operand_cap_; }
 
   void ensure_rows(size_t rows) {
     if (rows <= row_cap_) return;
@@ -381,7 +434,7 @@ class Layer {
     }
     // route() over the demand and the dispatch plan in one single-block launch
     launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s,
-                counts_dev_.as<int32_t>(), routed, route_status_.as<int32_t>());
+                counts_dev_, routed, route_status_.as<int32_t>());
     timer_.end(s);
   }
 
@@ -444,11 +497,13 @@ class Layer {
     const int rows = static_cast<int>(row_cap_);
     timer_.begin(FM_PHASE_FFN1_FWD, s);
     grouped_gemm(FM_GEMM_FWD_BIAS_RELU, x_perm_.p, w1, act_.p, b1, relu_mask_.p, plan_.seg_start,
-                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s, gate);
+                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s, gate, operand_slots_dev(),
+                 operand_groups());
     timer_.end(s);
     timer_.begin(FM_PHASE_FFN2_FWD, s);
     grouped_gemm(FM_GEMM_FWD_BIAS, act_.p, w2, y_perm_.p, b2, nullptr, plan_.seg_start,
-                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s);
+                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s, nullptr, operand_slots_dev(),
+                 operand_groups());
     timer_.end(s);
   }
 
@@ -478,12 +533,14 @@ class Layer {
     timer_.begin(FM_PHASE_FFN2_DGRAD, s);
     grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p,
                  db1 ? tile_colsum_.as<float>() : nullptr, relu_mask_.p, plan_.seg_start,
-                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s, gate);
+                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s, gate, operand_slots_dev(),
+                 operand_groups());
     timer_.end(s);
     // dX = dH . W1 -> [rows, d]
     timer_.begin(FM_PHASE_FFN1_DGRAD, s);
     grouped_gemm(FM_GEMM_DGRAD, dh_.p, w1, dx_perm_.p, nullptr, nullptr, plan_.seg_start,
-                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s);
+                 plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s, nullptr, operand_slots_dev(),
+                 operand_groups());
     timer_.end(s);
   }
 
@@ -848,6 +905,10 @@ class Layer {
 
  public:
   ~Layer() {
+    for (Staging& st : staging_) {
+      if (st.done) cudaEventDestroy(st.done);
+      if (st.host) cudaFreeHost(st.host);
+    }
     if (p2p_)
       for (int g = 0; g < cfg_.num_gpus; ++g)
         if (peer_ipc_[g] && pp_.base[g]) cudaIpcCloseMemHandle(pp_.base[g]);
@@ -863,7 +924,18 @@ class Layer {
   int32_t* peer_row_mem_ = nullptr;
   std::vector<int32_t> counts_, local_;
   DevBuf topk_idx_, topk_w_, tile_rank_, pos_, dl_, tile_counts_, tile_base_, hist_, demand_,
-      flows_, counts_dev_, route_status_, plan_mem_;
+      flows_, route_status_, plan_mem_, ctl_mem_;
+  int32_t* counts_dev_ = nullptr;
+  int32_t* local_slot_dev_ = nullptr;
+  std::vector<int32_t> operand_slot_;  // [N] or empty (packed layout)
+  int operand_cap_ = 0;
+  struct Staging {
+    int32_t* host = nullptr;
+    cudaEvent_t done = nullptr;
+  };
+  static constexpr int kStaging = 16;  // table uploads in flight before a reuse waits
+  Staging staging_[kStaging];
+  int staging_next_ = 0;
   DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_, relu_mask_, tile_colsum_,
       row_expert_, tile_sum_;
   std::vector<int32_t> host_counts_;
@@ -904,6 +976,21 @@ int fm_layer_destroy(fm_layer* h) {
 
 int fm_layer_set_placement(fm_layer* h, const int32_t* replica_counts_NG) {
   return fm::guarded([&] { h->impl->set_placement(replica_counts_NG); });
+}
+
+int fm_layer_set_placement_async(fm_layer* h, const int32_t* replica_counts_NG, const int32_t* hosted_N,
+                                 void* stream) {
+  return fm::guarded([&] {
+    if (!h || !replica_counts_NG) throw std::invalid_argument("fm_layer_set_placement_async: null argument");
+    h->impl->set_placement(replica_counts_NG, hosted_N, static_cast<cudaStream_t>(stream), /*sync=*/false);
+  });
+}
+
+int fm_layer_set_operand_slots(fm_layer* h, const int32_t* slot_N, int capacity, void* stream) {
+  return fm::guarded([&] {
+    if (!h) throw std::invalid_argument("fm_layer_set_operand_slots: null layer");
+    h->impl->set_operand_slots(slot_N, capacity, static_cast<cudaStream_t>(stream));
+  });
 }
 
 int fm_layer_set_capacity_factor(fm_layer* h, double capacity_factor) {

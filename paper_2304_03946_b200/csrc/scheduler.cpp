@@ -648,10 +648,30 @@ Scheduler::Scheduler(const ClusterProfile& prof, const SchedulerConfig& cfg, int
   if (cfg.max_live_groups < 1) throw std::invalid_argument("SimConfig: max_live_groups must be >= 1");
 }
 
+Scheduler::~Scheduler() {
+  if (worker_.joinable()) worker_.join();
+}
+
+std::vector<Op> Scheduler::join_policy() {
+  if (!worker_.joinable()) return {};
+  worker_.join();
+  std::vector<Op> ops = std::move(worker_ops_);
+  worker_ops_.clear();
+  commit(ops);
+  return ops;
+}
+
+void Scheduler::commit(const std::vector<Op>& ops) {
+  for (const Op& op : ops) queue_.push(op, target_.apply(op, prof_));
+}
+
 void Scheduler::reset(const SlotPlacement& p) {
+  if (worker_.joinable()) worker_.join();
+  worker_ops_.clear();
   effective_ = p;
   target_ = p;
   queue_ = TransferQueue();
+  inflight_.clear();
   prev_makespan_ = 0;
 }
 
@@ -671,12 +691,68 @@ StepOutcome Scheduler::step(const std::vector<int64_t>& D) {
 }
 
 const StepOutcome& Scheduler::begin_step() {
-  // 1. transfers that overlapped the previous step land (best-effort budget)
   cur_ = StepOutcome{};
-  cur_.applied = queue_.drain(cfg_.adjust_bandwidth_fraction * prev_makespan_, prof_, effective_,
-                              cur_.adjust_bytes, cur_.adjust_seconds);
+  if (cfg_.flip_mode == 0) {
+    // 1. transfers that overlapped the previous step land (best-effort budget)
+    cur_.applied = queue_.drain(cfg_.adjust_bandwidth_fraction * prev_makespan_, prof_, effective_,
+                                cur_.adjust_bytes, cur_.adjust_seconds);
+  } else {
+    // 1'. the copies issued at the previous boundary completed inside that
+    // step: those ops become effective, in queue order
+    for (size_t i = 0; i < inflight_.size(); ++i) {
+      const Op op = queue_.pending().front().op;
+      effective_.apply(op, prof_);
+      cur_.applied.push_back(op);
+      queue_.pop_front();
+    }
+    inflight_.clear();
+    // ... and the next queue prefix within the adjustment budget starts
+    const double budget = cfg_.adjust_bandwidth_fraction * prev_makespan_;
+    double used = 0;
+    for (const auto& p : queue_.pending()) {
+      double t = 0;
+      for (const Transfer& x : p.left) t += x.bytes > 0 ? transfer_seconds(x, prof_) : 0.0;
+      if (!inflight_.empty() && used + t > budget) break;
+      used += t;
+      for (const Transfer& x : p.left) cur_.adjust_bytes += std::max(0.0, x.bytes);
+      inflight_.push_back(p.op);
+    }
+    cur_.adjust_seconds = used;
+    cur_.issued = inflight_;
+  }
   begun_ = true;
   return cur_;
+}
+
+std::vector<Op> Scheduler::run_policy(const std::vector<int64_t>& D, SlotPlacement target, bool policy_step,
+                                      bool triggered) const {
+  const int N = target.experts();
+  std::vector<Op> ops;
+  // 3. policy on the target placement (pending adjustments are not re-planned)
+  if (policy_step && triggered) {
+    while (true) {
+      if (trigger(flows_for(D, target), N) <= cfg_.threshold) break;
+      const std::vector<Op> plan = plan_balance(D, target, prof_, cfg_.horizon);
+      if (plan.empty()) break;
+      for (const Op& op : plan) {
+        target.apply(op, prof_);
+        ops.push_back(op);
+      }
+    }
+  }
+  // 4. one replica-locality migration, confirmed by the full cost model
+  if (cfg_.policy_mode != 2) {
+    const std::vector<Op> mig = plan_relocation(target, prof_, cfg_.horizon);
+    if (!mig.empty()) {
+      const Op& op = mig.front();
+      const double before = step_time(D, target, flows_for(D, target), prof_).makespan;
+      SlotPlacement swapped = target;
+      swapped.migrate(op.a_gpu, op.a_slot, op.b_gpu, op.b_slot, prof_);
+      const double after = step_time(D, swapped, flows_for(D, swapped), prof_).makespan;
+      if (after <= before * (1.0 + 1e-12)) ops.push_back(op);
+    }
+  }
+  return ops;
 }
 
 StepOutcome Scheduler::finish_step(const std::vector<int64_t>& D) {
@@ -699,33 +775,18 @@ StepOutcome Scheduler::finish_step(const std::vector<int64_t>& D) {
   out.makespan = st.makespan;
   out.balance_ratio = balance_of(flows, N, G);
   out.metric_value = cfg_.metric == 0 ? out.balance_ratio : variance_of(flows, N, G);
-  // 3. policy on the target placement (pending adjustments are not re-planned)
   const bool policy_step = cfg_.policy_mode == 0 || (cfg_.policy_mode == 1 && step_ % cfg_.interval_steps == 0);
-  if (policy_step && trigger(flows, N) > cfg_.threshold) {
-    while (true) {
-      if (trigger(flows_for(D, target_), N) <= cfg_.threshold) break;
-      const std::vector<Op> plan = plan_balance(D, target_, prof_, cfg_.horizon);
-      if (plan.empty()) break;
-      for (const Op& op : plan) {
-        queue_.push(op, target_.apply(op, prof_));
-        out.accepted.push_back(op);
-      }
-    }
-  }
-  // 4. one replica-locality migration, confirmed by the full cost model
-  if (cfg_.policy_mode != 2) {
-    const std::vector<Op> mig = plan_relocation(target_, prof_, cfg_.horizon);
-    if (!mig.empty()) {
-      const Op& op = mig.front();
-      const double before = step_time(D, target_, flows_for(D, target_), prof_).makespan;
-      SlotPlacement swapped = target_;
-      swapped.migrate(op.a_gpu, op.a_slot, op.b_gpu, op.b_slot, prof_);
-      const double after = step_time(D, swapped, flows_for(D, swapped), prof_).makespan;
-      if (after <= before * (1.0 + 1e-12)) {
-        queue_.push(op, target_.apply(op, prof_));
-        out.accepted.push_back(op);
-      }
-    }
+  const bool triggered = policy_step && trigger(flows, N) > cfg_.threshold;
+  if (cfg_.async_policy) {
+    // the previous step's policy (it ran while this step was enqueued) enters
+    // the queue now; this step's starts on a snapshot of the new target
+    out.accepted = join_policy();
+    worker_ = std::thread([this, D, snap = target_, policy_step, triggered] {
+      worker_ops_ = run_policy(D, snap, policy_step, triggered);
+    });
+  } else {
+    out.accepted = run_policy(D, target_, policy_step, triggered);
+    commit(out.accepted);
   }
   prev_makespan_ = out.makespan;
   ++step_;

@@ -17,6 +17,7 @@
 #include <list>
 #include <map>
 #include <optional>
+#include <thread>
 #include <vector>
 
 namespace fm {
@@ -142,6 +143,7 @@ class TransferQueue {
   std::vector<Op> drain(double seconds, const ClusterProfile& prof, SlotPlacement& effective,
                         double& bytes_moved, double& seconds_used);
   size_t size() const { return q_.size(); }
+  void pop_front() { q_.pop_front(); }
   double pending_bytes() const;
   const std::deque<Pending>& pending() const { return q_; }
 
@@ -171,6 +173,19 @@ struct SchedulerConfig {
   double adjust_bandwidth_fraction = 0.5;
   int max_live_groups = 64;
   double group_creation_latency_s = 0.005;
+  // 0 (reference): an op becomes effective once its modelled bytes drain
+  //   within adjust_bandwidth_fraction x the previous makespan
+  //   (sim_engine.cpp:331-336, :208-262).
+  // 1 (device): begin_step makes the ops issued at the previous boundary
+  //   effective — their state copies ran during that step and completed
+  //   before its replica-group all-reduce (stream-ordered, no host sync) —
+  //   and issues the next queue prefix whose modelled transfer time fits the
+  //   same budget (at least one op).
+  int flip_mode = 0;
+  // 1: the policy half of finish_step (trigger loop + migration pass) runs on
+  //   a worker thread over a snapshot of the target placement; its ops enter
+  //   the queue at the next finish_step (one step later than the reference).
+  int async_policy = 0;
 };
 
 struct StepOutcome {
@@ -182,11 +197,15 @@ struct StepOutcome {
   int group_misses = 0;
   std::vector<Op> accepted;  // entered the queue this step (target placement)
   std::vector<Op> applied;   // became effective this step
+  std::vector<Op> issued;    // flip_mode 1: state copies start this step (effective next step)
 };
 
 class Scheduler {
  public:
   Scheduler(const ClusterProfile& prof, const SchedulerConfig& cfg, int num_experts);
+  ~Scheduler();
+  Scheduler(const Scheduler&) = delete;
+  Scheduler& operator=(const Scheduler&) = delete;
   StepOutcome step(const std::vector<int64_t>& D);
   // step() in two halves: the drain (ops that become effective at the step
   // boundary, before the device routes) and the rest, once the step's
@@ -196,10 +215,19 @@ class Scheduler {
   const SlotPlacement& effective() const { return effective_; }
   const SlotPlacement& target() const { return target_; }
   const TransferQueue& queue() const { return queue_; }
+  // flip_mode 1: the ops whose copies are in flight (a queue prefix)
+  const std::vector<Op>& inflight() const { return inflight_; }
   void reset(const SlotPlacement& p);
+  // async_policy: wait for the worker and enqueue its ops (also done by the
+  // next finish_step, reset and the destructor)
+  std::vector<Op> join_policy();
 
  private:
   double trigger(const std::vector<int64_t>& flows, int N) const;
+  // steps 3-4 of run_step on `target` (no side effects on the scheduler)
+  std::vector<Op> run_policy(const std::vector<int64_t>& D, SlotPlacement target, bool policy_step,
+                             bool triggered) const;
+  void commit(const std::vector<Op>& ops);
   ClusterProfile prof_;
   SchedulerConfig cfg_;
   SlotPlacement effective_, target_;
@@ -209,6 +237,9 @@ class Scheduler {
   int step_ = 0;
   StepOutcome cur_;
   bool begun_ = false;
+  std::vector<Op> inflight_;
+  std::thread worker_;
+  std::vector<Op> worker_ops_;
 };
 
 }  // namespace sched

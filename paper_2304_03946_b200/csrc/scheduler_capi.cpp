@@ -148,6 +148,9 @@ int fm_scheduler_create(const fm_cluster_profile* prof, const fm_scheduler_confi
     c.adjust_bandwidth_fraction = cfg->adjust_bandwidth_fraction;
     c.max_live_groups = cfg->max_live_groups;
     c.group_creation_latency_s = cfg->group_creation_latency_s;
+    if (cfg->flip_mode < 0 || cfg->flip_mode > 1) throw std::invalid_argument("scheduler: flip_mode must be 0 or 1");
+    c.flip_mode = cfg->flip_mode;
+    c.async_policy = cfg->async_policy ? 1 : 0;
     auto h = std::make_unique<fm_scheduler>();
     h->s = std::make_unique<Scheduler>(to_profile(prof), c, num_experts);
     *out = h.release();
@@ -171,6 +174,7 @@ int fm_scheduler_step(fm_scheduler* h, const int64_t* D, fm_step_report* out) {
       out->group_misses = h->last.group_misses;
       out->n_accepted = static_cast<int>(h->last.accepted.size());
       out->n_applied = static_cast<int>(h->last.applied.size());
+      out->n_issued = static_cast<int>(h->last.issued.size());
       out->pending_ops = static_cast<int>(h->s->queue().size());
     }
   });
@@ -185,6 +189,7 @@ int fm_scheduler_begin_step(fm_scheduler* h, fm_step_report* out) {
       out->adjust_s = o.adjust_seconds;
       out->adjust_bytes = o.adjust_bytes;
       out->n_applied = static_cast<int>(o.applied.size());
+      out->n_issued = static_cast<int>(o.issued.size());
       out->pending_ops = static_cast<int>(h->s->queue().size());
     }
   });
@@ -203,6 +208,7 @@ int fm_scheduler_finish_step(fm_scheduler* h, const int64_t* D, fm_step_report* 
       out->group_misses = h->last.group_misses;
       out->n_accepted = static_cast<int>(h->last.accepted.size());
       out->n_applied = static_cast<int>(h->last.applied.size());
+      out->n_issued = static_cast<int>(h->last.issued.size());
       out->pending_ops = static_cast<int>(h->s->queue().size());
     }
   });
@@ -210,7 +216,8 @@ int fm_scheduler_finish_step(fm_scheduler* h, const int64_t* D, fm_step_report* 
 
 int fm_scheduler_ops(fm_scheduler* h, int which, fm_placement_op* ops, int max_ops, int* n_ops) {
   return fm::guarded([&] {
-    copy_ops(which == 0 ? h->last.accepted : h->last.applied, ops, max_ops, n_ops);
+    if (which < 0 || which > 2) throw std::invalid_argument("fm_scheduler_ops: which must be 0, 1 or 2");
+    copy_ops(which == 0 ? h->last.accepted : which == 1 ? h->last.applied : h->last.issued, ops, max_ops, n_ops);
   });
 }
 
@@ -219,6 +226,14 @@ int fm_scheduler_placement(fm_scheduler* h, int which, int32_t* slots_GE, int32_
     const SlotPlacement& p = which == 0 ? h->s->effective() : h->s->target();
     if (slots_GE) std::memcpy(slots_GE, p.slot_table().data(), sizeof(int32_t) * p.slot_table().size());
     if (counts_NG) std::memcpy(counts_NG, p.counts().data(), sizeof(int32_t) * p.counts().size());
+  });
+}
+
+int fm_scheduler_join_policy(fm_scheduler* h, int* n_committed) {
+  return fm::guarded([&] {
+    const std::vector<Op> ops = h->s->join_policy();
+    h->last.accepted.insert(h->last.accepted.end(), ops.begin(), ops.end());
+    if (n_committed) *n_committed = static_cast<int>(ops.size());
   });
 }
 

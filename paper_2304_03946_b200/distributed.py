@@ -234,7 +234,7 @@ class LoopbackHub:
 
     def __init__(self, world):
         self.world = world
-        self.barrier = threading.Barrier(world)
+        self.barrier = threading.Barrier(world, timeout=120)  # a failed rank breaks it, not a hang
         self.slots = [None] * world
         self.groups = LruGroupCache(64)
 
@@ -495,7 +495,7 @@ class DistributedMoELayer:
         self.last_demand = gathered
         return y
 
-    def _backward_p2p(self, dy, sync):
+    def _backward_p2p(self, dy, sync, before_sync=None):
         T, wg, w1, w2, _x = self._saved
         lay, dev, stream = self.layer, dy.device, L.stream_ptr()
         nl = len(lay.local_experts)
@@ -509,6 +509,8 @@ class DistributedMoELayer:
         if nl == 0:
             g.dw1, g.db1, g.dw2, g.db2 = (t[:0] for t in (g.dw1, g.db1, g.dw2, g.db2))
         if sync:  # dwg holds this GPU's share: the all-GPU sum below completes it
+            if before_sync is not None:
+                before_sync()
             self._x("grad_sync", self.sync_grads, g)
         return g
 
@@ -516,9 +518,12 @@ class DistributedMoELayer:
         """True if a device-side P2P arrival wait gave up (synchronises)."""
         return self.layer.p2p_status() != 0
 
-    def backward(self, dy, sync=True):
+    def backward(self, dy, sync=True, before_sync=None):
+        """before_sync(): called right before the replica-group all-reduces
+        are enqueued (the runtime makes the stream wait there for the state
+        copies of replicas that join a group this step, flip_mode 1)."""
         if self.transport == "p2p":
-            return self._backward_p2p(dy, sync)
+            return self._backward_p2p(dy, sync, before_sync)
         T, wg, w1, w2, _x = self._saved
         st = self._st
         lay = self.layer
@@ -544,11 +549,17 @@ class DistributedMoELayer:
         if nl == 0:
             g.dw1, g.db1, g.dw2, g.db2 = (t[:0] for t in (g.dw1, g.db1, g.dw2, g.db2))
         if sync:
+            if before_sync is not None:
+                before_sync()
             self._x("grad_sync", self.sync_grads, g)
         return g
 
     def sync_grads(self, g):
-        return sync_replica_grads(self.ex, self.layer.replica_counts, self.layer.local_experts, g)
+        """Replica groups = the GPUs holding each expert's state: the routing
+        replica counts, or `group_counts` when the runtime sets it (replicas
+        whose state copy is in flight take part with zero gradients)."""
+        cnt = self.group_counts if getattr(self, "group_counts", None) is not None else self.layer.replica_counts
+        return sync_replica_grads(self.ex, cnt, self.layer.local_experts, g)
 
 
 def sync_replica_grads(ex: Exchange, replica_counts, local_experts, g):

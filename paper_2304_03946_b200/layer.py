@@ -91,6 +91,25 @@ class MoELayer:
         L.check(L.lib().fm_layer_set_placement(self._h, cnt.ctypes.data))
         self.replica_counts = cnt.copy()
 
+    def set_placement_async(self, replica_counts, hosted=None, stream=None):
+        """The placement switch enqueued on the stream (no allocation, no host
+        sync). hosted ([N] bool, optional): experts this rank keeps state for
+        with replica count 0 (a replica whose state copy is in flight): local,
+        with zero rows."""
+        cnt = np.ascontiguousarray(replica_counts, np.int32)
+        h = None if hosted is None else np.ascontiguousarray(np.asarray(hosted, bool).astype(np.int32))
+        L.check(L.lib().fm_layer_set_placement_async(self._h, cnt.ctypes.data,
+                                                     None if h is None else h.ctypes.data, L.stream_ptr(stream)))
+        self.replica_counts = cnt.copy()
+
+    def set_operand_slots(self, slot_of, capacity, stream=None):
+        """slot_of [N]: operand row of every local expert (None: packed layout)."""
+        if slot_of is None:
+            L.check(L.lib().fm_layer_set_operand_slots(self._h, None, 0, L.stream_ptr(stream)))
+            return
+        t = np.ascontiguousarray(slot_of, np.int32)
+        L.check(L.lib().fm_layer_set_operand_slots(self._h, t.ctypes.data, int(capacity), L.stream_ptr(stream)))
+
     def set_capacity_factor(self, capacity_factor: float) -> None:
         """StaticEP mode (baselines.cpp:81-131): > 0 drops units beyond capacity
         (bit-exact with fm_static_ep_kept); 0 / inf = no drops (FlexMoE)."""

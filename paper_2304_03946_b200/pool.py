@@ -209,12 +209,19 @@ class ExpertStore:
     buffers allocated once, so side-stream packing never races the allocator)."""
 
     def __init__(self, d, f, device, capacity, world=1, max_local=None, lr=1e-4, betas=(0.9, 0.999),
-                 eps=1e-8, allocator: SlotAllocator | None = None):
+                 eps=1e-8, allocator: SlotAllocator | None = None, by_slot=False):
+        """by_slot: the operands are indexed by pool slot (capacity rows; the
+        layer addresses them through MoELayer.set_operand_slots), so placement
+        changes move no weights and a migration re-packs only pulled slots.
+        Otherwise they are packed in ascending local order (max_local rows)."""
         self.d, self.f, self.device = d, f, device
         self.lr, self.betas, self.eps = lr, betas, eps
         self.pool = ExpertPool(capacity, d, f, world)
         self.alloc = allocator or SlotAllocator(capacity)
-        n = max(1, max_local or capacity)
+        self.by_slot = by_slot
+        if by_slot:
+            L.check(L.lib().fm_pool_set_operand_layout(self.pool._h, 1))
+        n = capacity if by_slot else max(1, max_local or capacity)
         bf = torch.bfloat16
         self._packed = (torch.zeros(n, f, d, dtype=bf, device=device), torch.zeros(n, f, device=device),
                         torch.zeros(n, d, f, dtype=bf, device=device), torch.zeros(n, d, device=device))
@@ -260,15 +267,25 @@ class ExpertStore:
     def slots(self, local) -> list[int]:
         return [self.alloc.slot_of[e] for e in local]
 
-    def packed(self, n):
+    def packed(self, n=None):
+        if self.by_slot:
+            return self._packed
         return tuple(t[:n] for t in self._packed)
 
     def pack(self, local):
-        """Layer operands for the local experts (ascending id), packed on the current stream."""
+        """Layer operands for the local experts (ascending id; by_slot: at
+        their slots), packed on the current stream."""
         if not local:
             return self.packed(1)
         self.pool.pack(self.slots(local), self._packed)
         return self.packed(len(local))
+
+    def slot_table(self, num_experts) -> np.ndarray:
+        """[N] operand row (= pool slot) of every hosted expert, -1 elsewhere."""
+        t = -np.ones(num_experts, np.int32)
+        for e, s in self.alloc.slot_of.items():
+            t[e] = s
+        return t
 
     def tick(self) -> int:
         """Advance the optimizer step count. Called on EVERY rank every step,

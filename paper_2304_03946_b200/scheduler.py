@@ -174,12 +174,14 @@ class SchedulerConfig(C.Structure):
     _fields_ = [("threshold", C.c_double), ("metric", C.c_int), ("policy_mode", C.c_int),
                 ("interval_steps", C.c_int), ("amortization_horizon", C.c_int),
                 ("adjust_bandwidth_fraction", C.c_double), ("max_live_groups", C.c_int),
-                ("group_creation_latency_s", C.c_double)]
+                ("group_creation_latency_s", C.c_double), ("flip_mode", C.c_int), ("async_policy", C.c_int)]
 
     @classmethod
     def defaults(cls, **kw):
-        """SimConfig defaults (sim_engine.hpp:35-49)."""
-        c = cls(1.1, 0, 0, 10, 50, 0.5, 64, 0.005)
+        """SimConfig defaults (sim_engine.hpp:35-49); flip_mode / async_policy
+        0 = the reference's modelled drain and inline policy
+        (include/flexmoe_b200.h documents the device modes)."""
+        c = cls(1.1, 0, 0, 10, 50, 0.5, 64, 0.005, 0, 0)
         for k, v in kw.items():
             setattr(c, k, v)
         return c
@@ -188,7 +190,8 @@ class SchedulerConfig(C.Structure):
 class StepReport(C.Structure):
     _fields_ = [("balance_ratio", C.c_double), ("metric_value", C.c_double), ("makespan_s", C.c_double),
                 ("adjust_s", C.c_double), ("adjust_bytes", C.c_double), ("group_misses", C.c_int),
-                ("n_accepted", C.c_int), ("n_applied", C.c_int), ("pending_ops", C.c_int)]
+                ("n_accepted", C.c_int), ("n_applied", C.c_int), ("pending_ops", C.c_int),
+                ("n_issued", C.c_int)]
 
 
 def slots_from_counts(counts, slots_per_gpu):
@@ -292,11 +295,24 @@ class Scheduler:
         return StepResult(rep, self._ops(0, rep.n_accepted), self._ops(1, rep.n_applied))
 
     def begin_step(self) -> list:
-        """Drain half: returns the ops that became effective at this boundary."""
+        """Drain half: returns the ops that became effective at this boundary
+        (flip_mode 1: `self.issued` holds the ops whose copies start now)."""
         rep = StepReport()
         L.check(L.lib().fm_scheduler_begin_step(self._h, C.byref(rep)))
         self._begin = rep
+        self.issued = self._ops(2, rep.n_issued)
         return self._ops(1, rep.n_applied)
+
+    def join_policy(self) -> list:
+        """async_policy: wait for the worker, enqueue its ops, return them."""
+        n = C.c_int()
+        L.check(L.lib().fm_scheduler_join_policy(self._h, C.byref(n)))
+        if n.value == 0:
+            return []
+        buf = (PlacementOp * 4096)()
+        got = C.c_int()
+        L.check(L.lib().fm_scheduler_ops(self._h, 0, buf, 4096, C.byref(got)))
+        return _ops(buf, got)[-n.value:]
 
     def finish_step(self, D) -> StepResult:
         D = np.ascontiguousarray(D, np.int64)

@@ -53,7 +53,7 @@ def run(mode, N, k, d, f, T, G, steps, zipf, transport):
     E = 2 * -(-N // G)
     prof = b200_profile(G, E, tps=2.0e7, d=d, f=f)
     baseline = mode in ("static-ep", "full-replicate")
-    cfg = S.SchedulerConfig.defaults(policy_mode={"dynamic": 0, "static": 2}.get(mode, 2))
+    cfg = S.SchedulerConfig.defaults(policy_mode={"dynamic": 0, "dynamic-copy": 0, "static": 2}.get(mode, 2))
     g = torch.Generator(device="cpu").manual_seed(1234)
     wg0 = torch.randn(N, d, generator=g) * d**-0.5
     logp0 = zipf_logp(N, zipf, 42)
@@ -72,8 +72,10 @@ def run(mode, N, k, d, f, T, G, steps, zipf, transport):
                                      S.BaselineConfig.make(mode, capacity_factor=1.0, replicate_top=1),
                                      max_tokens=T, gate_weight=wg0.clone(), lr=1e-4, transport=transport)
             else:
+                copy = mode == "dynamic-copy"  # flips on completed copies, policy on the worker thread
                 rt = FlexMoERuntime(N, k, d, f, hub.endpoint(r), prof, sched_cfg=cfg, max_tokens=T,
-                                    gate_weight=wg0.clone(), lr=1e-4, transport=transport)
+                                    gate_weight=wg0.clone(), lr=1e-4, transport=transport,
+                                    flip="copy" if copy else "modelled", async_policy=copy)
             x, dy = xs[r].cuda(), dys[r].cuda()
             walk = np.random.default_rng(42)  # the same drift on every rank
             logp = logp0.copy()
@@ -93,7 +95,8 @@ def run(mode, N, k, d, f, T, G, steps, zipf, transport):
                     continue
                 out.append({"step": s, "balance_ratio": float(recv.max() / recv.mean()),
                             "scheduler_ratio": st.balance_ratio, "applied": [list(o) for o in st.applied],
-                            "pulled_bytes": int(st.migration_bytes),
+                            "pulled_bytes": int(st.migration_bytes), "issued": [list(o) for o in st.issued],
+                            "switch_host_us": rt.last_switch_us, "finish_host_us": rt.last_finish_us,
                             "replicas": [int(c) for c in st.replica_counts]})
             torch.cuda.synchronize()
             mig = {"bytes": 0, "copy_ms": 0.0, "copies": 0} if baseline else rt.migration_stats()
@@ -120,6 +123,8 @@ def run(mode, N, k, d, f, T, G, steps, zipf, transport):
         "balance_ratio_tail_mean": float(np.mean(tail)),
         "balance_ratio_tail_max": float(np.max(tail)),
         "ops_applied": sum(len(s["applied"]) for s in steps0),
+        "switch_host_us_max": max((s.get("switch_host_us", 0.0) for s in steps0), default=0.0),
+        "finish_host_us_mean": float(np.mean([s.get("finish_host_us", 0.0) for s in steps0])),
         "expert_state_pulled_bytes": sum(rec[r]["migration"]["bytes"] for r in range(G)),
         "expert_state_copy_ms": sum(rec[r]["migration"]["copy_ms"] for r in range(G)),
         "slots_pulled": sum(rec[r]["migration"]["copies"] for r in range(G)),
@@ -136,16 +141,18 @@ def run(mode, N, k, d, f, T, G, steps, zipf, transport):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=120)
-    ap.add_argument("--out", default=str(ROOT / "profiles" / "r01_dynamic_loopback.json"))
+    ap.add_argument("--out", default=str(ROOT / "profiles" / "r02_dynamic_loopback.json"))
+    ap.add_argument("--modes", default="static,static-ep,full-replicate,dynamic,dynamic-copy")
+    ap.add_argument("--shape", default="32,2,768,3072,8192,4,1.25", help="N,k,d,f,T,G,zipf")
     a = ap.parse_args()
-    # BERT-MoE-like layer (configs[3] dims) at 4 virtual GPUs, 8K tokens per GPU
-    N, k, d, f, T, G, zipf = 32, 2, 768, 3072, 8192, 4, 1.25
+    # default: BERT-MoE-like layer (configs[3] dims) at 4 virtual GPUs, 8K tokens per GPU
+    N, k, d, f, T, G, zipf = (t(v) for t, v in zip((int,) * 6 + (float,), a.shape.split(",")))
     res = {"what": __doc__.strip().splitlines()[0],
            "workload": {"experts": N, "top_k": k, "d_model": d, "d_ff": f, "tokens_per_gpu": T, "gpus_virtual": G,
                         "zipf": zipf, "drift": "p *= exp(U[-0.02, 0.02]) per step (workload.cpp:164-170)",
                         "transport": "p2p", "steps": a.steps},
            "runs": [run(m, N, k, d, f, T, G, a.steps, zipf, "p2p")
-                    for m in ("static", "static-ep", "full-replicate", "dynamic")]}
+                    for m in a.modes.split(",")]}
     Path(a.out).write_text(json.dumps(res, indent=1))
     for r in res["runs"]:
         print(json.dumps({kk: v for kk, v in r.items() if kk != "per_step"}))
