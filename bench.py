@@ -18,9 +18,11 @@ tokens, Zipf(1.25)-skewed routing produced by the real gate, static placement.
 * roofline: dominant kernel = the tcgen05 grouped GEMM (six launches per
            step), achieved = 12*U*d*f FLOP (U = tokens*k units, padding not
            counted) / summed CUDA-event time of those launches, against the
-           measured sustained bf16 peak (MEASURED_PEAKS.json).
-* cpu_baseline: the CPU oracle port (numpy, float64) of the same layer step
-           on a bounded token sample, rank 0 at N=1 only.
+           measured burst bf16 peak (MEASURED_PEAKS.json; frac_sustained
+           beside it against the sustained peak, with this run's SM clock).
+* cpu_baseline: the CPU oracle port of the same layer step in float32
+           (numpy on multithreaded OpenBLAS + the C oracle's OpenMP bf16
+           rounding, all host cores) on a bounded token sample, rank 0 at N=1.
 `--impl reference` times the reference's own CPU path (oracle/_ref: the
 unmodified moesim route() on the step's demand) plus the oracle port of the
 layer math, on the host cores, same metric.
@@ -162,21 +164,23 @@ def cpu_layer_sample(cfg, tokens, seed=0):
 
     N, k, d, f = cfg["N"], cfg["k"], cfg["d"], cfg["f"]
     key = (N, d, f, cfg["zipf"])
-    if key not in _CPU_WEIGHTS:
+    f32 = np.float32
+    if key not in _CPU_WEIGHTS:  # bf16-valued weights, held in float32
         wr = np.random.default_rng(0)
         wg = OL.bf16(wr.standard_normal((N, d)) * d**-0.5)
         wg[:, 0] = zipf_log_popularity(N, cfg["zipf"], 0)
-        _CPU_WEIGHTS[key] = (wg, OL.bf16(wr.standard_normal((N, f, d)) * d**-0.5),
-                             OL.bf16(wr.standard_normal((N, d, f)) * f**-0.5))
+        _CPU_WEIGHTS[key] = (wg.astype(f32),
+                             OL.bf16_f32(wr.standard_normal((N, f, d), dtype=f32) * f32(d**-0.5)),
+                             OL.bf16_f32(wr.standard_normal((N, d, f), dtype=f32) * f32(f**-0.5)))
     wg, w1, w2 = _CPU_WEIGHTS[key]
     rng = np.random.default_rng(seed)
-    x = OL.bf16(rng.standard_normal((tokens, d)))
+    x = OL.bf16_f32(rng.standard_normal((tokens, d), dtype=f32))
     x[:, 0] = 1.0
-    b1 = np.zeros((N, f))
-    b2 = np.zeros((N, d))
-    dy = OL.bf16(rng.standard_normal((tokens, d)))
-    t0 = time.perf_counter()
-    st = OL.forward(x, wg, w1, b1, w2, b2, k)
+    b1 = np.zeros((N, f), f32)
+    b2 = np.zeros((N, d), f32)
+    dy = OL.bf16_f32(rng.standard_normal((tokens, d), dtype=f32))
+    t0 = time.perf_counter()  # fp32 on multithreaded BLAS (all host cores)
+    st = OL.forward(x, wg, w1, b1, w2, b2, k, dtype=f32)
     OL.backward(st, dy)
     return time.perf_counter() - t0, st["hist"]
 
@@ -237,8 +241,8 @@ def cpu_baseline(cfg, budget_s=12.0):
     tokens = max(512, tokens // 512 * 512)
     secs, hist = cpu_layer_sample(cfg, tokens)
     out = {"value": tokens / secs, "unit": "tokens/s", "cores": host_threads(), "kind": "port",
-           "sample": f"oracle/layer.py float64 numpy fwd+bwd of {tokens} tokens of the bench "
-                     f"workload ({secs:.1f} s); host nproc={os.cpu_count()}, {cpu_model()}"}
+           "sample": f"oracle/layer.py float32 fwd+bwd (multithreaded BLAS, OpenMP rounding) of {tokens} "
+                     f"tokens of the bench workload ({secs:.1f} s); host nproc={os.cpu_count()}, {cpu_model()}"}
     try:
         import oracle
 
@@ -291,7 +295,7 @@ def run_reference_arm(args, world, rank):
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
             "higher_is_better": True, "scaling": cfg.get("scaling", "weak"), "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": line_config(cfg, world, multi),
             "sample": {"tokens_per_step": tokens, "tokens_per_gpu_in_config": cfg["T"],
                        "extrapolation": (f"tokens/s measured on {tokens} of the config's {cfg['T']} tokens per "
@@ -305,7 +309,8 @@ def run_reference_arm(args, world, rank):
                              "sample": f"{tokens} tokens/step of {cfg['T']}: the reference's own SimEngine step "
                                        f"({'oracle/_ref' if count_path else 'unavailable'}, 1 thread, "
                                        f"{count_path.get('engine_step', 0):.1f} us) + the oracle port of the "
-                                       "gate/FFN/combine fwd+bwd (float64 numpy, all host threads); "
+                                       "gate/FFN/combine fwd+bwd (float32: multithreaded OpenBLAS + OpenMP "
+                                       "bf16 rounding, all host threads); "
                                        f"host nproc={os.cpu_count()}, {cpu_model()}",
                              "reference_count_path_us": {ref_name: count_path} if count_path else None},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,

@@ -89,7 +89,13 @@ class Oracle(_Base):
             C.c_int,
         ),
         "orc_mt64_first": ([C.c_uint64, C.c_int], C.c_uint64),
+        "orc_bf16_round_f32": ([_P, C.c_int64], None),
     }
+
+    def bf16_round_f32(self, a):
+        """In place (contiguous float32), OpenMP."""
+        self.lib.orc_bf16_round_f32(_p(a), a.size)
+        return a
 
     def route(self, D, cnt):
         D, cnt = _i64(D), _i32(cnt)

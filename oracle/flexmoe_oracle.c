@@ -358,3 +358,18 @@ int orc_generate_trace(int N, int G, int64_t tokens_per_step, double zipf, doubl
   free(col);
   return ORC_OK;
 }
+
+/* ---------------------------------------------------------------- layer math helper
+ * bf16 storage rounding (round to nearest even) of a float32 array, in place,
+ * OpenMP over the host cores — the hot elementwise op of the float32 layer
+ * restatement (oracle/layer.py) that bench.py times as the CPU baseline. */
+void orc_bf16_round_f32(float* a, int64_t n) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t u;
+    memcpy(&u, a + i, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    u &= 0xFFFF0000u;
+    memcpy(a + i, &u, 4);
+  }
+}

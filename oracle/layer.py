@@ -16,7 +16,10 @@ reference"); this module restates them from the paper and the SPEC:
 Arithmetic: float64 with the product's bf16 storage points mirrored
 (activations after ReLU, expert outputs, dY rows, dH, dX rows, y, dx are
 rounded to bf16 exactly where the device stores bf16), so remaining
-differences are f32-vs-f64 accumulation order only.
+differences are f32-vs-f64 accumulation order only. `dtype=np.float32` runs
+the same math in float32 on multithreaded BLAS (all host cores): that is the
+CPU layer baseline bench.py times, checked against the
+float64 path in tests/test_oracle_layer_cpu.py.
 """
 from __future__ import annotations
 
@@ -37,16 +40,24 @@ def bf16(a) -> np.ndarray:
 
 def bf16_f32(a) -> np.ndarray:
     """bf16 rounding (RNE) of a float32 array, kept in float32 (in place;
-    finite inputs)."""
-    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    finite inputs). Large arrays go through the C oracle's OpenMP loop."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if a.size >= (1 << 20):
+        return Oracle().bf16_round_f32(a)
+    u = a.view(np.uint32)
     u += np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))
     u &= np.uint32(0xFFFF0000)
     return u.view(np.float32)
 
 
-def gate(x, wg, k):
-    """Returns (idx [T,k] int32, w [T,k] f64, logits [T,N])."""
-    logits = np.asarray(x, np.float64) @ np.asarray(wg, np.float64).T
+def _bf16(a, dt):
+    """bf16 storage rounding in the working precision."""
+    return bf16(a) if dt == np.float64 else bf16_f32(np.asarray(a, np.float32))
+
+
+def gate(x, wg, k, dt=np.float64):
+    """Returns (idx [T,k] int32, w [T,k], logits [T,N])."""
+    logits = np.asarray(x, dt) @ np.asarray(wg, dt).T
     order = np.argsort(-logits, axis=1, kind="stable")  # equal logits keep ascending id
     idx = order[:, :k].astype(np.int32)
     kept = np.take_along_axis(logits, idx, axis=1)
@@ -60,14 +71,14 @@ def histogram(idx, N):
 
 
 def unit_ranks(idx, N):
-    """Rank of each unit among units of the same expert, ascending token order."""
+    """Rank of each unit among units of the same expert, ascending token order
+    (units are in (token, slot) order; a stable sort by expert keeps it)."""
     T, k = idx.shape
-    flat = idx.reshape(-1)
-    ranks = np.zeros(flat.shape[0], np.int64)
-    seen = np.zeros(N, np.int64)
-    for u, e in enumerate(flat):  # units are already in (token, slot) order
-        ranks[u] = seen[e]
-        seen[e] += 1
+    flat = idx.reshape(-1).astype(np.int64)
+    order = np.argsort(flat, kind="stable")
+    start = np.concatenate([[0], np.cumsum(np.bincount(flat, minlength=N))[:-1]])
+    ranks = np.empty(flat.shape[0], np.int64)
+    ranks[order] = np.arange(flat.shape[0]) - start[flat[order]]
     return ranks.reshape(T, k)
 
 
@@ -130,71 +141,75 @@ def single_gpu_positions(idx, N, capacity_factor=0.0):
     return pos, segs, flows, hist
 
 
-def forward(x, wg, w1, b1, w2, b2, k, capacity_factor=0.0):
+def forward(x, wg, w1, b1, w2, b2, k, capacity_factor=0.0, dtype=np.float64):
     """Single-GPU layer forward. Weights [N,...] in expert order. Returns a state dict."""
-    x = np.asarray(x, np.float64)
+    dt = dtype
+    x = np.asarray(x, dt)
     T, d = x.shape
     N = wg.shape[0]
-    idx, w, logits = gate(x, wg, k)
+    idx, w, logits = gate(x, wg, k, dt)
     pos, segs, flows, hist = single_gpu_positions(idx, N, capacity_factor)
     rows = sum(s[2] for s in segs)
     f = w1.shape[1]
-    x_perm = np.zeros((rows, d))
+    x_perm = np.zeros((rows, d), dt)
     for j in range(k):
         kept = pos[:, j] >= 0
         x_perm[pos[kept, j]] = x[kept]
-    act = np.zeros((rows, f))
-    y_perm = np.zeros((rows, d))
+    act = np.zeros((rows, f), dt)
+    y_perm = np.zeros((rows, d), dt)
     for e, (s0, real, r) in enumerate(segs):
         if r == 0:
             continue
         seg = slice(s0, s0 + r)
-        act[seg] = bf16(np.maximum(x_perm[seg] @ np.asarray(w1[e], np.float64).T + b1[e], 0.0))
-        y_perm[seg] = bf16(act[seg] @ np.asarray(w2[e], np.float64).T + b2[e])
-    live = (pos >= 0).astype(np.float64)  # dropped units contribute nothing
-    y = bf16(np.einsum("tk,tkd->td", w.astype(np.float32).astype(np.float64) * live,
-                       y_perm[np.maximum(pos, 0)]))
-    return dict(x=x, wg=np.asarray(wg, np.float64), w1=w1, w2=w2, idx=idx, w=w, logits=logits,
+        act[seg] = _bf16(np.maximum(x_perm[seg] @ np.asarray(w1[e], dt).T + np.asarray(b1[e], dt), 0), dt)
+        y_perm[seg] = _bf16(act[seg] @ np.asarray(w2[e], dt).T + np.asarray(b2[e], dt), dt)
+    live = (pos >= 0).astype(dt)  # dropped units contribute nothing
+    y = _bf16(np.einsum("tk,tkd->td", w.astype(np.float32).astype(dt) * live, y_perm[np.maximum(pos, 0)]), dt)
+    return dict(x=x, wg=np.asarray(wg, dt), w1=w1, w2=w2, idx=idx, w=w, logits=logits,
                 pos=pos, segs=segs, flows=flows, hist=hist, x_perm=x_perm, act=act,
-                y_perm=y_perm, y=y, k=k)
+                y_perm=y_perm, y=y, k=k, dt=dt)
 
 
 def backward(st, dy):
-    dy = np.asarray(dy, np.float64)
+    dt = st.get("dt", np.float64)
+    dy = np.asarray(dy, dt)
     idx, w, pos, segs = st["idx"], st["w"], st["pos"], st["segs"]
     x_perm, act, y_perm = st["x_perm"], st["act"], st["y_perm"]
     T, k = idx.shape
     N, d = st["wg"].shape
     f = act.shape[1]
-    wf = w.astype(np.float32).astype(np.float64)
+    wf = w.astype(np.float32).astype(dt)
     dy_perm = np.zeros_like(y_perm)
     live = pos >= 0
     for j in range(k):
-        dy_perm[pos[live[:, j], j]] = bf16(wf[live[:, j], j : j + 1] * dy[live[:, j]])
+        dy_perm[pos[live[:, j], j]] = _bf16(wf[live[:, j], j : j + 1] * dy[live[:, j]], dt)
     dw = np.einsum("td,tkd->tk", dy, y_perm[np.maximum(pos, 0)]) * live
     dl = wf * (dw - (wf * dw).sum(axis=1, keepdims=True))
-    dh = np.zeros((x_perm.shape[0], f))
+    dh = np.zeros((x_perm.shape[0], f), dt)
     dx_perm = np.zeros_like(x_perm)
-    dw1 = np.zeros((N, f, d))
-    dw2 = np.zeros((N, d, f))
-    db1 = np.zeros((N, f))
-    db2 = np.zeros((N, d))
+    dw1 = np.zeros((N, f, d), dt)
+    dw2 = np.zeros((N, d, f), dt)
+    db1 = np.zeros((N, f), dt)
+    db2 = np.zeros((N, d), dt)
     for e, (s0, real, r) in enumerate(segs):
         if r == 0:
             continue
         seg = slice(s0, s0 + r)
-        da = dy_perm[seg] @ np.asarray(st["w2"][e], np.float64)
-        dh[seg] = bf16(da * (act[seg] > 0))
-        dx_perm[seg] = bf16(dh[seg] @ np.asarray(st["w1"][e], np.float64))
+        da = dy_perm[seg] @ np.asarray(st["w2"][e], dt)
+        dh[seg] = _bf16(da * (act[seg] > 0), dt)
+        dx_perm[seg] = _bf16(dh[seg] @ np.asarray(st["w1"][e], dt), dt)
         dw1[e] = dh[seg].T @ x_perm[seg]
         dw2[e] = dy_perm[seg].T @ act[seg]
         db1[e] = dh[seg].sum(axis=0)
         db2[e] = dy_perm[seg].sum(axis=0)
     gate_in = np.einsum("tk,tkd->td", dl, st["wg"][idx]) if k > 1 else 0.0
-    dx = bf16((dx_perm[np.maximum(pos, 0)] * live[:, :, None]).sum(axis=1) + gate_in)
-    dwg = np.zeros((N, d))
-    if k > 1:
-        np.add.at(dwg, idx.reshape(-1), dl.reshape(-1, 1) * np.repeat(st["x"], k, axis=0))
+    dx = _bf16((dx_perm[np.maximum(pos, 0)] * live[:, :, None]).sum(axis=1) + gate_in, dt)
+    dwg = np.zeros((N, d), dt)
+    if k > 1:  # sum over units of expert e of dl * x: one [N, T] x [T, d] product per k-slot
+        for j in range(k):
+            sel = np.zeros((N, T), dt)
+            sel[idx[:, j], np.arange(T)] = dl[:, j]
+            dwg += sel @ st["x"]
     return dict(dx=dx, dwg=dwg, dw1=dw1, dw2=dw2, db1=db1, db2=db2, dl=dl, dy_perm=dy_perm,
                 dh=dh, dx_perm=dx_perm)
 

@@ -23,11 +23,13 @@
 #include "layer_plan.h"
 #include "routing.cuh"
 
-// A/B knob: 1 = backward as combine^T, dgrads, un-permute, tile sums, then the
-// two weight-gradient GEMMs last (measured: the next step's gate is not faster,
-// profiles/r02_gate_context.log; default keeps the round-1 order)
+// A/B knob (fused single-GPU backward): 0 = combine^T, dgrad2, dgrad1, wgrad2,
+// wgrad1, tile sums, un-permute (round 1); 1 = the two weight-gradient GEMMs
+// last (measured: the next step's gate is not faster, profiles/r02_gate_context.log);
+// 2 = wgrad2, dgrad2, wgrad1, dgrad1 (each f32 weight-gradient drain overlaps a
+// tensor-bound GEMM)
 #ifndef FM_BWD_ORDER
-#define FM_BWD_ORDER 0
+#define FM_BWD_ORDER 2
 #endif
 
 namespace fm {
@@ -383,7 +385,21 @@ class Layer {
     // the dispatched units' share of dWg = per-tile column sums of X_perm
     // weighted by dl per row, reduced with db1 / db2 (dropped units: below)
     const bool dwg_tiles = dwg && cfg_.top_k > 1 && nl() > 0;
-#if FM_BWD_ORDER == 1
+#if FM_BWD_ORDER == 2
+    // each weight-gradient GEMM right before a dgrad GEMM: the dirty f32 dW
+    // lines it leaves in L2 are written back while the next GEMM is
+    // tensor-bound (HBM idle), not by the memory-bound kernels that follow
+    // the last one (the next step's gate paid it: profiles/r02_gate_context.log)
+    if (nl() > 0) {
+      wgrad2(dw2, s);                  // dY_perm, act
+      dgrad2(saved_w2_, db1, s);       // dY_perm, W2 -> dH (+ db1 tile partials)
+      wgrad1(dw1, s);                  // dH, X_perm
+      dgrad1(saved_w1_, s);            // dH, W1 -> dX_perm
+      bias_grads(db1, db2, s, dwg_tiles ? dwg : nullptr);
+    }
+    unpermute_backward(dx_perm_.p, x_perm_.p, plan_.totals, static_cast<int>(row_cap_), saved_wg_, dx,
+                       dwg, s, dwg_tiles);
+#elif FM_BWD_ORDER == 1
     // memory-bound work first (dx right after the dgrad that produced dX_perm,
     // then the bias / gate tile sums), the weight-gradient GEMMs last
     expert_dgrad(saved_w1_, saved_w2_, db1, s);
@@ -526,17 +542,26 @@ class Layer {
 
   // dH (masked by relu'), db1 tile partials, dX_perm
   void expert_dgrad(const void* w1, const void* w2, float* db1, cudaStream_t s, const ArrivalGate* gate = nullptr) {
+    dgrad2(w2, db1, s, gate);
+    dgrad1(w1, s);
+  }
+  // dA = dY . W2 masked by relu'(H) -> dH [rows, f]; db1 partials per 128-row tile
+  void dgrad2(const void* w2, float* db1, cudaStream_t s, const ArrivalGate* gate = nullptr) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0) return;
     const int rows = static_cast<int>(row_cap_);
-    // dA = dY . W2 masked by relu'(H) -> dH [rows, f]; db1 partials per 128-row tile
     timer_.begin(FM_PHASE_FFN2_DGRAD, s);
     grouped_gemm(FM_GEMM_DGRAD_RELU_MASK, dy_perm_.p, w2, dh_.p,
                  db1 ? tile_colsum_.as<float>() : nullptr, relu_mask_.p, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, f, d, s, gate, operand_slots_dev(),
                  operand_groups());
     timer_.end(s);
-    // dX = dH . W1 -> [rows, d]
+  }
+  // dX = dH . W1 -> [rows, d]
+  void dgrad1(const void* w1, cudaStream_t s) {
+    const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
+    if (Nl == 0) return;
+    const int rows = static_cast<int>(row_cap_);
     timer_.begin(FM_PHASE_FFN1_DGRAD, s);
     grouped_gemm(FM_GEMM_DGRAD, dh_.p, w1, dx_perm_.p, nullptr, nullptr, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s, nullptr, operand_slots_dev(),
@@ -545,22 +570,26 @@ class Layer {
   }
 
   void expert_wgrad(float* dw1, float* dw2, cudaStream_t s) {
+    wgrad2(dw2, s);
+    wgrad1(dw1, s);
+  }
+  // dW2[li] = dY^T . act  [d, f]
+  void wgrad2(float* dw2, cudaStream_t s) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
-    if (Nl == 0) return;
-    const int rows = static_cast<int>(row_cap_);
-    // dW2[li] = dY^T . act  [d, f];  dW1[li] = dH^T . X  [f, d]
-    if (dw2) {
-      timer_.begin(FM_PHASE_FFN2_WGRAD, s);
-      grouped_gemm(FM_GEMM_WGRAD, dy_perm_.p, act_.p, dw2, nullptr, nullptr, plan_.seg_start,
-                   plan_.seg_rows, nullptr, Nl, rows, d, f, 0, s);
-      timer_.end(s);
-    }
-    if (dw1) {
-      timer_.begin(FM_PHASE_FFN1_WGRAD, s);
-      grouped_gemm(FM_GEMM_WGRAD, dh_.p, x_perm_.p, dw1, nullptr, nullptr, plan_.seg_start,
-                   plan_.seg_rows, nullptr, Nl, rows, f, d, 0, s);
-      timer_.end(s);
-    }
+    if (Nl == 0 || !dw2) return;
+    timer_.begin(FM_PHASE_FFN2_WGRAD, s);
+    grouped_gemm(FM_GEMM_WGRAD, dy_perm_.p, act_.p, dw2, nullptr, nullptr, plan_.seg_start,
+                 plan_.seg_rows, nullptr, Nl, static_cast<int>(row_cap_), d, f, 0, s);
+    timer_.end(s);
+  }
+  // dW1[li] = dH^T . X  [f, d]
+  void wgrad1(float* dw1, cudaStream_t s) {
+    const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
+    if (Nl == 0 || !dw1) return;
+    timer_.begin(FM_PHASE_FFN1_WGRAD, s);
+    grouped_gemm(FM_GEMM_WGRAD, dh_.p, x_perm_.p, dw1, nullptr, nullptr, plan_.seg_start,
+                 plan_.seg_rows, nullptr, Nl, static_cast<int>(row_cap_), f, d, 0, s);
+    timer_.end(s);
   }
 
   // bias / gate-weight gradients: per-128-row-tile column sums (db1's come from

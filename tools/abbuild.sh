@@ -6,7 +6,7 @@ mkdir -p ${LIBDIR:-abtest}
 while [ $# -ge 2 ]; do
   NVCC_EXTRA="$2" python paper_2304_03946_b200/build.py >/dev/null
   cp paper_2304_03946_b200/libflexmoe_b200.so ${LIBDIR:-abtest}/lib$1.so
-  touch paper_2304_03946_b200/csrc/*.cu  # force the next variant to recompile
+  touch paper_2304_03946_b200/csrc/*.cu paper_2304_03946_b200/csrc/*.cpp  # force the next variant to recompile
   shift 2
 done
 python paper_2304_03946_b200/build.py >/dev/null
