@@ -48,11 +48,110 @@ struct Args {
   int32_t* tile_counts;  // [num_tiles][N]
 };
 
+#ifdef FM_GATE_TRACE
+// diagnostic build only: globaltimer stamps of block 0's pipeline events
+__device__ unsigned long long g_gate_trace[256];
+__device__ unsigned long long g_gate_blocks[1024];  // [block][start, exit]
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GATE_TRACE(i) \
+  do {                \
+    if (blockIdx.x == 0 && (i) < 256) g_gate_trace[(i)] = gtime(); \
+  } while (0)
+#else
+#define GATE_TRACE(i) \
+  do {                \
+  } while (0)
+#endif
+
+#ifdef FM_GATE_SPIN
+#define GATE_WAIT ptx::mbar_wait_spin
+#else
+#define GATE_WAIT ptx::mbar_wait
+#endif
+
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// KT = top_k (compile-time: the insertion network is KT slots deep, not 8).
+// Top-1 / top-2 of a token's logits as a pairwise tree (depth log2(32) per
+// 32-column chunk instead of a 32-step dependent insertion chain). Every merge
+// takes a left list A whose expert ids are all lower than the right list B's,
+// so "B wins only when strictly greater" is the reference's lower-id tie rule
+// — the same selection as the sorted insertion for KT >= 3.
+template <int KT>
+struct TopK {
+  float v[KT];
+  int e[KT];
+};
+
+__device__ __forceinline__ TopK<1> topk_merge(const TopK<1>& A, const TopK<1>& B) {
+  const bool p = B.v[0] > A.v[0];
+  return TopK<1>{{p ? B.v[0] : A.v[0]}, {p ? B.e[0] : A.e[0]}};
+}
+
+__device__ __forceinline__ TopK<2> topk_merge(const TopK<2>& A, const TopK<2>& B) {
+  const bool p = B.v[0] > A.v[0];
+  TopK<2> o;
+  o.v[0] = p ? B.v[0] : A.v[0];
+  o.e[0] = p ? B.e[0] : A.e[0];
+  // runner-up: the best of what is left on each side (A's candidate has the lower id)
+  const float c1v = p ? A.v[0] : A.v[1], c2v = p ? B.v[1] : B.v[0];
+  const int c1e = p ? A.e[0] : A.e[1], c2e = p ? B.e[1] : B.e[0];
+  const bool r = c2v > c1v;
+  o.v[1] = r ? c2v : c1v;
+  o.e[1] = r ? c2e : c1e;
+  return o;
+}
+
+template <int KT>
+__device__ __forceinline__ TopK<KT> topk_leaf(float v, int e) {
+  TopK<KT> o;
+  o.v[0] = v;
+  o.e[0] = e;
+  if constexpr (KT == 2) {
+    o.v[1] = -INFINITY;
+    o.e[1] = -1;
+  }
+  return o;
+}
+
+// columns >= N (padding) enter as -inf with their (higher) ids: any real
+// expert beats or ties them and wins the tie
+template <int KT>
+__device__ __forceinline__ void tree_topk(uint32_t t_row, int N, int Npad, float (&best_v)[KT],
+                                          int (&best_e)[KT]) {
+  TopK<KT> run;
+  for (int c = 0; c < Npad; c += 32) {
+    uint32_t r[32];
+    ptx::tmem_ld_32x32b_x32(t_row + c, r);
+    ptx::tmem_ld_wait();
+    TopK<KT> n[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int e0 = c + 2 * i, e1 = e0 + 1;
+      const float v0 = e0 < N ? __uint_as_float(r[2 * i]) : -INFINITY;
+      const float v1 = e1 < N ? __uint_as_float(r[2 * i + 1]) : -INFINITY;
+      n[i] = topk_merge(topk_leaf<KT>(v0, e0), topk_leaf<KT>(v1, e1));
+    }
+#pragma unroll
+    for (int w = 1; w < 16; w <<= 1)
+#pragma unroll
+      for (int i = 0; i < 16; i += 2 * w) n[i] = topk_merge(n[i], n[i + w]);
+    run = c == 0 ? n[0] : topk_merge(run, n[0]);
+  }
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    best_v[j] = run.v[j];
+    best_e[j] = run.e[j];
+  }
+}
+
+// KT = top_k (compile-time: top-1 / top-2 run the pairwise tree, KT >= 3 a
+// KT-slot sorted insertion).
 // Two CTAs per SM: the per-tile chain (TMA -> MMA -> top-k epilogue) is
 // latency-bound, a second resident CTA overlaps it (measured: 1.3x over one).
 template <int KT>
@@ -80,6 +179,10 @@ __global__ void __launch_bounds__(kThreads, kCtas)
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(2 * a.Npad)) tmem_cols <<= 1;
 
+  if (threadIdx.x == 0) GATE_TRACE(0);
+#ifdef FM_GATE_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 512) g_gate_blocks[2 * blockIdx.x] = gtime();
+#endif
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&map_x);
     ptx::tma_prefetch_desc(&map_w);
@@ -93,35 +196,39 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     }
     ptx::fence_mbar_init();
   }
+#if FM_GATE_X_EVICT_FIRST
+  // x is streamed once: its lines are the first L2 victims, so the gate does
+  // not evict (and pay the write-back of) the predecessor's dirty lines
+  const uint64_t pol_x = ptx::l2_policy_evict_first();
+#endif
+  auto issue = [&](int stage, int tile, int kb) {
+    ptx::mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
+#if FM_GATE_X_EVICT_FIRST
+    ptx::tma_load_2d_hint(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM, pol_x);
+#else
+    ptx::tma_load_2d(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM);
+#endif
+    ptx::tma_load_2d(smem_b + stage * b_bytes, &map_w, &full_bar[stage], kb * kBK, 0);
+  };
   for (int i = threadIdx.x; i < 4 * a.Npad; i += blockDim.x) masks[i] = 0;
   if (warp == 2) ptx::tmem_alloc(tmem_holder, tmem_cols);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) GATE_TRACE(1);
 
   // producer and MMA issuer: the whole warp runs the (warp-uniform) loop, one
   // elected lane issues — no per-instruction register->uniform shuffles
   if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
-#if FM_GATE_X_EVICT_FIRST
-    // x is streamed once: its lines are the first L2 victims, so the gate does
-    // not evict (and pay the write-back of) the predecessor's dirty lines
-    const uint64_t pol_x = ptx::l2_policy_evict_first();
-#endif
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       for (int kb = 0; kb < num_kb; ++kb) {
-        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-        if (ptx::elect_one()) {
-          ptx::mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
-#if FM_GATE_X_EVICT_FIRST
-          ptx::tma_load_2d_hint(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM, pol_x);
-#else
-          ptx::tma_load_2d(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM);
-#endif
-          ptx::tma_load_2d(smem_b + stage * b_bytes, &map_w, &full_bar[stage], kb * kBK, 0);
-        }
+        GATE_WAIT(&empty_bar[stage], phase ^ 1);
+        if (lane == 0) GATE_TRACE(2 + it * 16 + kb);
+        if (ptx::elect_one()) issue(stage, tile, kb);
         __syncwarp();
         if (++stage == a.stages) {
           stage = 0;
@@ -138,11 +245,12 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     int iter = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
       const int ab = iter & 1;
-      ptx::mbar_wait(&tempty_bar[ab], ((iter >> 1) & 1) ^ 1);
+      GATE_WAIT(&tempty_bar[ab], ((iter >> 1) & 1) ^ 1);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + ab * a.Npad;
       for (int kb = 0; kb < num_kb; ++kb) {
-        ptx::mbar_wait(&full_bar[stage], phase);
+        GATE_WAIT(&full_bar[stage], phase);
+        if (lane == 0) GATE_TRACE(66 + iter * 16 + kb);
         ptx::tc_fence_after();
         // descriptor start addresses are in 16-byte units: offsets are adds
         const uint64_t da = da0 + static_cast<uint32_t>((stage * kABytes) >> 4);
@@ -170,39 +278,44 @@ __global__ void __launch_bounds__(kThreads, kCtas)
       const int ab = iter & 1;
       const int t = tile * kTM + q * 32 + lane;
       const bool valid = t < a.T;
-      ptx::mbar_wait(&tfull_bar[ab], (iter >> 1) & 1);
+      GATE_WAIT(&tfull_bar[ab], (iter >> 1) & 1);
+      if (q == 0 && lane == 0) GATE_TRACE(130 + 2 * iter);
       ptx::tc_fence_after();
 
       float best_v[KT];
       int best_e[KT];
-#pragma unroll
-      for (int j = 0; j < KT; ++j) {
-        best_v[j] = -INFINITY;
-        best_e[j] = -1;
-      }
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + ab * a.Npad;
-      for (int c = 0; c < a.Npad; c += 32) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(t_row + c, r);
-        ptx::tmem_ld_wait();
+      if constexpr (KT <= 2) {
+        tree_topk<KT>(t_row, a.N, a.Npad, best_v, best_e);
+      } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int e = c + i;
-          const float v = __uint_as_float(r[i]);
-          // Sorted insertion, walking slots bottom-up: slot j takes slot j-1's
-          // entry when v beats it, else v itself when v beats slot j. Strict '>'
-          // while ids ascend keeps the lower id ahead on ties.
-          if (e < a.N) {
+        for (int j = 0; j < KT; ++j) {
+          best_v[j] = -INFINITY;
+          best_e[j] = -1;
+        }
+        for (int c = 0; c < a.Npad; c += 32) {
+          uint32_t r[32];
+          ptx::tmem_ld_32x32b_x32(t_row + c, r);
+          ptx::tmem_ld_wait();
 #pragma unroll
-            for (int j = KT - 1; j >= 0; --j) {
-              const bool beats_prev = j > 0 && (best_e[j - 1] < 0 || v > best_v[j - 1]);
-              const bool beats_cur = best_e[j] < 0 || v > best_v[j];
-              if (beats_prev) {
-                best_v[j] = best_v[j - 1];
-                best_e[j] = best_e[j - 1];
-              } else if (beats_cur) {
-                best_v[j] = v;
-                best_e[j] = e;
+          for (int i = 0; i < 32; ++i) {
+            const int e = c + i;
+            const float v = __uint_as_float(r[i]);
+            // Sorted insertion, walking slots bottom-up: slot j takes slot j-1's
+            // entry when v beats it, else v itself when v beats slot j. Strict '>'
+            // while ids ascend keeps the lower id ahead on ties.
+            if (e < a.N) {
+#pragma unroll
+              for (int j = KT - 1; j >= 0; --j) {
+                const bool beats_prev = j > 0 && (best_e[j - 1] < 0 || v > best_v[j - 1]);
+                const bool beats_cur = best_e[j] < 0 || v > best_v[j];
+                if (beats_prev) {
+                  best_v[j] = best_v[j - 1];
+                  best_e[j] = best_e[j - 1];
+                } else if (beats_cur) {
+                  best_v[j] = v;
+                  best_e[j] = e;
+                }
               }
             }
           }
@@ -225,7 +338,9 @@ __global__ void __launch_bounds__(kThreads, kCtas)
 #pragma unroll
         for (int j = 0; j < KT; ++j) atomicOr(&my_mask[best_e[j]], 1u << lane);
       }
+      if (q == 0 && lane == 0 && iter == 0) GATE_TRACE(141);
       named_bar_sync(1, 128);  // all four masks of this tile are final
+      if (q == 0 && lane == 0 && iter == 0) GATE_TRACE(142);
       if (valid) {
         const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
@@ -239,15 +354,19 @@ __global__ void __launch_bounds__(kThreads, kCtas)
           a.tile_rank[u] = rank;
         }
       }
+      if (q == 0 && lane == 0 && iter == 0) GATE_TRACE(143);
       const int et = q * 32 + lane;
       for (int e = et; e < a.N; e += 128) {
         a.tile_counts[static_cast<size_t>(tile) * a.N + e] =
             __popc(masks[e]) + __popc(masks[a.Npad + e]) + __popc(masks[2 * a.Npad + e]) +
             __popc(masks[3 * a.Npad + e]);
       }
+      if (q == 0 && lane == 0 && iter == 0) GATE_TRACE(144);
       named_bar_sync(1, 128);  // everyone done reading masks
+      if (q == 0 && lane == 0 && iter == 0) GATE_TRACE(145);
       for (int e = lane; e < a.Npad; e += 32) my_mask[e] = 0;
       __syncwarp();
+      if (q == 0 && lane == 0) GATE_TRACE(131 + 2 * iter);
     }
   }
 
@@ -257,9 +376,22 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, tmem_cols);
   }
+  if (threadIdx.x == 0) GATE_TRACE(150);
+#ifdef FM_GATE_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 512) g_gate_blocks[2 * blockIdx.x + 1] = gtime();
+#endif
 }
 
 }  // namespace gate
+
+#ifdef FM_GATE_TRACE
+extern "C" int fm_debug_gate_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, gate::g_gate_trace, sizeof(gate::g_gate_trace)) == cudaSuccess ? 0 : 5;
+}
+extern "C" int fm_debug_gate_blocks(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, gate::g_gate_blocks, sizeof(gate::g_gate_blocks)) == cudaSuccess ? 0 : 5;
+}
+#endif
 
 int gate_num_tiles(int T) { return (T + gate::kTM - 1) / gate::kTM; }
 

@@ -385,7 +385,21 @@ class Layer {
     // the dispatched units' share of dWg = per-tile column sums of X_perm
     // weighted by dl per row, reduced with db1 / db2 (dropped units: below)
     const bool dwg_tiles = dwg && cfg_.top_k > 1 && nl() > 0;
-#if FM_BWD_ORDER == 2
+#if FM_BWD_ORDER == 3
+    // as order 2, then un-permute right after the dgrad that produced dX_perm
+    // (its reads hit the dX_perm lines still in L2) and the bias / gate tile
+    // sums last: they only read, so the step ends with a clean L2 and the
+    // next step's gate does not pay the write-back of dx
+    if (nl() > 0) {
+      wgrad2(dw2, s);
+      dgrad2(saved_w2_, db1, s);
+      wgrad1(dw1, s);
+      dgrad1(saved_w1_, s);
+    }
+    unpermute(dx_perm_.p, saved_wg_, dx, s);
+    if (nl() > 0) bias_grads(db1, db2, s, dwg_tiles ? dwg : nullptr);
+    gate_wgrad(x_perm_.p, plan_.totals, static_cast<int>(row_cap_), dwg, s, dwg_tiles);
+#elif FM_BWD_ORDER == 2
     // each weight-gradient GEMM right before a dgrad GEMM: the dirty f32 dW
     // lines it leaves in L2 are written back while the next GEMM is
     // tensor-bound (HBM idle), not by the memory-bound kernels that follow
