@@ -131,6 +131,11 @@ __device__ __forceinline__ void wait_tile_sources(const Args& a, int mtile) {
 #ifndef FM_WGRAD_HINT
 #define FM_WGRAD_HINT 0
 #endif
+// wgrad tile order inside a group: 1 = the longer tile dimension outermost
+// (see decode_tile), 0 = row-major (round 1)
+#ifndef FM_WGRAD_RASTER
+#define FM_WGRAD_RASTER 1
+#endif
 
 struct Tile {
   int group;
@@ -219,8 +224,23 @@ __device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g, const 
     const int local = t - slot * per_group;
     g = tb.order_s[slot];
     tl.group = g;
-    tl.m0 = (local / n_tiles) * Cfg<CG>::kTileM + rank * kBM;
-    tl.n0 = (local % n_tiles) * kBN;
+    // Tiles of a group that run together share operand slices (each a
+    // K_g x 256 column block of A or B) through L2; a group whose tiles
+    // straddle two waves of clusters streams the slices of both parts.
+    // The longer tile dimension walks outermost, so a wave boundary cuts
+    // across it: the part before the cut needs every slice of the short
+    // dimension but few of the long one (dW2: 4 x 16 tiles, a 10-tile head
+    // reads 4 + 3 slices instead of 1 + 10).
+    const int m_tiles = a.M_w / Cfg<CG>::kTileM;
+#if FM_WGRAD_RASTER
+    const bool n_outer = n_tiles > m_tiles;
+#else
+    const bool n_outer = false;
+#endif
+    const int mi = n_outer ? local % m_tiles : local / n_tiles;
+    const int ni = n_outer ? local / m_tiles : local % n_tiles;
+    tl.m0 = mi * Cfg<CG>::kTileM + rank * kBM;
+    tl.n0 = ni * kBN;
     tl.k_row0 = tb.ss_s[g];
     tl.num_kb = tb.tp_s[slot];  // kb_s
     tl.mtile = 0;
