@@ -136,6 +136,13 @@ __device__ __forceinline__ void wait_tile_sources(const Args& a, int mtile) {
 #ifndef FM_WGRAD_RASTER
 #define FM_WGRAD_RASTER 1
 #endif
+// wgrad grid: 1 = group-aligned cluster count (see launch_cg), 0 = every SM
+// (default). Measured (profiles/r02_wgrad_traffic.log): aligned cuts the
+// configs[1] wgrad DRAM reads 19 % but costs 3-6 % of wgrad time at configs[2],
+// configs[4] and balanced loads (64 of 74 CTA pairs busy); steps unchanged.
+#ifndef FM_WGRAD_ALIGN
+#define FM_WGRAD_ALIGN 0
+#endif
 
 struct Tile {
   int group;
@@ -660,8 +667,28 @@ void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
   auto kern = grouped_gemm_kernel<SCHED, A_MN, B_MN, EPI, CG>;
   ensure_dynamic_smem(reinterpret_cast<const void*>(kern), C::kSmemBytes);
   int grid = num_sms() / CG * CG;
-  if (SCHED == kWgrad)
-    grid = std::min(grid, CG * std::max(1, args.num_groups * (args.M_w / C::kTileM) * (args.N / kBN)));
+  if (SCHED == kWgrad) {
+    const int tpg = (args.M_w / C::kTileM) * (args.N / kBN);  // output tiles per group
+    int clusters = grid / CG;
+#if FM_WGRAD_ALIGN
+    // Group-aligned waves: a cluster count that is a multiple (or a divisor) of
+    // the tiles per group puts all tiles of a group on the same wave, so they
+    // advance through the group's K rows together and read each operand slice
+    // from DRAM once (a group straddling two waves streams it twice). Each
+    // cluster walks the LPT-ordered groups with an identical history, so the
+    // waves stay aligned whatever the group sizes. Used when it keeps >= 3/4
+    // of the SMs busy (64 of 74 CTA pairs at d 1024 / f 4096, 72 at 768 / 3072).
+    int aligned = 0;
+    if (tpg <= clusters) {
+      aligned = tpg * (clusters / tpg);
+    } else {
+      for (int c = clusters; c >= 1 && !aligned; --c)
+        if (tpg % c == 0) aligned = c;
+    }
+    if (aligned * 4 >= clusters * 3) clusters = aligned;
+#endif
+    grid = std::min(clusters * CG, CG * std::max(1, args.num_groups * tpg));
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(C::kThreads);

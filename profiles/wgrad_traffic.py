@@ -31,8 +31,13 @@ def cfg1_rows():
     return rows
 
 
-DISTS = {"balanced": lambda: [8192] * 16, "one": lambda: [131072], "cfg1": cfg1_rows}
+DISTS = {"balanced": lambda: [8192] * 16, "one": lambda: [131072], "cfg1": cfg1_rows,
+         "two": lambda: [65536] * 2, "four": lambda: [32768] * 4, "eight": lambda: [16384] * 8}
 names = sys.argv[1:] or ["cfg1", "balanced", "one"]
+shapes = [(d, f), (f, d)]
+if names and names[0] in ("dW2", "dW1"):
+    shapes = [(d, f)] if names[0] == "dW2" else [(f, d)]
+    names = names[1:]
 for name in names:
     rows = DISTS[name]()
     pad = [((r + 127) // 128) * 128 for r in rows]
@@ -43,7 +48,7 @@ for name in names:
     st = torch.tensor(start, dtype=torch.int32, device="cuda")
     pr = torch.tensor(pad, dtype=torch.int32, device="cuda")
     G = len(rows)
-    for Mw, N in ((d, f), (f, d)):
+    for Mw, N in shapes:
         A = torch.randn(total, Mw, device="cuda").to(torch.bfloat16)
         B = torch.randn(total, N, device="cuda").to(torch.bfloat16)
         C = torch.empty(G, Mw, N, device="cuda", dtype=torch.float32)
