@@ -22,8 +22,10 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "fm_internal.h"
+#include "layer_plan.h"
 #include "sm100_ptx.cuh"
 
 namespace fm {
@@ -94,7 +96,60 @@ struct Args {
   const unsigned long long* tile_src_mask;
   unsigned long long epoch;
   int* arrive_err;
+  // kWgrad: the first gemm_clusters clusters run the tiles; the rest run the
+  // side job (per-tile column sums, memory-bound) concurrently on their SMs
+  int gemm_clusters;
+  ColsumSide side;
 };
+
+// Side role of a wgrad launch: the tile column sums of ColsumSide, one thread
+// group of cols/8 threads per (job, 128-row tile) item, 16 rows in flight.
+template <int THREADS>
+__device__ __forceinline__ void colsum_side(const ColsumSide& sd, int cta, int num_ctas) {
+  const int gt = sd.cols / 8;  // threads per item (one 16-byte column vector each)
+  const int groups = THREADS / gt;
+  const int grp = static_cast<int>(threadIdx.x) / gt, c8 = (static_cast<int>(threadIdx.x) % gt) * 8;
+  if (grp >= groups) return;
+  const int ntiles = sd.mtile_prefix[sd.Nl];
+  const int items = sd.njobs * ntiles;
+  for (int it = cta * groups + grp; it < items; it += num_ctas * groups) {
+    const int j = it / ntiles, tile = it - j * ntiles;
+    const __nv_bfloat16* buf = static_cast<const __nv_bfloat16*>(sd.buf[j]);
+    const float* row_w = sd.row_w[j];
+    int lo = 0, hi = sd.Nl;  // segment with mtile_prefix[lo] <= tile < mtile_prefix[lo + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (sd.mtile_prefix[mid] <= tile) lo = mid; else hi = mid;
+    }
+    while (lo + 1 < sd.Nl && sd.mtile_prefix[lo + 1] <= tile) ++lo;  // skip empty segments
+    const int r0 = tile * kBM;
+    const int r1 = min(r0 + kBM, sd.seg_start[lo] + sd.seg_real[lo]);  // pad rows carry nothing
+    float acc[8] = {};
+    constexpr int kB = 16;
+    for (int rb = r0; rb < r1; rb += kB) {
+      uint4 v[kB];
+      float w[kB];
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const int r = min(rb + i, r1 - 1);
+        v[i] = __ldg(reinterpret_cast<const uint4*>(buf + static_cast<size_t>(r) * sd.cols + c8));
+        w[i] = rb + i < r1 ? (row_w ? __ldg(row_w + r) : 1.0f) : 0.0f;
+      }
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const uint32_t q[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[2 * c] = fmaf(w[i], __uint_as_float(q[c] << 16), acc[2 * c]);
+          acc[2 * c + 1] = fmaf(w[i], __uint_as_float(q[c] & 0xffff0000u), acc[2 * c + 1]);
+        }
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(sd.partial[j] + static_cast<size_t>(tile) * sd.cols + c8);
+    dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
 
 // Producer-side wait for the sources of one A tile (acquire at system scope,
 // then a proxy fence so the TMA (async proxy) reads see the peers' stores).
@@ -295,7 +350,9 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
   const uint32_t lane = ptx::lane_id();
   const int rank = CG == 2 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
   const bool leader = rank == 0;
-  const int cluster = blockIdx.x / CG, num_clusters = gridDim.x / CG;
+  const int cluster = blockIdx.x / CG;
+  const int num_clusters = SCHED == kWgrad ? args.gemm_clusters : static_cast<int>(gridDim.x) / CG;
+  const bool side_cta = SCHED == kWgrad && cluster >= num_clusters;  // column-sum CTAs
   build_tables<SCHED, CG>(args, tb);
 
   if (warp == 0 && lane == 0) {
@@ -320,7 +377,10 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
 
   const int ntiles = total_tiles<SCHED, CG>(args, tb);
 
-  if (warp == 0) {
+  if (side_cta) {
+    colsum_side<C::kThreads>(args.side, static_cast<int>(blockIdx.x) - num_clusters * CG,
+                             static_cast<int>(gridDim.x) - num_clusters * CG);
+  } else if (warp == 0) {
     // ------------------------------------------------------------ producer (every CTA)
     // Whole warp, one elected lane issues (as for the MMA issuer below).
     {
@@ -662,32 +722,55 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
 
 template <int SCHED, bool A_MN, bool B_MN, int EPI, int CG>
 void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Args& args,
-               cudaStream_t stream) {
+               cudaStream_t stream, int* side_out = nullptr) {
   using C = Cfg<CG>;
   auto kern = grouped_gemm_kernel<SCHED, A_MN, B_MN, EPI, CG>;
   ensure_dynamic_smem(reinterpret_cast<const void*>(kern), C::kSmemBytes);
   int grid = num_sms() / CG * CG;
+  Args a = args;
   if (SCHED == kWgrad) {
     const int tpg = (args.M_w / C::kTileM) * (args.N / kBN);  // output tiles per group
     int clusters = grid / CG;
-#if FM_WGRAD_ALIGN
-    // Group-aligned waves: a cluster count that is a multiple (or a divisor) of
-    // the tiles per group puts all tiles of a group on the same wave, so they
-    // advance through the group's K rows together and read each operand slice
-    // from DRAM once (a group straddling two waves streams it twice). Each
-    // cluster walks the LPT-ordered groups with an identical history, so the
-    // waves stay aligned whatever the group sizes. Used when it keeps >= 3/4
-    // of the SMs busy (64 of 74 CTA pairs at d 1024 / f 4096, 72 at 768 / 3072).
-    int aligned = 0;
-    if (tpg <= clusters) {
-      aligned = tpg * (clusters / tpg);
-    } else {
-      for (int c = clusters; c >= 1 && !aligned; --c)
-        if (tpg % c == 0) aligned = c;
+    int side = 0;
+    if (args.side.njobs > 0) {
+      // Side clusters for the tile column sums: the spare clusters of a
+      // group-aligned split (64 of 74 CTA pairs at 64 tiles per group), used
+      // only when they can finish the sums inside the GEMM (~45 GB/s per SM
+      // next to a tensor-bound neighbour); otherwise no side job — the caller
+      // runs its own column-sum launch (measured: taking SMs the alignment
+      // does not free costs the GEMM more than the sums save).
+      const int aligned = tpg <= clusters ? tpg * (clusters / tpg) : 0;
+      const int spare = aligned ? clusters - aligned : 0;
+      const double gemm_s = 2.0 * args.side.est_rows * args.M_w * args.N / 1.1e15;
+      const double bytes = 2.0 * args.side.njobs * static_cast<double>(args.side.est_rows) * args.side.cols;
+      const double need = bytes / (std::max(gemm_s, 1e-9) * 45e9 * CG);
+      if (spare > 0 && spare >= need && spare * 4 <= clusters) side = spare;
+      clusters -= side;
     }
-    if (aligned * 4 >= clusters * 3) clusters = aligned;
+#if FM_WGRAD_ALIGN
+    else {
+      // Group-aligned waves: a cluster count that is a multiple (or a divisor) of
+      // the tiles per group puts all tiles of a group on the same wave, so they
+      // advance through the group's K rows together and read each operand slice
+      // from DRAM once (a group straddling two waves streams it twice). Each
+      // cluster walks the LPT-ordered groups with an identical history, so the
+      // waves stay aligned whatever the group sizes. Used when it keeps >= 3/4
+      // of the SMs busy (64 of 74 CTA pairs at d 1024 / f 4096, 72 at 768 / 3072).
+      int aligned = 0;
+      if (tpg <= clusters) {
+        aligned = tpg * (clusters / tpg);
+      } else {
+        for (int c = clusters; c >= 1 && !aligned; --c)
+          if (tpg % c == 0) aligned = c;
+      }
+      if (aligned * 4 >= clusters * 3) clusters = aligned;
+    }
 #endif
-    grid = std::min(clusters * CG, CG * std::max(1, args.num_groups * tpg));
+    a.gemm_clusters = std::min(clusters, std::max(1, args.num_groups * tpg));
+    a.side.clusters = side;
+    if (side == 0) a.side.njobs = 0;
+    if (side_out) *side_out = side;
+    grid = (a.gemm_clusters + side) * CG;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -701,7 +784,7 @@ void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  FM_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, args));
+  FM_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, a));
 }
 
 // CTA-pair tiles unless overridden (FM_GEMM_CTA_GROUP / fm_set_gemm_cta_group)
@@ -709,9 +792,9 @@ int g_cta_group = 0;  // 0 = auto
 
 template <int SCHED, bool A_MN, bool B_MN, int EPI>
 void launch(const CUtensorMap* maps1, const CUtensorMap* maps2, const Args& args, int cg,
-            cudaStream_t stream) {
-  if (cg == 2) launch_cg<SCHED, A_MN, B_MN, EPI, 2>(maps2[0], maps2[1], maps2[2], args, stream);
-  else launch_cg<SCHED, A_MN, B_MN, EPI, 1>(maps1[0], maps1[1], maps1[2], args, stream);
+            cudaStream_t stream, int* side_out = nullptr) {
+  if (cg == 2) launch_cg<SCHED, A_MN, B_MN, EPI, 2>(maps2[0], maps2[1], maps2[2], args, stream, side_out);
+  else launch_cg<SCHED, A_MN, B_MN, EPI, 1>(maps1[0], maps1[1], maps1[2], args, stream, side_out);
 }
 
 }  // namespace gemm
@@ -725,7 +808,8 @@ void set_gemm_cta_group(int cg) {
 void grouped_gemm(int variant, const void* A, const void* B, void* C, const float* bias,
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
-                  cudaStream_t stream, const ArrivalGate* gate, const int* b_slot, int b_groups) {
+                  cudaStream_t stream, const ArrivalGate* gate, const int* b_slot, int b_groups,
+                  ColsumSide* side) {
   using namespace gemm;
   if (N % kBN != 0) throw std::invalid_argument("grouped_gemm: N must be a multiple of 256");
   if (num_groups < 1 || num_groups > kMaxGroups)
@@ -808,7 +892,14 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
       m1[1] = m2[1] = make_tmap_bf16(B, N, total_rows, N, 64, kBK);
       m1[2] = m2[2] = make_tmap_2d(C, true, N, static_cast<uint64_t>(num_groups) * M_w, N, 16, 32, 64);
       a.b_rows_per_group = 0;
-      launch<kWgrad, true, true, kEpiF32>(m1, m2, a, cg, stream);
+      if (side && side->njobs > 0) {
+        if (side->cols % 8 != 0 || side->cols > 8 * Cfg<1>::kThreads)
+          throw std::invalid_argument("grouped_gemm: side column sums need cols % 8 == 0, cols <= 2048");
+        a.side = *side;
+      }
+      int side_clusters = 0;
+      launch<kWgrad, true, true, kEpiF32>(m1, m2, a, cg, stream, &side_clusters);
+      if (side) side->clusters = side_clusters;  // 0: the column sums did not run
       break;
     }
     default:

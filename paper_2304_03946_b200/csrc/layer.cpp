@@ -31,6 +31,11 @@
 #ifndef FM_BWD_ORDER
 #define FM_BWD_ORDER 2
 #endif
+// A/B knob: the bias / gate-weight tile column sums run on spare CTA pairs of
+// the FFN2 weight-gradient GEMM launch (1) instead of their own launch (0)
+#ifndef FM_COLSUM_SIDE
+#define FM_COLSUM_SIDE 1
+#endif
 
 namespace fm {
 
@@ -405,11 +410,14 @@ class Layer {
     // tensor-bound (HBM idle), not by the memory-bound kernels that follow
     // the last one (the next step's gate paid it: profiles/r02_gate_context.log)
     if (nl() > 0) {
-      wgrad2(dw2, s);                  // dY_perm, act
+      // the db2 / dWg tile column sums (memory-bound) ride on spare CTA pairs
+      // of the first weight-gradient launch (tensor-bound)
+      ColsumSide side = tile_sum_side(db2, dwg_tiles ? dwg : nullptr);
+      wgrad2(dw2, s, &side);           // dY_perm, act (+ tile column sums)
       dgrad2(saved_w2_, db1, s);       // dY_perm, W2 -> dH (+ db1 tile partials)
       wgrad1(dw1, s);                  // dH, X_perm
       dgrad1(saved_w1_, s);            // dH, W1 -> dX_perm
-      bias_grads(db1, db2, s, dwg_tiles ? dwg : nullptr);
+      bias_grads(db1, db2, s, dwg_tiles ? dwg : nullptr, /*sums_done=*/side.clusters > 0);
     }
     unpermute_backward(dx_perm_.p, x_perm_.p, plan_.totals, static_cast<int>(row_cap_), saved_wg_, dx,
                        dwg, s, dwg_tiles);
@@ -550,8 +558,10 @@ class Layer {
     }
     expert_dgrad(w1, w2, db1, s, gate);
     if (signal_dx) p2p_signal(3, s);
-    expert_wgrad(dw1, dw2, s);
-    bias_grads(db1, db2, s, dwg_tiles);
+    ColsumSide side = tile_sum_side(db2, dwg_tiles);
+    wgrad2(dw2, s, &side);
+    wgrad1(dw1, s);
+    bias_grads(db1, db2, s, dwg_tiles, /*sums_done=*/side.clusters > 0);
   }
 
   // dH (masked by relu'), db1 tile partials, dX_perm
@@ -587,13 +597,15 @@ class Layer {
     wgrad2(dw2, s);
     wgrad1(dw1, s);
   }
-  // dW2[li] = dY^T . act  [d, f]
-  void wgrad2(float* dw2, cudaStream_t s) {
+  // dW2[li] = dY^T . act  [d, f]; side (optional): tile column sums run by
+  // spare CTA pairs of the same launch
+  void wgrad2(float* dw2, cudaStream_t s, ColsumSide* side = nullptr) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0 || !dw2) return;
     timer_.begin(FM_PHASE_FFN2_WGRAD, s);
     grouped_gemm(FM_GEMM_WGRAD, dy_perm_.p, act_.p, dw2, nullptr, nullptr, plan_.seg_start,
-                 plan_.seg_rows, nullptr, Nl, static_cast<int>(row_cap_), d, f, 0, s);
+                 plan_.seg_rows, nullptr, Nl, static_cast<int>(row_cap_), d, f, 0, s, nullptr, nullptr, 0,
+                 side);
     timer_.end(s);
   }
   // dW1[li] = dH^T . X  [f, d]
@@ -606,18 +618,48 @@ class Layer {
     timer_.end(s);
   }
 
+  // The db2 / dWg tile column-sum jobs (dY_perm; dl-weighted X_perm) as a
+  // side job of a weight-gradient launch (FM_COLSUM_SIDE), else none.
+  ColsumSide tile_sum_side(float* db2, float* dwg_tiles) {
+    ColsumSide sd{};
+    const int Nl = nl(), d = cfg_.d_model;
+    if (!FM_COLSUM_SIDE || Nl == 0) return sd;
+    const int max_tiles = static_cast<int>(row_cap_ / 128);
+    float* part_db2 = tile_sum_.as<float>();
+    float* part_dwg = part_db2 + static_cast<size_t>(max_tiles) * d;
+    if (dwg_tiles) {
+      sd.buf[sd.njobs] = x_perm_.p;
+      sd.row_w[sd.njobs] = dl_rows_.as<float>();
+      sd.partial[sd.njobs++] = part_dwg;
+    }
+    if (db2) {
+      sd.buf[sd.njobs] = dy_perm_.p;
+      sd.row_w[sd.njobs] = nullptr;
+      sd.partial[sd.njobs++] = part_db2;
+    }
+    sd.cols = d;
+    sd.mtile_prefix = plan_.mtile_prefix;
+    sd.seg_start = plan_.seg_start;
+    sd.seg_real = plan_.seg_real;
+    sd.Nl = Nl;
+    sd.est_rows = cur_T_ * cfg_.top_k;
+    return sd;
+  }
+
   // bias / gate-weight gradients: per-128-row-tile column sums (db1's come from
-  // the dgrad epilogue; dY_perm's and the dl-weighted X_perm's here), then one
+  // the dgrad epilogue; dY_perm's and the dl-weighted X_perm's here, or already
+  // on the side of the FFN2 weight-gradient launch: sums_done), then one
   // fixed-order reduce per segment (deterministic, no atomics)
-  void bias_grads(float* db1, float* db2, cudaStream_t s, float* dwg_tiles) {
+  void bias_grads(float* db1, float* db2, cudaStream_t s, float* dwg_tiles, bool sums_done = false) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0) return;
     timer_.begin(FM_PHASE_BIAS_GRAD, s);
     const int max_tiles = static_cast<int>(row_cap_ / 128);
     float* part_db2 = tile_sum_.as<float>();
     float* part_dwg = part_db2 + static_cast<size_t>(max_tiles) * d;
-    launch_segment_tile_colsum(dwg_tiles ? x_perm_.p : nullptr, dl_rows_.as<float>(), part_dwg,
-                               db2 ? dy_perm_.p : nullptr, nullptr, part_db2, d, plan_, Nl, max_tiles, s);
+    if (!sums_done)
+      launch_segment_tile_colsum(dwg_tiles ? x_perm_.p : nullptr, dl_rows_.as<float>(), part_dwg,
+                                 db2 ? dy_perm_.p : nullptr, nullptr, part_db2, d, plan_, Nl, max_tiles, s);
     if (dwg_tiles && Nl < cfg_.num_experts)  // experts hosted elsewhere keep a zero row here
       FM_CUDA(cudaMemsetAsync(dwg_tiles, 0, sizeof(float) * cfg_.num_experts * d, s));
     launch_segment_tile_reduce(tile_colsum_.as<float>(), f, nullptr, db1, part_db2, d, nullptr, db2, part_dwg, d,

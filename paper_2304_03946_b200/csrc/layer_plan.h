@@ -25,6 +25,24 @@ struct PlanDev {
   unsigned long long* tile_src_mask;  // [rows/128] P2P: sources with rows in each 128-row tile
 };
 
+// Per-128-row-tile column sums run by spare CTA pairs of a weight-gradient
+// GEMM launch: job j writes partial[j][tile][c] = sum over the
+// tile's real rows r of (row_w[j] ? row_w[j][r] : 1) * buf[j][r][c], exactly
+// what segment_tile_colsum_kernel computes (same row order, same fmaf chain).
+struct ColsumSide {
+  const void* buf[2];  // bf16 [rows][cols]
+  const float* row_w[2];
+  float* partial[2];   // f32 [tiles][cols]
+  int njobs;           // 0 = no side work
+  int cols;
+  const int32_t* mtile_prefix;  // PlanDev fields of the segments
+  const int32_t* seg_start;
+  const int32_t* seg_real;
+  int Nl;
+  int clusters;   // CTA pairs (or CTAs) of the launch given to the sums; set by the launcher
+  int est_rows;   // host estimate of the GEMM's reduction rows (sizes `clusters`)
+};
+
 // Peer-to-peer transport: every GPU's exchange arena holds its
 // X_perm, Y_perm, dY_perm, dX_perm (bf16 rows), dl per X_perm row (f32) and
 // the arrival flags, at the same offsets on every GPU; base[g] is GPU g's
