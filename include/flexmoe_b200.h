@@ -34,6 +34,9 @@ extern "C" {
 
 const char* fm_last_error(void);
 const char* fm_version(void);
+/* Diagnostics: kernels this library has launched in this process (all
+ * devices, all threads); bench.py reports the count over its timed region. */
+unsigned long long fm_kernel_launches(void);
 
 /* ------------------------------------------------------------------------
  * Count-level routing (host). Layouts follow the reference value types:

@@ -150,7 +150,7 @@ _SIGNATURES = {
     "fm_pool_adam": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "fm_pool_migration_stats": [_P, _P, _P, _P],
 }
-_RESTYPES = {"fm_last_error": C.c_char_p, "fm_version": C.c_char_p}
+_RESTYPES = {"fm_last_error": C.c_char_p, "fm_version": C.c_char_p, "fm_kernel_launches": C.c_ulonglong}
 
 _lib = None
 
@@ -166,8 +166,9 @@ def lib() -> C.CDLL:
             )
         handle = C.CDLL(str(_LIB_PATH))
         for name, res in _RESTYPES.items():
-            getattr(handle, name).restype = res
-            getattr(handle, name).argtypes = []
+            if hasattr(handle, name):
+                getattr(handle, name).restype = res
+                getattr(handle, name).argtypes = []
         for name, args in _SIGNATURES.items():
             if hasattr(handle, name):
                 fn = getattr(handle, name)

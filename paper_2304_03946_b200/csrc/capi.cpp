@@ -2,6 +2,7 @@
 // thin extern "C" wrappers that translate exceptions into status codes.
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -16,6 +17,11 @@ thread_local std::string g_last_error;
 }
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+std::atomic<unsigned long long> g_launches{0};
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int num_sms() {
   static int sms = [] {
@@ -93,6 +99,8 @@ extern "C" {
 const char* fm_last_error(void) { return fm::g_last_error.c_str(); }
 
 const char* fm_version(void) { return "flexmoe_b200 0.1 (sm_100a)"; }
+
+unsigned long long fm_kernel_launches(void) { return fm::g_launches.load(std::memory_order_relaxed); }
 
 int fm_set_gemm_cta_group(int cta_group) {
   return fm::guarded([&] { fm::set_gemm_cta_group(cta_group); });

@@ -51,8 +51,12 @@ inline void check_cuda(cudaError_t err, const char* what) {
   }
 }
 
+// Kernels this library launched in the process (fm_kernel_launches): every
+// launch site ends in FM_LAUNCH_CHECK, or calls count_launch() itself.
+void count_launch();
+
 #define FM_CUDA(call) ::fm::check_cuda((call), #call)
-#define FM_LAUNCH_CHECK(name) ::fm::check_cuda(cudaGetLastError(), name)
+#define FM_LAUNCH_CHECK(name) (::fm::count_launch(), ::fm::check_cuda(cudaGetLastError(), name))
 
 // 2-D bf16 tensor map, 128B swizzle: inner dimension `inner` (contiguous),
 // `outer` rows `row_stride_elems` apart; box = box_inner x box_outer.
@@ -72,7 +76,7 @@ int num_sms();
 void ensure_dynamic_smem(const void* kernel, int bytes);
 
 // P2P arrival gating of a token-row grouped GEMM (see grouped_gemm.cu Args).
-struct ColsumSide;  // layer_plan.h
+struct SideJob;  // layer_plan.h
 
 struct ArrivalGate {
   const unsigned long long* flags = nullptr;          // this GPU's flags of one exchange slot [src]
@@ -85,6 +89,6 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
                   cudaStream_t stream, const ArrivalGate* gate = nullptr, const int* b_slot = nullptr,
-                  int b_groups = 0, ColsumSide* side = nullptr);
+                  int b_groups = 0, SideJob* side = nullptr);
 
 }  // namespace fm

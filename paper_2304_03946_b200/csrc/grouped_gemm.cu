@@ -99,13 +99,13 @@ struct Args {
   // kWgrad: the first gemm_clusters clusters run the tiles; the rest run the
   // side job (per-tile column sums, memory-bound) concurrently on their SMs
   int gemm_clusters;
-  ColsumSide side;
+  SideJob side;
 };
 
-// Side role of a wgrad launch: the tile column sums of ColsumSide, one thread
+// Side role of a wgrad launch: the tile column sums of SideJob, one thread
 // group of cols/8 threads per (job, 128-row tile) item, 16 rows in flight.
 template <int THREADS>
-__device__ __forceinline__ void colsum_side(const ColsumSide& sd, int cta, int num_ctas) {
+__device__ __forceinline__ void colsum_side(const SideJob& sd, int cta, int num_ctas) {
   const int gt = sd.cols / 8;  // threads per item (one 16-byte column vector each)
   const int groups = THREADS / gt;
   const int grp = static_cast<int>(threadIdx.x) / gt, c8 = (static_cast<int>(threadIdx.x) % gt) * 8;
@@ -310,6 +310,97 @@ __device__ __forceinline__ Tile decode_tile(const Args& a, int t, int& g, const 
   return tl;
 }
 
+// Side role, kind 2: un-permute, warp per token (VPL = d / 256 16-byte
+// vectors per lane), the unpermute_bwd_kernel arithmetic: the k dX rows added
+// in unit order, then the k gate rows scaled by dl, one bf16 rounding.
+template <int VPL>
+__device__ __forceinline__ void unpermute_side_vpl(const SideJob& sd, int cta, int num_ctas, int threads) {
+  const int lane = threadIdx.x & 31;
+  const int warps = threads >> 5;
+  const __nv_bfloat16* dXp = static_cast<const __nv_bfloat16*>(sd.dXp);
+  const __nv_bfloat16* wg = static_cast<const __nv_bfloat16*>(sd.wg);
+  __nv_bfloat16* dx = static_cast<__nv_bfloat16*>(sd.dx);
+  const int d = VPL * 256, k = sd.k;
+  auto load = [&](const __nv_bfloat16* base, size_t row, uint4 (&q)[VPL]) {
+    const uint4* src = reinterpret_cast<const uint4*>(base + row * static_cast<size_t>(d));
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) q[i] = __ldg(src + lane + 32 * i);
+  };
+  auto axpy = [&](float (&acc)[VPL][8], const uint4 (&q)[VPL], float a) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const uint32_t qs[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        acc[i][2 * c] = fmaf(a, __uint_as_float(qs[c] << 16), acc[i][2 * c]);
+        acc[i][2 * c + 1] = fmaf(a, __uint_as_float(qs[c] & 0xffff0000u), acc[i][2 * c + 1]);
+      }
+    }
+  };
+  for (int t = cta * warps + static_cast<int>(threadIdx.x >> 5); t < sd.T; t += num_ctas * warps) {
+    const size_t base = static_cast<size_t>(t) * k;
+    int my_pos = 0, my_e = 0;
+    float my_dl = 0.0f;
+    if (lane < k) {
+      my_pos = __ldg(sd.pos + base + lane);
+      my_e = __ldg(sd.idx + base + lane);
+      if (sd.gate_grad) my_dl = __ldg(sd.dl + base + lane);
+    }
+    float acc[VPL][8];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[i][c] = 0.0f;
+    for (int j = 0; j < k; j += 2) {
+      const bool two = j + 1 < k;
+      const int p0 = __shfl_sync(0xffffffffu, my_pos, j);
+      const int p1 = __shfl_sync(0xffffffffu, my_pos, two ? j + 1 : j);
+      uint4 q0[VPL], q1[VPL];
+      const bool h0 = p0 >= 0, h1 = two && p1 >= 0;
+      if (h0) load(dXp, p0, q0);
+      if (h1) load(dXp, p1, q1);
+      if (h0) axpy(acc, q0, 1.0f);
+      if (h1) axpy(acc, q1, 1.0f);
+    }
+    if (sd.gate_grad) {
+      for (int j = 0; j < k; ++j) {
+        const int e = __shfl_sync(0xffffffffu, my_e, j);
+        const float g_l = __shfl_sync(0xffffffffu, my_dl, j);
+        uint4 q[VPL];
+        load(wg, e, q);
+        axpy(acc, q, g_l);
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(dx + static_cast<size_t>(t) * d);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      uint32_t pk[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        __nv_bfloat162 v = __floats2bfloat162_rn(acc[i][2 * c], acc[i][2 * c + 1]);
+        pk[c] = *reinterpret_cast<uint32_t*>(&v);
+      }
+      dst[lane + 32 * i] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+  }
+}
+
+template <int THREADS>
+__device__ __forceinline__ void run_side(const SideJob& sd, int cta, int num_ctas) {
+  if (sd.kind == 1) {
+    colsum_side<THREADS>(sd, cta, num_ctas);
+  } else if (sd.kind == 2) {
+    switch (sd.d / 256) {
+      case 1: unpermute_side_vpl<1>(sd, cta, num_ctas, THREADS); break;
+      case 2: unpermute_side_vpl<2>(sd, cta, num_ctas, THREADS); break;
+      case 3: unpermute_side_vpl<3>(sd, cta, num_ctas, THREADS); break;
+      case 4: unpermute_side_vpl<4>(sd, cta, num_ctas, THREADS); break;
+      case 6: unpermute_side_vpl<6>(sd, cta, num_ctas, THREADS); break;
+      default: unpermute_side_vpl<8>(sd, cta, num_ctas, THREADS); break;
+    }
+  }
+}
+
 // relu + round to a bf16 pair in one instruction (lo in the low half)
 __device__ __forceinline__ uint32_t pack_relu_bf16(float lo, float hi) {
   uint32_t r;
@@ -378,8 +469,8 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
   const int ntiles = total_tiles<SCHED, CG>(args, tb);
 
   if (side_cta) {
-    colsum_side<C::kThreads>(args.side, static_cast<int>(blockIdx.x) - num_clusters * CG,
-                             static_cast<int>(gridDim.x) - num_clusters * CG);
+    run_side<C::kThreads>(args.side, static_cast<int>(blockIdx.x) - num_clusters * CG,
+                          static_cast<int>(gridDim.x) - num_clusters * CG);
   } else if (warp == 0) {
     // ------------------------------------------------------------ producer (every CTA)
     // Whole warp, one elected lane issues (as for the MMA issuer below).
@@ -732,7 +823,7 @@ void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
     const int tpg = (args.M_w / C::kTileM) * (args.N / kBN);  // output tiles per group
     int clusters = grid / CG;
     int side = 0;
-    if (args.side.njobs > 0) {
+    if (args.side.kind != 0) {
       // Side clusters for the tile column sums: the spare clusters of a
       // group-aligned split (64 of 74 CTA pairs at 64 tiles per group), used
       // only when they can finish the sums inside the GEMM (~45 GB/s per SM
@@ -742,7 +833,9 @@ void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
       const int aligned = tpg <= clusters ? tpg * (clusters / tpg) : 0;
       const int spare = aligned ? clusters - aligned : 0;
       const double gemm_s = 2.0 * args.side.est_rows * args.M_w * args.N / 1.1e15;
-      const double bytes = 2.0 * args.side.njobs * static_cast<double>(args.side.est_rows) * args.side.cols;
+      const double bytes =
+          args.side.kind == 1 ? 2.0 * args.side.njobs * static_cast<double>(args.side.est_rows) * args.side.cols
+                              : 2.0 * (static_cast<double>(args.side.T) * args.side.k + args.side.T) * args.side.d;
       const double need = bytes / (std::max(gemm_s, 1e-9) * 45e9 * CG);
       if (spare > 0 && spare >= need && spare * 4 <= clusters) side = spare;
       clusters -= side;
@@ -768,7 +861,7 @@ void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
 #endif
     a.gemm_clusters = std::min(clusters, std::max(1, args.num_groups * tpg));
     a.side.clusters = side;
-    if (side == 0) a.side.njobs = 0;
+    if (side == 0) a.side.kind = 0;
     if (side_out) *side_out = side;
     grid = (a.gemm_clusters + side) * CG;
   }
@@ -785,6 +878,7 @@ void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   FM_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, a));
+  count_launch();
 }
 
 // CTA-pair tiles unless overridden (FM_GEMM_CTA_GROUP / fm_set_gemm_cta_group)
@@ -809,7 +903,7 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
                   cudaStream_t stream, const ArrivalGate* gate, const int* b_slot, int b_groups,
-                  ColsumSide* side) {
+                  SideJob* side) {
   using namespace gemm;
   if (N % kBN != 0) throw std::invalid_argument("grouped_gemm: N must be a multiple of 256");
   if (num_groups < 1 || num_groups > kMaxGroups)
@@ -892,9 +986,14 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
       m1[1] = m2[1] = make_tmap_bf16(B, N, total_rows, N, 64, kBK);
       m1[2] = m2[2] = make_tmap_2d(C, true, N, static_cast<uint64_t>(num_groups) * M_w, N, 16, 32, 64);
       a.b_rows_per_group = 0;
-      if (side && side->njobs > 0) {
-        if (side->cols % 8 != 0 || side->cols > 8 * Cfg<1>::kThreads)
+      if (side && side->kind == 1) {
+        if (side->njobs < 1 || side->cols % 8 != 0 || side->cols > 8 * Cfg<1>::kThreads)
           throw std::invalid_argument("grouped_gemm: side column sums need cols % 8 == 0, cols <= 2048");
+        a.side = *side;
+      } else if (side && side->kind == 2) {
+        const int v = side->d / 256;
+        if (side->d % 256 != 0 || !(v == 1 || v == 2 || v == 3 || v == 4 || v == 6 || v == 8) || side->k < 1)
+          throw std::invalid_argument("grouped_gemm: side un-permute needs d in {256,512,768,1024,1536,2048}");
         a.side = *side;
       }
       int side_clusters = 0;

@@ -29,7 +29,7 @@
 // 2 = wgrad2, dgrad2, wgrad1, dgrad1 (each f32 weight-gradient drain overlaps a
 // tensor-bound GEMM)
 #ifndef FM_BWD_ORDER
-#define FM_BWD_ORDER 2
+#define FM_BWD_ORDER 4
 #endif
 // A/B knob: the bias / gate-weight tile column sums run on spare CTA pairs of
 // the FFN2 weight-gradient GEMM launch (1) instead of their own launch (0)
@@ -390,7 +390,27 @@ class Layer {
     // the dispatched units' share of dWg = per-tile column sums of X_perm
     // weighted by dl per row, reduced with db1 / db2 (dropped units: below)
     const bool dwg_tiles = dwg && cfg_.top_k > 1 && nl() > 0;
-#if FM_BWD_ORDER == 3
+#if FM_BWD_ORDER == 4
+    // The memory-bound backward work rides on spare CTA pairs of the two
+    // weight-gradient launches (each runs group-aligned on 64 of 74 pairs):
+    // the db2 / dWg tile column sums beside FFN2's (they need dY_perm, dl),
+    // the un-permute beside FFN1's, which therefore runs after both dgrads
+    // (it needs dX_perm). What a launch cannot host (no spare pairs at this
+    // shape) runs as its own kernel afterwards.
+    bool unpermuted = false;
+    if (nl() > 0) {
+      SideJob sums = tile_sum_side(db2, dwg_tiles ? dwg : nullptr);
+      wgrad2(dw2, s, &sums);           // dY_perm, act (+ tile column sums)
+      dgrad2(saved_w2_, db1, s);       // dY_perm, W2 -> dH (+ db1 tile partials)
+      dgrad1(saved_w1_, s);            // dH, W1 -> dX_perm
+      SideJob unp = unpermute_side(dx);
+      wgrad1(dw1, s, &unp);            // dH, X_perm (+ un-permute)
+      unpermuted = unp.clusters > 0;
+      bias_grads(db1, db2, s, dwg_tiles ? dwg : nullptr, /*sums_done=*/sums.clusters > 0);
+    }
+    if (!unpermuted) unpermute(dx_perm_.p, saved_wg_, dx, s);
+    gate_wgrad(x_perm_.p, plan_.totals, static_cast<int>(row_cap_), dwg, s, dwg_tiles);
+#elif FM_BWD_ORDER == 3
     // as order 2, then un-permute right after the dgrad that produced dX_perm
     // (its reads hit the dX_perm lines still in L2) and the bias / gate tile
     // sums last: they only read, so the step ends with a clean L2 and the
@@ -412,7 +432,7 @@ class Layer {
     if (nl() > 0) {
       // the db2 / dWg tile column sums (memory-bound) ride on spare CTA pairs
       // of the first weight-gradient launch (tensor-bound)
-      ColsumSide side = tile_sum_side(db2, dwg_tiles ? dwg : nullptr);
+      SideJob side = tile_sum_side(db2, dwg_tiles ? dwg : nullptr);
       wgrad2(dw2, s, &side);           // dY_perm, act (+ tile column sums)
       dgrad2(saved_w2_, db1, s);       // dY_perm, W2 -> dH (+ db1 tile partials)
       wgrad1(dw1, s);                  // dH, X_perm
@@ -558,7 +578,7 @@ class Layer {
     }
     expert_dgrad(w1, w2, db1, s, gate);
     if (signal_dx) p2p_signal(3, s);
-    ColsumSide side = tile_sum_side(db2, dwg_tiles);
+    SideJob side = tile_sum_side(db2, dwg_tiles);
     wgrad2(dw2, s, &side);
     wgrad1(dw1, s);
     bias_grads(db1, db2, s, dwg_tiles, /*sums_done=*/side.clusters > 0);
@@ -599,7 +619,7 @@ class Layer {
   }
   // dW2[li] = dY^T . act  [d, f]; side (optional): tile column sums run by
   // spare CTA pairs of the same launch
-  void wgrad2(float* dw2, cudaStream_t s, ColsumSide* side = nullptr) {
+  void wgrad2(float* dw2, cudaStream_t s, SideJob* side = nullptr) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0 || !dw2) return;
     timer_.begin(FM_PHASE_FFN2_WGRAD, s);
@@ -608,22 +628,45 @@ class Layer {
                  side);
     timer_.end(s);
   }
-  // dW1[li] = dH^T . X  [f, d]
-  void wgrad1(float* dw1, cudaStream_t s) {
+  // dW1[li] = dH^T . X  [f, d]; side (optional): memory-bound work run by
+  // spare CTA pairs of the same launch
+  void wgrad1(float* dw1, cudaStream_t s, SideJob* side = nullptr) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0 || !dw1) return;
     timer_.begin(FM_PHASE_FFN1_WGRAD, s);
     grouped_gemm(FM_GEMM_WGRAD, dh_.p, x_perm_.p, dw1, nullptr, nullptr, plan_.seg_start,
-                 plan_.seg_rows, nullptr, Nl, static_cast<int>(row_cap_), f, d, 0, s);
+                 plan_.seg_rows, nullptr, Nl, static_cast<int>(row_cap_), f, d, 0, s, nullptr, nullptr, 0,
+                 side);
     timer_.end(s);
+  }
+
+  // The single-GPU un-permute (dx from dX_perm and the gate rows) as a side
+  // job of a weight-gradient launch.
+  SideJob unpermute_side(void* dx) {
+    SideJob sd{};
+    if (!FM_COLSUM_SIDE || cfg_.num_gpus != 1 || !dx || cur_T_ <= 0) return sd;
+    sd.kind = 2;
+    sd.dXp = dx_perm_.p;
+    sd.pos = pos_.as<int32_t>();
+    sd.idx = topk_idx_.as<int32_t>();
+    sd.dl = dl_.as<float>();
+    sd.wg = saved_wg_;
+    sd.dx = dx;
+    sd.T = cur_T_;
+    sd.k = cfg_.top_k;
+    sd.d = cfg_.d_model;
+    sd.gate_grad = cfg_.top_k > 1 ? 1 : 0;
+    sd.est_rows = cur_T_ * cfg_.top_k;
+    return sd;
   }
 
   // The db2 / dWg tile column-sum jobs (dY_perm; dl-weighted X_perm) as a
   // side job of a weight-gradient launch (FM_COLSUM_SIDE), else none.
-  ColsumSide tile_sum_side(float* db2, float* dwg_tiles) {
-    ColsumSide sd{};
+  SideJob tile_sum_side(float* db2, float* dwg_tiles) {
+    SideJob sd{};
     const int Nl = nl(), d = cfg_.d_model;
     if (!FM_COLSUM_SIDE || Nl == 0) return sd;
+    sd.kind = 1;
     const int max_tiles = static_cast<int>(row_cap_ / 128);
     float* part_db2 = tile_sum_.as<float>();
     float* part_dwg = part_db2 + static_cast<size_t>(max_tiles) * d;
@@ -637,6 +680,7 @@ class Layer {
       sd.row_w[sd.njobs] = nullptr;
       sd.partial[sd.njobs++] = part_db2;
     }
+    if (sd.njobs == 0) return SideJob{};
     sd.cols = d;
     sd.mtile_prefix = plan_.mtile_prefix;
     sd.seg_start = plan_.seg_start;
