@@ -554,6 +554,7 @@ def run_ours(args, world, rank, local_rank):
         ms = float(t.item())
     ms_step = ms / args.steps
     hist = arm.hist()
+    side = arm.layer.side_jobs if hasattr(arm.layer, "side_jobs") else 0
     flows = arm.flows()
     units = int(hist.sum())  # this GPU's demand units (T * k)
     recv_units = int(flows[:, :, rank].sum())  # units this GPU's experts processed
@@ -638,10 +639,14 @@ def run_ours(args, world, rank, local_rank):
         "combine_bwd": T * d * 2 + units * (d * 2 * 2 + 12),
         "unpermute": units * (d * 2 + 12) + T * d * 2,
         # fused path: per-tile column sums of dY_perm (db2) and dl-weighted X_perm (dWg)
-        # + the db1/db2/dWg partial reduces
-        "bias_grad": (units * (2 * d * 2 + 4) + 4 * (units // 128) * (f + 2 * d) * 2) if not multi else None,
+        # + the db1/db2/dWg partial reduces; the reduces alone when the sums ran
+        # beside the FFN2 weight-gradient GEMM (side_jobs bit 0)
+        "bias_grad": (None if multi else 4 * (units // 128) * (f + 2 * d) * 2 if side & 1 else
+                      units * (2 * d * 2 + 4) + 4 * (units // 128) * (f + 2 * d) * 2),
         "relayout": 4 * recv_units * d * 2,
     }
+    side_bytes = {"ffn2_wgrad": (1, "db2 / dWg tile column sums", units * (2 * d * 2 + 4)),
+                  "ffn1_wgrad": (2, "un-permute", units * (d * 2 + 12) + T * d * 2)}
     kernels = {}
     for name, (pms, n) in phases.items():
         if n == 0:
@@ -654,6 +659,9 @@ def run_ours(args, world, rank, local_rank):
         if name in gemm_names and per > 0:
             tf = 2.0 * recv_units * d * f / (per * 1e-3) / 1e12
             ent.update({"achieved_TFLOPs": round(tf, 1), "frac_bf16": round(tf / peaks["bf16"], 3)})
+            if name in side_bytes and side & side_bytes[name][0]:
+                ent["side_job"] = {"what": side_bytes[name][1] + " on the launch's spare CTA pairs",
+                                   "hbm_bytes_per_step": side_bytes[name][2]}
         kernels[name] = ent
     for name, (cms, n) in comm.items():
         kernels["comm_" + name] = {"ms_per_step": round(cms / args.steps, 4),

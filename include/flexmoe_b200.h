@@ -359,6 +359,11 @@ int fm_layer_set_operand_slots(fm_layer* layer, const int32_t* slot_N, int capac
  * 0 or +inf disables drops (the FlexMoE mode, which never drops). */
 int fm_layer_set_capacity_factor(fm_layer* layer, double capacity_factor);
 int fm_layer_local_experts(const fm_layer* layer, int* num_local, int32_t* experts_out);
+/* Which memory-bound backward work of the last backward ran on spare CTA pairs
+ * of a weight-gradient GEMM launch instead of its own kernel:
+ * bit 0 the db2 / dWg tile column sums (FFN2 wgrad), bit 1 the un-permute
+ * (FFN1 wgrad). Results are the same either way. */
+int fm_layer_side_jobs(const fm_layer* layer, int* mask);
 
 /* Single-GPU (num_gpus == 1) fused step; no host synchronisation.
  * forward keeps what backward needs (routing, permuted activations); x and

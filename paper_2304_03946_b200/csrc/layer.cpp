@@ -386,6 +386,7 @@ class Layer {
     if (cfg_.num_gpus != 1)
       throw std::logic_error("fm_layer_backward: fused path is single-GPU; use the phase API");
     if (!fused_state_) throw std::logic_error("fm_layer_backward: no forward state");
+    side_jobs_ = 0;
     combine_backward(dy, y_perm_.p, dy_perm_.p, s, /*zero_pads=*/true);
     // the dispatched units' share of dWg = per-tile column sums of X_perm
     // weighted by dl per row, reduced with db1 / db2 (dropped units: below)
@@ -406,6 +407,7 @@ class Layer {
       SideJob unp = unpermute_side(dx);
       wgrad1(dw1, s, &unp);            // dH, X_perm (+ un-permute)
       unpermuted = unp.clusters > 0;
+      side_jobs_ = (sums.clusters > 0 ? 1 : 0) | (unpermuted ? 2 : 0);
       bias_grads(db1, db2, s, dwg_tiles ? dwg : nullptr, /*sums_done=*/sums.clusters > 0);
     }
     if (!unpermuted) unpermute(dx_perm_.p, saved_wg_, dx, s);
@@ -572,6 +574,7 @@ class Layer {
   void expert_backward(const void* w1, const void* w2, float* dw1, float* db1, float* dw2,
                        float* db2, cudaStream_t s, float* dwg_tiles = nullptr, bool signal_dx = false,
                        const ArrivalGate* gate = nullptr) {
+    side_jobs_ = 0;
     if (nl() == 0) {
       if (signal_dx) p2p_signal(3, s);
       return;
@@ -581,6 +584,7 @@ class Layer {
     SideJob side = tile_sum_side(db2, dwg_tiles);
     wgrad2(dw2, s, &side);
     wgrad1(dw1, s);
+    side_jobs_ = side.clusters > 0 ? 1 : 0;
     bias_grads(db1, db2, s, dwg_tiles, /*sums_done=*/side.clusters > 0);
   }
 
@@ -953,6 +957,7 @@ class Layer {
   // ------------------------------------------------------------ introspection
   int nl() const { return static_cast<int>(local_.size()); }
   const std::vector<int32_t>& local() const { return local_; }
+  int side_jobs() const { return side_jobs_; }
   const fm_layer_config& cfg() const { return cfg_; }
 
   // stream == nullptr: synchronise the device, then copy; else enqueue the copy
@@ -1070,6 +1075,7 @@ class Layer {
   std::vector<int32_t> host_counts_;
   double capacity_factor_ = 0.0;  // 0 / inf: no drops (FlexMoE)
   const void* saved_x_ = nullptr;  // gate input of the current step (must outlive backward)
+  int side_jobs_ = 0;              // fm_layer_side_jobs of the last backward
   DevBuf kept_, dropped_;
   int recv_total_ = 0, send_total_ = 0;
   bool fused_state_ = false;
@@ -1124,6 +1130,10 @@ int fm_layer_set_operand_slots(fm_layer* h, const int32_t* slot_N, int capacity,
 
 int fm_layer_set_capacity_factor(fm_layer* h, double capacity_factor) {
   return fm::guarded([&] { h->impl->set_capacity_factor(capacity_factor); });
+}
+
+int fm_layer_side_jobs(const fm_layer* h, int* mask) {
+  return fm::guarded([&] { *mask = h->impl->side_jobs(); });
 }
 
 int fm_layer_local_experts(const fm_layer* h, int* num_local, int32_t* experts) {

@@ -86,6 +86,14 @@ class MoELayer:
         L.check(L.lib().fm_layer_local_experts(self._h, C.byref(n), buf.ctypes.data))
         return buf[: n.value].tolist()
 
+    @property
+    def side_jobs(self) -> int:
+        """fm_layer_side_jobs: bit 0 = the tile column sums ran beside the FFN2
+        weight-gradient GEMM, bit 1 = the un-permute beside the FFN1 one."""
+        m = C.c_int(0)
+        L.check(L.lib().fm_layer_side_jobs(self._h, C.byref(m)))
+        return m.value
+
     def set_placement(self, replica_counts):
         cnt = np.ascontiguousarray(replica_counts, np.int32)
         L.check(L.lib().fm_layer_set_placement(self._h, cnt.ctypes.data))
