@@ -701,7 +701,10 @@ def run_ours(args, world, rank, local_rank):
                      "peak_note": ("frac is against the burst peak (cuBLAS at full clock); the sustained peak "
                                    f"was measured at a {peaks.get('sus_mhz')} MHz median SM clock, this run's "
                                    "median is in clocks.sm_mhz"),
-                     "gemm_ms_per_step": round(gemm_ms, 4), "gemm_launches_per_step": gemm_launches},
+                     "gemm_ms_per_step": round(gemm_ms, 4), "gemm_launches_per_step": gemm_launches,
+                     **({"side_jobs": "the weight-gradient launches also run memory-bound backward work on "
+                                      "their spare CTA pairs (kernels.*.side_job); their durations include it"}
+                        if side else {})},
         "kernels": kernels,
         "clocks": clocks.summary(),
         "balance_ratio": balance,
