@@ -364,6 +364,8 @@ int fm_layer_local_experts(const fm_layer* layer, int* num_local, int32_t* exper
  * bit 0 the db2 / dWg tile column sums (FFN2 wgrad), bit 1 the un-permute
  * (FFN1 wgrad). Results are the same either way. */
 int fm_layer_side_jobs(const fm_layer* layer, int* mask);
+/* enable = 0: run that work as standalone kernels (default 1). */
+int fm_layer_set_side_jobs(fm_layer* layer, int enable);
 
 /* Single-GPU (num_gpus == 1) fused step; no host synchronisation.
  * forward keeps what backward needs (routing, permuted activations); x and

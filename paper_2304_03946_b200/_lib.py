@@ -93,6 +93,7 @@ _SIGNATURES = {
     "fm_layer_set_operand_slots": [_P, _P, _I, _P],
     "fm_layer_local_experts": [_P, C.POINTER(_I), _P],
     "fm_layer_side_jobs": [_P, C.POINTER(_I)],
+    "fm_layer_set_side_jobs": [_P, _I],
     "fm_layer_forward": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P],
     "fm_layer_backward": [_P] * 9,
     "fm_layer_copy_out": [_P, _I, _P, C.c_size_t, C.POINTER(C.c_size_t)],

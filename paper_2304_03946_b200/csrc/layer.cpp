@@ -31,8 +31,9 @@
 #ifndef FM_BWD_ORDER
 #define FM_BWD_ORDER 4
 #endif
-// A/B knob: the bias / gate-weight tile column sums run on spare CTA pairs of
-// the FFN2 weight-gradient GEMM launch (1) instead of their own launch (0)
+// Default of fm_layer_set_side_jobs: memory-bound backward work (tile column
+// sums, un-permute) on spare CTA pairs of the weight-gradient launches (1)
+// instead of their own kernels (0)
 #ifndef FM_COLSUM_SIDE
 #define FM_COLSUM_SIDE 1
 #endif
@@ -648,7 +649,7 @@ class Layer {
   // job of a weight-gradient launch.
   SideJob unpermute_side(void* dx) {
     SideJob sd{};
-    if (!FM_COLSUM_SIDE || cfg_.num_gpus != 1 || !dx || cur_T_ <= 0) return sd;
+    if (!side_enabled_ || cfg_.num_gpus != 1 || !dx || cur_T_ <= 0) return sd;
     sd.kind = 2;
     sd.dXp = dx_perm_.p;
     sd.pos = pos_.as<int32_t>();
@@ -665,11 +666,11 @@ class Layer {
   }
 
   // The db2 / dWg tile column-sum jobs (dY_perm; dl-weighted X_perm) as a
-  // side job of a weight-gradient launch (FM_COLSUM_SIDE), else none.
+  // side job of a weight-gradient launch (fm_layer_set_side_jobs), else none.
   SideJob tile_sum_side(float* db2, float* dwg_tiles) {
     SideJob sd{};
     const int Nl = nl(), d = cfg_.d_model;
-    if (!FM_COLSUM_SIDE || Nl == 0) return sd;
+    if (!side_enabled_ || Nl == 0) return sd;
     sd.kind = 1;
     const int max_tiles = static_cast<int>(row_cap_ / 128);
     float* part_db2 = tile_sum_.as<float>();
@@ -958,6 +959,7 @@ class Layer {
   int nl() const { return static_cast<int>(local_.size()); }
   const std::vector<int32_t>& local() const { return local_; }
   int side_jobs() const { return side_jobs_; }
+  void set_side_enabled(bool on) { side_enabled_ = on; }
   const fm_layer_config& cfg() const { return cfg_; }
 
   // stream == nullptr: synchronise the device, then copy; else enqueue the copy
@@ -1076,6 +1078,7 @@ class Layer {
   double capacity_factor_ = 0.0;  // 0 / inf: no drops (FlexMoE)
   const void* saved_x_ = nullptr;  // gate input of the current step (must outlive backward)
   int side_jobs_ = 0;              // fm_layer_side_jobs of the last backward
+  bool side_enabled_ = FM_COLSUM_SIDE != 0;  // fm_layer_set_side_jobs
   DevBuf kept_, dropped_;
   int recv_total_ = 0, send_total_ = 0;
   bool fused_state_ = false;
@@ -1130,6 +1133,10 @@ int fm_layer_set_operand_slots(fm_layer* h, const int32_t* slot_N, int capacity,
 
 int fm_layer_set_capacity_factor(fm_layer* h, double capacity_factor) {
   return fm::guarded([&] { h->impl->set_capacity_factor(capacity_factor); });
+}
+
+int fm_layer_set_side_jobs(fm_layer* h, int enable) {
+  return fm::guarded([&] { h->impl->set_side_enabled(enable != 0); });
 }
 
 int fm_layer_side_jobs(const fm_layer* h, int* mask) {

@@ -94,6 +94,11 @@ class MoELayer:
         L.check(L.lib().fm_layer_side_jobs(self._h, C.byref(m)))
         return m.value
 
+    def set_side_jobs(self, enable: bool) -> None:
+        """fm_layer_set_side_jobs: False runs the column sums and the un-permute
+        as their own kernels (same results, bit for bit)."""
+        L.check(L.lib().fm_layer_set_side_jobs(self._h, 1 if enable else 0))
+
     def set_placement(self, replica_counts):
         cnt = np.ascontiguousarray(replica_counts, np.int32)
         L.check(L.lib().fm_layer_set_placement(self._h, cnt.ctypes.data))

@@ -1,0 +1,52 @@
+"""Side jobs: the db2 / dWg tile column sums and the un-permute
+run on spare CTA pairs of the weight-gradient GEMM launches when the shape
+leaves spare pairs (64 output tiles per expert: d 1024, f 4096). Their code is
+the standalone kernels' arithmetic, so every output of the backward must be
+bit-identical with the side jobs on and off — checked here at the configs[1]
+shape (where both side jobs run) and at a d 768 / f 3072 shape (where the
+launcher declines them and the standalone kernels run in both modes).
+"""
+from __future__ import annotations
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2304_03946_b200.layer import MoELayer  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = {
+    # N, k, d, f, T, expected side_jobs mask with the side jobs enabled
+    "configs1": (16, 2, 1024, 4096, 65536, 0b11),
+    "top1_d1024": (64, 1, 1024, 4096, 32768, 0b11),
+    "d768": (32, 2, 768, 3072, 32768, 0b00),
+}
+
+
+def _step(layer, x, dy, params, side):
+    layer.set_side_jobs(side)
+    y = layer.forward(x, *params)
+    g = layer.backward(dy)
+    torch.cuda.synchronize()
+    return y.clone(), {k: v.clone() for k, v in vars(g).items() if torch.is_tensor(v)}, layer.side_jobs
+
+
+@pytest.mark.parametrize("name", list(SHAPES))
+def test_side_jobs_bit_identical(name):
+    N, k, d, f, T, mask = SHAPES[name]
+    torch.manual_seed(7)
+    dev = torch.device("cuda", 0)
+    layer = MoELayer(N, k, d, f, max_tokens=T)
+    p = layer.init_params(seed=11)
+    params = (p["wg"], p["w1"], p["b1"], p["w2"], p["b2"])
+    x = torch.randn(T, d, device=dev).to(torch.bfloat16)
+    dy = (torch.randn(T, d, device=dev) * 0.5).to(torch.bfloat16)
+    y_on, g_on, m_on = _step(layer, x, dy, params, True)
+    y_off, g_off, m_off = _step(layer, x, dy, params, False)
+    assert m_on == mask, f"side jobs ran: {m_on:#b}, expected {mask:#b}"
+    assert m_off == 0
+    assert torch.equal(y_on, y_off)
+    assert set(g_on) == set(g_off) and len(g_on) >= 5
+    for key in g_on:
+        assert torch.equal(g_on[key], g_off[key]), f"{key} differs between side jobs on and off"
