@@ -88,28 +88,43 @@ __global__ void expert_scan_kernel(const int32_t* __restrict__ tile_counts, int 
 
 // ----------------------------------------------------------------- plan
 // Exclusive prefix sum of v[0, n) in shared memory, in place; returns the
-// total. Every thread of the block calls it (scratch: blockDim.x ints).
+// total. Every thread of the block calls it (scratch: >= 32 ints). Each thread
+// scans a contiguous run, warps combine their run totals with shuffles, one
+// warp scans the warp totals: two block barriers per call (a Hillis-Steele
+// pass over the block would take 2 log2(blockDim) of them — the plan kernel
+// is a chain of such scans and runs single-block on the critical path).
 __device__ int block_exclusive_scan(int32_t* v, int n, int32_t* scratch) {
   const int per = (n + blockDim.x - 1) / blockDim.x;
   const int lo = min(n, static_cast<int>(threadIdx.x) * per), hi = min(n, lo + per);
   int sum = 0;
   for (int i = lo; i < hi; ++i) sum += v[i];
-  scratch[threadIdx.x] = sum;
-  __syncthreads();
-  for (int off = 1; off < static_cast<int>(blockDim.x); off <<= 1) {
-    const int t = threadIdx.x >= static_cast<unsigned>(off) ? scratch[threadIdx.x - off] : 0;
-    __syncthreads();
-    scratch[threadIdx.x] += t;
-    __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
   }
-  int run = scratch[threadIdx.x] - sum;
+  if (lane == 31) scratch[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int w = lane < nw ? scratch[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    if (lane < nw) scratch[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  int run = incl - sum + (wid > 0 ? scratch[wid - 1] : 0);
   for (int i = lo; i < hi; ++i) {
     const int x = v[i];
     v[i] = run;
     run += x;
   }
-  const int total = scratch[blockDim.x - 1];
-  __syncthreads();
+  const int total = scratch[nw - 1];
+  __syncthreads();  // scratch reuse by the next call
   return total;
 }
 
