@@ -664,6 +664,7 @@ class Runtime {
       // ---- backward
       ck(fm_layer_combine_backward_p2p(layer_, dy, s_), "combine_backward_p2p");
       ex_.fence();
+      ck(fm_layer_p2p_bind_dx(layer_, wg, dx_), "p2p_bind_dx");  // un-permute beside the FFN1 wgrad
       ck(fm_layer_expert_backward_p2p(layer_, w1_, w2_, dw1_, db1_, dw2_, db2_, dwg_, s_), "expert_backward_p2p");
       ex_.fence();
       ck(fm_layer_unpermute_backward_p2p(layer_, wg, dx_, dwg_, s_), "unpermute_backward_p2p");

@@ -196,6 +196,7 @@ int run_rank(const Args& a, int rank, const ncclUniqueId& id) {
     ck(fm_layer_expert_forward_p2p(layer, w1, b1, w2, b2, s), "expert_forward");
     ck(fm_layer_combine_p2p(layer, y, s), "combine");
     ck(fm_layer_combine_backward_p2p(layer, dy, s), "combine_backward");
+    ck(fm_layer_p2p_bind_dx(layer, wg, dx), "p2p_bind_dx");  // un-permute beside the FFN1 wgrad
     ck(fm_layer_expert_backward_p2p(layer, w1, w2, dw1, db1, dw2, db2, dwg, s), "expert_backward");
     ck(fm_layer_unpermute_backward_p2p(layer, wg, dx, dwg, s), "unpermute_backward");
     for (const auto& [li, comm] : sync_list) {  // ascending expert id on every GPU

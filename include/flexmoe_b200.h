@@ -454,6 +454,13 @@ int fm_layer_combine_p2p(fm_layer* layer, void* y, void* stream);
 int fm_layer_combine_backward_p2p(fm_layer* layer, const void* dy, void* stream);
 int fm_layer_expert_backward_p2p(fm_layer* layer, const void* w1, const void* w2, float* dw1, float* db1,
                                  float* dw2, float* db2, float* dwg, void* stream);
+/* Optional, before fm_layer_expert_backward_p2p: the gate weight and dx
+ * buffer the step's fm_layer_unpermute_backward_p2p will be given. The layer
+ * then runs the un-permute on spare CTA pairs of the FFN1 weight-gradient
+ * launch (after every peer's "dX ready"); the later
+ * fm_layer_unpermute_backward_p2p call with the same pointers only adds the
+ * dropped units' gate gradient. Must still be called. */
+int fm_layer_p2p_bind_dx(fm_layer* layer, const void* wg, void* dx);
 int fm_layer_unpermute_backward_p2p(fm_layer* layer, const void* wg, void* dx, float* dwg, void* stream);
 
 /* Introspection (synchronous device->host copy, for tests / metrics). */

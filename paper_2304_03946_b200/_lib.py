@@ -138,6 +138,7 @@ _SIGNATURES = {
     "fm_layer_combine_backward_p2p": [_P, _P, _P],
     "fm_layer_expert_backward_p2p": [_P] * 9,
     "fm_layer_unpermute_backward_p2p": [_P] * 5,
+    "fm_layer_p2p_bind_dx": [_P] * 3,
     "fm_pool_create": [_I, _I, _I, _I, C.POINTER(_P)],
     "fm_pool_destroy": [_P],
     "fm_pool_info": [_P, _P, _P],

@@ -337,14 +337,47 @@ __device__ __forceinline__ void unpermute_side_vpl(const SideJob& sd, int cta, i
       }
     }
   };
+  const P2P& pp = sd.pp;
+  if (pp.unit_dst && pp.wait_slot >= 0) {
+    // P2P: every expert GPU (this one included) published "dX ready" for this
+    // epoch (bounded wait, as the standalone kernel's p2p_block_wait)
+    if (static_cast<int>(threadIdx.x) < pp.world) {
+      const unsigned long long* f = reinterpret_cast<const unsigned long long*>(pp.base[pp.me] + pp.flag_off) +
+                                    pp.wait_slot * kMaxPeers + threadIdx.x;
+      unsigned long long t0, now, v;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      while (true) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+        if (v >= pp.epoch) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (now - t0 > 20000000000ull) {
+          atomicExch(pp.err, 1);
+          break;
+        }
+        __nanosleep(128);
+      }
+    }
+    __syncthreads();
+  }
+  // rows written by another GPU in this step: L2-coherent loads, no L1 reuse
+  auto load_cg = [&](const __nv_bfloat16* base, size_t row, uint4 (&q)[VPL]) {
+    const uint4* src = reinterpret_cast<const uint4*>(base + row * static_cast<size_t>(d));
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) q[i] = __ldcg(src + lane + 32 * i);
+  };
+  auto load_unit = [&](int to, size_t row, uint4 (&q)[VPL]) {
+    if (to >= 0) load_cg(reinterpret_cast<const __nv_bfloat16*>(pp.base[to] + pp.dx_off), row, q);
+    else load(dXp, row, q);
+  };
   for (int t = cta * warps + static_cast<int>(threadIdx.x >> 5); t < sd.T; t += num_ctas * warps) {
     const size_t base = static_cast<size_t>(t) * k;
-    int my_pos = 0, my_e = 0;
+    int my_pos = 0, my_e = 0, my_to = -1;
     float my_dl = 0.0f;
     if (lane < k) {
       my_pos = __ldg(sd.pos + base + lane);
       my_e = __ldg(sd.idx + base + lane);
       if (sd.gate_grad) my_dl = __ldg(sd.dl + base + lane);
+      if (pp.unit_dst) my_to = pp.unit_dst[base + lane];
     }
     float acc[VPL][8];
 #pragma unroll
@@ -355,10 +388,12 @@ __device__ __forceinline__ void unpermute_side_vpl(const SideJob& sd, int cta, i
       const bool two = j + 1 < k;
       const int p0 = __shfl_sync(0xffffffffu, my_pos, j);
       const int p1 = __shfl_sync(0xffffffffu, my_pos, two ? j + 1 : j);
+      const int to0 = __shfl_sync(0xffffffffu, my_to, j);
+      const int to1 = __shfl_sync(0xffffffffu, my_to, two ? j + 1 : j);
       uint4 q0[VPL], q1[VPL];
       const bool h0 = p0 >= 0, h1 = two && p1 >= 0;
-      if (h0) load(dXp, p0, q0);
-      if (h1) load(dXp, p1, q1);
+      if (h0) load_unit(to0, p0, q0);
+      if (h1) load_unit(to1, p1, q1);
       if (h0) axpy(acc, q0, 1.0f);
       if (h1) axpy(acc, q1, 1.0f);
     }

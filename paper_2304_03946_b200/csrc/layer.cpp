@@ -576,6 +576,7 @@ class Layer {
                        float* db2, cudaStream_t s, float* dwg_tiles = nullptr, bool signal_dx = false,
                        const ArrivalGate* gate = nullptr) {
     side_jobs_ = 0;
+    unpermuted_ = false;
     if (nl() == 0) {
       if (signal_dx) p2p_signal(3, s);
       return;
@@ -584,8 +585,12 @@ class Layer {
     if (signal_dx) p2p_signal(3, s);
     SideJob side = tile_sum_side(db2, dwg_tiles);
     wgrad2(dw2, s, &side);
-    wgrad1(dw1, s);
-    side_jobs_ = side.clusters > 0 ? 1 : 0;
+    // P2P with the un-permute bound (fm_layer_p2p_bind_dx): it rides beside
+    // the FFN1 weight gradients, reading the peers' dX rows once they are ready
+    SideJob unp = (signal_dx && p2p_ && bound_dx_) ? unpermute_side(bound_dx_, bound_wg_) : SideJob{};
+    wgrad1(dw1, s, unp.kind ? &unp : nullptr);
+    unpermuted_ = unp.clusters > 0;
+    side_jobs_ = (side.clusters > 0 ? 1 : 0) | (unpermuted_ ? 2 : 0);
     bias_grads(db1, db2, s, dwg_tiles, /*sums_done=*/side.clusters > 0);
   }
 
@@ -647,16 +652,18 @@ class Layer {
 
   // The single-GPU un-permute (dx from dX_perm and the gate rows) as a side
   // job of a weight-gradient launch.
-  SideJob unpermute_side(void* dx) {
+  SideJob unpermute_side(void* dx, const void* wg = nullptr) {
     SideJob sd{};
-    if (!side_enabled_ || cfg_.num_gpus != 1 || !dx || cur_T_ <= 0) return sd;
+    if (!side_enabled_ || !dx || cur_T_ <= 0) return sd;
+    if (cfg_.num_gpus != 1 && !p2p_) return sd;  // NCCL layouts: dX rows come back through the a2a
     sd.kind = 2;
     sd.dXp = dx_perm_.p;
     sd.pos = pos_.as<int32_t>();
     sd.idx = topk_idx_.as<int32_t>();
     sd.dl = dl_.as<float>();
-    sd.wg = saved_wg_;
+    sd.wg = wg ? wg : saved_wg_;
     sd.dx = dx;
+    if (p2p_) sd.pp = p2p_args(-1, /*wait for "dX ready"*/ 3);
     sd.T = cur_T_;
     sd.k = cfg_.top_k;
     sd.d = cfg_.d_model;
@@ -834,6 +841,7 @@ class Layer {
     FM_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
     close_peer(peer);
     pp_.base[peer] = static_cast<char*>(ptr);
+    peers_distinct_ = -1;
     peer_ipc_[peer] = true;
   }
   void p2p_link_peer(int peer, Layer& other) {
@@ -843,6 +851,7 @@ class Layer {
       throw std::invalid_argument("fm_layer_p2p_link_peer: peer layer has a different P2P arena");
     close_peer(peer);
     pp_.base[peer] = other.arena_.as<char>();
+    peers_distinct_ = -1;
   }
   int p2p_status() {
     if (!p2p_) return 0;
@@ -923,11 +932,16 @@ class Layer {
   void unpermute_backward_p2p(const void* wg, void* dx, float* dwg, cudaStream_t s) {
     const int T = cur_T_, d = cfg_.d_model, k = cfg_.top_k;
     const bool gate_grad = k > 1;
-    timer_.begin(FM_PHASE_UNPERMUTE, s);
-    const P2P p = p2p_args(-1, /*wait for "dX ready"*/ 3);
-    launch_unpermute_bwd(dx_perm_.p, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(), wg, T, d, k,
-                         gate_grad, dx, s, &p);
-    timer_.end(s);
+    if (!(unpermuted_ && dx == bound_dx_ && wg == bound_wg_)) {  // not done beside the FFN1 wgrad
+      timer_.begin(FM_PHASE_UNPERMUTE, s);
+      const P2P p = p2p_args(-1, /*wait for "dX ready"*/ 3);
+      launch_unpermute_bwd(dx_perm_.p, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(), wg, T, d,
+                           k, gate_grad, dx, s, &p);
+      timer_.end(s);
+    }
+    unpermuted_ = false;
+    bound_dx_ = nullptr;
+    bound_wg_ = nullptr;
     if (dwg && gate_grad && drops_enabled()) {  // dropped units are in no X_perm: add them here
       timer_.begin(FM_PHASE_GATE_WGRAD, s);
       launch_dropped_gate_wgrad(saved_x_, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(), T, d, k,
@@ -960,6 +974,34 @@ class Layer {
   const std::vector<int32_t>& local() const { return local_; }
   int side_jobs() const { return side_jobs_; }
   void set_side_enabled(bool on) { side_enabled_ = on; }
+  // The bound un-permute waits inside a persistent GEMM launch for the peers'
+  // "dX ready": only safe when every peer runs on another device (ranks
+  // sharing one GPU — in-process loopback, several processes on one device —
+  // could wait on a signal queued behind that launch). Otherwise the binding
+  // is ignored and fm_layer_unpermute_backward_p2p runs the standalone kernel.
+  bool peers_on_other_devices() const {
+    int me = -1;
+    if (cudaGetDevice(&me) != cudaSuccess) return false;
+    for (int g = 0; g < cfg_.num_gpus; ++g) {
+      if (g == cfg_.rank) continue;
+      cudaPointerAttributes a{};
+      if (!pp_.base[g] || cudaPointerGetAttributes(&a, pp_.base[g]) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      if (a.device == me) return false;
+    }
+    return true;
+  }
+  void bind_dx(const void* wg, void* dx) {
+    if (!p2p_) throw std::logic_error("fm_layer_p2p_bind_dx: P2P transport not enabled");
+#ifndef FM_P2P_UNPERMUTE_SIDE
+#define FM_P2P_UNPERMUTE_SIDE 1
+#endif
+    if (peers_distinct_ < 0) peers_distinct_ = (FM_P2P_UNPERMUTE_SIDE && peers_on_other_devices()) ? 1 : 0;
+    bound_wg_ = peers_distinct_ ? wg : nullptr;
+    bound_dx_ = peers_distinct_ ? dx : nullptr;
+  }
   const fm_layer_config& cfg() const { return cfg_; }
 
   // stream == nullptr: synchronise the device, then copy; else enqueue the copy
@@ -1078,6 +1120,10 @@ class Layer {
   double capacity_factor_ = 0.0;  // 0 / inf: no drops (FlexMoE)
   const void* saved_x_ = nullptr;  // gate input of the current step (must outlive backward)
   int side_jobs_ = 0;              // fm_layer_side_jobs of the last backward
+  const void* bound_wg_ = nullptr;  // fm_layer_p2p_bind_dx: where this step's un-permute
+  void* bound_dx_ = nullptr;        //   reads the gate rows / writes dx
+  bool unpermuted_ = false;         // the bound un-permute ran beside the FFN1 wgrad
+  int peers_distinct_ = -1;         // every peer arena on another device (-1: unknown)
   bool side_enabled_ = FM_COLSUM_SIDE != 0;  // fm_layer_set_side_jobs
   DevBuf kept_, dropped_;
   int recv_total_ = 0, send_total_ = 0;
@@ -1133,6 +1179,10 @@ int fm_layer_set_operand_slots(fm_layer* h, const int32_t* slot_N, int capacity,
 
 int fm_layer_set_capacity_factor(fm_layer* h, double capacity_factor) {
   return fm::guarded([&] { h->impl->set_capacity_factor(capacity_factor); });
+}
+
+int fm_layer_p2p_bind_dx(fm_layer* h, const void* wg, void* dx) {
+  return fm::guarded([&] { h->impl->bind_dx(wg, dx); });
 }
 
 int fm_layer_set_side_jobs(fm_layer* h, int enable) {

@@ -25,38 +25,6 @@ struct PlanDev {
   unsigned long long* tile_src_mask;  // [rows/128] P2P: sources with rows in each 128-row tile
 };
 
-// Memory-bound work run by spare CTA pairs of a weight-gradient GEMM launch
-// next to its tensor-bound tiles (DESIGN.md §4), bit-identical to the
-// standalone kernels it replaces:
-//  kind 1, column sums: job j writes partial[j][tile][c] = sum over the
-//    tile's real rows r of (row_w[j] ? row_w[j][r] : 1) * buf[j][r][c]
-//    (segment_tile_colsum_kernel: same rows, same fmaf chain);
-//  kind 2, un-permute (single GPU): dx[t] = sum_j dXp[pos[t,j]] +
-//    [gate_grad] sum_j dl[t,j] * wg[idx[t,j]] (unpermute_bwd_kernel).
-struct SideJob {
-  int kind;       // 0 = none
-  int clusters;   // CTA pairs (or CTAs) given to it; set by the launcher (0: did not run)
-  int est_rows;   // host estimate of the GEMM's reduction rows (sizes `clusters`)
-  // kind 1
-  const void* buf[2];  // bf16 [rows][cols]
-  const float* row_w[2];
-  float* partial[2];   // f32 [tiles][cols]
-  int njobs;
-  int cols;
-  const int32_t* mtile_prefix;  // PlanDev fields of the segments
-  const int32_t* seg_start;
-  const int32_t* seg_real;
-  int Nl;
-  // kind 2
-  const void* dXp;  // bf16 [rows][d]
-  const int32_t* pos;
-  const int32_t* idx;
-  const float* dl;
-  const void* wg;   // bf16 [N][d]
-  void* dx;         // bf16 [T][d]
-  int T, k, d, gate_grad;
-};
-
 // Peer-to-peer transport: every GPU's exchange arena holds its
 // X_perm, Y_perm, dY_perm, dX_perm (bf16 rows), dl per X_perm row (f32) and
 // the arrival flags, at the same offsets on every GPU; base[g] is GPU g's
@@ -79,6 +47,41 @@ struct P2P {
   // every peer has published flags[wait_slot][src] >= epoch in this GPU's arena.
   int wait_slot;
   int* err;
+};
+
+// Memory-bound work run by spare CTA pairs of a weight-gradient GEMM launch
+// next to its tensor-bound tiles (DESIGN.md §4), bit-identical to the
+// standalone kernels it replaces:
+//  kind 1, column sums: job j writes partial[j][tile][c] = sum over the
+//    tile's real rows r of (row_w[j] ? row_w[j][r] : 1) * buf[j][r][c]
+//    (segment_tile_colsum_kernel: same rows, same fmaf chain);
+//  kind 2, un-permute: dx[t] = sum_j dXp[pos[t,j]] + [gate_grad]
+//    sum_j dl[t,j] * wg[idx[t,j]] (unpermute_bwd_kernel); with pp.unit_dst
+//    set (P2P) the dX rows are read from the expert GPUs' arenas after the
+//    side CTAs waited for every peer's "dX ready" flag (pp.wait_slot).
+struct SideJob {
+  int kind;       // 0 = none
+  int clusters;   // CTA pairs (or CTAs) given to it; set by the launcher (0: did not run)
+  int est_rows;   // host estimate of the GEMM's reduction rows (sizes `clusters`)
+  // kind 1
+  const void* buf[2];  // bf16 [rows][cols]
+  const float* row_w[2];
+  float* partial[2];   // f32 [tiles][cols]
+  int njobs;
+  int cols;
+  const int32_t* mtile_prefix;  // PlanDev fields of the segments
+  const int32_t* seg_start;
+  const int32_t* seg_real;
+  int Nl;
+  // kind 2
+  const void* dXp;  // bf16 [rows][d]
+  const int32_t* pos;
+  const int32_t* idx;
+  const float* dl;
+  const void* wg;   // bf16 [N][d]
+  void* dx;         // bf16 [T][d]
+  int T, k, d, gate_grad;
+  P2P pp;           // P2P transport (pp.unit_dst == nullptr: local rows)
 };
 
 }  // namespace fm

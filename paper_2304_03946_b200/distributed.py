@@ -502,6 +502,8 @@ class DistributedMoELayer:
         g = self._grads(T, nl, dev)
         self._call("fm_layer_combine_backward_p2p", dy.data_ptr(), stream)
         self.ex.fence()
+        # the un-permute may ride beside this GPU's FFN1 weight gradients
+        self._call("fm_layer_p2p_bind_dx", wg.data_ptr(), g.dx.data_ptr())
         self._call("fm_layer_expert_backward_p2p", w1.data_ptr(), w2.data_ptr(), g.dw1.data_ptr(),
                    g.db1.data_ptr(), g.dw2.data_ptr(), g.db2.data_ptr(), g.dwg.data_ptr(), stream)
         self.ex.fence()

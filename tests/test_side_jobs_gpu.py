@@ -50,3 +50,34 @@ def test_side_jobs_bit_identical(name):
     assert set(g_on) == set(g_off) and len(g_on) >= 5
     for key in g_on:
         assert torch.equal(g_on[key], g_off[key]), f"{key} differs between side jobs on and off"
+
+
+def test_p2p_world1_side_jobs_bit_identical():
+    """The P2P phase path at world 1 (what torchrun --nproc-per-node 1 runs):
+    with fm_layer_p2p_bind_dx the un-permute rides beside the FFN1 weight
+    gradients and waits on the arena's own "dX ready" flag; every output must
+    match the standalone kernels bit for bit, and no P2P wait may time out."""
+    from paper_2304_03946_b200.distributed import DistributedMoELayer, LoopbackHub
+
+    N, k, d, f, T = 16, 2, 1024, 4096, 32768
+    torch.manual_seed(3)
+    dev = torch.device("cuda", 0)
+    lay = MoELayer(N, k, d, f, max_tokens=T)
+    p = lay.init_params(seed=5)
+    dl = DistributedMoELayer(lay, LoopbackHub(1).endpoint(0), transport="p2p")
+    x = torch.randn(T, d, device=dev).to(torch.bfloat16)
+    dy = (torch.randn(T, d, device=dev) * 0.5).to(torch.bfloat16)
+    runs = []
+    for side in (True, False):
+        lay.set_side_jobs(side)
+        y = dl.forward(x, p["wg"], p["w1"], p["b1"], p["w2"], p["b2"])
+        g = dl.backward(dy)
+        torch.cuda.synchronize()
+        assert not dl.p2p_timed_out()
+        runs.append((y.clone(), {key: v.clone() for key, v in vars(g).items() if torch.is_tensor(v)},
+                     lay.side_jobs))
+    (y_on, g_on, m_on), (y_off, g_off, m_off) = runs
+    assert m_on == 0b11 and m_off == 0
+    assert torch.equal(y_on, y_off)
+    for key in g_on:
+        assert torch.equal(g_on[key], g_off[key]), f"{key} differs between side jobs on and off"
