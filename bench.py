@@ -529,7 +529,11 @@ def run_ours(args, world, rank, local_rank):
     torch.cuda.synchronize()
 
     # ---------------- device-timed region (value), live per-phase timing
-    arm.set_timing(True)
+    # The timed region runs the plain steps; the per-phase CUDA events (two
+    # records per kernel, ~1.4 % of a configs[1] step) are recorded in a
+    # second pass of the same K steps right after it, which feeds `kernels`
+    # and the roofline's per-launch durations.
+    arm.set_timing(False)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
@@ -545,8 +549,20 @@ def run_ours(args, world, rank, local_rank):
     if dist:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    phases, comm = arm.timing()
     dyn = arm.summary(args.steps) if multi else None
+    # ---------------- kernel-timing pass: K more steps with per-phase events
+    arm.set_timing(True)
+    kev0, kev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    kev0.record(stream)
+    for _ in range(args.steps):
+        arm.step(x, dy)
+    kev1.record(stream)
+    torch.cuda.synchronize()
+    ms_instr = kev0.elapsed_time(kev1) / args.steps
+    phases, comm = arm.timing()
     arm.set_timing(False)
     if dist:
         t = torch.tensor([ms], device=dev)
@@ -692,6 +708,10 @@ def run_ours(args, world, rank, local_rank):
                                       "feed the on-device optimizer; copying them to the host would time "
                                       "PCIe, not the layer")},
         "gpu_launches": int(launches),
+        "timing": {"value": "CUDA events around the K timed steps, no per-phase events inside",
+                   "kernels": "a second pass of K steps with two CUDA events per kernel on the launching "
+                              "stream (roofline achieved, kernels.*)",
+                   "ms_per_step_instrumented": round(ms_instr, 4)},
         "roofline": {"bound": "tensor", "kernel": "grouped_gemm (tcgen05, 6 launches/step)",
                      "achieved": round(achieved, 1), "peak": peaks["bf16"],
                      "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16"], 4),
