@@ -136,56 +136,10 @@ __device__ int block_exclusive_scan(int32_t* v, int n, int32_t* scratch) {
 // Every offset table is a block-wide scan over shared memory: a serial walk
 // by one thread is a dependent chain of ~7 cycles per instruction, which at
 // 64 experts cost ~100 us per step.
-// Fused expert scan (single GPU, small N x tiles): the gate's per-tile counts
-// -> per-expert exclusive prefix over tiles (tile_base), the histogram and the
-// demand column, as expert_scan_kernel, before route() reads that demand.
-struct PlanScan {
-  const int32_t* tile_counts;  // null: the scan ran as its own kernel
-  int num_tiles;
-  int32_t* tile_base;
-  int64_t* hist;
-};
-constexpr int kPlanScanPerLane = 16;  // tiles per lane: fused when num_tiles <= 32 * 16
-
 __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
                             const int32_t* __restrict__ local_expert, int Nl, PlanDev p,
                             const int32_t* __restrict__ counts, const int64_t* __restrict__ demand,
-                            int32_t* __restrict__ status, bool flows_in_smem, PlanScan scan) {
-  if (scan.tile_counts) {
-    // warp per expert; lane = a contiguous run of tiles, all its loads in flight together
-    int64_t* demand_col = const_cast<int64_t*>(demand);  // [N][1]: this GPU's column
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int per = (scan.num_tiles + 31) / 32;
-    const int t0 = lane * per;
-    for (int e = wid; e < N; e += nw) {
-      int v[kPlanScanPerLane];
-      int sum = 0;
-#pragma unroll
-      for (int i = 0; i < kPlanScanPerLane; ++i) {
-        const int t = t0 + i;
-        v[i] = (i < per && t < scan.num_tiles) ? scan.tile_counts[static_cast<size_t>(t) * N + e] : 0;
-        sum += v[i];
-      }
-      int incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
-      }
-      int run = incl - sum;
-#pragma unroll
-      for (int i = 0; i < kPlanScanPerLane; ++i) {
-        const int t = t0 + i;
-        if (i < per && t < scan.num_tiles) scan.tile_base[static_cast<size_t>(t) * N + e] = run;
-        run += v[i];
-      }
-      if (lane == 31) {
-        scan.hist[e] = incl;
-        demand_col[e] = incl;
-      }
-    }
-    __syncthreads();  // the block's global demand writes are visible to route() below
-  }
+                            int32_t* __restrict__ status, bool flows_in_smem) {
   // shared: flows as int32 [N][G][G] (when they fit) | local experts [Nl] | segment starts [Nl]
   //       | replica counts [N][G] | mtile prefix [Nl] | scan buffer [N*G] | scratch [blockDim]
   extern __shared__ int32_t sf[];
@@ -1030,20 +984,9 @@ void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_
   FM_LAUNCH_CHECK("expert_scan_kernel");
 }
 
-bool plan_can_fuse_scan(int N, int G, int num_tiles) {
-#ifdef FM_NO_PLAN_SCAN  // A/B knob: the expert scan always as its own kernel
-  return false;
-#endif
-  return G == 1 && N <= 32 && num_tiles <= 32 * kPlanScanPerLane;
-}
-
 void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
                  const PlanDev& p, cudaStream_t s, const int32_t* counts, const int64_t* demand,
-                 int32_t* status, const int32_t* scan_tile_counts, int scan_num_tiles, int32_t* scan_tile_base,
-                 int64_t* scan_hist) {
-  PlanScan scan{scan_tile_counts, scan_num_tiles, scan_tile_base, scan_hist};
-  if (scan.tile_counts && (!demand || !plan_can_fuse_scan(N, G, scan_num_tiles)))
-    throw std::invalid_argument("plan: fused expert scan needs G == 1, N <= 32, tiles <= 512 and a demand");
+                 int32_t* status) {
   if (demand && (N > 256 || G > kMaxGpus)) throw std::invalid_argument("route: bad dimensions");
   constexpr int kPlanThreads = 256;
   // the flows are staged in shared memory when they fit; beyond that (e.g.
@@ -1055,7 +998,7 @@ void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expe
   if (smem > 200 * 1024) throw std::invalid_argument("plan: num_experts * num_gpus too large");
   ensure_dynamic_smem(reinterpret_cast<const void*>(plan_kernel), smem);
   plan_kernel<<<1, kPlanThreads, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status,
-                                            flows_in_smem, scan);
+                                            flows_in_smem);
   FM_LAUNCH_CHECK("plan_kernel");
 }
 
