@@ -3,9 +3,12 @@
 // Owns the device workspace (routing state, dispatch plan, permuted
 // activations) sized for `max_tokens`, and runs the hot path on a caller
 // stream with no host synchronisation when num_gpus == 1:
-//   forward : gate(+hist) -> scan -> route -> plan -> dispatch -> FFN1 -> FFN2 -> combine
-//   backward: combine^T(+gate softmax^T) -> dgrad1 -> dgrad2 -> wgrad2 -> wgrad1
-//             -> bias grads -> un-permute (+gate input grad) -> gate weight grad
+//   forward : gate(+hist) -> scan -> route + plan -> dispatch -> FFN1 -> FFN2 -> combine
+//   backward: combine^T(+gate softmax^T) -> FFN2 wgrad (+ db2 / dWg tile sums on
+//             its spare CTA pairs) -> FFN2 dgrad (+ db1 tile sums) -> FFN1 dgrad
+//             -> FFN1 wgrad (+ un-permute, dx, on its spare CTA pairs) -> reduce
+//             (FM_BWD_ORDER 4; the side work runs standalone where a launch has
+//             no spare pairs)
 // With num_gpus > 1 the same kernels run as phases around the host's
 // all-to-all (see the fm_layer_* phase entry points in flexmoe_b200.h).
 //
@@ -27,7 +30,9 @@
 // wgrad1, tile sums, un-permute (round 1); 1 = the two weight-gradient GEMMs
 // last (measured: the next step's gate is not faster, profiles/r02_gate_context.log);
 // 2 = wgrad2, dgrad2, wgrad1, dgrad1 (each f32 weight-gradient drain overlaps a
-// tensor-bound GEMM)
+// tensor-bound GEMM); 3 = 2 with un-permute before the tile sums; 4 (default) =
+// wgrad2 (+ tile sums), dgrad2, dgrad1, wgrad1 (+ un-permute): side jobs
+// (profiles/r02_colsum_side.log)
 #ifndef FM_BWD_ORDER
 #define FM_BWD_ORDER 4
 #endif
