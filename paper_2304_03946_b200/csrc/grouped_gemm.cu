@@ -102,6 +102,9 @@ struct Args {
   SideJob side;
 };
 
+// kernel parameters = 3 tensor maps + Args (SideJob carries a P2P struct)
+static_assert(sizeof(Args) + 3 * sizeof(CUtensorMap) <= 4096, "grouped GEMM kernel parameters exceed 4 KB");
+
 // Side role of a wgrad launch: the tile column sums of SideJob, one thread
 // group of cols/8 threads per (job, 128-row tile) item, 16 rows in flight.
 template <int THREADS>
