@@ -820,13 +820,18 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
         if (CG == 1 || leader) ptx::mbar_arrive(&tempty_bar[ab]);
         else ptx::mbar_arrive_cluster(lead_tempty + ab * 8);
       }
-      if (EPI == kEpiReluMask && args.colsum && tl.valid) {
-        // combine the four row quarters in a fixed order (deterministic)
+      if (EPI == kEpiReluMask && args.colsum) {
+        // combine the four row quarters in a fixed order (deterministic). The
+        // barrier runs for every tile, valid or not (tl.valid is uniform over
+        // the CTA): it is also what orders this tile's reads of buffer ab
+        // before the writes of the tile after next into the same buffer.
         ptx::named_bar_sync(2, kEpiThreads);
-        const float* cs = colsum_s + ab * 4 * kBN;
-        float* dst = args.colsum + static_cast<size_t>(tl.mtile) * args.N + tl.n0;
-        for (int col = et; col < kBN; col += kEpiThreads)
-          dst[col] = ((cs[col] + cs[kBN + col]) + cs[2 * kBN + col]) + cs[3 * kBN + col];
+        if (tl.valid) {
+          const float* cs = colsum_s + ab * 4 * kBN;
+          float* dst = args.colsum + static_cast<size_t>(tl.mtile) * args.N + tl.n0;
+          for (int col = et; col < kBN; col += kEpiThreads)
+            dst[col] = ((cs[col] + cs[kBN + col]) + cs[2 * kBN + col]) + cs[3 * kBN + col];
+        }
       }
       if (EPI == kEpiBiasRelu && args.mask && tl.valid) {
         uint4* mp = reinterpret_cast<uint4*>(args.mask + static_cast<size_t>(tl.m0 + row) * mask_ld +
