@@ -81,3 +81,33 @@ def test_p2p_world1_side_jobs_bit_identical():
     assert torch.equal(y_on, y_off)
     for key in g_on:
         assert torch.equal(g_on[key], g_off[key]), f"{key} differs between side jobs on and off"
+
+
+@pytest.mark.parametrize("T,cf", [(1000, 0.0), (3333, 0.0), (4096, 1.0), (2500, 1.25)])
+def test_side_jobs_edge_shapes(T, cf):
+    """Ragged token counts (partial 128-token gate tiles, experts with no
+    rows, pair-tail tiles) and StaticEP capacity drops (cf > 0: dropped units
+    carry no dispatch row, their gate gradient goes through the drop kernel):
+    side jobs on and off stay bit-identical — except dWg under drops, whose
+    dropped-unit share is added with f32 atomics (StaticEP baseline only;
+    order-dependent in the last bits, so compared within 1e-6 relative)."""
+    N, k, d, f = 16, 2, 1024, 4096
+    torch.manual_seed(T)
+    dev = torch.device("cuda", 0)
+    layer = MoELayer(N, k, d, f, max_tokens=T)
+    if cf:
+        layer.set_capacity_factor(cf)
+    p = layer.init_params(seed=T)
+    params = (p["wg"], p["w1"], p["b1"], p["w2"], p["b2"])
+    x = torch.randn(T, d, device=dev).to(torch.bfloat16)
+    dy = (torch.randn(T, d, device=dev) * 0.5).to(torch.bfloat16)
+    y_on, g_on, _ = _step(layer, x, dy, params, True)
+    y_off, g_off, m_off = _step(layer, x, dy, params, False)
+    assert m_off == 0
+    assert torch.equal(y_on, y_off)
+    for key in g_on:
+        if cf and key == "dwg":
+            rel = ((g_on[key] - g_off[key]).norm() / g_off[key].norm()).item()
+            assert rel < 1e-6, f"dwg: {rel}"
+            continue
+        assert torch.equal(g_on[key], g_off[key]), f"{key} differs between side jobs on and off"
