@@ -39,6 +39,12 @@ constexpr int kCtas = FM_GATE_CTAS;  // resident CTAs per SM (A/B knob)
 #ifndef FM_GATE_X_EVICT_FIRST
 #define FM_GATE_X_EVICT_FIRST 1
 #endif
+// A/B knob: tiles walked last-to-first, so the first tokens are the most
+// recent x lines in L2 when the dispatch (which walks tokens first-to-last)
+// re-reads x
+#ifndef FM_GATE_REVERSE
+#define FM_GATE_REVERSE 0
+#endif
 
 struct Args {
   int T, N, Npad, K, top_k, stages;
@@ -224,7 +230,8 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int ti = blockIdx.x; ti < num_tiles; ti += gridDim.x, ++it) {
+      const int tile = FM_GATE_REVERSE ? num_tiles - 1 - ti : ti;
       for (int kb = 0; kb < num_kb; ++kb) {
         GATE_WAIT(&empty_bar[stage], phase ^ 1);
         if (lane == 0) GATE_TRACE(2 + it * 16 + kb);
@@ -243,7 +250,8 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     int stage = 0;
     uint32_t phase = 0;
     int iter = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+    for (int ti = blockIdx.x; ti < num_tiles; ti += gridDim.x, ++iter) {
+      const int tile = FM_GATE_REVERSE ? num_tiles - 1 - ti : ti;
       const int ab = iter & 1;
       GATE_WAIT(&tempty_bar[ab], ((iter >> 1) & 1) ^ 1);
       ptx::tc_fence_after();
@@ -274,7 +282,8 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     constexpr int k = KT;
     uint32_t* my_mask = masks + q * a.Npad;
     int iter = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+    for (int ti = blockIdx.x; ti < num_tiles; ti += gridDim.x, ++iter) {
+      const int tile = FM_GATE_REVERSE ? num_tiles - 1 - ti : ti;
       const int ab = iter & 1;
       const int t = tile * kTM + q * 32 + lane;
       const bool valid = t < a.T;
