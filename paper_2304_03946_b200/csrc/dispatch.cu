@@ -769,26 +769,48 @@ __global__ void gate_wgrad_kernel(const __nv_bfloat16* __restrict__ buf, const i
 
 // Gate-weight gradient of units dropped by the capacity rule (in no dispatch
 // row): dWg[e] += dl[u] * x[t], warp per token, f32 atomics.
-__global__ void dropped_gate_wgrad_kernel(const __nv_bfloat16* __restrict__ x,
-                                          const int32_t* __restrict__ pos,
-                                          const int32_t* __restrict__ idx,
-                                          const float* __restrict__ dl, int T, int d, int k,
-                                          float* __restrict__ dwg) {
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= T) return;
-  for (int j = 0; j < k; ++j) {
-    const size_t u = static_cast<size_t>(t) * k + j;
-    if (pos[u] >= 0) continue;
-    const float g = dl[u];
-    float* out = dwg + static_cast<size_t>(idx[u]) * d;
-    const __nv_bfloat16* xr = x + static_cast<size_t>(t) * d;
-    for (int c = 2 * lane; c < d; c += 64) {
-      const uint32_t v = *reinterpret_cast<const uint32_t*>(xr + c);
-      atomicAdd(out + c, g * bf16lo(v));
-      atomicAdd(out + c + 1, g * bf16hi(v));
+// Gate-weight gradient of the units the capacity rule dropped (no dispatch
+// row): dWg[e] += sum over dropped units u = (t, j) of expert e of
+// dl[u] * x[t], deterministic. Block (chunk c, expert e): the chunk's tokens
+// ascending, thread = 8 columns (16-byte loads), partial[e][c][:]; then one
+// fixed-order pass over the chunks adds the sum to dwg[e] (after the tile-sum
+// reduce wrote it).
+__global__ void dropped_gate_partial_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ pos,
+                                            const int32_t* __restrict__ idx, const float* __restrict__ dl,
+                                            int T, int d, int k, int chunk, int nchunks,
+                                            float* __restrict__ partial) {
+  const int c = blockIdx.x, e = blockIdx.y;
+  const int c8 = threadIdx.x * 8;
+  if (c8 >= d) return;
+  float acc[8] = {};
+  const int t1 = min(T, (c + 1) * chunk);
+  for (int t = c * chunk; t < t1; ++t) {
+    for (int j = 0; j < k; ++j) {
+      const size_t u = static_cast<size_t>(t) * k + j;
+      if (__ldg(idx + u) != e || __ldg(pos + u) >= 0) continue;
+      const float g = __ldg(dl + u);
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * d + c8));
+      const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[2 * i] = fmaf(g, bf16lo(q[i]), acc[2 * i]);
+        acc[2 * i + 1] = fmaf(g, bf16hi(q[i]), acc[2 * i + 1]);
+      }
     }
   }
+  float4* dst = reinterpret_cast<float4*>(partial + (static_cast<size_t>(e) * nchunks + c) * d + c8);
+  dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+__global__ void dropped_gate_reduce_kernel(const float* __restrict__ partial, int nchunks, int d,
+                                           float* __restrict__ dwg) {
+  const int e = blockIdx.y, col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= d) return;
+  const float* src = partial + static_cast<size_t>(e) * nchunks * d + col;
+  float s = 0.0f;
+  for (int c = 0; c < nchunks; ++c) s += src[static_cast<size_t>(c) * d];
+  dwg[static_cast<size_t>(e) * d + col] += s;
 }
 
 // demand[e][g] = gathered[g][e]  (all-gathered per-GPU histograms -> TokenDemand layout)
@@ -927,12 +949,19 @@ void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int
   FM_LAUNCH_CHECK("gate_wgrad_kernel");
 }
 
+int dropped_gate_chunks(int T) { return std::max(1, std::min(128, (T + 255) / 256)); }
+
 void launch_dropped_gate_wgrad(const void* x, const int32_t* pos, const int32_t* idx, const float* dl,
-                               int T, int d, int k, float* dwg, cudaStream_t s) {
+                               int T, int d, int k, int N, float* partial, float* dwg, cudaStream_t s) {
   if (T <= 0) return;
-  dropped_gate_wgrad_kernel<<<(T + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), pos,
-                                                         idx, dl, T, d, k, dwg);
-  FM_LAUNCH_CHECK("dropped_gate_wgrad_kernel");
+  if (d % 8 != 0 || d > 8 * 1024) throw std::invalid_argument("dropped gate wgrad: d % 8 == 0, d <= 8192");
+  const int nchunks = dropped_gate_chunks(T);
+  const int chunk = (T + nchunks - 1) / nchunks;
+  dropped_gate_partial_kernel<<<dim3(nchunks, N), ((d / 8 + 31) / 32) * 32, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(x), pos, idx, dl, T, d, k, chunk, nchunks, partial);
+  FM_LAUNCH_CHECK("dropped_gate_partial_kernel");
+  dropped_gate_reduce_kernel<<<dim3((d + 255) / 256, N), 256, 0, s>>>(partial, nchunks, d, dwg);
+  FM_LAUNCH_CHECK("dropped_gate_reduce_kernel");
 }
 
 void launch_demand_transpose(const int64_t* gathered_GN, int N, int G, int64_t* demand_NG,

@@ -82,7 +82,8 @@ void launch_segment_tile_reduce(const float* partial0, int cols0, const int32_t*
                                 const PlanDev& p, int Nl, cudaStream_t s);
 void launch_p2p_signal(const P2P& pp, int G, int me, int slot, unsigned long long epoch, cudaStream_t s);
 void launch_dropped_gate_wgrad(const void* x, const int32_t* pos, const int32_t* idx, const float* dl,
-                               int T, int d, int k, float* dwg, cudaStream_t s);
+                               int T, int d, int k, int N, float* partial, float* dwg, cudaStream_t s);
+int dropped_gate_chunks(int T);
 
 
 namespace {
@@ -777,7 +778,7 @@ class Layer {
         // units dropped by the capacity rule are in no dispatch row
         if (drops_enabled())
           launch_dropped_gate_wgrad(saved_x_, pos_.as<int32_t>(), topk_idx_.as<int32_t>(),
-                                    dl_.as<float>(), T, d, k, dwg, s);
+                                    dl_.as<float>(), T, d, k, N, drop_partial(T), dwg, s);
       }
       timer_.end(s);
     }
@@ -950,7 +951,7 @@ class Layer {
     if (dwg && gate_grad && drops_enabled()) {  // dropped units are in no X_perm: add them here
       timer_.begin(FM_PHASE_GATE_WGRAD, s);
       launch_dropped_gate_wgrad(saved_x_, pos_.as<int32_t>(), topk_idx_.as<int32_t>(), dl_.as<float>(), T, d, k,
-                                dwg, s);
+                                cfg_.num_experts, drop_partial(T), dwg, s);
       timer_.end(s);
     }
   }
@@ -1053,6 +1054,12 @@ class Layer {
 
   size_t row_capacity() const { return row_cap_; }
   bool drops_enabled() const { return capacity_factor_ > 0 && std::isfinite(capacity_factor_); }
+  // per-(expert, token chunk) partials of the dropped units' dWg share
+  float* drop_partial(int T) {
+    const size_t need = sizeof(float) * cfg_.num_experts * dropped_gate_chunks(T) * cfg_.d_model;
+    if (drop_partial_.bytes < need) drop_partial_.reset(need);
+    return drop_partial_.as<float>();
+  }
   void set_capacity_factor(double cf) {
     if (!(cf >= 0)) throw std::invalid_argument("fm_layer: capacity_factor must be >= 0");
     capacity_factor_ = cf;
@@ -1120,7 +1127,7 @@ class Layer {
   Staging staging_[kStaging];
   int staging_next_ = 0;
   DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_, relu_mask_, tile_colsum_,
-      row_expert_, tile_sum_;
+      row_expert_, tile_sum_, drop_partial_;
   std::vector<int32_t> host_counts_;
   double capacity_factor_ = 0.0;  // 0 / inf: no drops (FlexMoE)
   const void* saved_x_ = nullptr;  // gate input of the current step (must outlive backward)

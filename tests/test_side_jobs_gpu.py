@@ -88,9 +88,7 @@ def test_side_jobs_edge_shapes(T, cf):
     """Ragged token counts (partial 128-token gate tiles, experts with no
     rows, pair-tail tiles) and StaticEP capacity drops (cf > 0: dropped units
     carry no dispatch row, their gate gradient goes through the drop kernel):
-    side jobs on and off stay bit-identical — except dWg under drops, whose
-    dropped-unit share is added with f32 atomics (StaticEP baseline only;
-    order-dependent in the last bits, so compared within 1e-6 relative)."""
+    side jobs on and off stay bit-identical."""
     N, k, d, f = 16, 2, 1024, 4096
     torch.manual_seed(T)
     dev = torch.device("cuda", 0)
@@ -106,8 +104,4 @@ def test_side_jobs_edge_shapes(T, cf):
     assert m_off == 0
     assert torch.equal(y_on, y_off)
     for key in g_on:
-        if cf and key == "dwg":
-            rel = ((g_on[key] - g_off[key]).norm() / g_off[key].norm()).item()
-            assert rel < 1e-6, f"dwg: {rel}"
-            continue
         assert torch.equal(g_on[key], g_off[key]), f"{key} differs between side jobs on and off"
