@@ -704,71 +704,69 @@ __global__ void __launch_bounds__(256) unpermute_bwd_kernel(
   store_row<VPL>(dx, t, d, lane, acc);
 }
 
-// Gate-weight gradient: dWg[e][:] += sum over dispatch rows r with
-// row_expert[r] == e of dl_rows[r] * buf[r][:]. Rows of one expert are
-// contiguous runs (segments / send chunks), so each block accumulates a run
-// and flushes one f32 atomic per column when the expert changes.
-__global__ void gate_wgrad_kernel(const __nv_bfloat16* __restrict__ buf, const int* __restrict__ rows_ptr,
-                                  int rows_fixed, int d, const float* __restrict__ dl_rows,
-                                  const int32_t* __restrict__ row_expert, float* __restrict__ dwg) {
-  // block: 256 rows x all d columns (blockDim = d/8); thread: one 16-B column
-  // vector. The expert sequence is uniform across the block, so flushes are
-  // block-wide: partial sums are transposed through smem and added with
-  // coalesced f32 atomics (one per column per run of an expert).
-  constexpr int kRows = 256, kBatch = 8;
-  extern __shared__ float flush_s[];  // [d]
-  const int rows = rows_ptr ? *rows_ptr : rows_fixed;
-  const int r0 = blockIdx.x * kRows;
-  if (r0 >= rows) return;
-  const int r1 = min(r0 + kRows, rows);
-  const int c8 = threadIdx.x * 8;
-  int cur = -1;
-  float acc[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-  auto flush = [&]() {
-    if (cur < 0) return;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) flush_s[c8 + i] = acc[i];
-    __syncthreads();
-    float* o = dwg + static_cast<size_t>(cur) * d;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(o + c, flush_s[c]);
-    __syncthreads();
-  };
-  for (int rb = r0; rb < r1; rb += kBatch) {
-    int e[kBatch];
-    float g[kBatch];
-    uint4 v[kBatch];
-#pragma unroll
-    for (int i = 0; i < kBatch; ++i) {  // all loads of the batch in flight together
-      const int r = min(rb + i, r1 - 1);
-      e[i] = __ldg(row_expert + r);
-      g[i] = __ldg(dl_rows + r);
-      v[i] = __ldg(reinterpret_cast<const uint4*>(buf + static_cast<size_t>(r) * d + c8));
-    }
-#pragma unroll
-    for (int i = 0; i < kBatch; ++i) {
-      if (rb + i >= r1) break;
-      if (e[i] != cur) {
-        flush();
-        cur = e[i];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[c] = 0.0f;
-      }
-      if (e[i] < 0) continue;
-      const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        acc[2 * c] = fmaf(g[i], bf16lo(w[c]), acc[2 * c]);
-        acc[2 * c + 1] = fmaf(g[i], bf16hi(w[c]), acc[2 * c + 1]);
-      }
-    }
-  }
-  flush();
+// Gate-weight gradient over the NCCL send buffer (dispatch order: chunk
+// (dst, e) of expert e's units for destination dst at send_off[e][dst], rows
+// in rank order), deterministic: every chunk is cut into pieces of kPieceRows
+// rows (piece table: an exclusive scan over the chunks in expert-major order),
+// one block sums a piece in row order, and one pass per expert adds its pieces
+// in table order: dwg[e] = sum over its (dst, piece) of dl_rows[r] * buf[r].
+constexpr int kPieceRows = 512;
+
+__global__ void piece_table_kernel(const int32_t* __restrict__ chunk_cnt, int N, int G,
+                                   int32_t* __restrict__ piece_off) {
+  extern __shared__ int32_t pt_s[];  // [N*G] counts, then [blockDim] scratch
+  int32_t* scratch = pt_s + N * G;
+  for (int j = threadIdx.x; j < N * G; j += blockDim.x)
+    pt_s[j] = (chunk_cnt[j] + kPieceRows - 1) / kPieceRows;  // j = e * G + dst (expert-major)
+  __syncthreads();
+  const int total = block_exclusive_scan(pt_s, N * G, scratch);
+  for (int j = threadIdx.x; j < N * G; j += blockDim.x) piece_off[j] = pt_s[j];
+  if (threadIdx.x == 0) piece_off[N * G] = total;
 }
 
-// Gate-weight gradient of units dropped by the capacity rule (in no dispatch
-// row): dWg[e] += dl[u] * x[t], warp per token, f32 atomics.
+__global__ void piece_sum_kernel(const __nv_bfloat16* __restrict__ buf, const float* __restrict__ dl_rows,
+                                 const int32_t* __restrict__ send_off, const int32_t* __restrict__ chunk_cnt,
+                                 const int32_t* __restrict__ piece_off, int N, int G, int d,
+                                 float* __restrict__ partial) {
+  const int b = blockIdx.x;
+  const int nc = N * G;
+  if (b >= piece_off[nc]) return;
+  int lo = 0, hi = nc;  // chunk j with piece_off[j] <= b < piece_off[j + 1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (piece_off[mid] <= b) lo = mid; else hi = mid;
+  }
+  while (lo + 1 < nc && piece_off[lo + 1] <= b) ++lo;  // skip empty chunks
+  const int e = lo / G, dst = lo % G;
+  const int base = send_off[e * G + dst], cnt = chunk_cnt[e * G + dst];
+  const int r0 = base + (b - piece_off[lo]) * kPieceRows, r1 = min(base + cnt, r0 + kPieceRows);
+  const int c8 = threadIdx.x * 8;
+  if (c8 >= d) return;
+  float acc[8] = {};
+  for (int r = r0; r < r1; ++r) {
+    const float g = __ldg(dl_rows + r);
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(buf + static_cast<size_t>(r) * d + c8));
+    const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[2 * i] = fmaf(g, bf16lo(q[i]), acc[2 * i]);
+      acc[2 * i + 1] = fmaf(g, bf16hi(q[i]), acc[2 * i + 1]);
+    }
+  }
+  float4* dst4 = reinterpret_cast<float4*>(partial + static_cast<size_t>(b) * d + c8);
+  dst4[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  dst4[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+__global__ void piece_reduce_kernel(const float* __restrict__ partial, const int32_t* __restrict__ piece_off,
+                                    int G, int d, float* __restrict__ dwg) {
+  const int e = blockIdx.y, col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= d) return;
+  float s = 0.0f;
+  for (int b = piece_off[e * G]; b < piece_off[(e + 1) * G]; ++b) s += partial[static_cast<size_t>(b) * d + col];
+  dwg[static_cast<size_t>(e) * d + col] = s;
+}
+
 // Gate-weight gradient of the units the capacity rule dropped (no dispatch
 // row): dWg[e] += sum over dropped units u = (t, j) of expert e of
 // dl[u] * x[t], deterministic. Block (chunk c, expert e): the chunk's tokens
@@ -940,13 +938,29 @@ __global__ void p2p_signal_kernel(const P2P pp, int G, int me, int slot, unsigne
 
 
 // ------------------------------------------------------------------ launchers
-void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int max_rows, int d,
-                       const float* dl_rows, const int32_t* row_expert, float* dwg, cudaStream_t s) {
-  if (max_rows <= 0) return;
-  gate_wgrad_kernel<<<(max_rows + 255) / 256, d / 8, d * 4, s>>>(static_cast<const __nv_bfloat16*>(buf),
-                                                           rows_dev, rows_fixed, d, dl_rows,
-                                                           row_expert, dwg);
-  FM_LAUNCH_CHECK("gate_wgrad_kernel");
+int gate_wgrad_pieces(int rows, int N, int G) { return (rows + kPieceRows - 1) / kPieceRows + N * G; }
+
+// dWg over the NCCL send buffer (see piece_sum_kernel); partial holds
+// gate_wgrad_pieces(max_rows, N, G) rows of d floats plus N*G+1 ints.
+void launch_gate_wgrad(const void* buf, int max_rows, int d, const float* dl_rows, const PlanDev& p, int N,
+                       int G, float* partial, float* dwg, cudaStream_t s) {
+  if (max_rows <= 0) {
+    FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
+    return;
+  }
+  if (d % 8 != 0 || d > 8 * 1024) throw std::invalid_argument("gate wgrad: d % 8 == 0, d <= 8192");
+  const int pieces = gate_wgrad_pieces(max_rows, N, G);
+  int32_t* piece_off = reinterpret_cast<int32_t*>(partial + static_cast<size_t>(pieces) * d);
+  constexpr int kT = 256;
+  const int tsmem = (N * G + kT) * 4;
+  ensure_dynamic_smem(reinterpret_cast<const void*>(piece_table_kernel), tsmem);
+  piece_table_kernel<<<1, kT, tsmem, s>>>(p.chunk_cnt, N, G, piece_off);
+  FM_LAUNCH_CHECK("piece_table_kernel");
+  piece_sum_kernel<<<pieces, ((d / 8 + 31) / 32) * 32, 0, s>>>(static_cast<const __nv_bfloat16*>(buf), dl_rows,
+                                                               p.send_off, p.chunk_cnt, piece_off, N, G, d, partial);
+  FM_LAUNCH_CHECK("piece_sum_kernel");
+  piece_reduce_kernel<<<dim3((d + 255) / 256, N), 256, 0, s>>>(partial, piece_off, G, d, dwg);
+  FM_LAUNCH_CHECK("piece_reduce_kernel");
 }
 
 int dropped_gate_chunks(int T) { return std::max(1, std::min(128, (T + 255) / 256)); }

@@ -59,8 +59,9 @@ void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, b
                      const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
                      cudaStream_t s, const P2P* pp = nullptr, void* pad_buf = nullptr, int Nl = 0);
 void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, int32_t* row_expert, cudaStream_t s);
-void launch_gate_wgrad(const void* buf, const int* rows_dev, int rows_fixed, int max_rows, int d,
-                       const float* dl_rows, const int32_t* row_expert, float* dwg, cudaStream_t s);
+void launch_gate_wgrad(const void* buf, int max_rows, int d, const float* dl_rows, const PlanDev& p, int N,
+                       int G, float* partial, float* dwg, cudaStream_t s);
+int gate_wgrad_pieces(int rows, int N, int G);
 void launch_demand_transpose(const int64_t* gathered_GN, int N, int G, int64_t* demand_NG,
                              cudaStream_t s);
 void launch_relayout(void* recv, void* perm, int d, int G, int Nl, const PlanDev& p, int max_rows,
@@ -770,11 +771,21 @@ class Layer {
     const bool gate_grad = k > 1;
     if (dwg) {
       timer_.begin(FM_PHASE_GATE_WGRAD, s);
-      if (!dwg_done) FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
+      if (!dwg_done && !gate_grad) FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
       if (gate_grad) {
-        if (!dwg_done)
-          launch_gate_wgrad(xrows, rows_dev, rows, rows, d, dl_rows_.as<float>(),
-                            row_expert_.as<int32_t>(), dwg, s);
+        // the send buffer's (dst, expert) chunks, piece by piece (deterministic);
+        // only the NCCL layout gets here (fused / P2P: tile sums, dwg_done)
+        if (!dwg_done) {
+          if (rows_dev) {  // fused layout with no local expert: no dispatch rows here
+            FM_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * N * d, s));
+          } else {
+          const size_t need = sizeof(float) * static_cast<size_t>(gate_wgrad_pieces(rows, N, cfg_.num_gpus)) * d +
+                              sizeof(int32_t) * (N * cfg_.num_gpus + 1);
+          if (gw_partial_.bytes < need) gw_partial_.reset(need);
+          launch_gate_wgrad(xrows, rows, d, dl_rows_.as<float>(), plan_, N, cfg_.num_gpus, gw_partial_.as<float>(),
+                            dwg, s);
+          }
+        }
         // units dropped by the capacity rule are in no dispatch row
         if (drops_enabled())
           launch_dropped_gate_wgrad(saved_x_, pos_.as<int32_t>(), topk_idx_.as<int32_t>(),
@@ -1127,7 +1138,7 @@ class Layer {
   Staging staging_[kStaging];
   int staging_next_ = 0;
   DevBuf x_perm_, act_, y_perm_, dy_perm_, dh_, dx_perm_, dl_rows_, relu_mask_, tile_colsum_,
-      row_expert_, tile_sum_, drop_partial_;
+      row_expert_, tile_sum_, drop_partial_, gw_partial_;
   std::vector<int32_t> host_counts_;
   double capacity_factor_ = 0.0;  // 0 / inf: no drops (FlexMoE)
   const void* saved_x_ = nullptr;  // gate input of the current step (must outlive backward)

@@ -105,3 +105,49 @@ def test_side_jobs_edge_shapes(T, cf):
     assert torch.equal(y_on, y_off)
     for key in g_on:
         assert torch.equal(g_on[key], g_off[key]), f"{key} differs between side jobs on and off"
+
+
+def test_nccl_transport_deterministic():
+    """NCCL transport (staging all-to-alls), 2 loopback ranks: the gate-weight
+    gradient is summed piece by piece over the send buffer in a fixed order, so
+    two runs of the same step give bit-identical gradients (StaticEP drops on)."""
+    import threading
+
+    from paper_2304_03946_b200.distributed import DistributedMoELayer, LoopbackHub
+
+    N, k, d, f, T, G = 8, 2, 256, 512, 3000, 2
+    cnt = torch.zeros(N, G, dtype=torch.int32)
+    for e in range(N):
+        cnt[e, e % G] = 1
+    cnt[0, 1] = 1  # expert 0 replicated
+    torch.manual_seed(9)
+    xs = [torch.randn(T, d).to(torch.bfloat16) for _ in range(G)]
+    dys = [(torch.randn(T, d) * 0.5).to(torch.bfloat16) for _ in range(G)]
+
+    def run():
+        hub = LoopbackHub(G)
+        outs = [None] * G
+
+        def body(r):
+            torch.cuda.set_device(0)
+            lay = MoELayer(N, k, d, f, replica_counts=cnt.numpy(), num_gpus=G, rank=r, max_tokens=T)
+            lay.set_capacity_factor(1.0)
+            p = lay.init_params(seed=4)
+            dl = DistributedMoELayer(lay, hub.endpoint(r), transport="nccl")
+            dev = torch.device("cuda", 0)
+            y = dl.forward(xs[r].to(dev), p["wg"], p["w1"], p["b1"], p["w2"], p["b2"])
+            g = dl.backward(dys[r].to(dev))
+            torch.cuda.synchronize()
+            outs[r] = (y.cpu(), g.dwg.cpu(), g.dx.cpu())
+
+        th = [threading.Thread(target=body, args=(r,)) for r in range(G)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=300)
+        return outs
+
+    a, b = run(), run()
+    for r in range(G):
+        for i, name in enumerate(("y", "dwg", "dx")):
+            assert torch.equal(a[r][i], b[r][i]), f"rank {r}: {name} differs between two runs"
