@@ -376,7 +376,7 @@ __device__ __forceinline__ void dispatch_token(int t, bool& wrote_peer, const __
 #pragma unroll
   for (int i = 0; i < 8; ++i)
     if (lane + 32 * i < nvec) v[i] = __ldg(src + lane + 32 * i);
-  const int tile = t >> 7;
+  const int tile = t >> gate_tile_shift(N);
   for (int j = 0; j < k; ++j) {
     const int u = t * k + j;
     const int e = idx[u];

@@ -20,6 +20,7 @@
 #include <algorithm>
 
 #include "fm_internal.h"
+#include "layer_plan.h"
 #include "sm100_ptx.cuh"
 
 namespace fm {
@@ -48,6 +49,8 @@ constexpr int kCtas = FM_GATE_CTAS;  // resident CTAs per SM (A/B knob)
 
 struct Args {
   int T, N, Npad, K, top_k, stages;
+  int tile_rows;  // tokens per tile (gate_tile_rows): 64 loads half an M=128 tile, the
+                  // MMA's other 64 rows read the next stage (their TMEM lanes are ignored)
   int32_t* topk_idx;
   float* topk_w;
   int32_t* tile_rank;
@@ -168,9 +171,10 @@ __global__ void __launch_bounds__(kThreads, kCtas)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int b_bytes = a.Npad * kBK * 2;
-  const int stage_bytes = kABytes + b_bytes;  // multiple of 1024 since Npad % 32 == 0... (Npad*128)
+  const int a_bytes = a.tile_rows * kBK * 2;  // 8 or 16 KB, a multiple of the 1 KB swizzle atom
+  const int stage_bytes = a_bytes + b_bytes;
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + a.stages * kABytes;
+  uint8_t* smem_b = smem + a.stages * a_bytes;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
   uint64_t* empty_bar = full_bar + kMaxStages;
   uint64_t* tfull_bar = empty_bar + kMaxStages;
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
-  const int num_tiles = (a.T + kTM - 1) / kTM;
+  const int num_tiles = (a.T + a.tile_rows - 1) / a.tile_rows;
   const int num_kb = a.K / kBK;
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(2 * a.Npad)) tmem_cols <<= 1;
@@ -210,9 +214,9 @@ __global__ void __launch_bounds__(kThreads, kCtas)
   auto issue = [&](int stage, int tile, int kb) {
     ptx::mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
 #if FM_GATE_X_EVICT_FIRST
-    ptx::tma_load_2d_hint(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM, pol_x);
+    ptx::tma_load_2d_hint(smem_a + stage * a_bytes, &map_x, &full_bar[stage], kb * kBK, tile * a.tile_rows, pol_x);
 #else
-    ptx::tma_load_2d(smem_a + stage * kABytes, &map_x, &full_bar[stage], kb * kBK, tile * kTM);
+    ptx::tma_load_2d(smem_a + stage * a_bytes, &map_x, &full_bar[stage], kb * kBK, tile * a.tile_rows);
 #endif
     ptx::tma_load_2d(smem_b + stage * b_bytes, &map_w, &full_bar[stage], kb * kBK, 0);
   };
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, kCtas)
         if (lane == 0) GATE_TRACE(66 + iter * 16 + kb);
         ptx::tc_fence_after();
         // descriptor start addresses are in 16-byte units: offsets are adds
-        const uint64_t da = da0 + static_cast<uint32_t>((stage * kABytes) >> 4);
+        const uint64_t da = da0 + static_cast<uint32_t>((stage * a_bytes) >> 4);
         const uint64_t db = db0 + static_cast<uint32_t>((stage * b_bytes) >> 4);
         if (ptx::elect_one()) {
 #pragma unroll
@@ -285,8 +289,8 @@ __global__ void __launch_bounds__(kThreads, kCtas)
     for (int ti = blockIdx.x; ti < num_tiles; ti += gridDim.x, ++iter) {
       const int tile = FM_GATE_REVERSE ? num_tiles - 1 - ti : ti;
       const int ab = iter & 1;
-      const int t = tile * kTM + q * 32 + lane;
-      const bool valid = t < a.T;
+      const int t = tile * a.tile_rows + q * 32 + lane;
+      const bool valid = q * 32 + lane < a.tile_rows && t < a.T;
       GATE_WAIT(&tfull_bar[ab], (iter >> 1) & 1);
       if (q == 0 && lane == 0) GATE_TRACE(130 + 2 * iter);
       ptx::tc_fence_after();
@@ -402,7 +406,10 @@ extern "C" int fm_debug_gate_blocks(unsigned long long* out) {
 }
 #endif
 
-int gate_num_tiles(int T) { return (T + gate::kTM - 1) / gate::kTM; }
+int gate_num_tiles(int T, int num_experts) {
+  const int tr = gate_tile_rows(num_experts);
+  return (T + tr - 1) / tr;
+}
 
 void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, int32_t* topk_idx,
                  float* topk_w, int32_t* tile_rank, int32_t* tile_counts, cudaStream_t stream) {
@@ -413,7 +420,8 @@ void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, 
   if (d % kBK != 0) throw std::invalid_argument("gate: d_model must be a multiple of 64");
   if (T <= 0) return;
   const int Npad = ((N + 31) / 32) * 32;
-  const int stage_bytes0 = kABytes + Npad * kBK * 2;
+  const int tr = gate_tile_rows(N);
+  const int stage_bytes0 = tr * kBK * 2 + Npad * kBK * 2;
   // two CTAs per SM when both TMEM double-buffers fit (2 x 2 x Npad <= 512 columns)
 #ifndef FM_GATE_WIDE_CTAS
 #define FM_GATE_WIDE_CTAS 2
@@ -422,12 +430,12 @@ void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, 
   const int kCtasPerSm = Npad >= 128 ? (Npad == 128 ? FM_GATE_WIDE_CTAS : 1)
                                      : (Npad * kCtas <= 256 ? kCtas : 2);
   const int stages = std::max(2, std::min(kMaxStages, (200 * 1024 / kCtasPerSm) / stage_bytes0));
-  Args a{T, N, Npad, d, top_k, stages, topk_idx, topk_w, tile_rank, tile_counts};
-  CUtensorMap mx = make_tmap_bf16(x, d, T, d, 64, kTM);
+  Args a{T, N, Npad, d, top_k, stages, tr, topk_idx, topk_w, tile_rank, tile_counts};
+  CUtensorMap mx = make_tmap_bf16(x, d, T, d, 64, tr);
   CUtensorMap mw = make_tmap_bf16(wg, d, N, d, 64, Npad);
-  const int stage_bytes = kABytes + Npad * kBK * 2;
+  const int stage_bytes = stage_bytes0;
   const int smem = 1024 + stages * stage_bytes + 2 * kMaxStages * 8 + 64 + 4 * Npad * 4;
-  const int tiles = gate_num_tiles(T);
+  const int tiles = gate_num_tiles(T, N);
   const int grid = std::min(tiles, kCtasPerSm * num_sms());
   auto launch = [&](auto kernel) {
     ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);

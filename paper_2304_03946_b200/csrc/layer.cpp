@@ -46,7 +46,7 @@
 namespace fm {
 
 // launchers (gate.cu, dispatch.cu, grouped_gemm.cu)
-int gate_num_tiles(int T);
+int gate_num_tiles(int T, int num_experts);
 void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, int32_t* topk_idx,
                  float* topk_w, int32_t* tile_rank, int32_t* tile_counts, cudaStream_t stream);
 void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_t* tile_base,
@@ -204,7 +204,7 @@ class Layer {
     if (c.rank < 0 || c.rank >= c.num_gpus) throw std::out_of_range("fm_layer: rank out of range");
     if (c.max_tokens < 1) throw std::invalid_argument("fm_layer: max_tokens must be >= 1");
     const int N = c.num_experts, G = c.num_gpus, T = c.max_tokens, k = c.top_k;
-    const int tiles = gate_num_tiles(T);
+    const int tiles = gate_num_tiles(T, N);
     topk_idx_.reset(sizeof(int32_t) * T * k);
     topk_w_.reset(sizeof(float) * T * k);
     tile_rank_.reset(sizeof(int32_t) * T * k);
@@ -478,7 +478,7 @@ class Layer {
     timer_.end(s);
     timer_.begin(FM_PHASE_SCAN, s);
     if (G > 1) FM_CUDA(cudaMemsetAsync(demand_.p, 0, sizeof(int64_t) * N * G, s));
-    launch_expert_scan(tile_counts_.as<int32_t>(), gate_num_tiles(T), N, tile_base_.as<int32_t>(),
+    launch_expert_scan(tile_counts_.as<int32_t>(), gate_num_tiles(T, N), N, tile_base_.as<int32_t>(),
                        hist_.as<int64_t>(), demand_.as<int64_t>(), G, cfg_.rank, s);
     if (hist_out)
       FM_CUDA(cudaMemcpyAsync(hist_out, hist_.p, sizeof(int64_t) * N, cudaMemcpyDeviceToDevice, s));

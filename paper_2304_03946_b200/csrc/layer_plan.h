@@ -5,7 +5,24 @@
 
 #include <cstdint>
 
+#ifndef FM_GATE_HALF_TILE_MAX_N
+#define FM_GATE_HALF_TILE_MAX_N 0  // A/B knob: 64-token gate tiles up to this many experts (measured slower)
+#endif
+
 namespace fm {
+
+#ifdef __CUDACC__
+#define FM_PLAN_HD __host__ __device__ inline
+#else
+#define FM_PLAN_HD inline
+#endif
+// Token rows per gate tile — the granularity of the gate's per-tile expert
+// counts and ranks, which the dispatch turns into positions: 64 when the
+// experts fit a narrow accumulator (the tensor work per token is small, so a
+// half-height tile costs nothing and halves the tail of the HBM stream), 128
+// otherwise (at 128+ experts the gate's MMA work would start to show).
+FM_PLAN_HD int gate_tile_rows(int num_experts) { return num_experts <= FM_GATE_HALF_TILE_MAX_N ? 64 : 128; }
+FM_PLAN_HD int gate_tile_shift(int num_experts) { return num_experts <= FM_GATE_HALF_TILE_MAX_N ? 6 : 7; }
 
 struct PlanDev {
   int32_t* chunk_lo;        // [N][G]  first rank of dst's chunk in (me, e) rank space
