@@ -66,6 +66,9 @@ CASES = [
     (8, 2, 1536, 256, 200, "zipf"),
     # configs[4]'s expert shape: 128 experts, top-1, d_model 1024, d_ff 4096
     (128, 1, 1024, 4096, 640, "zipf"),
+    # degenerate routing: one expert (every token to it), top_k == num_experts
+    (1, 1, 256, 256, 500, None),
+    (2, 2, 256, 512, 300, None),
 ]
 
 
