@@ -77,6 +77,7 @@ void ensure_dynamic_smem(const void* kernel, int bytes);
 
 // P2P arrival gating of a token-row grouped GEMM (see grouped_gemm.cu Args).
 struct SideJob;  // layer_plan.h
+struct P2P;      // layer_plan.h
 
 struct ArrivalGate {
   const unsigned long long* flags = nullptr;          // this GPU's flags of one exchange slot [src]
@@ -89,6 +90,6 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
                   cudaStream_t stream, const ArrivalGate* gate = nullptr, const int* b_slot = nullptr,
-                  int b_groups = 0, SideJob* side = nullptr);
+                  int b_groups = 0, SideJob* side = nullptr, const P2P* ready = nullptr);
 
 }  // namespace fm

@@ -100,6 +100,10 @@ struct Args {
   // side job (per-tile column sums, memory-bound) concurrently on their SMs
   int gemm_clusters;
   SideJob side;
+  // P2P "ready" signal (optional, ready.signal_slot >= 0): once every CTA's
+  // output stores completed, the last CTA publishes flags[slot][me] = epoch
+  // to every peer (what p2p_signal_kernel does one launch later)
+  P2P ready;
 };
 
 // kernel parameters = 3 tensor maps + Args (SideJob carries a P2P struct)
@@ -848,6 +852,23 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
 
   ptx::tc_fence_before();
   if (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  if (args.ready.signal_slot >= 0 && threadIdx.x == 0) {
+    // this CTA's TMA stores completed (bulk_wait 0 before the barrier):
+    // order them (async proxy) before the system-scope release, count the CTA
+    const P2P& rp = args.ready;
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence_system();
+    unsigned int* ctr = rp.done + rp.signal_slot;
+    if (atomicAdd(ctr, 1u) == gridDim.x - 1) {
+      *ctr = 0;  // the next launch with this slot is stream-ordered after this one
+      __threadfence_system();
+      for (int dst = 0; dst < rp.world; ++dst) {
+        unsigned long long* f =
+            reinterpret_cast<unsigned long long*>(rp.base[dst] + rp.flag_off) + rp.signal_slot * kMaxPeers + rp.me;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(rp.epoch) : "memory");
+      }
+    }
+  }
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc_cg<CG>(tmem_base, kTmemCols);
@@ -946,7 +967,7 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
                   const void* aux, const int* seg_start, const int* seg_rows,
                   const int* tile_prefix, int num_groups, int total_rows, int M_w, int N, int K,
                   cudaStream_t stream, const ArrivalGate* gate, const int* b_slot, int b_groups,
-                  SideJob* side) {
+                  SideJob* side, const P2P* ready) {
   using namespace gemm;
   if (N % kBN != 0) throw std::invalid_argument("grouped_gemm: N must be a multiple of 256");
   if (num_groups < 1 || num_groups > kMaxGroups)
@@ -954,6 +975,8 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
   if (total_rows % kBM != 0 || total_rows <= 0)
     throw std::invalid_argument("grouped_gemm: total_rows must be a positive multiple of 128");
   Args a{};
+  a.ready.signal_slot = -1;
+  if (ready && ready->signal_slot >= 0) a.ready = *ready;
   a.num_groups = num_groups;
   a.seg_start = seg_start;
   a.seg_rows = seg_rows;

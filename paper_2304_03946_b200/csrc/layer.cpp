@@ -558,10 +558,14 @@ class Layer {
   }
 
   // gate (P2P): FFN1 waits per 128-row tile for the sources whose rows it holds
+  // ready (P2P, optional): the FFN2 GEMM's last CTA publishes "Y ready"
   void expert_forward(const void* w1, const float* b1, const void* w2, const float* b2,
-                      cudaStream_t s, const ArrivalGate* gate = nullptr) {
+                      cudaStream_t s, const ArrivalGate* gate = nullptr, const P2P* ready = nullptr) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
-    if (Nl == 0) return;
+    if (Nl == 0) {
+      if (ready) launch_p2p_signal(*ready, cfg_.num_gpus, cfg_.rank, ready->signal_slot, ready->epoch, s);
+      return;
+    }
     const int rows = static_cast<int>(row_cap_);
     timer_.begin(FM_PHASE_FFN1_FWD, s);
     grouped_gemm(FM_GEMM_FWD_BIAS_RELU, x_perm_.p, w1, act_.p, b1, relu_mask_.p, plan_.seg_start,
@@ -571,7 +575,7 @@ class Layer {
     timer_.begin(FM_PHASE_FFN2_FWD, s);
     grouped_gemm(FM_GEMM_FWD_BIAS, act_.p, w2, y_perm_.p, b2, nullptr, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s, nullptr, operand_slots_dev(),
-                 operand_groups());
+                 operand_groups(), nullptr, ready);
     timer_.end(s);
   }
 
@@ -588,8 +592,10 @@ class Layer {
       if (signal_dx) p2p_signal(3, s);
       return;
     }
-    expert_dgrad(w1, w2, db1, s, gate);
-    if (signal_dx) p2p_signal(3, s);
+    // "dX ready" published by the FFN1 dgrad GEMM's last CTA (no signal launch)
+    const P2P dx_ready = p2p_args(3);
+    dgrad2(w2, db1, s, gate);
+    dgrad1(w1, s, signal_dx ? &dx_ready : nullptr);
     SideJob side = tile_sum_side(db2, dwg_tiles);
     wgrad2(dw2, s, &side);
     // P2P with the un-permute bound (fm_layer_p2p_bind_dx): it rides beside
@@ -618,15 +624,15 @@ class Layer {
                  operand_groups());
     timer_.end(s);
   }
-  // dX = dH . W1 -> [rows, d]
-  void dgrad1(const void* w1, cudaStream_t s) {
+  // dX = dH . W1 -> [rows, d]; ready (P2P, optional): its last CTA publishes "dX ready"
+  void dgrad1(const void* w1, cudaStream_t s, const P2P* ready = nullptr) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
     if (Nl == 0) return;
     const int rows = static_cast<int>(row_cap_);
     timer_.begin(FM_PHASE_FFN1_DGRAD, s);
     grouped_gemm(FM_GEMM_DGRAD, dh_.p, w1, dx_perm_.p, nullptr, nullptr, plan_.seg_start,
                  plan_.seg_rows, plan_.mtile_prefix, Nl, rows, 0, d, f, s, nullptr, operand_slots_dev(),
-                 operand_groups());
+                 operand_groups(), nullptr, ready);
     timer_.end(s);
   }
 
@@ -915,8 +921,8 @@ class Layer {
   // compute while remote ones are still arriving over NVLink.
   void expert_forward_p2p(const void* w1, const float* b1, const void* w2, const float* b2, cudaStream_t s) {
     const ArrivalGate gate = p2p_gate(0);
-    expert_forward(w1, b1, w2, b2, s, &gate);
-    p2p_signal(1, s);
+    const P2P y_ready = p2p_args(1);  // "Y ready" published by the FFN2 GEMM's last CTA
+    expert_forward(w1, b1, w2, b2, s, &gate, &y_ready);
   }
   void combine_p2p(void* y, cudaStream_t s) {
     timer_.begin(FM_PHASE_COMBINE_FWD, s);
