@@ -136,10 +136,19 @@ __device__ int block_exclusive_scan(int32_t* v, int n, int32_t* scratch) {
 // Every offset table is a block-wide scan over shared memory: a serial walk
 // by one thread is a dependent chain of ~7 cycles per instruction, which at
 // 64 experts cost ~100 us per step.
+// gathered_GN (optional): the all-gathered per-GPU histograms [G][N]; the
+// block first transposes them into `demand` ([N][G], TokenDemand layout) —
+// the demand_transpose launch folded into this one.
 __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
                             const int32_t* __restrict__ local_expert, int Nl, PlanDev p,
                             const int32_t* __restrict__ counts, const int64_t* __restrict__ demand,
-                            int32_t* __restrict__ status, bool flows_in_smem) {
+                            int32_t* __restrict__ status, bool flows_in_smem,
+                            const int64_t* __restrict__ gathered_GN) {
+  if (gathered_GN) {
+    int64_t* dem = const_cast<int64_t*>(demand);
+    for (int i = threadIdx.x; i < N * G; i += blockDim.x) dem[i] = gathered_GN[static_cast<size_t>(i % G) * N + i / G];
+    __syncthreads();  // the block's global writes are visible to route() below
+  }
   // shared: flows as int32 [N][G][G] (when they fit) | local experts [Nl] | segment starts [Nl]
   //       | replica counts [N][G] | mtile prefix [Nl] | scan buffer [N*G] | scratch [blockDim]
   extern __shared__ int32_t sf[];
@@ -1029,7 +1038,8 @@ void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_
 
 void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
                  const PlanDev& p, cudaStream_t s, const int32_t* counts, const int64_t* demand,
-                 int32_t* status) {
+                 int32_t* status, const int64_t* gathered_GN) {
+  if (gathered_GN && !demand) throw std::invalid_argument("plan: the transposed demand needs a demand buffer");
   if (demand && (N > 256 || G > kMaxGpus)) throw std::invalid_argument("route: bad dimensions");
   constexpr int kPlanThreads = 256;
   // the flows are staged in shared memory when they fit; beyond that (e.g.
@@ -1041,7 +1051,7 @@ void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expe
   if (smem > 200 * 1024) throw std::invalid_argument("plan: num_experts * num_gpus too large");
   ensure_dynamic_smem(reinterpret_cast<const void*>(plan_kernel), smem);
   plan_kernel<<<1, kPlanThreads, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status,
-                                            flows_in_smem);
+                                            flows_in_smem, gathered_GN);
   FM_LAUNCH_CHECK("plan_kernel");
 }
 

@@ -52,8 +52,8 @@ void launch_gate(const void* x, const void* wg, int T, int N, int d, int top_k, 
 void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_t* tile_base,
                         int64_t* hist, int64_t* demand_NG, int G, int me, cudaStream_t s);
 void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
-                 const PlanDev& p, cudaStream_t s, const int32_t* counts, const int64_t* demand = nullptr,
-                 int32_t* status = nullptr);
+                 const PlanDev& p, cudaStream_t s, const int32_t* counts, const int64_t* demand,
+                 int32_t* status, const int64_t* gathered_GN = nullptr);
 void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
                      const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
                      const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
@@ -491,10 +491,16 @@ class Layer {
 
   // route() on the device over demand_ (already complete), then the plan. In
   // StaticEP mode the demand first goes through the capacity-drop rule.
-  void route_device(cudaStream_t s) {
+  // gathered_GN (optional): the all-gathered histograms, transposed into the
+  // TokenDemand by the plan launch itself (no separate transpose kernel)
+  void route_device(cudaStream_t s, const int64_t* gathered_GN = nullptr) {
     const int N = cfg_.num_experts, G = cfg_.num_gpus;
     timer_.begin(FM_PHASE_ROUTE, s);
     const int64_t* routed = demand_.as<int64_t>();
+    if (gathered_GN && drops_enabled()) {  // the capacity rule reads the demand first
+      launch_demand_transpose(gathered_GN, N, G, demand_.as<int64_t>(), s);
+      gathered_GN = nullptr;
+    }
     if (drops_enabled()) {
       static_ep_kept_device(demand_.as<int64_t>(), N, G, capacity_factor_, kept_.as<int64_t>(),
                             dropped_.as<int64_t>(), s);
@@ -502,7 +508,7 @@ class Layer {
     }
     // route() over the demand and the dispatch plan in one single-block launch
     launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s,
-                counts_dev_, routed, route_status_.as<int32_t>());
+                counts_dev_, routed, route_status_.as<int32_t>(), gathered_GN);
     timer_.end(s);
   }
 
@@ -512,8 +518,7 @@ class Layer {
   void route_gathered(const int64_t* gathered_GN, int32_t* send_rows, int32_t* recv_rows,
                       cudaStream_t s) {
     const int N = cfg_.num_experts, G = cfg_.num_gpus;
-    launch_demand_transpose(gathered_GN, N, G, demand_.as<int64_t>(), s);
-    route_device(s);
+    route_device(s, gathered_GN);
     FM_CUDA(cudaMemcpyAsync(host_counts_.data(), plan_.send_rows, sizeof(int32_t) * 2 * G,
                             cudaMemcpyDeviceToHost, s));
     FM_CUDA(cudaMemcpyAsync(host_counts_.data() + 2 * G, route_status_.p, sizeof(int32_t),
@@ -884,8 +889,7 @@ class Layer {
   }
   void route_p2p(const int64_t* gathered_GN, cudaStream_t s) {
     require_linked();
-    launch_demand_transpose(gathered_GN, cfg_.num_experts, cfg_.num_gpus, demand_.as<int64_t>(), s);
-    route_device(s);  // flows + plan incl. every destination's X_perm rows; no host sync
+    route_device(s, gathered_GN);  // demand transpose + flows + plan incl. every destination's X_perm rows
   }
   // P2P launch parameters; with slot >= 0 the kernel's last block releases
   // the rows it pushed (flags[slot][me] = epoch on every peer).
