@@ -662,7 +662,8 @@ def run_ours(args, world, rank, local_rank):
         "relayout": 4 * recv_units * d * 2,
     }
     side_bytes = {"ffn2_wgrad": (1, "db2 / dWg tile column sums", units * (2 * d * 2 + 4)),
-                  "ffn1_wgrad": (2, "un-permute", units * (d * 2 + 12) + T * d * 2)}
+                  "ffn1_wgrad": (2, "un-permute" + (" + bias / gate-weight partial reduce" if side & 4 else ""),
+                                 units * (d * 2 + 12) + T * d * 2)}
     kernels = {}
     for name, (pms, n) in phases.items():
         if n == 0:

@@ -362,7 +362,8 @@ int fm_layer_local_experts(const fm_layer* layer, int* num_local, int32_t* exper
 /* Which memory-bound backward work of the last backward ran on spare CTA pairs
  * of a weight-gradient GEMM launch instead of its own kernel:
  * bit 0 the db2 / dWg tile column sums (FFN2 wgrad), bit 1 the un-permute
- * (FFN1 wgrad). Results are the same either way. */
+ * (FFN1 wgrad), bit 2 the per-expert reduce of the bias / gate-weight
+ * gradient partials (FFN1 wgrad). Results are the same either way. */
 int fm_layer_side_jobs(const fm_layer* layer, int* mask);
 /* enable = 0: run that work as standalone kernels (default 1). */
 int fm_layer_set_side_jobs(fm_layer* layer, int enable);

@@ -427,8 +427,46 @@ __device__ __forceinline__ void unpermute_side_vpl(const SideJob& sd, int cta, i
   }
 }
 
+// Side role, reduce: thread = (job, column); for every segment, eight
+// running sums over its tiles t0 + j, t0 + j + 8, ... (j = 0..7, tiles in
+// increasing order) combined in j order — exactly segment_tile_reduce_kernel's
+// arithmetic, with the eight tile lanes folded into one thread. Loads of the
+// eight chains are independent: eight in flight per thread.
+template <int THREADS>
+__device__ __forceinline__ void reduce_side(const SideJob& sd, int cta, int num_ctas) {
+  int total = 0;
+  for (int q = 0; q < sd.reduce_jobs; ++q) total += sd.r_cols[q];
+  for (int g = cta * THREADS + static_cast<int>(threadIdx.x); g < total; g += num_ctas * THREADS) {
+    int q = 0, col = g;
+    while (col >= sd.r_cols[q]) col -= sd.r_cols[q++];
+    const int cols = sd.r_cols[q];
+    const float* src = sd.r_partial[q] + col;
+    for (int li = 0; li < sd.Nl; ++li) {
+      const int t0 = sd.mtile_prefix[li], t1 = sd.mtile_prefix[li + 1];
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+      int t = t0;
+      for (; t + 8 <= t1; t += 8) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldg(src + static_cast<size_t>(t + j) * cols);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += v[j];
+      }
+      for (int j = 0; t + j < t1; ++j) acc[j] += __ldg(src + static_cast<size_t>(t + j) * cols);
+      float ssum = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ssum += acc[j];
+      const int oi = sd.r_out_index[q] ? sd.r_out_index[q][li] : li;
+      sd.r_out[q][static_cast<size_t>(oi) * cols + col] = ssum;
+    }
+  }
+}
+
 template <int THREADS>
 __device__ __forceinline__ void run_side(const SideJob& sd, int cta, int num_ctas) {
+  if (sd.reduce_jobs > 0) reduce_side<THREADS>(sd, cta, num_ctas);  // short: first
   if (sd.kind == 1) {
     colsum_side<THREADS>(sd, cta, num_ctas);
   } else if (sd.kind == 2) {
@@ -887,7 +925,7 @@ void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
     const int tpg = (args.M_w / C::kTileM) * (args.N / kBN);  // output tiles per group
     int clusters = grid / CG;
     int side = 0;
-    if (args.side.kind != 0) {
+    if (args.side.kind != 0 || args.side.reduce_jobs > 0) {
       // Side clusters for the tile column sums: the spare clusters of a
       // group-aligned split (64 of 74 CTA pairs at 64 tiles per group), used
       // only when they can finish the sums inside the GEMM (~45 GB/s per SM
@@ -925,7 +963,10 @@ void launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
 #endif
     a.gemm_clusters = std::min(clusters, std::max(1, args.num_groups * tpg));
     a.side.clusters = side;
-    if (side == 0) a.side.kind = 0;
+    if (side == 0) {
+      a.side.kind = 0;
+      a.side.reduce_jobs = 0;
+    }
     if (side_out) *side_out = side;
     grid = (a.gemm_clusters + side) * CG;
   }
@@ -1055,6 +1096,8 @@ void grouped_gemm(int variant, const void* A, const void* B, void* C, const floa
       if (side && side->kind == 1) {
         if (side->njobs < 1 || side->cols % 8 != 0 || side->cols > 8 * Cfg<1>::kThreads)
           throw std::invalid_argument("grouped_gemm: side column sums need cols % 8 == 0, cols <= 2048");
+        a.side = *side;
+      } else if (side && side->kind == 0 && side->reduce_jobs > 0) {
         a.side = *side;
       } else if (side && side->kind == 2) {
         const int v = side->d / 256;

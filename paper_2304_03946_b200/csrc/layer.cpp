@@ -413,10 +413,14 @@ class Layer {
       dgrad2(saved_w2_, db1, s);       // dY_perm, W2 -> dH (+ db1 tile partials)
       dgrad1(saved_w1_, s);            // dH, W1 -> dX_perm
       SideJob unp = unpermute_side(dx);
-      wgrad1(dw1, s, &unp);            // dH, X_perm (+ un-permute)
-      unpermuted = unp.clusters > 0;
-      side_jobs_ = (sums.clusters > 0 ? 1 : 0) | (unpermuted ? 2 : 0);
-      bias_grads(db1, db2, s, dwg_tiles ? dwg : nullptr, /*sums_done=*/sums.clusters > 0);
+      // the tile partials are complete once the column sums ran beside FFN2's
+      // wgrad: their per-expert reduce rides beside FFN1's too
+      if (sums.clusters > 0) add_reduce_jobs(unp, db1, db2, dwg_tiles ? dwg : nullptr);
+      wgrad1(dw1, s, (unp.kind || unp.reduce_jobs) ? &unp : nullptr);  // dH, X_perm (+ un-permute, reduce)
+      unpermuted = unp.clusters > 0 && unp.kind == 2;
+      const bool reduced = unp.clusters > 0 && unp.reduce_jobs > 0;
+      side_jobs_ = (sums.clusters > 0 ? 1 : 0) | (unpermuted ? 2 : 0) | (reduced ? 4 : 0);
+      if (!reduced) bias_grads(db1, db2, s, dwg_tiles ? dwg : nullptr, /*sums_done=*/sums.clusters > 0);
     }
     if (!unpermuted) unpermute(dx_perm_.p, saved_wg_, dx, s);
     gate_wgrad(x_perm_.p, plan_.totals, static_cast<int>(row_cap_), dwg, s, dwg_tiles);
@@ -688,6 +692,30 @@ class Layer {
     sd.gate_grad = cfg_.top_k > 1 ? 1 : 0;
     sd.est_rows = cur_T_ * cfg_.top_k;
     return sd;
+  }
+
+  // The per-expert reduce of the db1 / db2 / dWg tile partials (what
+  // bias_grads launches) appended to a side job. Single GPU with every expert
+  // local (no dWg rows of remote experts to clear first).
+  void add_reduce_jobs(SideJob& sd, float* db1, float* db2, float* dwg_tiles) {
+    const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
+    if (Nl == 0 || cfg_.num_gpus != 1 || Nl < cfg_.num_experts) return;
+    const int max_tiles = static_cast<int>(row_cap_ / 128);
+    float* part_db2 = tile_sum_.as<float>();
+    float* part_dwg = part_db2 + static_cast<size_t>(max_tiles) * d;
+    auto add = [&](const float* partial, int cols, const int32_t* oi, float* out) {
+      if (!out) return;
+      sd.r_partial[sd.reduce_jobs] = partial;
+      sd.r_cols[sd.reduce_jobs] = cols;
+      sd.r_out_index[sd.reduce_jobs] = oi;
+      sd.r_out[sd.reduce_jobs++] = out;
+    };
+    add(tile_colsum_.as<float>(), f, nullptr, db1);
+    add(part_db2, d, nullptr, db2);
+    add(part_dwg, d, local_expert_dev_, dwg_tiles);
+    sd.mtile_prefix = plan_.mtile_prefix;
+    sd.Nl = Nl;
+    if (!sd.est_rows) sd.est_rows = cur_T_ * cfg_.top_k;
   }
 
   // The db2 / dWg tile column-sum jobs (dY_perm; dl-weighted X_perm) as a

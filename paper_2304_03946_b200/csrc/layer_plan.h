@@ -99,6 +99,16 @@ struct SideJob {
   void* dx;         // bf16 [T][d]
   int T, k, d, gate_grad;
   P2P pp;           // P2P transport (pp.unit_dst == nullptr: local rows)
+  // then, on the same side CTAs, the per-segment reduce of tile partials
+  // (out[oi(li)][c] = sum over the segment's 128-row tiles of partial[tile][c]
+  // in segment_tile_reduce_kernel's order: eight running sums over the tiles
+  // congruent mod 8, combined in lane order); thread = one column of one
+  // job, all segments. Uses mtile_prefix / Nl.
+  int reduce_jobs;  // 0..3
+  const float* r_partial[3];
+  int r_cols[3];
+  const int32_t* r_out_index[3];  // null: li
+  float* r_out[3];
 };
 
 }  // namespace fm

@@ -18,8 +18,8 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = {
     # N, k, d, f, T, expected side_jobs mask with the side jobs enabled
-    "configs1": (16, 2, 1024, 4096, 65536, 0b11),
-    "top1_d1024": (64, 1, 1024, 4096, 32768, 0b11),
+    "configs1": (16, 2, 1024, 4096, 65536, 0b111),
+    "top1_d1024": (64, 1, 1024, 4096, 32768, 0b111),
     "d768": (32, 2, 768, 3072, 32768, 0b00),
 }
 
