@@ -610,10 +610,18 @@ class Layer {
     // P2P with the un-permute bound (fm_layer_p2p_bind_dx): it rides beside
     // the FFN1 weight gradients, reading the peers' dX rows once they are ready
     SideJob unp = (signal_dx && p2p_ && bound_dx_) ? unpermute_side(bound_dx_, bound_wg_) : SideJob{};
-    wgrad1(dw1, s, unp.kind ? &unp : nullptr);
-    unpermuted_ = unp.clusters > 0;
-    side_jobs_ = (side.clusters > 0 ? 1 : 0) | (unpermuted_ ? 2 : 0);
-    bias_grads(db1, db2, s, dwg_tiles, /*sums_done=*/side.clusters > 0);
+    // the reduce of the tile partials beside it too, once the column sums ran
+    // beside FFN2's wgrad (rows of experts hosted elsewhere zeroed first)
+    if (side.clusters > 0) {
+      if (dwg_tiles && nl() < cfg_.num_experts)
+        FM_CUDA(cudaMemsetAsync(dwg_tiles, 0, sizeof(float) * cfg_.num_experts * cfg_.d_model, s));
+      add_reduce_jobs(unp, db1, db2, dwg_tiles, /*remote_rows_zeroed=*/true);
+    }
+    wgrad1(dw1, s, (unp.kind || unp.reduce_jobs) ? &unp : nullptr);
+    unpermuted_ = unp.clusters > 0 && unp.kind == 2;
+    const bool reduced = unp.clusters > 0 && unp.reduce_jobs > 0;
+    side_jobs_ = (side.clusters > 0 ? 1 : 0) | (unpermuted_ ? 2 : 0) | (reduced ? 4 : 0);
+    if (!reduced) bias_grads(db1, db2, s, dwg_tiles, /*sums_done=*/side.clusters > 0);
   }
 
   // dH (masked by relu'), db1 tile partials, dX_perm
@@ -695,11 +703,12 @@ class Layer {
   }
 
   // The per-expert reduce of the db1 / db2 / dWg tile partials (what
-  // bias_grads launches) appended to a side job. Single GPU with every expert
-  // local (no dWg rows of remote experts to clear first).
-  void add_reduce_jobs(SideJob& sd, float* db1, float* db2, float* dwg_tiles) {
+  // bias_grads launches) appended to a side job. The dWg rows of experts
+  // hosted elsewhere must already be zero (remote_rows_zeroed) unless every
+  // expert is local.
+  void add_reduce_jobs(SideJob& sd, float* db1, float* db2, float* dwg_tiles, bool remote_rows_zeroed = false) {
     const int Nl = nl(), d = cfg_.d_model, f = cfg_.d_ff;
-    if (Nl == 0 || cfg_.num_gpus != 1 || Nl < cfg_.num_experts) return;
+    if (Nl == 0 || (Nl < cfg_.num_experts && dwg_tiles && !remote_rows_zeroed)) return;
     const int max_tiles = static_cast<int>(row_cap_ / 128);
     float* part_db2 = tile_sum_.as<float>();
     float* part_dwg = part_db2 + static_cast<size_t>(max_tiles) * d;

@@ -77,7 +77,7 @@ def test_p2p_world1_side_jobs_bit_identical():
         runs.append((y.clone(), {key: v.clone() for key, v in vars(g).items() if torch.is_tensor(v)},
                      lay.side_jobs))
     (y_on, g_on, m_on), (y_off, g_off, m_off) = runs
-    assert m_on == 0b11 and m_off == 0
+    assert m_on == 0b111 and m_off == 0
     assert torch.equal(y_on, y_off)
     for key in g_on:
         assert torch.equal(g_on[key], g_off[key]), f"{key} differs between side jobs on and off"
