@@ -139,11 +139,62 @@ __device__ int block_exclusive_scan(int32_t* v, int n, int32_t* scratch) {
 // gathered_GN (optional): the all-gathered per-GPU histograms [G][N]; the
 // block first transposes them into `demand` ([N][G], TokenDemand layout) —
 // the demand_transpose launch folded into this one.
+// Fused expert scan (single GPU, N x tiles <= 8192): the gate's per-tile
+// counts -> per-expert exclusive prefix over tiles (tile_base), the histogram
+// and the demand column, as expert_scan_kernel, before route() reads that
+// demand. 256 threads = N groups of 256/N threads; a thread keeps a run of up
+// to 32 consecutive tiles of its expert in registers (independent loads), the
+// group scans its run totals with shuffles, then the thread writes its bases.
+struct PlanScan {
+  const int32_t* tile_counts;  // null: the scan ran as its own kernel
+  int num_tiles;
+  int32_t* tile_base;
+  int64_t* hist;
+};
+constexpr int kPlanScanRun = 32;
+
+__device__ __forceinline__ void plan_fused_scan(const PlanScan& sc, int N, int64_t* demand_col) {
+  int tpe = static_cast<int>(blockDim.x) / N;  // threads per expert: a power of two <= 32
+  tpe = tpe >= 32 ? 32 : tpe >= 16 ? 16 : tpe >= 8 ? 8 : tpe >= 4 ? 4 : tpe >= 2 ? 2 : 1;
+  const int e = static_cast<int>(threadIdx.x) / tpe, r = static_cast<int>(threadIdx.x) % tpe;
+  const bool active = e < N;
+  const int per = (sc.num_tiles + tpe - 1) / tpe, t0 = r * per;
+  int v[kPlanScanRun];
+  int sum = 0;
+#pragma unroll
+  for (int i = 0; i < kPlanScanRun; ++i) {
+    const int t = t0 + i;
+    v[i] = (active && i < per && t < sc.num_tiles) ? __ldg(sc.tile_counts + static_cast<size_t>(t) * N + e) : 0;
+  }
+#pragma unroll
+  for (int i = 0; i < kPlanScanRun; ++i) sum += v[i];
+  int incl = sum;  // inclusive scan over the tpe lanes of this expert's group
+  for (int o = 1; o < tpe; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, o, tpe);
+    if (r >= o) incl += u;
+  }
+  int run = incl - sum;
+#pragma unroll
+  for (int i = 0; i < kPlanScanRun; ++i) {
+    const int t = t0 + i;
+    if (active && i < per && t < sc.num_tiles) sc.tile_base[static_cast<size_t>(t) * N + e] = run;
+    run += v[i];
+  }
+  if (active && r == tpe - 1) {
+    sc.hist[e] = incl;
+    demand_col[e] = incl;
+  }
+}
+
 __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
                             const int32_t* __restrict__ local_expert, int Nl, PlanDev p,
                             const int32_t* __restrict__ counts, const int64_t* __restrict__ demand,
                             int32_t* __restrict__ status, bool flows_in_smem,
-                            const int64_t* __restrict__ gathered_GN) {
+                            const int64_t* __restrict__ gathered_GN, PlanScan scan) {
+  if (scan.tile_counts) {
+    plan_fused_scan(scan, N, const_cast<int64_t*>(demand));
+    __syncthreads();  // the block's demand writes are visible to route() below
+  }
   if (gathered_GN) {
     int64_t* dem = const_cast<int64_t*>(demand);
     for (int i = threadIdx.x; i < N * G; i += blockDim.x) dem[i] = gathered_GN[static_cast<size_t>(i % G) * N + i / G];
@@ -1036,10 +1087,24 @@ void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_
   FM_LAUNCH_CHECK("expert_scan_kernel");
 }
 
+bool plan_can_fuse_scan(int N, int G, int num_tiles) {
+#ifdef FM_NO_PLAN_SCAN  // A/B knob: the expert scan always as its own kernel
+  return false;
+#endif
+  if (G != 1 || N > 256) return false;
+  int tpe = 256 / N;
+  tpe = tpe >= 32 ? 32 : tpe >= 16 ? 16 : tpe >= 8 ? 8 : tpe >= 4 ? 4 : tpe >= 2 ? 2 : 1;
+  return (num_tiles + tpe - 1) / tpe <= kPlanScanRun;
+}
+
 void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
                  const PlanDev& p, cudaStream_t s, const int32_t* counts, const int64_t* demand,
-                 int32_t* status, const int64_t* gathered_GN) {
+                 int32_t* status, const int64_t* gathered_GN, const int32_t* scan_tile_counts,
+                 int scan_num_tiles, int32_t* scan_tile_base, int64_t* scan_hist) {
   if (gathered_GN && !demand) throw std::invalid_argument("plan: the transposed demand needs a demand buffer");
+  const PlanScan scan{scan_tile_counts, scan_num_tiles, scan_tile_base, scan_hist};
+  if (scan.tile_counts && (!demand || gathered_GN || !plan_can_fuse_scan(N, G, scan_num_tiles)))
+    throw std::invalid_argument("plan: the fused expert scan needs G == 1, <= 32 tiles per thread and a demand");
   if (demand && (N > 256 || G > kMaxGpus)) throw std::invalid_argument("route: bad dimensions");
   constexpr int kPlanThreads = 256;
   // the flows are staged in shared memory when they fit; beyond that (e.g.
@@ -1051,7 +1116,7 @@ void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expe
   if (smem > 200 * 1024) throw std::invalid_argument("plan: num_experts * num_gpus too large");
   ensure_dynamic_smem(reinterpret_cast<const void*>(plan_kernel), smem);
   plan_kernel<<<1, kPlanThreads, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status,
-                                            flows_in_smem, gathered_GN);
+                                            flows_in_smem, gathered_GN, scan);
   FM_LAUNCH_CHECK("plan_kernel");
 }
 

@@ -53,7 +53,9 @@ void launch_expert_scan(const int32_t* tile_counts, int num_tiles, int N, int32_
                         int64_t* hist, int64_t* demand_NG, int G, int me, cudaStream_t s);
 void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expert, int Nl,
                  const PlanDev& p, cudaStream_t s, const int32_t* counts, const int64_t* demand,
-                 int32_t* status, const int64_t* gathered_GN = nullptr);
+                 int32_t* status, const int64_t* gathered_GN = nullptr, const int32_t* scan_tile_counts = nullptr,
+                 int scan_num_tiles = 0, int32_t* scan_tile_base = nullptr, int64_t* scan_hist = nullptr);
+bool plan_can_fuse_scan(int N, int G, int num_tiles);
 void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
                      const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
                      const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
@@ -373,7 +375,7 @@ class Layer {
     if (cfg_.num_gpus != 1)
       throw std::logic_error("fm_layer_forward: fused path is single-GPU; use the phase API");
     check_tokens(T);
-    gate(x, T, wg, nullptr, s);
+    gate(x, T, wg, nullptr, s, /*defer_scan=*/true);
     route_device(s);
     timer_.begin(FM_PHASE_DISPATCH, s);
     launch_dispatch(x, T, cfg_.d_model, cfg_.top_k, cfg_.num_experts, 1, 0, true,
@@ -473,13 +475,22 @@ class Layer {
   // ------------------------------------------------------------ phases
   // Gate + per-expert scan. hist_out (device int64 [N], optional) receives
   // this GPU's TokenDemand column for the all-gather.
-  void gate(const void* x, int T, const void* wg, int64_t* hist_out, cudaStream_t s) {
+  // defer_scan (fused single-GPU step): the expert scan runs inside the plan
+  // launch (route_device) when the shape allows — one launch less between
+  // the gate and the dispatch
+  void gate(const void* x, int T, const void* wg, int64_t* hist_out, cudaStream_t s, bool defer_scan = false) {
     check_tokens(T);
     const int N = cfg_.num_experts, G = cfg_.num_gpus;
     timer_.begin(FM_PHASE_GATE, s);
     launch_gate(x, wg, T, N, cfg_.d_model, cfg_.top_k, topk_idx_.as<int32_t>(),
                 topk_w_.as<float>(), tile_rank_.as<int32_t>(), tile_counts_.as<int32_t>(), s);
     timer_.end(s);
+    cur_T_ = T;
+    saved_x_ = x;
+    fused_state_ = false;
+    scan_deferred_ =
+        defer_scan && !hist_out && plan_can_fuse_scan(N, G, gate_num_tiles(T, N)) && !drops_enabled();
+    if (scan_deferred_) return;
     timer_.begin(FM_PHASE_SCAN, s);
     if (G > 1) FM_CUDA(cudaMemsetAsync(demand_.p, 0, sizeof(int64_t) * N * G, s));
     launch_expert_scan(tile_counts_.as<int32_t>(), gate_num_tiles(T, N), N, tile_base_.as<int32_t>(),
@@ -487,9 +498,6 @@ class Layer {
     if (hist_out)
       FM_CUDA(cudaMemcpyAsync(hist_out, hist_.p, sizeof(int64_t) * N, cudaMemcpyDeviceToDevice, s));
     timer_.end(s);
-    cur_T_ = T;
-    saved_x_ = x;
-    fused_state_ = false;
     if (p2p_) ++epoch_;  // one exchange epoch per step, the same on every GPU
   }
 
@@ -511,8 +519,15 @@ class Layer {
       routed = kept_.as<int64_t>();
     }
     // route() over the demand and the dispatch plan in one single-block launch
-    launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s,
-                counts_dev_, routed, route_status_.as<int32_t>(), gathered_GN);
+    if (scan_deferred_) {  // expert scan + route + plan in one launch
+      launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s, counts_dev_, routed,
+                  route_status_.as<int32_t>(), nullptr, tile_counts_.as<int32_t>(), gate_num_tiles(cur_T_, N),
+                  tile_base_.as<int32_t>(), hist_.as<int64_t>());
+      scan_deferred_ = false;
+    } else {
+      launch_plan(flows_.as<int64_t>(), N, G, cfg_.rank, local_expert_dev_, nl(), plan_, s,
+                  counts_dev_, routed, route_status_.as<int32_t>(), gathered_GN);
+    }
     timer_.end(s);
   }
 
@@ -1190,6 +1205,7 @@ class Layer {
   double capacity_factor_ = 0.0;  // 0 / inf: no drops (FlexMoE)
   const void* saved_x_ = nullptr;  // gate input of the current step (must outlive backward)
   int side_jobs_ = 0;              // fm_layer_side_jobs of the last backward
+  bool scan_deferred_ = false;     // the expert scan runs inside the next plan launch
   const void* bound_wg_ = nullptr;  // fm_layer_p2p_bind_dx: where this step's un-permute
   void* bound_dx_ = nullptr;        //   reads the gate rows / writes dx
   bool unpermuted_ = false;         // the bound un-permute ran beside the FFN1 wgrad
