@@ -81,6 +81,10 @@ def main(tag="r01"):
     summary = {}
     if (OUT / "launches.csv").exists():
         L = launches()
+        # one complete steady-state step: from a gate launch to the next
+        starts = [i for i, (n, _) in enumerate(L) if "gate_kernel" in n]
+        if len(starts) >= 2:
+            L = L[starts[-2]:starts[-1]]
         tot = sum(t for _, t in L)
         lines += ["## Launch list of one step (cold-cache, serialised: compare shares)", "",
                   "| kernel | µs | share |", "|---|---:|---:|"]

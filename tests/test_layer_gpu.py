@@ -69,6 +69,12 @@ CASES = [
     # degenerate routing: one expert (every token to it), top_k == num_experts
     (1, 1, 256, 256, 500, None),
     (2, 2, 256, 512, 300, None),
+    # the expert scan fused into the plan launch: at its limit (64 experts x 128
+    # gate tiles = 32 tiles per thread), one tile past it (separate scan
+    # kernel), and a non-power-of-two expert count (groups of 8 threads, 3 idle)
+    (64, 2, 256, 256, 16384, "zipf"),
+    (64, 2, 256, 256, 16385, "zipf"),
+    (29, 3, 256, 256, 4000, "zipf"),
 ]
 
 
