@@ -93,7 +93,7 @@ __global__ void expert_scan_kernel(const int32_t* __restrict__ tile_counts, int 
 // warp scans the warp totals: two block barriers per call (a Hillis-Steele
 // pass over the block would take 2 log2(blockDim) of them — the plan kernel
 // is a chain of such scans and runs single-block on the critical path).
-__device__ int block_exclusive_scan(int32_t* v, int n, int32_t* scratch) {
+__device__ __noinline__ int block_exclusive_scan(int32_t* v, int n, int32_t* scratch) {
   const int per = (n + blockDim.x - 1) / blockDim.x;
   const int lo = min(n, static_cast<int>(threadIdx.x) * per), hi = min(n, lo + per);
   int sum = 0;
@@ -159,13 +159,13 @@ __device__ __forceinline__ void plan_fused_scan(const PlanScan& sc, int N, int64
   const int e = static_cast<int>(threadIdx.x) / tpe, r = static_cast<int>(threadIdx.x) % tpe;
   const bool active = e < N;
   const int per = (sc.num_tiles + tpe - 1) / tpe, t0 = r * per;
+  const int lim = active ? max(0, min(per, sc.num_tiles - t0)) : 0;  // tiles of this thread's run
+  const size_t at = active ? static_cast<size_t>(t0) * N + e : 0;
+  const int32_t* src = sc.tile_counts + at;
   int v[kPlanScanRun];
   int sum = 0;
 #pragma unroll
-  for (int i = 0; i < kPlanScanRun; ++i) {
-    const int t = t0 + i;
-    v[i] = (active && i < per && t < sc.num_tiles) ? __ldg(sc.tile_counts + static_cast<size_t>(t) * N + e) : 0;
-  }
+  for (int i = 0; i < kPlanScanRun; ++i) v[i] = i < lim ? __ldg(src + static_cast<size_t>(i) * N) : 0;
 #pragma unroll
   for (int i = 0; i < kPlanScanRun; ++i) sum += v[i];
   int incl = sum;  // inclusive scan over the tpe lanes of this expert's group
@@ -174,10 +174,10 @@ __device__ __forceinline__ void plan_fused_scan(const PlanScan& sc, int N, int64
     if (r >= o) incl += u;
   }
   int run = incl - sum;
+  int32_t* dst = sc.tile_base + at;
 #pragma unroll
   for (int i = 0; i < kPlanScanRun; ++i) {
-    const int t = t0 + i;
-    if (active && i < per && t < sc.num_tiles) sc.tile_base[static_cast<size_t>(t) * N + e] = run;
+    if (i < lim) dst[static_cast<size_t>(i) * N] = run;
     run += v[i];
   }
   if (active && r == tpe - 1) {
@@ -186,10 +186,18 @@ __device__ __forceinline__ void plan_fused_scan(const PlanScan& sc, int N, int64
   }
 }
 
+// route() for one expert, one out-of-line copy: the plan kernel runs once per
+// step on one SM, so its time is mostly instruction fetch (ncu: "no
+// instruction" the top stall) — its code is kept small rather than inlined.
+__device__ __noinline__ int route_one_expert(int e, const int64_t* D, const int32_t* cnt, int G, int64_t* flows) {
+  return split_expert_demand(e, D, cnt, G, flows);
+}
+
+template <bool flows_in_smem>
 __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
                             const int32_t* __restrict__ local_expert, int Nl, PlanDev p,
                             const int32_t* __restrict__ counts, const int64_t* __restrict__ demand,
-                            int32_t* __restrict__ status, bool flows_in_smem,
+                            int32_t* __restrict__ status,
                             const int64_t* __restrict__ gathered_GN, PlanScan scan) {
   if (scan.tile_counts) {
     plan_fused_scan(scan, N, const_cast<int64_t*>(demand));
@@ -219,7 +227,12 @@ __global__ void plan_kernel(int64_t* __restrict__ flows, int N, int G, int me,
     for (int e = threadIdx.x; e < N; e += blockDim.x) {
       int64_t* fe = flows + static_cast<size_t>(e) * G * G;
       for (int i = 0; i < G * G; ++i) fe[i] = 0;
-      const int st = split_expert_demand(e, demand, counts, G, flows);
+      // one GPU: Alg. 3 keeps every unit where it is (share = load, keep =
+      // min(share, D) = load; nothing remote) — the same result without
+      // fetching route()'s code
+      const int st = G == 1 ? (demand[e] == 0 ? kRouteOk : counts[e] > 0 ? (flows[e] = demand[e], kRouteOk)
+                                                                         : kRouteNoReplica)
+                            : route_one_expert(e, demand, counts, G, flows);
       if (st != kRouteOk && status)
         atomicCAS(status, 0, st == kRouteNoReplica ? FM_ERR_INVALID_ARGUMENT : FM_ERR_LOGIC);
     }
@@ -1114,9 +1127,15 @@ void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expe
   const bool flows_in_smem = base + N * G * G * 4 <= 200 * 1024;
   const int smem = base + (flows_in_smem ? N * G * G * 4 : 0);
   if (smem > 200 * 1024) throw std::invalid_argument("plan: num_experts * num_gpus too large");
-  ensure_dynamic_smem(reinterpret_cast<const void*>(plan_kernel), smem);
-  plan_kernel<<<1, kPlanThreads, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status,
-                                            flows_in_smem, gathered_GN, scan);
+  if (flows_in_smem) {
+    ensure_dynamic_smem(reinterpret_cast<const void*>(plan_kernel<true>), smem);
+    plan_kernel<true><<<1, kPlanThreads, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status,
+                                                    gathered_GN, scan);
+  } else {
+    ensure_dynamic_smem(reinterpret_cast<const void*>(plan_kernel<false>), smem);
+    plan_kernel<false><<<1, kPlanThreads, smem, s>>>(flows, N, G, me, local_expert, Nl, p, counts, demand, status,
+                                                     gathered_GN, scan);
+  }
   FM_LAUNCH_CHECK("plan_kernel");
 }
 
