@@ -13,6 +13,7 @@
 //     inside a segment rows are ordered by source GPU, then rank.
 // Everything here is integer-exact and deterministic; the only atomics are
 // fp32 additions into bias / gate-weight gradients.
+#include <map>
 #include <mutex>
 #include <unordered_map>
 #include <cuda_bf16.h>
@@ -728,6 +729,131 @@ __global__ void __launch_bounds__(256, VPL <= 4 ? 3 : 1) combine_bwd_kernel(
   p2p_release_when_last(pp, wrote_peer);  // P2P: dY rows and dl are in the expert GPUs' arenas
 }
 
+// Pipelined combine backward (top_k <= 2, d <= 1024): the register-held kernel
+// above keeps <= 2 rows per warp in flight (80 registers, 3 blocks per SM:
+// 0.87 of copy bandwidth at full clock, the lowest of the gathers). Here each
+// warp copies its NEXT token's dy row and expert-output rows into its shared-
+// memory stage with cp.async (16 B per lane, L2 only — coherent with rows a
+// peer wrote this step) while it computes the current token, and the unit
+// indices are loaded one token further ahead. A lane reads back only the
+// chunks it copied itself, so cp.async.wait_group orders it without a warp
+// barrier. Same arithmetic in the same order as combine_bwd_token.
+#ifndef FM_COMBINE_BWD_PIPE
+#define FM_COMBINE_BWD_PIPE 1
+#endif
+constexpr int kCbWarps = 8;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(__cvta_generic_to_global(gmem))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+struct CbMeta {
+  int pos, to;  // lane j < k: unit j's row and destination GPU
+  float w;
+};
+
+template <int VPL>
+__global__ void __launch_bounds__(kCbWarps * 32, 2) combine_bwd_pipe_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Yl,
+    const int32_t* __restrict__ pos, const float* __restrict__ w, int T, int k,
+    __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P pp,
+    int tok_blocks, PlanDev pad_plan) {
+  constexpr int kRow = 32 * VPL;  // uint4 per row
+  constexpr int d = VPL * 256;
+  extern __shared__ uint4 cb_ring[];  // [warp][2 stages][dy, Y_0, Y_1][kRow]
+  bool wrote_peer = false;
+  if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero dYl's padding rows
+    const int b = blockIdx.x - tok_blocks;
+    zero_pad_segment(dYl, d, pad_plan, b / kPadParts, b % kPadParts, kPadParts, nullptr);
+  } else {
+    const int lane = threadIdx.x & 31;
+    uint4* ring = cb_ring + (threadIdx.x >> 5) * (2 * 3 * kRow);
+    const int W = tok_blocks * kCbWarps;
+    auto meta = [&](int t) {
+      CbMeta m{0, -1, 0.0f};
+      if (t < T) {
+        unit_meta(pos, w, static_cast<size_t>(t) * k, k, lane, m.pos, m.w);
+        m.to = unit_dst_of(pp, static_cast<size_t>(t) * k, k, lane);
+      }
+      return m;
+    };
+    auto fetch = [&](int t, int stage, const CbMeta& m) {
+      if (t < T) {
+        uint4* s = ring + stage * 3 * kRow;
+        const uint4* g = reinterpret_cast<const uint4*>(dy + static_cast<size_t>(t) * d);
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) cp_async16(s + lane + 32 * i, g + lane + 32 * i);
+        for (int j = 0; j < k; ++j) {
+          const int row = __shfl_sync(0xffffffffu, m.pos, j);
+          const int to = __shfl_sync(0xffffffffu, m.to, j);
+          if (row < 0) continue;
+          const uint4* src = reinterpret_cast<const uint4*>(
+              (to >= 0 ? reinterpret_cast<const __nv_bfloat16*>(pp.base[to] + pp.y_off) : Yl) +
+              static_cast<size_t>(row) * d);
+#pragma unroll
+          for (int i = 0; i < VPL; ++i) cp_async16(s + (1 + j) * kRow + lane + 32 * i, src + lane + 32 * i);
+        }
+      }
+      cp_async_commit();  // one group per call, empty or not: wait_group 1 counts calls
+    };
+    int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    CbMeta cur = meta(t), nxt = meta(t + W);
+    fetch(t, 0, cur);
+    int stage = 0;
+    for (; t < T; t += W) {
+      const CbMeta after = meta(t + 2 * W);  // lands while this token computes
+      fetch(t + W, stage ^ 1, nxt);
+      cp_async_wait1();  // this lane's copies of token t are in shared memory
+      const uint4* s = ring + stage * 3 * kRow;
+      float my_dw = 0.0f;
+      for (int j = 0; j < k; ++j) {
+        const int row = __shfl_sync(0xffffffffu, cur.pos, j);
+        const float wj = __shfl_sync(0xffffffffu, cur.w, j);
+        if (row < 0) {
+          if (lane == j) my_dw = 0.0f;
+          continue;
+        }
+        const int to = __shfl_sync(0xffffffffu, cur.to, j);
+        wrote_peer |= to >= 0 && to != pp.me;
+        uint4* dst = reinterpret_cast<uint4*>(peer_rows(pp, pp.dy_off, to, dYl) + static_cast<size_t>(row) * d);
+        float dot = 0.0f;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const uint4 q = s[(1 + j) * kRow + lane + 32 * i], gv = s[lane + 32 * i];
+          const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
+          const uint32_t gs[4] = {gv.x, gv.y, gv.z, gv.w};
+          uint32_t o[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            dot = fmaf(bf16lo(gs[c]), bf16lo(qs[c]), dot);
+            dot = fmaf(bf16hi(gs[c]), bf16hi(qs[c]), dot);
+            o[c] = pack2(wj * bf16lo(gs[c]), wj * bf16hi(gs[c]));
+          }
+          dst[lane + 32 * i] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        dot = warp_sum(dot);
+        if (lane == j) my_dw = dot;
+      }
+      float wdw = lane < k ? cur.w * my_dw : 0.0f;
+      wdw = warp_sum(wdw);
+      if (lane < k) {
+        const float g_l = cur.w * (my_dw - wdw);
+        dl[static_cast<size_t>(t) * k + lane] = g_l;
+        float* dl_rows = peer_rows(pp, pp.dl_off, cur.to, dl_rows_l);
+        if (dl_rows && cur.pos >= 0) dl_rows[cur.pos] = g_l;
+      }
+      cur = nxt;
+      nxt = after;
+      stage ^= 1;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // no copy outstanding at exit
+  }
+  p2p_release_when_last(pp, wrote_peer);
+}
+
 // dx[t] = sum_j dXbuf[pos[t,j]] + sum_j dl[t,j] * Wg[idx[t,j], :]
 // P2P: dX rows are read from the expert's GPU (NVLink loads from its dX_perm).
 template <int VPL>
@@ -1215,6 +1341,43 @@ void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T
   FM_LAUNCH_CHECK("combine_fwd_kernel");
 }
 
+// The pipelined combine backward (V <= 4): one resident wave of warps striding
+// over the tokens, so every warp pipelines across its tokens.
+template <int V>
+bool launch_combine_bwd_pipe(const void* dy, const void* Y, const int32_t* pos, const float* w, int T, int k,
+                             void* dYbuf, float* dl, float* dl_rows, cudaStream_t s, const P2P& pp,
+                             int pad_blocks, const PlanDev& pad_plan) {
+  if constexpr (V > 4) {
+    return false;
+  } else {
+    const void* kern = reinterpret_cast<const void*>(combine_bwd_pipe_kernel<V>);
+    const int smem = kCbWarps * 2 * 3 * 32 * V * 16;
+    ensure_dynamic_smem(kern, smem);
+    static std::mutex mu;
+    static std::map<int, int> per_sm_cache;  // device -> resident blocks per SM
+    int dev = 0;
+    FM_CUDA(cudaGetDevice(&dev));
+    int per_sm = 0;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      auto it = per_sm_cache.find(dev);
+      if (it == per_sm_cache.end()) {
+        int n = 0;
+        FM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kCbWarps * 32, smem));
+        it = per_sm_cache.emplace(dev, std::max(1, n)).first;
+      }
+      per_sm = it->second;
+    }
+    const int tok_blocks = std::min((std::max(T, 0) + kCbWarps - 1) / kCbWarps, per_sm * num_sms());
+    if (tok_blocks + pad_blocks == 0) return true;
+    combine_bwd_pipe_kernel<V><<<tok_blocks + pad_blocks, kCbWarps * 32, smem, s>>>(
+        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(Y), pos, w, T, k,
+        static_cast<__nv_bfloat16*>(dYbuf), dl, dl_rows, pp, tok_blocks, pad_plan);
+    FM_LAUNCH_CHECK("combine_bwd_pipe_kernel");
+    return true;
+  }
+}
+
 void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const float* w, int T,
                         int d, int k, void* dYbuf, float* dl, float* dl_rows, cudaStream_t s, const P2P* pp,
                         const PlanDev* pad_plan, int Nl) {
@@ -1223,6 +1386,15 @@ void launch_combine_bwd(const void* dy, const void* Y, const int32_t* pos, const
   const int warps = 8;
   const int pad_blocks = pad_plan ? Nl * kPadParts : 0;
   const PlanDev nop{};
+#if FM_COMBINE_BWD_PIPE
+  if (k <= 2 && d <= 1024) {
+    bool launched = false;
+    FM_VPL_DISPATCH(d, (launched = launch_combine_bwd_pipe<V>(dy, Y, pos, w, T, k, dYbuf, dl, dl_rows, s,
+                                                              pp ? *pp : none, pad_blocks,
+                                                              pad_plan ? *pad_plan : nop)));
+    if (launched) return;
+  }
+#endif
   int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
   if (pp && pp->signal_slot >= 0)  // P2P pushes: one resident wave (see launch_dispatch)
     FM_VPL_DISPATCH(d, (tok_blocks = std::min(tok_blocks, resident_grid(
