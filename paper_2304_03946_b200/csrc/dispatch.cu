@@ -741,6 +741,16 @@ __global__ void __launch_bounds__(256, VPL <= 4 ? 3 : 1) combine_bwd_kernel(
 #ifndef FM_COMBINE_BWD_PIPE
 #define FM_COMBINE_BWD_PIPE 1
 #endif
+// A/B knobs, measured and off (profiles/r02_gather_pipe.log): the same
+// pipelining for the combine forward (-7 µs, but the combine backward after it
+// +6 µs: no net change) and for the dispatch (+4 µs: its per-token index chain
+// is not what limits it)
+#ifndef FM_COMBINE_FWD_PIPE
+#define FM_COMBINE_FWD_PIPE 0
+#endif
+#ifndef FM_DISPATCH_PIPE
+#define FM_DISPATCH_PIPE 0
+#endif
 constexpr int kCbWarps = 8;
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
@@ -850,6 +860,167 @@ __global__ void __launch_bounds__(kCbWarps * 32, 2) combine_bwd_pipe_kernel(
       stage ^= 1;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");  // no copy outstanding at exit
+  }
+  p2p_release_when_last(pp, wrote_peer);
+}
+
+// Pipelined combine forward (top_k <= 2, d <= 1024): as combine_bwd_pipe_kernel,
+// each warp prefetches its next token's expert-output rows into shared memory
+// while it sums the current one (same f32 fmaf order as combine_fwd_kernel).
+template <int VPL>
+__global__ void __launch_bounds__(kCbWarps * 32, 3) combine_fwd_pipe_kernel(
+    const __nv_bfloat16* __restrict__ Yl, const int32_t* __restrict__ pos, const float* __restrict__ w, int T,
+    int k, __nv_bfloat16* __restrict__ y, const P2P pp) {
+  constexpr int kRow = 32 * VPL;
+  constexpr int d = VPL * 256;
+  extern __shared__ uint4 cf_ring[];  // [warp][2 stages][Y_0, Y_1][kRow]
+  p2p_block_wait(pp);  // P2P: the expert GPUs' Y rows are complete
+  const int lane = threadIdx.x & 31;
+  uint4* ring = cf_ring + (threadIdx.x >> 5) * (2 * 2 * kRow);
+  const int W = gridDim.x * kCbWarps;
+  auto meta = [&](int t) {
+    CbMeta m{0, -1, 0.0f};
+    if (t < T) {
+      unit_meta(pos, w, static_cast<size_t>(t) * k, k, lane, m.pos, m.w);
+      m.to = unit_dst_of(pp, static_cast<size_t>(t) * k, k, lane);
+    }
+    return m;
+  };
+  auto fetch = [&](int t, int stage, const CbMeta& m) {
+    if (t < T) {
+      uint4* s = ring + stage * 2 * kRow;
+      for (int j = 0; j < k; ++j) {
+        const int row = __shfl_sync(0xffffffffu, m.pos, j);
+        const int to = __shfl_sync(0xffffffffu, m.to, j);
+        if (row < 0) continue;
+        const uint4* src = reinterpret_cast<const uint4*>(
+            (to >= 0 ? reinterpret_cast<const __nv_bfloat16*>(pp.base[to] + pp.y_off) : Yl) +
+            static_cast<size_t>(row) * d);
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) cp_async16(s + j * kRow + lane + 32 * i, src + lane + 32 * i);
+      }
+    }
+    cp_async_commit();
+  };
+  int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  CbMeta cur = meta(t), nxt = meta(t + W);
+  fetch(t, 0, cur);
+  int stage = 0;
+  for (; t < T; t += W) {
+    const CbMeta after = meta(t + 2 * W);
+    fetch(t + W, stage ^ 1, nxt);
+    cp_async_wait1();
+    const uint4* s = ring + stage * 2 * kRow;
+    float acc[VPL][8];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[i][c] = 0.0f;
+    for (int j = 0; j < k; ++j) {
+      const int row = __shfl_sync(0xffffffffu, cur.pos, j);
+      const float wj = __shfl_sync(0xffffffffu, cur.w, j);
+      if (row < 0) continue;  // dropped units contribute nothing
+      uint4 q[VPL];
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) q[i] = s[j * kRow + lane + 32 * i];
+      axpy_row<VPL>(acc, q, wj);
+    }
+    store_row<VPL>(y, t, d, lane, acc);
+    cur = nxt;
+    nxt = after;
+    stage ^= 1;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// Pipelined dispatch (d <= 1024): each warp copies its next token's x row into
+// shared memory (cp.async) and resolves that token's unit rows (lane j: unit j,
+// the same rule as dispatch_token) while the current token's row copy is in
+// flight, then writes the current token's k rows from shared memory.
+template <int VPL>
+__global__ void __launch_bounds__(256) dispatch_pipe_kernel(
+    const __nv_bfloat16* __restrict__ x, int T, int k, int N, int G, int me, int direct,
+    const int32_t* __restrict__ idx, const int32_t* __restrict__ tile_rank, const int32_t* __restrict__ tile_base,
+    PlanDev p, int32_t* __restrict__ pos_out, __nv_bfloat16* __restrict__ buf, int32_t* __restrict__ row_expert,
+    const P2P pp, int tok_blocks, __nv_bfloat16* __restrict__ pad_buf) {
+  constexpr int kRow = 32 * VPL;
+  constexpr int d = VPL * 256;
+  extern __shared__ uint4 dp_ring[];  // [warp][2 stages][kRow]
+  bool wrote_peer = false;
+  if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero pad_buf's padding rows
+    const int b = blockIdx.x - tok_blocks;
+    zero_pad_segment(pad_buf, d, p, b / kPadParts, b % kPadParts, kPadParts, row_expert);
+  } else {
+    const int lane = threadIdx.x & 31;
+    uint4* ring = dp_ring + (threadIdx.x >> 5) * (2 * kRow);
+    const int W = tok_blocks * (blockDim.x >> 5);
+    const int shift = gate_tile_shift(N);
+    auto route_units = [&](int t, int& row, int& to, int& e) {
+      row = -1;
+      to = -1;
+      e = 0;
+      if (t < T && lane < k) {
+        const int u = t * k + lane;
+        e = idx[u];
+        const int r = tile_base[static_cast<size_t>(t >> shift) * N + e] + tile_rank[u];
+        if (direct) {
+          row = r < p.chunk_cnt[e] ? p.seg_start[p.local_index[e]] + r : -1;
+        } else {
+          for (int i = 0; i < G; ++i) {
+            const int dst = (i == 0) ? me : (i <= me ? i - 1 : i);
+            const int lo = p.chunk_lo[e * G + dst];
+            if (r < lo + p.chunk_cnt[e * G + dst]) {
+              row = pp.unit_dst ? p.peer_row[e * G + dst] + (r - lo) : p.send_off[e * G + dst] + (r - lo);
+              to = dst;
+              break;
+            }
+          }
+        }
+      }
+    };
+    auto fetch = [&](int t, int stage) {
+      if (t < T) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * d);
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) cp_async16(ring + stage * kRow + lane + 32 * i, src + lane + 32 * i);
+      }
+      cp_async_commit();
+    };
+    int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int row0, to0, e0;
+    route_units(t, row0, to0, e0);
+    fetch(t, 0);
+    int stage = 0;
+    for (; t < T; t += W) {
+      fetch(t + W, stage ^ 1);
+      int row1, to1, e1;
+      route_units(t + W, row1, to1, e1);  // its loads overlap both rows' copies
+      if (lane < k) {
+        const int u = t * k + lane;
+        pos_out[u] = row0;  // -1: dropped by the capacity rule (StaticEP)
+        if (pp.unit_dst) pp.unit_dst[u] = row0 >= 0 ? to0 : -1;
+        if (row_expert && row0 >= 0) row_expert[row0] = e0;
+      }
+      cp_async_wait1();
+      uint4 v[VPL];
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) v[i] = ring[stage * kRow + lane + 32 * i];
+      for (int j = 0; j < k; ++j) {
+        const int row = __shfl_sync(0xffffffffu, row0, j);
+        const int to = __shfl_sync(0xffffffffu, to0, j);
+        if (row < 0) continue;
+        wrote_peer |= pp.unit_dst && to != pp.me;
+        __nv_bfloat16* out = pp.unit_dst ? reinterpret_cast<__nv_bfloat16*>(pp.base[to] + pp.x_off) : buf;
+        uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d);
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) dst[lane + 32 * i] = v[i];
+      }
+      row0 = row1;
+      to0 = to1;
+      e0 = e1;
+      stage ^= 1;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   p2p_release_when_last(pp, wrote_peer);
 }
@@ -1280,27 +1451,6 @@ int resident_grid(const void* kern, int threads) {
   return grid;
 }
 
-void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
-                     const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
-                     const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
-                     cudaStream_t s, const P2P* pp, void* pad_buf, int Nl) {
-  const P2P none = no_p2p();
-  if (d % 8 != 0 || d > 2048) throw std::invalid_argument("dispatch: d_model must be a multiple of 8, <= 2048");
-  const int warps = 8;
-  // P2P pushes: one resident wave striding over the tokens, so each block's
-  // system-scope release is paid once per block rather than per 8 tokens
-  int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
-  if (pp && pp->signal_slot >= 0)
-    tok_blocks = std::min(tok_blocks, resident_grid(reinterpret_cast<const void*>(dispatch_kernel), warps * 32));
-  const int pad_blocks = pad_buf ? Nl * kPadParts : 0;
-  if (tok_blocks + pad_blocks == 0) return;
-  dispatch_kernel<<<tok_blocks + pad_blocks, warps * 32, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(x), T, d, k, N, G, me, direct ? 1 : 0, idx, tile_rank,
-      tile_base, p, pos, static_cast<__nv_bfloat16*>(buf), row_expert, pp ? *pp : none, tok_blocks,
-      static_cast<__nv_bfloat16*>(pad_buf), Nl);
-  FM_LAUNCH_CHECK("dispatch_kernel");
-}
-
 void launch_zero_pad(void* buf, int d, const PlanDev& p, int Nl, int32_t* row_expert, cudaStream_t s) {
   if (Nl <= 0) return;
   dim3 grid(kPadParts, Nl);
@@ -1328,11 +1478,107 @@ void launch_relayout(void* recv, void* perm, int d, int G, int Nl, const PlanDev
     default: throw std::invalid_argument("d_model must be 256*{1,2,3,4,6,8}"); \
   }
 
+// Resident blocks per SM of a pipelined gather kernel at its dynamic shared
+// memory (sets the attribute; cached per device and kernel).
+int pipe_blocks_per_sm(const void* kern, int threads, int smem) {
+  ensure_dynamic_smem(kern, smem);
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> cache;
+  int dev = 0;
+  FM_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({dev, kern});
+  if (it == cache.end()) {
+    int n = 0;
+    FM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem));
+    it = cache.emplace(std::make_pair(dev, kern), std::max(1, n)).first;
+  }
+  return it->second;
+}
+
+// The pipelined dispatch (V <= 4): one resident wave of warps.
+template <int V>
+bool launch_dispatch_pipe(const void* x, int T, int k, int N, int G, int me, bool direct, const int32_t* idx,
+                          const int32_t* tile_rank, const int32_t* tile_base, const PlanDev& p, int32_t* pos,
+                          void* buf, int32_t* row_expert, cudaStream_t s, const P2P& pp, void* pad_buf, int Nl) {
+  if constexpr (V > 4) {
+    return false;
+  } else {
+    const void* kern = reinterpret_cast<const void*>(dispatch_pipe_kernel<V>);
+    const int smem = 8 * 2 * 32 * V * 16;
+    const int per_sm = pipe_blocks_per_sm(kern, 256, smem);
+    const int tok_blocks = std::min((std::max(T, 0) + 7) / 8, per_sm * num_sms());
+    const int pad_blocks = pad_buf ? Nl * kPadParts : 0;
+    if (tok_blocks + pad_blocks == 0) return true;
+    dispatch_pipe_kernel<V><<<tok_blocks + pad_blocks, 256, smem, s>>>(
+        static_cast<const __nv_bfloat16*>(x), T, k, N, G, me, direct ? 1 : 0, idx, tile_rank, tile_base, p, pos,
+        static_cast<__nv_bfloat16*>(buf), row_expert, pp, tok_blocks, static_cast<__nv_bfloat16*>(pad_buf));
+    FM_LAUNCH_CHECK("dispatch_pipe_kernel");
+    return true;
+  }
+}
+
+
+void launch_dispatch(const void* x, int T, int d, int k, int N, int G, int me, bool direct,
+                     const int32_t* idx, const int32_t* tile_rank, const int32_t* tile_base,
+                     const PlanDev& p, int32_t* pos, void* buf, int32_t* row_expert,
+                     cudaStream_t s, const P2P* pp, void* pad_buf, int Nl) {
+  const P2P none = no_p2p();
+  if (d % 8 != 0 || d > 2048) throw std::invalid_argument("dispatch: d_model must be a multiple of 8, <= 2048");
+#if FM_DISPATCH_PIPE
+  if (d % 256 == 0 && d <= 1024 && k <= 32) {
+    bool launched = false;
+    FM_VPL_DISPATCH(d, (launched = launch_dispatch_pipe<V>(x, T, k, N, G, me, direct, idx, tile_rank, tile_base,
+                                                           p, pos, buf, row_expert, s, pp ? *pp : none,
+                                                           pad_buf, Nl)));
+    if (launched) return;
+  }
+#endif
+  const int warps = 8;
+  // P2P pushes: one resident wave striding over the tokens, so each block's
+  // system-scope release is paid once per block rather than per 8 tokens
+  int tok_blocks = (std::max(T, 0) + warps - 1) / warps;
+  if (pp && pp->signal_slot >= 0)
+    tok_blocks = std::min(tok_blocks, resident_grid(reinterpret_cast<const void*>(dispatch_kernel), warps * 32));
+  const int pad_blocks = pad_buf ? Nl * kPadParts : 0;
+  if (tok_blocks + pad_blocks == 0) return;
+  dispatch_kernel<<<tok_blocks + pad_blocks, warps * 32, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(x), T, d, k, N, G, me, direct ? 1 : 0, idx, tile_rank,
+      tile_base, p, pos, static_cast<__nv_bfloat16*>(buf), row_expert, pp ? *pp : none, tok_blocks,
+      static_cast<__nv_bfloat16*>(pad_buf), Nl);
+  FM_LAUNCH_CHECK("dispatch_kernel");
+}
+
+// The pipelined combine forward (V <= 4): one resident wave of warps.
+template <int V>
+bool launch_combine_fwd_pipe(const void* Y, const int32_t* pos, const float* w, int T, int k, void* y,
+                             cudaStream_t s, const P2P& pp) {
+  if constexpr (V > 4) {
+    return false;
+  } else {
+    const void* kern = reinterpret_cast<const void*>(combine_fwd_pipe_kernel<V>);
+    const int smem = kCbWarps * 2 * 2 * 32 * V * 16;
+    const int per_sm = pipe_blocks_per_sm(kern, kCbWarps * 32, smem);
+    const int grid = std::min((T + kCbWarps - 1) / kCbWarps, per_sm * num_sms());
+    combine_fwd_pipe_kernel<V><<<grid, kCbWarps * 32, smem, s>>>(
+        static_cast<const __nv_bfloat16*>(Y), pos, w, T, k, static_cast<__nv_bfloat16*>(y), pp);
+    FM_LAUNCH_CHECK("combine_fwd_pipe_kernel");
+    return true;
+  }
+}
+
 void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T, int d, int k,
                         void* y, cudaStream_t s, const P2P* pp) {
   const P2P none = no_p2p();
   if (T <= 0) return;
   if (d % 256 != 0) throw std::invalid_argument("combine: d_model must be a multiple of 256");
+#if FM_COMBINE_FWD_PIPE
+  if (k <= 2 && d <= 1024) {
+    bool launched = false;
+    FM_VPL_DISPATCH(d, (launched = launch_combine_fwd_pipe<V>(Y, pos, w, T, k, y, s, pp ? *pp : none)));
+    if (launched) return;
+  }
+#endif
   const int warps = 8;
   const int grid = (T + warps - 1) / warps;
   FM_VPL_DISPATCH(d, (combine_fwd_kernel<V><<<grid, warps * 32, 0, s>>>(
@@ -1352,22 +1598,7 @@ bool launch_combine_bwd_pipe(const void* dy, const void* Y, const int32_t* pos, 
   } else {
     const void* kern = reinterpret_cast<const void*>(combine_bwd_pipe_kernel<V>);
     const int smem = kCbWarps * 2 * 3 * 32 * V * 16;
-    ensure_dynamic_smem(kern, smem);
-    static std::mutex mu;
-    static std::map<int, int> per_sm_cache;  // device -> resident blocks per SM
-    int dev = 0;
-    FM_CUDA(cudaGetDevice(&dev));
-    int per_sm = 0;
-    {
-      std::lock_guard<std::mutex> lock(mu);
-      auto it = per_sm_cache.find(dev);
-      if (it == per_sm_cache.end()) {
-        int n = 0;
-        FM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kCbWarps * 32, smem));
-        it = per_sm_cache.emplace(dev, std::max(1, n)).first;
-      }
-      per_sm = it->second;
-    }
+    const int per_sm = pipe_blocks_per_sm(kern, kCbWarps * 32, smem);
     const int tok_blocks = std::min((std::max(T, 0) + kCbWarps - 1) / kCbWarps, per_sm * num_sms());
     if (tok_blocks + pad_blocks == 0) return true;
     combine_bwd_pipe_kernel<V><<<tok_blocks + pad_blocks, kCbWarps * 32, smem, s>>>(

@@ -13,7 +13,7 @@ ncu --set full --clock-control none --import-source on -k regex:grouped_gemm -s 
     -o gpurun_out/prof_gemm -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_gemm.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"gate_kernel|dispatch_kernel|combine_fwd|combine_bwd|unpermute|segment_tile|expert_scan|plan_kernel" \
+    -k regex:"gate_kernel|dispatch_kernel|dispatch_pipe|combine_fwd|combine_bwd|unpermute|segment_tile|expert_scan|plan_kernel" \
     -s 15 -c 5 -o gpurun_out/prof_hbm -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_hbm.log 2>&1
 ncu --target-processes all --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
