@@ -759,6 +759,18 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// combine-backward ring: stages per warp (tokens in flight + 1) and warps per block
+#ifndef FM_CB_STAGES
+#define FM_CB_STAGES 2
+#endif
+#ifndef FM_CB_WARPS
+#define FM_CB_WARPS 8
+#endif
+constexpr int kCbStages = FM_CB_STAGES, kCbBwdWarps = FM_CB_WARPS;
 
 struct CbMeta {
   int pos, to;  // lane j < k: unit j's row and destination GPU
@@ -766,22 +778,23 @@ struct CbMeta {
 };
 
 template <int VPL>
-__global__ void __launch_bounds__(kCbWarps * 32, 2) combine_bwd_pipe_kernel(
+__global__ void __launch_bounds__(kCbBwdWarps * 32, 16 / kCbBwdWarps) combine_bwd_pipe_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ Yl,
     const int32_t* __restrict__ pos, const float* __restrict__ w, int T, int k,
     __nv_bfloat16* __restrict__ dYl, float* __restrict__ dl, float* __restrict__ dl_rows_l, const P2P pp,
     int tok_blocks, PlanDev pad_plan) {
   constexpr int kRow = 32 * VPL;  // uint4 per row
   constexpr int d = VPL * 256;
-  extern __shared__ uint4 cb_ring[];  // [warp][2 stages][dy, Y_0, Y_1][kRow]
+  constexpr int S = kCbStages;
+  extern __shared__ uint4 cb_ring[];  // [warp][S stages][dy, Y_0, Y_1][kRow]
   bool wrote_peer = false;
   if (static_cast<int>(blockIdx.x) >= tok_blocks) {  // trailing blocks: zero dYl's padding rows
     const int b = blockIdx.x - tok_blocks;
     zero_pad_segment(dYl, d, pad_plan, b / kPadParts, b % kPadParts, kPadParts, nullptr);
   } else {
     const int lane = threadIdx.x & 31;
-    uint4* ring = cb_ring + (threadIdx.x >> 5) * (2 * 3 * kRow);
-    const int W = tok_blocks * kCbWarps;
+    uint4* ring = cb_ring + (threadIdx.x >> 5) * (S * 3 * kRow);
+    const int W = tok_blocks * kCbBwdWarps;
     auto meta = [&](int t) {
       CbMeta m{0, -1, 0.0f};
       if (t < T) {
@@ -810,13 +823,19 @@ __global__ void __launch_bounds__(kCbWarps * 32, 2) combine_bwd_pipe_kernel(
       cp_async_commit();  // one group per call, empty or not: wait_group 1 counts calls
     };
     int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    CbMeta cur = meta(t), nxt = meta(t + W);
-    fetch(t, 0, cur);
+    CbMeta m[S];  // m[i]: token t + i*W (indices fixed after unrolling: registers)
+#pragma unroll
+    for (int i = 0; i < S - 1; ++i) {
+      m[i] = meta(t + i * W);
+      fetch(t + i * W, i, m[i]);
+    }
+    m[S - 1] = meta(t + (S - 1) * W);
     int stage = 0;
     for (; t < T; t += W) {
-      const CbMeta after = meta(t + 2 * W);  // lands while this token computes
-      fetch(t + W, stage ^ 1, nxt);
-      cp_async_wait1();  // this lane's copies of token t are in shared memory
+      const CbMeta after = meta(t + S * W);  // lands while this token computes
+      fetch(t + (S - 1) * W, stage == 0 ? S - 1 : stage - 1, m[S - 1]);
+      cp_async_wait<S - 1>();  // this lane's copies of token t are in shared memory
+      const CbMeta& cur = m[0];
       const uint4* s = ring + stage * 3 * kRow;
       float my_dw = 0.0f;
       for (int j = 0; j < k; ++j) {
@@ -855,9 +874,10 @@ __global__ void __launch_bounds__(kCbWarps * 32, 2) combine_bwd_pipe_kernel(
         float* dl_rows = peer_rows(pp, pp.dl_off, cur.to, dl_rows_l);
         if (dl_rows && cur.pos >= 0) dl_rows[cur.pos] = g_l;
       }
-      cur = nxt;
-      nxt = after;
-      stage ^= 1;
+#pragma unroll
+      for (int i = 0; i < S - 1; ++i) m[i] = m[i + 1];
+      m[S - 1] = after;
+      stage = stage + 1 == S ? 0 : stage + 1;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");  // no copy outstanding at exit
   }
@@ -1597,11 +1617,11 @@ bool launch_combine_bwd_pipe(const void* dy, const void* Y, const int32_t* pos, 
     return false;
   } else {
     const void* kern = reinterpret_cast<const void*>(combine_bwd_pipe_kernel<V>);
-    const int smem = kCbWarps * 2 * 3 * 32 * V * 16;
-    const int per_sm = pipe_blocks_per_sm(kern, kCbWarps * 32, smem);
-    const int tok_blocks = std::min((std::max(T, 0) + kCbWarps - 1) / kCbWarps, per_sm * num_sms());
+    const int smem = kCbBwdWarps * kCbStages * 3 * 32 * V * 16;
+    const int per_sm = pipe_blocks_per_sm(kern, kCbBwdWarps * 32, smem);
+    const int tok_blocks = std::min((std::max(T, 0) + kCbBwdWarps - 1) / kCbBwdWarps, per_sm * num_sms());
     if (tok_blocks + pad_blocks == 0) return true;
-    combine_bwd_pipe_kernel<V><<<tok_blocks + pad_blocks, kCbWarps * 32, smem, s>>>(
+    combine_bwd_pipe_kernel<V><<<tok_blocks + pad_blocks, kCbBwdWarps * 32, smem, s>>>(
         static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(Y), pos, w, T, k,
         static_cast<__nv_bfloat16*>(dYbuf), dl, dl_rows, pp, tok_blocks, pad_plan);
     FM_LAUNCH_CHECK("combine_bwd_pipe_kernel");
