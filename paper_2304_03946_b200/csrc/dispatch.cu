@@ -741,12 +741,14 @@ __global__ void __launch_bounds__(256, VPL <= 4 ? 3 : 1) combine_bwd_kernel(
 #ifndef FM_COMBINE_BWD_PIPE
 #define FM_COMBINE_BWD_PIPE 1
 #endif
-// A/B knobs, measured and off (profiles/r02_gather_pipe.log): the same
-// pipelining for the combine forward (-7 µs, but the combine backward after it
-// +6 µs: no net change) and for the dispatch (+4 µs: its per-token index chain
-// is not what limits it)
+// The same pipelining for the combine forward: 2 = top-1 only (default: one
+// register-held row per warp there; -27..-30 % at configs[2] / [4], the
+// combine backward after it +3..+6 %), 1 = also top-2 (-7 µs at configs[1],
+// but +6 µs in the combine backward after it: no net change), 0 = off; and for
+// the dispatch (off: +4..+25 µs, its per-token index chain is not what limits
+// it). profiles/r02_gather_pipe.log, r02_gather_pipe_top1.log
 #ifndef FM_COMBINE_FWD_PIPE
-#define FM_COMBINE_FWD_PIPE 0
+#define FM_COMBINE_FWD_PIPE 2
 #endif
 #ifndef FM_DISPATCH_PIPE
 #define FM_DISPATCH_PIPE 0
@@ -1593,7 +1595,7 @@ void launch_combine_fwd(const void* Y, const int32_t* pos, const float* w, int T
   if (T <= 0) return;
   if (d % 256 != 0) throw std::invalid_argument("combine: d_model must be a multiple of 256");
 #if FM_COMBINE_FWD_PIPE
-  if (k <= 2 && d <= 1024) {
+  if (k <= (FM_COMBINE_FWD_PIPE == 1 ? 2 : 1) && d <= 1024) {
     bool launched = false;
     FM_VPL_DISPATCH(d, (launched = launch_combine_fwd_pipe<V>(Y, pos, w, T, k, y, s, pp ? *pp : none)));
     if (launched) return;

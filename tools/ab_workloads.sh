@@ -8,7 +8,8 @@ for i in $(seq 1 ${ITERS:-2}); do
         --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29617 bench.py --gpus 1 --workload $w \
         --steps ${STEPS:-30} --no-cpu-baseline 2>/dev/null | tail -1 | python -c "
 import json,sys; j=json.loads(sys.stdin.read()); k=j['kernels']
-print('$w $v', round(j['value']/1e6,3), 'Mtok/s', j['clocks']['sm_mhz'], 'MHz gemm', j['roofline']['achieved'], 'wgrad ms', k.get('ffn2_wgrad',{}).get('ms_per_step'), k.get('ffn1_wgrad',{}).get('ms_per_step'))"
+print('$w $v', round(j['value']/1e6,3), 'Mtok/s', j['clocks']['sm_mhz'], 'MHz gemm', j['roofline']['achieved'], 'wgrad ms', k.get('ffn2_wgrad',{}).get('ms_per_step'), k.get('ffn1_wgrad',{}).get('ms_per_step'),
+      {n: round(k[n]['ms_per_step'], 4) for n in ('dispatch', 'combine_fwd', 'combine_bwd', 'unpermute', 'bias_grad') if n in k})"
     done
   done
 done
