@@ -23,14 +23,21 @@ std::atomic<unsigned long long> g_launches{0};
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-int num_sms() {
-  static int sms = [] {
-    int dev = 0, n = 0;
-    FM_CUDA(cudaGetDevice(&dev));
+int num_sms() {  // of the current device (cached per device)
+  static std::atomic<int> sms[64];
+  int dev = 0;
+  FM_CUDA(cudaGetDevice(&dev));
+  if (dev >= 64) {
+    int n = 0;
     FM_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
     return n;
-  }();
-  return sms;
+  }
+  int n = sms[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    FM_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    sms[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
 }
 
 void ensure_dynamic_smem(const void* kernel, int bytes) {

@@ -1462,14 +1462,16 @@ void launch_plan(int64_t* flows, int N, int G, int me, const int32_t* local_expe
 // per kernel): the grid of the token-striding kernels.
 int resident_grid(const void* kern, int threads) {
   static std::mutex mu;
-  static std::unordered_map<const void*, int> cache;
+  static std::map<std::pair<int, const void*>, int> cache;  // (device, kernel) -> grid
+  int dev = 0;
+  FM_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
-  auto it = cache.find(kern);
+  auto it = cache.find({dev, kern});
   if (it != cache.end()) return it->second;
   int per_sm = 0;
   FM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
   const int grid = std::max(1, per_sm) * num_sms();
-  cache.emplace(kern, grid);
+  cache.emplace(std::make_pair(dev, kern), grid);
   return grid;
 }
 
