@@ -772,6 +772,9 @@ __device__ __forceinline__ void cp_async_wait() {
 #ifndef FM_CB_WARPS
 #define FM_CB_WARPS 8
 #endif
+#ifndef FM_CB_REVERSE
+#define FM_CB_REVERSE 1
+#endif
 constexpr int kCbStages = FM_CB_STAGES, kCbBwdWarps = FM_CB_WARPS;
 
 struct CbMeta {
@@ -797,18 +800,21 @@ __global__ void __launch_bounds__(kCbBwdWarps * 32, 16 / kCbBwdWarps) combine_bw
     const int lane = threadIdx.x & 31;
     uint4* ring = cb_ring + (threadIdx.x >> 5) * (S * 3 * kRow);
     const int W = tok_blocks * kCbBwdWarps;
+    // FM_CB_REVERSE: tokens last-to-first, so the first Y rows read are the
+    // ones the combine forward (first-to-last, just before) left in L2
+    auto tok = [&](int t) { return FM_CB_REVERSE ? T - 1 - t : t; };
     auto meta = [&](int t) {
       CbMeta m{0, -1, 0.0f};
       if (t < T) {
-        unit_meta(pos, w, static_cast<size_t>(t) * k, k, lane, m.pos, m.w);
-        m.to = unit_dst_of(pp, static_cast<size_t>(t) * k, k, lane);
+        unit_meta(pos, w, static_cast<size_t>(tok(t)) * k, k, lane, m.pos, m.w);
+        m.to = unit_dst_of(pp, static_cast<size_t>(tok(t)) * k, k, lane);
       }
       return m;
     };
     auto fetch = [&](int t, int stage, const CbMeta& m) {
       if (t < T) {
         uint4* s = ring + stage * 3 * kRow;
-        const uint4* g = reinterpret_cast<const uint4*>(dy + static_cast<size_t>(t) * d);
+        const uint4* g = reinterpret_cast<const uint4*>(dy + static_cast<size_t>(tok(t)) * d);
 #pragma unroll
         for (int i = 0; i < VPL; ++i) cp_async16(s + lane + 32 * i, g + lane + 32 * i);
         for (int j = 0; j < k; ++j) {
@@ -872,7 +878,7 @@ __global__ void __launch_bounds__(kCbBwdWarps * 32, 16 / kCbBwdWarps) combine_bw
       wdw = warp_sum(wdw);
       if (lane < k) {
         const float g_l = cur.w * (my_dw - wdw);
-        dl[static_cast<size_t>(t) * k + lane] = g_l;
+        dl[static_cast<size_t>(tok(t)) * k + lane] = g_l;
         float* dl_rows = peer_rows(pp, pp.dl_off, cur.to, dl_rows_l);
         if (dl_rows && cur.pos >= 0) dl_rows[cur.pos] = g_l;
       }
